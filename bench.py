@@ -1,0 +1,528 @@
+"""Benchmark driver for the B200 guided-filter layer.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg1] [--impl ours|reference]
+
+Prints ONE JSON line (rank 0).  Default workload: BASELINE.json configs[1],
+the full-resolution guided filter forward (4 x {1,3} x 2048^2, r=8,
+eps=1e-2, fp32), on seeded synthetic inputs with that config's shapes and
+value distributions (workloads.py).  Other configs: cfg0 (joint fwd 1024^2),
+cfg3 (joint fwd sweep point, --hr/--batch/--radius), cfg4a/cfg4b (joint
+fwd+bwd), cfg2 (training step).
+
+* ``value``: whole-job output Mpix/s with inputs resident in HBM, timed with
+  CUDA events on the launching stream over exactly K steps bracketed by a
+  barrier + synchronize, max over ranks.  A "step" is one call of the layer
+  over the whole batch.  Multi-GPU: every rank runs the full per-GPU batch on
+  its own GPU (weak scaling, batch sharding, no data-path collective).
+* ``e2e``: the same metric through the public Python API with pinned HOST
+  buffers: H2D of the step's inputs and D2H of its output inside the timed
+  region.
+* ``roofline``: algorithmic bytes per launch of the dominant kernel (SURVEY
+  8d) / its average CUDA-event duration, against the measured HBM copy peak
+  (MEASURED_PEAKS.json).
+* ``cpu_baseline``: the CPU oracle (numpy port of the reference algorithm)
+  on a bounded sample, rank 0, N=1 only.
+* ``--impl reference``: the oracle port on the host cores (multiprocessing
+  over images), same metric/config, bounded per-step sample.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "guided-filter output Mpix/s (fwd, fwd+bwd) and % of HBM roofline"
+
+
+# ---------------------------------------------------------------------------
+# workload descriptions
+# ---------------------------------------------------------------------------
+
+def workload_spec(args):
+    from workloads import CONFIGS
+
+    c = dict(CONFIGS[args.config])
+    if args.batch:
+        c["batch"] = args.batch
+    if args.hr:
+        c["hr"] = args.hr
+    if args.radius is not None:
+        c["r"] = args.radius
+    return c
+
+
+def algorithmic_bytes(c):
+    """SURVEY 8(d) compulsory bytes per step, fp32."""
+    B, C, H = c["batch"], c["channels"], c["hr"]
+    hw = H * H
+    if c["kind"] == "highres_fwd":
+        return 4 * B * (1 + 2 * C) * hw
+    h = H // c["factor"]
+    lw = h * h
+    if c["kind"] == "joint_fwd":
+        return 4 * B * C * (2 * hw + 2 * lw)
+    if c["kind"] == "joint_fwd_bwd":
+        return 4 * B * C * (2 * hw + 2 * lw) + 4 * B * C * (3 * hw + 4 * lw)
+    if c["kind"] == "train_step":
+        return 4 * B * C * (4 * hw + 4 * lw)
+    raise ValueError(c["kind"])
+
+
+# ---------------------------------------------------------------------------
+# clocks sampling (nvidia-smi during the timed region)
+# ---------------------------------------------------------------------------
+
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self.proc = None
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except (OSError, FileNotFoundError):
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 6:
+                self.samples.append(parts)
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        sm, mx, reasons = [], [], set()
+        for s in self.samples:
+            try:
+                sm.append(float(s[0]))
+                mx.append(float(s[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, s[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def measured_peak():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    except (OSError, KeyError, ValueError):
+        return 6650.0, "fallback"
+
+
+def ncu_traffic(config_name):
+    """Per-launch DRAM bytes of the dominant kernel from the committed ncu
+    capture summary (profiles/traffic.json), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            return json.load(f).get(config_name)
+    except (OSError, ValueError):
+        return None
+
+
+# ---------------------------------------------------------------------------
+# our implementation
+# ---------------------------------------------------------------------------
+
+class OursStep:
+    """Device-resident inputs; one step = one C-ABI layer call (plus, for the
+    training config, the full pipeline)."""
+
+    def __init__(self, c, device, seed):
+        import torch
+
+        import workloads
+        from paper_1803_05619_b200 import _lib
+
+        self.c, self.device = c, device
+        self.lib = _lib.load()
+        self.stream = torch.cuda.current_stream(device)
+        self.sp = self.stream.cuda_stream
+        self.status = torch.zeros(1, dtype=torch.int32, device=device)
+        B, C, H = c["batch"], c["channels"], c["hr"]
+        self.pixels = B * H * H
+        kind = c["kind"]
+        self.kind = kind
+        g = torch.Generator(device="cpu").manual_seed(seed)
+        if kind == "highres_fwd":
+            guide, src = workloads.highres_inputs(B, C, H, H, seed=seed, device=device)
+            self.inputs = [guide, src]
+            self.out = torch.empty_like(src)
+            fused = self.lib.gf_highres_fwd_is_fused(0, B, 1, C, H, H, c["r"])
+            nb = 16 if fused else self.lib.gf_highres_workspace_bytes(0, B, 1, C, H, H, c["r"])
+            self.ws = torch.empty(nb, dtype=torch.uint8, device=device)
+            # generic path: products, 4x(box_v, box_h), coeffs, 2 copies, 2x2 box, apply
+            self.launches = 1 if fused else 17
+        else:
+            f = c["factor"]
+            lr_x, lr_y, hr_x = workloads.joint_inputs(B, C, H, H, f, seed=seed, device=device)
+            self.inputs = [lr_x, lr_y, hr_x]
+            self.h = H // f
+            self.out = torch.empty_like(hr_x)
+            nb = self.lib.gf_joint_workspace_bytes(0, B, C, self.h, self.h, H, H, c["r"])
+            self.ws = torch.empty(max(nb, 16), dtype=torch.uint8, device=device)
+            if kind in ("joint_fwd_bwd", "train_step"):
+                self.d_out = torch.randn(hr_x.shape, generator=g).to(device)
+                self.d_lr_x = torch.empty_like(lr_x)
+                self.d_lr_y = torch.empty_like(lr_y)
+                self.d_hr_x = torch.empty_like(hr_x)
+            if kind == "train_step":
+                import numpy as np
+
+                import paper_1803_05619_b200 as gfb
+
+                self.net = gfb.GuidanceNet(3, 3, hidden=c["hidden"], kernel=1,
+                                           rng=np.random.default_rng(seed), device=device)
+                self.target = workloads.affine_target(hr_x).contiguous()
+                self.params = gfb.GuidedFilterParams(c["r"], c["eps"])
+            fused = self.lib.gf_joint_is_fused(0, B, C, self.h, self.h, H, H, c["r"])
+            fwd = 1 if fused else 12
+            bwd = 3 if fused else 26
+            self.launches = {"joint_fwd": fwd, "joint_fwd_bwd": fwd + bwd,
+                             "train_step": 2 * 3 + fwd + 2 + bwd + 2 * 8}[kind]
+
+    def step(self):
+        c, L = self.c, self.lib
+        B, C, H, r, eps = c["batch"], c["channels"], c["hr"], c["r"], c["eps"]
+        if self.kind == "highres_fwd":
+            g, s = self.inputs
+            rc = L.gf_highres_fwd(0, g.data_ptr(), s.data_ptr(), self.out.data_ptr(), B, 1, C, H,
+                                  H, r, eps, self.ws.data_ptr(), self.ws.numel(),
+                                  self.status.data_ptr(), self.sp)
+            assert rc == 0, L.gf_last_error()
+        elif self.kind in ("joint_fwd", "joint_fwd_bwd"):
+            lx, ly, hx = self.inputs
+            h = self.h
+            rc = L.gf_joint_fwd(0, lx.data_ptr(), ly.data_ptr(), hx.data_ptr(),
+                                self.out.data_ptr(), B, C, h, h, H, H, r, eps, self.ws.data_ptr(),
+                                self.ws.numel(), self.status.data_ptr(), self.sp)
+            assert rc == 0, L.gf_last_error()
+            if self.kind == "joint_fwd_bwd":
+                rc = L.gf_joint_bwd(0, lx.data_ptr(), ly.data_ptr(), hx.data_ptr(),
+                                    self.d_out.data_ptr(), self.d_lr_x.data_ptr(),
+                                    self.d_lr_y.data_ptr(), self.d_hr_x.data_ptr(), B, C, h, h, H,
+                                    H, r, eps, self.ws.data_ptr(), self.ws.numel(),
+                                    self.status.data_ptr(), self.sp)
+                assert rc == 0, L.gf_last_error()
+        else:  # train_step
+            import paper_1803_05619_b200 as gfb
+
+            lx, ly, hx = self.inputs
+            self.res = gfb.train_step(self.net, lx, hx, ly, self.target, self.params)
+
+    def e2e(self, steps, warmup):
+        """Public API with pinned host buffers, H2D + D2H inside the timed region."""
+        import torch
+
+        import paper_1803_05619_b200 as gfb
+
+        c = self.c
+        host_in = [t.cpu().pin_memory() for t in self.inputs]
+        host_out = torch.empty(self.out.shape, dtype=self.out.dtype).pin_memory()
+        p = gfb.GuidedFilterParams(c["r"], c["eps"])
+
+        def one():
+            dev = [t.to(self.device, non_blocking=True) for t in host_in]
+            if self.kind == "highres_fwd":
+                out, _ = gfb.forward_highres(dev[0], dev[1], p, check=False)
+                res = out
+            elif self.kind == "joint_fwd":
+                out, _ = gfb.forward_joint(dev[0], dev[2], dev[1], p, check=False)
+                res = out
+            elif self.kind == "joint_fwd_bwd":
+                out, tape = gfb.forward_joint(dev[0], dev[2], dev[1], p, check=False)
+                gr = gfb.backward(tape, out, check=False)  # d_out = out (<out,out>/2 probe)
+                res = gr.d_guide_hi
+            else:
+                r = gfb.train_step(self.net, dev[0], dev[2], dev[1], self.target, p)
+                res = r.out
+            host_out.copy_(res, non_blocking=True)
+
+        for _ in range(warmup):
+            one()
+        torch.cuda.synchronize(self.device)
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        t0.record()
+        for _ in range(steps):
+            one()
+        t1.record()
+        torch.cuda.synchronize(self.device)
+        ms = t0.elapsed_time(t1) / steps
+        h2d = sum(t.numel() * t.element_size() for t in host_in)
+        d2h = host_out.numel() * host_out.element_size()
+        return ms, h2d, d2h
+
+
+# ---------------------------------------------------------------------------
+# CPU oracle legs
+# ---------------------------------------------------------------------------
+
+def _oracle_image(args_tuple):
+    """Worker: one image (or a row band of it) of the config through the oracle."""
+    kind, C, H, rows, factor, r, eps, seed = args_tuple
+    import numpy as np
+
+    from oracle import gf_oracle as O
+
+    rng = np.random.default_rng(seed)
+    if kind == "highres_fwd":
+        g = rng.uniform(0, 1, (rows, H, 1))
+        s = rng.uniform(0, 1, (rows, H, C))
+        t0 = time.perf_counter()
+        O.forward_highres(np.repeat(g, C, axis=2), s, r, eps)
+        return time.perf_counter() - t0, rows * H
+    h_rows = max(1, rows // factor)
+    gl = rng.uniform(0, 1, (h_rows, H // factor, C))
+    sl = rng.uniform(0, 1, (h_rows, H // factor, C))
+    gh = rng.uniform(0, 1, (h_rows * factor, H, C))
+    t0 = time.perf_counter()
+    out, tape = O.forward_joint(gl, gh, sl, r, eps)
+    if kind != "joint_fwd":
+        O.backward(tape, out)
+    return time.perf_counter() - t0, h_rows * factor * H
+
+
+def cpu_sample(c, budget_s=12.0, procs=1, steps=1):
+    """Time the oracle on bounded row-band samples; returns Mpix/s and text."""
+    import multiprocessing as mp
+
+    kind = "joint_fwd_bwd" if c["kind"] in ("joint_fwd_bwd", "train_step") else c["kind"]
+    H, C = c["hr"], c["channels"]
+    rows = min(H, 256)
+    probe = _oracle_image((kind, C, H, rows, c.get("factor", 4), c["r"], c["eps"], 0))
+    per_row = probe[0] / rows
+    want_rows = int(max(16, min(H, budget_s / max(steps, 1) / max(per_row, 1e-9) / 2)))
+    want_rows -= want_rows % 16
+    want_rows = max(16, want_rows)
+    jobs = [(kind, C, H, want_rows, c.get("factor", 4), c["r"], c["eps"], k + 1)
+            for k in range(procs)]
+    results = []
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        if procs == 1:
+            res = [_oracle_image(jobs[0])]
+        else:
+            with mp.get_context("fork").Pool(procs) as pool:
+                res = pool.map(_oracle_image, jobs)
+        wall = time.perf_counter() - t0
+        px = sum(p for _, p in res)
+        results.append((wall, px))
+    wall = sum(w for w, _ in results)
+    px = sum(p for _, p in results)
+    sample = (f"{procs} x {want_rows}x{H} px row-band(s) of the {kind} workload "
+              f"(C={C}, r={c['r']}), float64 numpy oracle, {steps} step(s)")
+    return px / wall / 1e6, sample, wall / steps
+
+
+def run_reference(args, c, rank, world):
+    """--impl reference: the CPU oracle port on the host cores, rank 0 only."""
+    if rank != 0:
+        return
+    cores = len(os.sched_getaffinity(0))
+    procs = max(1, min(cores, c["batch"]))
+    budget = 150.0
+    total_steps = args.steps + args.warmup
+    # bounded per-step sample so the whole run stays within a few minutes
+    value, sample, _ = cpu_sample(c, budget_s=budget / max(total_steps, 1) * args.steps,
+                                  procs=procs, steps=args.steps)
+    line = {
+        "metric": METRIC, "value": round(value, 4), "unit": "Mpix/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": None,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded uniform [0,1])",
+        "config": config_block(args, c, world), "impl": "reference",
+        "cpu_baseline": {"value": round(value, 4), "unit": "Mpix/s", "cores": procs,
+                         "kind": "port", "sample": sample},
+        "e2e": {"value": round(value, 4), "unit": "Mpix/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+        "note": "reference is pure Python/numpy (no compiled CPU path to build); timed via the "
+                "pinned float64 oracle port, multiprocessing over images",
+    }
+    print(json.dumps(line), flush=True)
+
+
+def config_block(args, c, world):
+    B, C, H = c["batch"], c["channels"], c["hr"]
+    blk = {"workload": f"{args.config}: {c['kind']}", "batch_per_gpu": B, "channels": C,
+           "hr": [H, H], "radius": c["r"], "eps": c["eps"], "parallelism": f"batch-shard x{world}"}
+    if c["kind"] == "highres_fwd":
+        blk["guide_channels"] = 1
+    else:
+        blk["lr"] = [H // c["factor"], H // c["factor"]]
+    if c["kind"] == "train_step":
+        blk["guidance_hidden"] = c["hidden"]
+    bytes_ = algorithmic_bytes(c)
+    blk["l2"] = ("inputs+outputs %.0f MB > 126 MB L2 (no flush needed)" % (bytes_ / 1e6)
+                 if bytes_ > 2.5 * 126e6 else "L2 flushed between timed steps")
+    return blk
+
+
+# ---------------------------------------------------------------------------
+# main
+# ---------------------------------------------------------------------------
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="cfg1")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--batch", type=int, default=0)
+    ap.add_argument("--hr", type=int, default=0)
+    ap.add_argument("--radius", type=int, default=None)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--seed", type=int, default=0)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    c = workload_spec(args)
+
+    if args.impl == "reference":
+        run_reference(args, c, rank, world)
+        return
+
+    import torch
+
+    torch.cuda.set_device(local)
+    device = torch.device("cuda", local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=device)
+
+    st = OursStep(c, device, seed=args.seed + 1000 * rank)
+    flush = None
+    if algorithmic_bytes(c) <= 2.5 * 126e6:
+        flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=device)
+
+    for _ in range(args.warmup):
+        st.step()
+        if flush is not None:
+            flush.zero_()
+    torch.cuda.synchronize(device)
+    assert int(st.status.item()) == 0, f"status bits {int(st.status.item())}"
+
+    # timed region: K steps, barrier + sync both sides; per-step events so an
+    # L2 flush between steps stays outside the measured kernel time
+    sampler = ClockSampler(local) if rank == 0 else None
+    if sampler:
+        sampler.start()
+        time.sleep(0.3)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize(device)
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(args.steps)]
+    wall0 = time.perf_counter()
+    for k in range(args.steps):
+        if flush is not None:
+            flush.zero_()
+        evs[k][0].record()
+        st.step()
+        evs[k][1].record()
+    torch.cuda.synchronize(device)
+    if dist:
+        dist.barrier()
+    wall = time.perf_counter() - wall0
+    clocks = sampler.stop() if sampler else None
+    ms_steps = [a.elapsed_time(b) for a, b in evs]
+    ms = sum(ms_steps) / len(ms_steps)
+    if dist:
+        t = torch.tensor([ms], device=device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    assert int(st.status.item()) == 0, f"status bits {int(st.status.item())}"
+
+    px = st.pixels * world
+    value = px / (ms * 1e-3) / 1e6
+
+    e2e = None
+    if not args.no_e2e:
+        e_ms, h2d, d2h = st.e2e(steps=max(3, min(args.steps, 10)), warmup=2)
+        if dist:
+            t = torch.tensor([e_ms], device=device)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e_ms = float(t.item())
+        e2e = {"value": round(px / (e_ms * 1e-3) / 1e6, 3), "unit": "Mpix/s",
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+               "ms_per_step": round(e_ms, 4)}
+
+    if rank != 0:
+        if dist:
+            dist.destroy_process_group()
+        return
+
+    peak, peak_kind = measured_peak()
+    alg = algorithmic_bytes(c)
+    achieved = alg / (ms * 1e-3) / 1e9
+    roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                "frac": round(achieved / peak, 4), "traffic": ncu_traffic(args.config),
+                "peak_kind": peak_kind,
+                "algorithmic_bytes_per_launch": alg,
+                "frac_of_8TBps_nominal": round(achieved / 8000.0, 4)}
+
+    cpu = None
+    if world == 1 and not args.no_cpu:
+        v, sample, _ = cpu_sample(c, budget_s=12.0, procs=1, steps=1)
+        cpu = {"value": round(v, 4), "unit": "Mpix/s", "cores": 1, "kind": "port",
+               "sample": sample}
+
+    line = {
+        "metric": METRIC, "value": round(value, 3), "unit": "Mpix/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 5),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (seeded; BASELINE.json shapes and distributions, workloads.py)",
+        "config": config_block(args, c, world),
+        "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+        "gpu_launches": st.launches * args.steps,
+        "clocks": clocks, "wall_s_timed_region": round(wall, 4),
+        "ms_per_step_min": round(min(ms_steps), 5),
+    }
+    print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

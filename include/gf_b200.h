@@ -1,0 +1,160 @@
+/*
+ * gf_b200.h -- C ABI of the B200-native guided-filter layer (arXiv 1803.05619).
+ *
+ * Drop-in boundary for the reference package's layer path
+ * (/root/reference/pkg/src/guidedfilter, "gf/" below).  Every entry point is
+ * plain C: raw device pointers, 64-bit sizes, a dtype tag and a CUDA stream
+ * handle (cudaStream_t passed as void*; NULL = legacy default stream).  No
+ * torch types cross this boundary; the library never allocates or frees:
+ * callers pass every output and a workspace of the size the matching
+ * *_workspace_bytes() query returns.  All launches are asynchronous on the
+ * given stream; the library keeps no global state besides a thread-local
+ * error string, so it is reentrant.
+ *
+ * Layout: every image tensor is contiguous NCHW, i.e. B*C planes of H rows
+ * of W elements (index ((b*C + c)*H + y)*W + x).  The reference works on one
+ * HWC float64 image at a time (gf/tensor.py:1-11); its (h, w, c) image is
+ * the B=1 case after a transpose, which the Python mirror does.
+ *
+ * dtype: GF_F32 (float) is the production path; GF_F64 (double) reproduces
+ * the reference's float64 arithmetic to its own 1e-10 test bars.
+ *
+ * Errors: the int return is GF_OK or a GF_ERR_* code (argument/shape errors
+ * mirror the reference's ValueError sites; gf_last_error() has the text).
+ * Data-dependent errors are reported through a caller-owned DEVICE uint32
+ * status word that kernels OR bits into (GF_STATUS_*); the caller reads it
+ * back when it wants the reference's synchronous exception semantics.
+ */
+#ifndef GF_B200_H
+#define GF_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum { GF_F32 = 0, GF_F64 = 1 };
+
+enum {
+  GF_OK = 0,
+  GF_ERR_ARG = 1,         /* bad shape / radius / eps / dtype  -> ValueError      */
+  GF_ERR_WORKSPACE = 2,   /* workspace smaller than *_workspace_bytes()           */
+  GF_ERR_CUDA = 3,        /* launch failure (gf_last_error has cudaGetErrorString) */
+  GF_ERR_UNSUPPORTED = 4  /* a size beyond the library's limits                   */
+};
+
+/* Device status bits.  Priority when raising: INPUT, then DEGENERATE, then
+ * OUTPUT -- the order the reference checks them (gf/guided.py:156-180). */
+enum {
+  GF_STATUS_NONFINITE_INPUT = 1u,   /* validate(..., finite=True), gf/tensor.py:39-40 */
+  GF_STATUS_NONFINITE_OUTPUT = 2u,  /* gf/guided.py:179-180 / :216-217                */
+  GF_STATUS_DEGENERATE = 4u         /* DegenerateWindowError, gf/guided.py:142-146    */
+};
+
+int gf_version(void);              /* 100 * major + minor                    */
+const char* gf_last_error(void);   /* thread-local text of the last failure  */
+int gf_sm_count(void);             /* SMs of the current device (for sizing) */
+
+/* ---- linear operators: gf/filters.py (the reference's _kernels seam) ----
+ * P planes of (h, w).  No workspace. */
+
+/* gf/filters.py:96-103 mean_filter (and _kernels.box_sum(normalize=True),
+ * gf/_kernels.py:71-80): clamped window mean, true-count normalised. */
+int gf_mean_filter(int dtype, const void* in, void* out, int64_t planes, int64_t h,
+                   int64_t w, int radius, void* stream);
+
+/* gf/filters.py:106-116 mean_filter_adjoint: box_sum(g / N). */
+int gf_mean_filter_adjoint(int dtype, const void* g, void* out, int64_t planes, int64_t h,
+                           int64_t w, int radius, void* stream);
+
+/* gf/filters.py:134-156 bilinear_resize (gf/_kernels.py:83-101): half-pixel
+ * centres, edge clamp, rows then columns.  in (h, w) -> out (out_h, out_w). */
+int gf_bilinear_resize(int dtype, const void* in, void* out, int64_t planes, int64_t h,
+                       int64_t w, int64_t out_h, int64_t out_w, void* stream);
+
+/* gf/filters.py:168-188 bilinear_resize_adjoint: exact transpose, computed
+ * as a deterministic gather.  g (g_h, g_w) -> out (in_h, in_w). */
+int gf_bilinear_resize_adjoint(int dtype, const void* g, void* out, int64_t planes,
+                               int64_t g_h, int64_t g_w, int64_t in_h, int64_t in_w,
+                               void* stream);
+
+/* ---- the fast (joint-upsampling) layer: gf/guided.py:152-195, :267-283 ----
+ * lr_x = guide_lo, lr_y = src_lo: (B, C, h, w); hr_x = guide_hi: (B, C, H, W)
+ * with H >= h, W >= w (any ratio).  out: (B, C, H, W).  NO smoothing of A, b
+ * on this path (gf/guided.py:170-178). */
+size_t gf_joint_workspace_bytes(int dtype, int64_t B, int64_t C, int64_t h, int64_t w,
+                                int64_t H, int64_t W, int radius);
+
+int gf_joint_fwd(int dtype, const void* lr_x, const void* lr_y, const void* hr_x, void* out,
+                 int64_t B, int64_t C, int64_t h, int64_t w, int64_t H, int64_t W, int radius,
+                 double eps, void* workspace, size_t workspace_bytes, uint32_t* status,
+                 void* stream);
+
+/* Gradients of dot(d_out, out): d_lr_y = d_src, d_lr_x = d_guide_lo,
+ * d_hr_x = d_guide_hi (gf/guided.py:267-283).  The lr moments are recomputed
+ * from lr_x, lr_y (the tape keeps input references only). */
+int gf_joint_bwd(int dtype, const void* lr_x, const void* lr_y, const void* hr_x,
+                 const void* d_out, void* d_lr_x, void* d_lr_y, void* d_hr_x, int64_t B,
+                 int64_t C, int64_t h, int64_t w, int64_t H, int64_t W, int radius, double eps,
+                 void* workspace, size_t workspace_bytes, uint32_t* status, void* stream);
+
+/* ---- the full-resolution layer: gf/guided.py:198-233, :284-295 ----
+ * guide: (B, Cg, H, W) with Cg == C or Cg == 1 (a 1-channel guide is
+ * broadcast over the C source channels, BASELINE config 1); src, out:
+ * (B, C, H, W).  A and b are re-smoothed by the mean filter. */
+size_t gf_highres_workspace_bytes(int dtype, int64_t B, int64_t Cg, int64_t C, int64_t H,
+                                  int64_t W, int radius);
+
+int gf_highres_fwd(int dtype, const void* guide, const void* src, void* out, int64_t B,
+                   int64_t Cg, int64_t C, int64_t H, int64_t W, int radius, double eps,
+                   void* workspace, size_t workspace_bytes, uint32_t* status, void* stream);
+
+/* d_guide: (B, Cg, H, W) -- for Cg == 1 the sum over the C broadcast copies. */
+int gf_highres_bwd(int dtype, const void* guide, const void* src, const void* d_out,
+                   void* d_guide, void* d_src, int64_t B, int64_t Cg, int64_t C, int64_t H,
+                   int64_t W, int radius, double eps, void* workspace, size_t workspace_bytes,
+                   uint32_t* status, void* stream);
+
+/* ---- 1x1 guidance net F: gf/guidance.py:184-224 ----
+ * conv1 (hidden x Cin, no bias) -> AdaptiveNorm (scalar gain, norm_gain;
+ * per-image per-channel population statistics, var floor 1e-5) -> leaky
+ * ReLU 0.2 -> conv2 (Cout x hidden) + bias.  Parameters are one packed
+ * device array of dtype, in the reference's parameters() order:
+ *   conv1.weight[hidden*Cin], norm.gain[1], norm.norm_gain[1],
+ *   conv2.weight[Cout*hidden], conv2.bias[Cout]
+ * (gn_param_count() values).  x: (B, Cin, H, W); y: (B, Cout, H, W).
+ * Statistics are per image (the reference has no batch dimension). */
+int64_t gn_param_count(int64_t Cin, int64_t Cout, int64_t hidden);
+
+size_t gn_workspace_bytes(int dtype, int64_t B, int64_t Cin, int64_t Cout, int64_t hidden,
+                          int64_t H, int64_t W);
+
+int gn_forward(int dtype, const void* x, void* y, const void* params, int64_t B, int64_t Cin,
+               int64_t Cout, int64_t hidden, int64_t H, int64_t W, void* workspace,
+               size_t workspace_bytes, uint32_t* status, void* stream);
+
+/* dx: (B, Cin, H, W).  dparams (packed like params) is OVERWRITTEN with the
+ * gradient summed over the batch when accumulate == 0, or added to when
+ * accumulate != 0 (the two call sites of GuidedUpsampler.backward,
+ * gf/training.py:168-177, accumulate low-res first). */
+int gn_backward(int dtype, const void* x, const void* dy, void* dx, void* dparams,
+                int accumulate, const void* params, int64_t B, int64_t Cin, int64_t Cout,
+                int64_t hidden, int64_t H, int64_t W, void* workspace, size_t workspace_bytes,
+                uint32_t* status, void* stream);
+
+/* ---- mse_loss: gf/training.py:93-101 (batch-mean variant of config 2) ----
+ * loss = mean over the batch of per-image mean((out - target)^2); d_out =
+ * 2 (out - target) / (C*H*W) / B.  loss is one device double. */
+int gf_mse_loss(int dtype, const void* out, const void* target, void* d_out, double* loss,
+                int64_t B, int64_t C, int64_t H, int64_t W, void* workspace,
+                size_t workspace_bytes, void* stream);
+
+size_t gf_mse_workspace_bytes(int64_t B, int64_t C, int64_t H, int64_t W);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* GF_B200_H */

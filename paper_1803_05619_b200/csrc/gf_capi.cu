@@ -1,0 +1,385 @@
+// C ABI entry points (include/gf_b200.h): argument checks that mirror the
+// reference's ValueError sites, then dispatch to the fused sm_100a kernels
+// when the call is one they cover (fp32, NCHW, supported radius/ratio), or to
+// the general kernels otherwise.  Both are CUDA; there is no CPU path.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstdarg>
+#include <cstring>
+
+#include "../../include/gf_b200.h"
+#include "gf_internal.h"
+
+namespace {
+
+thread_local char g_err[512] = "";
+thread_local int g_force_generic = 0;
+
+int fail(int code, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+  return code;
+}
+
+int check_launch(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(GF_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+  return GF_OK;
+}
+
+bool dtype_ok(int dt) { return dt == GF_F32 || dt == GF_F64; }
+
+// GuidedFilterParams.__post_init__, gf/guided.py:50-53
+int check_params(int r, double eps) {
+  if (r < 0) return fail(GF_ERR_ARG, "radius must be a non-negative integer, got %d", r);
+  if (!std::isfinite(eps) || eps < 0.0)
+    return fail(GF_ERR_ARG, "eps must be finite and >= 0, got %g", eps);
+  return GF_OK;
+}
+
+int check_dims(const char* name, int64_t a, int64_t b, int64_t c, int64_t d) {
+  if (a < 1 || b < 1 || c < 1 || d < 1)
+    return fail(GF_ERR_ARG, "%s: all dimensions must be >= 1, got (%lld, %lld, %lld, %lld)",
+                name, (long long)a, (long long)b, (long long)c, (long long)d);
+  return GF_OK;
+}
+
+cudaStream_t S(void* s) { return (cudaStream_t)s; }
+
+bool use_fused_joint(int dtype, int64_t B, int64_t C, int64_t h, int64_t w, int64_t H, int64_t W,
+                     int r) {
+  return !g_force_generic && dtype == GF_F32 && gfb::fused_joint_ok(B, C, h, w, H, W, r);
+}
+
+bool use_fused_highres(int dtype, int64_t B, int64_t Cg, int64_t C, int64_t H, int64_t W, int r) {
+  return !g_force_generic && dtype == GF_F32 && gfb::fused_highres_fwd_ok(B, Cg, C, H, W, r);
+}
+
+}  // namespace
+
+extern "C" {
+
+int gf_version(void) { return 100; }
+
+const char* gf_last_error(void) { return g_err; }
+
+// Test hook (like the reference's flipped_term, gf/guided.py:124-133): route
+// every call of THIS thread through the general kernels.  Returns the old value.
+int gf_force_generic(int on) {
+  int old = g_force_generic;
+  g_force_generic = on ? 1 : 0;
+  return old;
+}
+
+// Introspection hooks (not in the public header): 1 when the call would take
+// the fused sm_100a kernels, 0 when it takes the general kernels.
+int gf_joint_is_fused(int dtype, int64_t B, int64_t C, int64_t h, int64_t w, int64_t H,
+                      int64_t W, int r) {
+  return use_fused_joint(dtype, B, C, h, w, H, W, r) ? 1 : 0;
+}
+
+int gf_highres_fwd_is_fused(int dtype, int64_t B, int64_t Cg, int64_t C, int64_t H, int64_t W,
+                            int r) {
+  return use_fused_highres(dtype, B, Cg, C, H, W, r) ? 1 : 0;
+}
+
+int gf_sm_count(void) {
+  int dev = 0, n = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 0;
+  if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return 0;
+  return n;
+}
+
+// ---------------------------------------------------------------------------
+// primitives
+// ---------------------------------------------------------------------------
+int gf_mean_filter(int dtype, const void* in, void* out, int64_t planes, int64_t h, int64_t w,
+                   int radius, void* stream) {
+  if (!dtype_ok(dtype)) return fail(GF_ERR_ARG, "bad dtype %d", dtype);
+  if (radius < 0) return fail(GF_ERR_ARG, "radius must be a non-negative integer, got %d", radius);
+  if (int e = check_dims("mean_filter", planes, h, w, 1)) return e;
+  if (dtype == GF_F32)
+    gfb::generic_mean_filter<float>((const float*)in, (float*)out, planes, h, w, radius, 0,
+                                    S(stream));
+  else
+    gfb::generic_mean_filter<double>((const double*)in, (double*)out, planes, h, w, radius, 0,
+                                     S(stream));
+  return check_launch("gf_mean_filter");
+}
+
+int gf_mean_filter_adjoint(int dtype, const void* g, void* out, int64_t planes, int64_t h,
+                           int64_t w, int radius, void* stream) {
+  if (!dtype_ok(dtype)) return fail(GF_ERR_ARG, "bad dtype %d", dtype);
+  if (radius < 0) return fail(GF_ERR_ARG, "radius must be a non-negative integer, got %d", radius);
+  if (int e = check_dims("mean_filter_adjoint", planes, h, w, 1)) return e;
+  if (dtype == GF_F32)
+    gfb::generic_mean_filter<float>((const float*)g, (float*)out, planes, h, w, radius, 1,
+                                    S(stream));
+  else
+    gfb::generic_mean_filter<double>((const double*)g, (double*)out, planes, h, w, radius, 1,
+                                     S(stream));
+  return check_launch("gf_mean_filter_adjoint");
+}
+
+int gf_bilinear_resize(int dtype, const void* in, void* out, int64_t planes, int64_t h, int64_t w,
+                       int64_t out_h, int64_t out_w, void* stream) {
+  if (!dtype_ok(dtype)) return fail(GF_ERR_ARG, "bad dtype %d", dtype);
+  if (out_h < 1 || out_w < 1)
+    return fail(GF_ERR_ARG, "output dims must be >= 1, got (%lld, %lld)", (long long)out_h,
+                (long long)out_w);
+  if (int e = check_dims("bilinear_resize", planes, h, w, 1)) return e;
+  if (dtype == GF_F32)
+    gfb::generic_resize<float>((const float*)in, (float*)out, planes, h, w, out_h, out_w,
+                               S(stream));
+  else
+    gfb::generic_resize<double>((const double*)in, (double*)out, planes, h, w, out_h, out_w,
+                                S(stream));
+  return check_launch("gf_bilinear_resize");
+}
+
+int gf_bilinear_resize_adjoint(int dtype, const void* g, void* out, int64_t planes, int64_t g_h,
+                               int64_t g_w, int64_t in_h, int64_t in_w, void* stream) {
+  if (!dtype_ok(dtype)) return fail(GF_ERR_ARG, "bad dtype %d", dtype);
+  if (in_h < 1 || in_w < 1)
+    return fail(GF_ERR_ARG, "input dims must be >= 1, got (%lld, %lld)", (long long)in_h,
+                (long long)in_w);
+  if (int e = check_dims("bilinear_resize_adjoint", planes, g_h, g_w, 1)) return e;
+  if (dtype == GF_F32)
+    gfb::generic_resize_adj<float>((const float*)g, (float*)out, planes, g_h, g_w, in_h, in_w,
+                                   S(stream));
+  else
+    gfb::generic_resize_adj<double>((const double*)g, (double*)out, planes, g_h, g_w, in_h, in_w,
+                                    S(stream));
+  return check_launch("gf_bilinear_resize_adjoint");
+}
+
+// ---------------------------------------------------------------------------
+// joint (fast) layer
+// ---------------------------------------------------------------------------
+static int check_joint(int dtype, int64_t B, int64_t C, int64_t h, int64_t w, int64_t H,
+                       int64_t W, int r, double eps) {
+  if (!dtype_ok(dtype)) return fail(GF_ERR_ARG, "bad dtype %d", dtype);
+  if (int e = check_params(r, eps)) return e;
+  if (int e = check_dims("guide_lo", B, C, h, w)) return e;
+  if (int e = check_dims("guide_hi", B, C, H, W)) return e;
+  // gf/guided.py:165-168
+  if (H < h || W < w)
+    return fail(GF_ERR_ARG, "guide_hi dims (%lld, %lld) smaller than guide_lo (%lld, %lld)",
+                (long long)H, (long long)W, (long long)h, (long long)w);
+  return GF_OK;
+}
+
+size_t gf_joint_workspace_bytes(int dtype, int64_t B, int64_t C, int64_t h, int64_t w, int64_t H,
+                                int64_t W, int radius) {
+  size_t gen = gfb::generic_workspace_bytes(B * C * h * w, 0);
+  if (use_fused_joint(dtype, B, C, h, w, H, W, radius))
+    return gfb::fused_joint_bwd_ws_bytes(B, C, h, w);
+  return gen;
+}
+
+int gf_joint_fwd(int dtype, const void* lr_x, const void* lr_y, const void* hr_x, void* out,
+                 int64_t B, int64_t C, int64_t h, int64_t w, int64_t H, int64_t W, int radius,
+                 double eps, void* workspace, size_t workspace_bytes, uint32_t* status,
+                 void* stream) {
+  if (int e = check_joint(dtype, B, C, h, w, H, W, radius, eps)) return e;
+  if (use_fused_joint(dtype, B, C, h, w, H, W, radius)) {
+    gfb::fused_joint_fwd((const float*)lr_x, (const float*)lr_y, (const float*)hr_x, (float*)out,
+                         B, C, h, w, H, W, radius, (float)eps, status, S(stream));
+    return check_launch("gf_joint_fwd[fused]");
+  }
+  size_t need = gf_joint_workspace_bytes(dtype, B, C, h, w, H, W, radius);
+  if (workspace_bytes < need)
+    return fail(GF_ERR_WORKSPACE, "joint workspace %zu < %zu bytes", workspace_bytes, need);
+  if (dtype == GF_F32)
+    gfb::generic_joint_fwd<float>((const float*)lr_x, (const float*)lr_y, (const float*)hr_x,
+                                  (float*)out, B, C, h, w, H, W, radius, eps, workspace, status,
+                                  S(stream));
+  else
+    gfb::generic_joint_fwd<double>((const double*)lr_x, (const double*)lr_y, (const double*)hr_x,
+                                   (double*)out, B, C, h, w, H, W, radius, eps, workspace, status,
+                                   S(stream));
+  return check_launch("gf_joint_fwd");
+}
+
+int gf_joint_bwd(int dtype, const void* lr_x, const void* lr_y, const void* hr_x,
+                 const void* d_out, void* d_lr_x, void* d_lr_y, void* d_hr_x, int64_t B,
+                 int64_t C, int64_t h, int64_t w, int64_t H, int64_t W, int radius, double eps,
+                 void* workspace, size_t workspace_bytes, uint32_t* status, void* stream) {
+  if (int e = check_joint(dtype, B, C, h, w, H, W, radius, eps)) return e;
+  size_t need = gf_joint_workspace_bytes(dtype, B, C, h, w, H, W, radius);
+  if (workspace_bytes < need)
+    return fail(GF_ERR_WORKSPACE, "joint workspace %zu < %zu bytes", workspace_bytes, need);
+  if (use_fused_joint(dtype, B, C, h, w, H, W, radius)) {
+    gfb::fused_joint_bwd((const float*)lr_x, (const float*)lr_y, (const float*)hr_x,
+                         (const float*)d_out, (float*)d_lr_x, (float*)d_lr_y, (float*)d_hr_x, B,
+                         C, h, w, H, W, radius, (float)eps, workspace, status, S(stream));
+    return check_launch("gf_joint_bwd[fused]");
+  }
+  if (dtype == GF_F32)
+    gfb::generic_joint_bwd<float>((const float*)lr_x, (const float*)lr_y, (const float*)hr_x,
+                                  (const float*)d_out, (float*)d_lr_x, (float*)d_lr_y,
+                                  (float*)d_hr_x, B, C, h, w, H, W, radius, eps, workspace,
+                                  status, S(stream));
+  else
+    gfb::generic_joint_bwd<double>((const double*)lr_x, (const double*)lr_y,
+                                   (const double*)hr_x, (const double*)d_out, (double*)d_lr_x,
+                                   (double*)d_lr_y, (double*)d_hr_x, B, C, h, w, H, W, radius,
+                                   eps, workspace, status, S(stream));
+  return check_launch("gf_joint_bwd");
+}
+
+// ---------------------------------------------------------------------------
+// full-resolution layer
+// ---------------------------------------------------------------------------
+static int check_highres(int dtype, int64_t B, int64_t Cg, int64_t C, int64_t H, int64_t W, int r,
+                         double eps) {
+  if (!dtype_ok(dtype)) return fail(GF_ERR_ARG, "bad dtype %d", dtype);
+  if (int e = check_params(r, eps)) return e;
+  if (int e = check_dims("src", B, C, H, W)) return e;
+  if (int e = check_dims("guide", B, Cg, H, W)) return e;
+  // gf/guided.py:204-205 requires equal shapes; a 1-channel guide is the
+  // broadcast extension of BASELINE config 1.
+  if (Cg != C && Cg != 1)
+    return fail(GF_ERR_ARG, "guide/src channel mismatch: %lld vs %lld", (long long)Cg,
+                (long long)C);
+  return GF_OK;
+}
+
+size_t gf_highres_workspace_bytes(int dtype, int64_t B, int64_t Cg, int64_t C, int64_t H,
+                                  int64_t W, int radius) {
+  (void)Cg;
+  return gfb::generic_workspace_bytes(B * C * H * W, 0);
+}
+
+static size_t highres_fwd_need(int dtype, int64_t B, int64_t Cg, int64_t C, int64_t H, int64_t W,
+                               int r) {
+  if (use_fused_highres(dtype, B, Cg, C, H, W, r)) return 0;
+  return gf_highres_workspace_bytes(dtype, B, Cg, C, H, W, r);
+}
+
+int gf_highres_fwd(int dtype, const void* guide, const void* src, void* out, int64_t B, int64_t Cg,
+                   int64_t C, int64_t H, int64_t W, int radius, double eps, void* workspace,
+                   size_t workspace_bytes, uint32_t* status, void* stream) {
+  if (int e = check_highres(dtype, B, Cg, C, H, W, radius, eps)) return e;
+  if (use_fused_highres(dtype, B, Cg, C, H, W, radius)) {
+    gfb::fused_highres_fwd((const float*)guide, (const float*)src, (float*)out, B, Cg, C, H, W,
+                           radius, (float)eps, status, S(stream));
+    return check_launch("gf_highres_fwd[fused]");
+  }
+  size_t need = highres_fwd_need(dtype, B, Cg, C, H, W, radius);
+  if (workspace_bytes < need)
+    return fail(GF_ERR_WORKSPACE, "highres workspace %zu < %zu bytes", workspace_bytes, need);
+  if (dtype == GF_F32)
+    gfb::generic_highres_fwd<float>((const float*)guide, (const float*)src, (float*)out, B, Cg, C,
+                                     H, W, radius, eps, workspace, status, S(stream));
+  else
+    gfb::generic_highres_fwd<double>((const double*)guide, (const double*)src, (double*)out, B,
+                                      Cg, C, H, W, radius, eps, workspace, status, S(stream));
+  return check_launch("gf_highres_fwd");
+}
+
+int gf_highres_bwd(int dtype, const void* guide, const void* src, const void* d_out,
+                   void* d_guide, void* d_src, int64_t B, int64_t Cg, int64_t C, int64_t H,
+                   int64_t W, int radius, double eps, void* workspace, size_t workspace_bytes,
+                   uint32_t* status, void* stream) {
+  if (int e = check_highres(dtype, B, Cg, C, H, W, radius, eps)) return e;
+  size_t need = gf_highres_workspace_bytes(dtype, B, Cg, C, H, W, radius);
+  if (workspace_bytes < need)
+    return fail(GF_ERR_WORKSPACE, "highres workspace %zu < %zu bytes", workspace_bytes, need);
+  if (dtype == GF_F32)
+    gfb::generic_highres_bwd<float>((const float*)guide, (const float*)src, (const float*)d_out,
+                                     (float*)d_guide, (float*)d_src, B, Cg, C, H, W, radius, eps,
+                                     workspace, status, S(stream));
+  else
+    gfb::generic_highres_bwd<double>((const double*)guide, (const double*)src,
+                                      (const double*)d_out, (double*)d_guide, (double*)d_src, B,
+                                      Cg, C, H, W, radius, eps, workspace, status, S(stream));
+  return check_launch("gf_highres_bwd");
+}
+
+// ---------------------------------------------------------------------------
+// guidance net + loss
+// ---------------------------------------------------------------------------
+int64_t gn_param_count(int64_t Cin, int64_t Cout, int64_t hidden) {
+  return hidden * Cin + 2 + Cout * hidden + Cout;
+}
+
+size_t gn_workspace_bytes(int dtype, int64_t B, int64_t Cin, int64_t Cout, int64_t hidden,
+                          int64_t H, int64_t W) {
+  (void)dtype;
+  (void)Cin;
+  (void)Cout;
+  (void)H;
+  (void)W;
+  return gfb::gn_ws_bytes(B, hidden);
+}
+
+static int check_gn(int dtype, int64_t B, int64_t Cin, int64_t Cout, int64_t hidden, int64_t H,
+                    int64_t W, size_t ws_bytes) {
+  if (!dtype_ok(dtype)) return fail(GF_ERR_ARG, "bad dtype %d", dtype);
+  if (int e = check_dims("x", B, Cin, H, W)) return e;
+  if (!gfb::gn_supported(Cin, Cout, hidden))
+    return fail(GF_ERR_UNSUPPORTED, "guidance net limits: Cin<=4, Cout<=4, hidden<=64 (got %lld, %lld, %lld)",
+                (long long)Cin, (long long)Cout, (long long)hidden);
+  size_t need = gfb::gn_ws_bytes(B, hidden);
+  if (ws_bytes < need) return fail(GF_ERR_WORKSPACE, "gn workspace %zu < %zu bytes", ws_bytes, need);
+  return GF_OK;
+}
+
+int gn_forward(int dtype, const void* x, void* y, const void* params, int64_t B, int64_t Cin,
+               int64_t Cout, int64_t hidden, int64_t H, int64_t W, void* workspace,
+               size_t workspace_bytes, uint32_t* status, void* stream) {
+  if (int e = check_gn(dtype, B, Cin, Cout, hidden, H, W, workspace_bytes)) return e;
+  if (dtype == GF_F32)
+    gfb::gn_forward_impl<float>((const float*)x, (float*)y, (const float*)params, B, Cin, Cout,
+                                hidden, H * W, workspace, status, S(stream));
+  else
+    gfb::gn_forward_impl<double>((const double*)x, (double*)y, (const double*)params, B, Cin,
+                                 Cout, hidden, H * W, workspace, status, S(stream));
+  return check_launch("gn_forward");
+}
+
+int gn_backward(int dtype, const void* x, const void* dy, void* dx, void* dparams, int accumulate,
+                const void* params, int64_t B, int64_t Cin, int64_t Cout, int64_t hidden,
+                int64_t H, int64_t W, void* workspace, size_t workspace_bytes, uint32_t* status,
+                void* stream) {
+  if (int e = check_gn(dtype, B, Cin, Cout, hidden, H, W, workspace_bytes)) return e;
+  if (dtype == GF_F32)
+    gfb::gn_backward_impl<float>((const float*)x, (const float*)dy, (float*)dx, (float*)dparams,
+                                 accumulate, (const float*)params, B, Cin, Cout, hidden, H * W,
+                                 workspace, status, S(stream));
+  else
+    gfb::gn_backward_impl<double>((const double*)x, (const double*)dy, (double*)dx,
+                                  (double*)dparams, accumulate, (const double*)params, B, Cin,
+                                  Cout, hidden, H * W, workspace, status, S(stream));
+  return check_launch("gn_backward");
+}
+
+size_t gf_mse_workspace_bytes(int64_t B, int64_t C, int64_t H, int64_t W) {
+  (void)C;
+  (void)H;
+  (void)W;
+  return gfb::mse_ws_bytes(B);
+}
+
+int gf_mse_loss(int dtype, const void* out, const void* target, void* d_out, double* loss,
+                int64_t B, int64_t C, int64_t H, int64_t W, void* workspace,
+                size_t workspace_bytes, void* stream) {
+  if (!dtype_ok(dtype)) return fail(GF_ERR_ARG, "bad dtype %d", dtype);
+  if (int e = check_dims("out", B, C, H, W)) return e;
+  if (workspace_bytes < gfb::mse_ws_bytes(B))
+    return fail(GF_ERR_WORKSPACE, "mse workspace too small");
+  if (dtype == GF_F32)
+    gfb::mse_impl<float>((const float*)out, (const float*)target, (float*)d_out, loss, B,
+                         C * H * W, workspace, S(stream));
+  else
+    gfb::mse_impl<double>((const double*)out, (const double*)target, (double*)d_out, loss, B,
+                          C * H * W, workspace, S(stream));
+  return check_launch("gf_mse_loss");
+}
+
+}  // extern "C"

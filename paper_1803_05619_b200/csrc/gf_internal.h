@@ -1,0 +1,72 @@
+// Internal declarations shared by the C-ABI layer and the kernel files.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stddef.h>
+#include <stdint.h>
+
+namespace gfb {
+
+// ---- generic (any shape / radius / dtype) ----
+size_t generic_workspace_bytes(int64_t n_moment_plane_total, int64_t extra_doubles);
+
+template <typename T>
+void generic_mean_filter(const T* in, T* out, int64_t P, int64_t h, int64_t w, int r, int adjoint,
+                         cudaStream_t s);
+template <typename T>
+void generic_resize(const T* in, T* out, int64_t P, int64_t h, int64_t w, int64_t oh, int64_t ow,
+                    cudaStream_t s);
+template <typename T>
+void generic_resize_adj(const T* g, T* out, int64_t P, int64_t gh, int64_t gw, int64_t h,
+                        int64_t w, cudaStream_t s);
+template <typename T>
+void generic_joint_fwd(const T* lr_x, const T* lr_y, const T* hr_x, T* out, int64_t B, int64_t C,
+                       int64_t h, int64_t w, int64_t H, int64_t W, int r, double eps, void* ws,
+                       uint32_t* status, cudaStream_t s);
+template <typename T>
+void generic_joint_bwd(const T* lr_x, const T* lr_y, const T* hr_x, const T* d_out, T* d_lr_x,
+                       T* d_lr_y, T* d_hr_x, int64_t B, int64_t C, int64_t h, int64_t w,
+                       int64_t H, int64_t W, int r, double eps, void* ws, uint32_t* status,
+                       cudaStream_t s);
+template <typename T>
+void generic_highres_fwd(const T* guide, const T* src, T* out, int64_t B, int64_t Cg, int64_t C,
+                         int64_t H, int64_t W, int r, double eps, void* ws, uint32_t* status,
+                         cudaStream_t s);
+template <typename T>
+void generic_highres_bwd(const T* guide, const T* src, const T* d_out, T* d_guide, T* d_src,
+                         int64_t B, int64_t Cg, int64_t C, int64_t H, int64_t W, int r,
+                         double eps, void* ws, uint32_t* status, cudaStream_t s);
+
+// ---- guidance net / loss ----
+size_t gn_ws_bytes(int64_t B, int64_t hidden);
+bool gn_supported(int64_t Cin, int64_t Cout, int64_t hidden);
+template <typename T>
+void gn_forward_impl(const T* x, T* y, const T* params, int64_t B, int64_t Cin, int64_t Cout,
+                     int64_t hidden, int64_t HW, void* ws, uint32_t* status, cudaStream_t s);
+template <typename T>
+void gn_backward_impl(const T* x, const T* dy, T* dx, T* dparams, int accumulate, const T* params,
+                      int64_t B, int64_t Cin, int64_t Cout, int64_t hidden, int64_t HW, void* ws,
+                      uint32_t* status, cudaStream_t s);
+size_t mse_ws_bytes(int64_t B);
+template <typename T>
+void mse_impl(const T* out, const T* tgt, T* d_out, double* loss, int64_t B, int64_t per_image,
+              void* ws, cudaStream_t s);
+
+// ---- fused fast paths (fp32, NCHW); return false when the shape is not
+// covered, in which case the caller takes the generic path ----
+bool fused_highres_fwd_ok(int64_t B, int64_t Cg, int64_t C, int64_t H, int64_t W, int r);
+void fused_highres_fwd(const float* guide, const float* src, float* out, int64_t B, int64_t Cg,
+                       int64_t C, int64_t H, int64_t W, int r, float eps, uint32_t* status,
+                       cudaStream_t s);
+
+bool fused_joint_ok(int64_t B, int64_t C, int64_t h, int64_t w, int64_t H, int64_t W, int r);
+void fused_joint_fwd(const float* lr_x, const float* lr_y, const float* hr_x, float* out,
+                     int64_t B, int64_t C, int64_t h, int64_t w, int64_t H, int64_t W, int r,
+                     float eps, uint32_t* status, cudaStream_t s);
+size_t fused_joint_bwd_ws_bytes(int64_t B, int64_t C, int64_t h, int64_t w);
+void fused_joint_bwd(const float* lr_x, const float* lr_y, const float* hr_x, const float* d_out,
+                     float* d_lr_x, float* d_lr_y, float* d_hr_x, int64_t B, int64_t C,
+                     int64_t h, int64_t w, int64_t H, int64_t W, int r, float eps, void* ws,
+                     uint32_t* status, cudaStream_t s);
+
+}  // namespace gfb

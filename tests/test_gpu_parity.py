@@ -1,0 +1,397 @@
+"""GPU parity: the CUDA path (through the C ABI) against the reference's golden
+vectors and the pinned CPU oracle.
+
+Bars (north_star / SURVEY 8c):
+  * fp64 instantiation vs reference golden values: the reference's own 1e-10
+    (outputs) and 1e-9 relative (gradients) bars;
+  * fp32 path: outputs max abs error <= 1e-4 on [0,1] images; gradients
+    max|g - g_ref| / max|g_ref| <= 1e-3 per tensor.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import gf_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+OUT_TOL32 = 1e-4
+GRAD_TOL32 = 1e-3
+
+
+@pytest.fixture(scope="module")
+def gfb():
+    import paper_1803_05619_b200 as m
+
+    assert torch.cuda.is_available(), "gpu tests need CUDA"
+    return m
+
+
+def rel_max(a, b):
+    a = np.asarray(a, dtype=np.float64)
+    b = np.asarray(b, dtype=np.float64)
+    return float(np.abs(a - b).max()) / max(float(np.abs(b).max()), 1e-30)
+
+
+def abs_max(a, b):
+    return float(np.abs(np.asarray(a, np.float64) - np.asarray(b, np.float64)).max())
+
+
+def t32(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).float().cuda()
+
+
+def npy(t):
+    return t.detach().double().cpu().numpy()
+
+
+# ---------------------------------------------------------------------------
+# primitives
+# ---------------------------------------------------------------------------
+
+def test_filters_fp64_match_reference(gfb, golden):
+    for name, c in golden.items():
+        if name.startswith("mean"):
+            r = int(c["r"])
+            assert abs_max(gfb.mean_filter(c["x"], r), c["mean"]) <= 1e-12
+            assert abs_max(gfb.mean_filter_adjoint(c["g"], r), c["adj"]) <= 1e-12
+        elif name.startswith("bil"):
+            oh, ow = c["out"].shape[:2]
+            h, w = c["x"].shape[:2]
+            assert abs_max(gfb.bilinear_resize(c["x"], oh, ow), c["out"]) <= 1e-14
+            assert abs_max(gfb.bilinear_resize_adjoint(c["g"], h, w), c["adj"]) <= 1e-13
+
+
+def test_filters_known_answers(gfb, golden):
+    m = gfb.mean_filter(golden["ka_box"]["x"], 1)
+    assert m[0, 0, 0] == pytest.approx(3.0, abs=1e-12)
+    assert m[1, 1, 0] == pytest.approx(5.0, abs=1e-12)
+    out = gfb.bilinear_resize(golden["ka_bilinear"]["x"], 1, 4)
+    assert out.ravel().tolist() == [0.0, 0.5, 1.5, 2.0]
+    g = np.random.default_rng(7).standard_normal((5, 4, 2))
+    assert np.array_equal(gfb.bilinear_resize_adjoint(g, 5, 4), g)
+
+
+def test_adjoint_identities(gfb):
+    rng = np.random.default_rng(50)
+    for _ in range(20):
+        h, w, c = int(rng.integers(4, 20)), int(rng.integers(4, 20)), int(rng.integers(1, 4))
+        r = int(rng.integers(0, 6))
+        u = rng.standard_normal((h, w, c))
+        v = rng.standard_normal((h, w, c))
+        lhs = float(np.vdot(u, gfb.mean_filter(v, r)))
+        rhs = float(np.vdot(gfb.mean_filter_adjoint(u, r), v))
+        assert abs(lhs - rhs) <= 1e-9 * (abs(lhs) + 1.0)
+        oh, ow = int(rng.integers(1, 24)), int(rng.integers(1, 24))
+        g = rng.standard_normal((oh, ow, c))
+        lhs = float(np.vdot(g, gfb.bilinear_resize(v, oh, ow)))
+        rhs = float(np.vdot(gfb.bilinear_resize_adjoint(g, h, w), v))
+        assert abs(lhs - rhs) <= 1e-9 * (abs(lhs) + 1.0)
+
+
+# ---------------------------------------------------------------------------
+# joint layer vs reference golden vectors
+# ---------------------------------------------------------------------------
+
+def _joint_cases(golden):
+    return [(k, c) for k, c in sorted(golden.items()) if k.startswith("joint")]
+
+
+def test_joint_fp64_matches_reference(gfb, golden):
+    for name, c in _joint_cases(golden):
+        p = gfb.GuidedFilterParams(int(c["r"]), float(c["eps"]))
+        out, tape = gfb.forward_joint(c["guide_lo"], c["guide_hi"], c["src_lo"], p)
+        assert isinstance(out, np.ndarray) and out.dtype == np.float64
+        assert abs_max(out, c["out"]) <= 1e-10, name
+        g = gfb.backward(tape, c["d_out"])
+        for f in ("d_src", "d_guide_lo", "d_guide_hi"):
+            assert rel_max(getattr(g, f), c[f]) <= 1e-9, (name, f)
+        assert abs_max(tape.slope, c["slope"]) <= 1e-10
+
+
+def test_joint_fp32_matches_reference(gfb, golden):
+    for name, c in _joint_cases(golden):
+        p = gfb.GuidedFilterParams(int(c["r"]), float(c["eps"]))
+        gl, gh, sl = t32(c["guide_lo"]), t32(c["guide_hi"]), t32(c["src_lo"])
+        out, tape = gfb.forward_joint(gl, gh, sl, p)
+        assert out.dtype == torch.float32 and out.shape == gh.shape
+        assert abs_max(npy(out), c["out"]) <= OUT_TOL32, name
+        g = gfb.backward(tape, t32(c["d_out"]))
+        for f in ("d_src", "d_guide_lo", "d_guide_hi"):
+            assert rel_max(npy(getattr(g, f)), c[f]) <= GRAD_TOL32, (name, f)
+
+
+def test_joint_fp32_generic_path_matches_reference(gfb, golden):
+    from paper_1803_05619_b200 import _lib
+
+    lib = _lib.load()
+    old = lib.gf_force_generic(1)
+    try:
+        test_joint_fp32_matches_reference(gfb, golden)
+    finally:
+        lib.gf_force_generic(old)
+
+
+# ---------------------------------------------------------------------------
+# highres layer vs reference golden vectors
+# ---------------------------------------------------------------------------
+
+def test_highres_fp64_matches_reference(gfb, golden):
+    for name, c in sorted(golden.items()):
+        if not name.startswith("hr"):
+            continue
+        p = gfb.GuidedFilterParams(int(c["r"]), float(c["eps"]))
+        if name.startswith("hrb"):  # 1-channel guide broadcast (NCHW extension)
+            g = torch.from_numpy(c["guide"].transpose(2, 0, 1)[None].copy()).cuda()
+            s = torch.from_numpy(c["src"].transpose(2, 0, 1)[None].copy()).cuda()
+            d = torch.from_numpy(c["d_out"].transpose(2, 0, 1)[None].copy()).cuda()
+            out, tape = gfb.forward_highres(g, s, p)
+            gr = gfb.backward(tape, d)
+            assert abs_max(npy(out)[0].transpose(1, 2, 0), c["out"]) <= 1e-10, name
+            assert rel_max(npy(gr.d_src)[0].transpose(1, 2, 0), c["d_src"]) <= 1e-9
+            assert rel_max(npy(gr.d_guide_hi)[0].transpose(1, 2, 0), c["d_guide"]) <= 1e-9
+            continue
+        out, tape = gfb.forward_highres(c["guide"], c["src"], p)
+        assert abs_max(out, c["out"]) <= 1e-10, name
+        gr = gfb.backward(tape, c["d_out"])
+        assert gr.d_guide_lo is None
+        assert rel_max(gr.d_src, c["d_src"]) <= 1e-9, name
+        assert rel_max(gr.d_guide_hi, c["d_guide"]) <= 1e-9, name
+
+
+def test_highres_fp32_matches_reference(gfb, golden):
+    for name, c in sorted(golden.items()):
+        if not name.startswith("hr"):
+            continue
+        p = gfb.GuidedFilterParams(int(c["r"]), float(c["eps"]))
+        g = t32(c["guide"].transpose(2, 0, 1)[None])
+        s = t32(c["src"].transpose(2, 0, 1)[None])
+        out, tape = gfb.forward_highres(g, s, p)
+        assert abs_max(npy(out)[0].transpose(1, 2, 0), c["out"]) <= OUT_TOL32, name
+        gr = gfb.backward(tape, t32(c["d_out"].transpose(2, 0, 1)[None]))
+        assert rel_max(npy(gr.d_src)[0].transpose(1, 2, 0), c["d_src"]) <= GRAD_TOL32, name
+        assert rel_max(npy(gr.d_guide_hi)[0].transpose(1, 2, 0), c["d_guide"]) <= GRAD_TOL32
+
+
+# ---------------------------------------------------------------------------
+# guidance net + training step vs reference golden vectors
+# ---------------------------------------------------------------------------
+
+def test_guidance_net_matches_reference(gfb, golden):
+    for name, c in sorted(golden.items()):
+        if not name.startswith("gn"):
+            continue
+        params = {k[2:]: v for k, v in c.items() if k.startswith("p:")}
+        cout, hidden, cin = params["conv2.weight"].shape[0], params["conv1.weight"].shape[0], \
+            params["conv1.weight"].shape[1]
+        net = gfb.GuidanceNet(cin, cout, hidden=hidden)
+        net.load_parameters(params)
+        y, tape = net.forward(c["x"])                    # float64 drop-in path
+        assert abs_max(y, c["y"]) <= 1e-10, name
+        dx, grads = net.backward(tape, c["dy"])
+        assert rel_max(dx, c["dx"]) <= 1e-9, name
+        for k, v in grads.items():
+            assert rel_max(v, c["g:" + k]) <= 1e-9, (name, k)
+        # fp32 path
+        y32, tape32 = net.forward(t32(c["x"]))
+        assert abs_max(npy(y32), c["y"]) <= 1e-5, name
+        dx32, g32 = net.backward(tape32, t32(c["dy"]))
+        assert rel_max(npy(dx32), c["dx"]) <= GRAD_TOL32, name
+        for k, v in g32.items():
+            assert rel_max(npy(v), c["g:" + k]) <= GRAD_TOL32, (name, k)
+
+
+def test_guidance_net_seeded_init_matches_reference_draws(gfb):
+    rng_a = np.random.default_rng(123)
+    net = gfb.GuidanceNet(3, 3, hidden=15, kernel=1, rng=rng_a)
+    want = O.guidance_init(3, 3, 15, np.random.default_rng(123))
+    for k, v in net.parameters().items():
+        assert np.array_equal(v.cpu().numpy(), want[k]), k
+
+
+def test_train_step_matches_reference(gfb, golden):
+    c = golden["train0"]
+    params = {k[2:]: v for k, v in c.items() if k.startswith("p:")}
+    net = gfb.GuidanceNet(3, 3, hidden=15)
+    net.load_parameters(params)
+    p = gfb.GuidedFilterParams(int(c["r"]), float(c["eps"]))
+    nchw = lambda a: t32(a.transpose(0, 3, 1, 2))  # noqa: E731
+    res = gfb.train_step(net, nchw(c["lr_x"]), nchw(c["hr_x"]), nchw(c["lr_y"]),
+                         nchw(c["target"]), p)
+    assert abs(float(res.loss) - float(c["loss"])) <= 1e-6 * max(1.0, float(c["loss"]))
+    assert abs_max(npy(res.out).transpose(0, 2, 3, 1), c["out"]) <= OUT_TOL32
+    assert rel_max(npy(res.d_lr_y).transpose(0, 2, 3, 1), c["d_lr_y"]) <= GRAD_TOL32
+    assert rel_max(npy(res.d_lr_x).transpose(0, 2, 3, 1), c["d_lr_x"]) <= GRAD_TOL32
+    assert rel_max(npy(res.d_hr_x).transpose(0, 2, 3, 1), c["d_hr_x"]) <= GRAD_TOL32
+    grads = net.unpack(res.dparams)
+    for k, v in grads.items():
+        assert rel_max(npy(v), c["g:" + k]) <= GRAD_TOL32, k
+
+
+# ---------------------------------------------------------------------------
+# error semantics (gf/guided.py:156-180)
+# ---------------------------------------------------------------------------
+
+def test_error_semantics(gfb):
+    rng = np.random.default_rng(5)
+    gl, gh, sl = rng.uniform(0, 1, (6, 8, 2)), rng.uniform(0, 1, (12, 16, 2)), \
+        rng.uniform(0, 1, (6, 8, 2))
+    p = gfb.GuidedFilterParams(1, 1e-2)
+    with pytest.raises(ValueError):
+        gfb.forward_joint(gl, gh, sl[:, :-1], p)
+    with pytest.raises(ValueError):
+        gfb.forward_joint(gl, gh[:, :, :1], sl, p)
+    with pytest.raises(ValueError):
+        gfb.forward_joint(gh, gl, gh, p)
+    bad = sl.copy()
+    bad[0, 0, 0] = np.nan
+    with pytest.raises(ValueError):
+        gfb.forward_joint(gl, gh, bad, p)
+    bad_hi = gh.copy()
+    bad_hi[3, 3, 1] = np.inf
+    with pytest.raises(ValueError):
+        gfb.forward_joint(gl, bad_hi, sl, p)
+    with pytest.raises(gfb.DegenerateWindowError):
+        gfb.forward_joint(np.full_like(gl, 0.25), gh, sl, gfb.GuidedFilterParams(1, 0.0))
+    for dt in (torch.float32,):
+        with pytest.raises(gfb.DegenerateWindowError):
+            gfb.forward_joint(torch.full((1, 2, 6, 8), 0.25, dtype=dt, device="cuda"),
+                              torch.rand(1, 2, 12, 16, dtype=dt, device="cuda"),
+                              torch.rand(1, 2, 6, 8, dtype=dt, device="cuda"),
+                              gfb.GuidedFilterParams(1, 0.0))
+    out, tape = gfb.forward_joint(gl, gh, sl, p)
+    with pytest.raises(ValueError):
+        gfb.backward(tape, np.zeros_like(sl))
+    g = gfb.backward(tape, np.zeros_like(out))
+    assert not g.d_src.any() and not g.d_guide_lo.any() and not g.d_guide_hi.any()
+    with pytest.raises(ValueError):
+        gfb.forward_highres(rng.uniform(0, 1, (8, 8, 1)), rng.uniform(0, 1, (8, 7, 1)), p)
+
+
+# ---------------------------------------------------------------------------
+# semantic properties (pkg/tests/test_guided.py analogues) in fp64
+# ---------------------------------------------------------------------------
+
+def test_semantic_properties_fp64(gfb):
+    rng = np.random.default_rng(1)
+    gl, gh = rng.uniform(0, 1, (6, 8, 2)), rng.uniform(0, 1, (12, 16, 2))
+    out, _ = gfb.forward_joint(gl, gh, np.full_like(gl, 5.0), gfb.GuidedFilterParams(1, 1e-8))
+    assert np.abs(out - 5.0).max() <= 1e-10
+    out, _ = gfb.forward_joint(gl, gh, 2.0 * gl + 3.0, gfb.GuidedFilterParams(1, 0.0))
+    assert np.abs(out - (2.0 * gh + 3.0)).max() <= 1e-8
+    g = rng.uniform(0, 1, (16, 14, 2))
+    out, _ = gfb.forward_highres(g, 0.7 * g - 0.2, gfb.GuidedFilterParams(1, 0.0))
+    assert np.abs(out - (0.7 * g - 0.2)).max() <= 1e-8
+    out, _ = gfb.forward_highres(g, np.full_like(g, 0.3), gfb.GuidedFilterParams(2, 1e-2))
+    assert np.abs(out - 0.3).max() <= 1e-10
+    # linearity of the backward in d_out
+    sl = rng.uniform(0, 1, (6, 8, 2))
+    _, tape = gfb.forward_joint(gl, gh, sl, gfb.GuidedFilterParams(1, 1e-2))
+    u, v = rng.standard_normal((12, 16, 2)), rng.standard_normal((12, 16, 2))
+    combo = gfb.backward(tape, 0.37 * u - 1.21 * v)
+    gu, gv = gfb.backward(tape, u), gfb.backward(tape, v)
+    for f in ("d_src", "d_guide_lo", "d_guide_hi"):
+        mixed = 0.37 * getattr(gu, f) - 1.21 * getattr(gv, f)
+        assert np.abs(getattr(combo, f) - mixed).max() <= 1e-10
+    # tape fields re-derive slope/intercept (pkg/tests/test_guided.py:91-98)
+    _, tape = gfb.forward_joint(gl, gh, sl, gfb.GuidedFilterParams(2, 1e-2))
+    slope = tape.cov_guide_src / (tape.var_guide + tape.params.eps)
+    assert np.abs(slope - tape.slope).max() <= 1e-12
+    assert tape.variant == "joint"
+
+
+# ---------------------------------------------------------------------------
+# BASELINE-config inputs (seeded synthetic) vs the oracle
+# ---------------------------------------------------------------------------
+
+def test_cfg0_full_size_vs_oracle(gfb):
+    import workloads
+
+    lr_x, lr_y, hr_x = workloads.joint_inputs(1, 3, 1024, 1024, 4, seed=0)
+    p = gfb.GuidedFilterParams(1, 1e-8)
+    out, tape = gfb.forward_joint(lr_x.cuda(), hr_x.cuda(), lr_y.cuda(), p)
+    want = O.joint_forward_nchw(lr_x.double().numpy(), lr_y.double().numpy(),
+                                hr_x.double().numpy(), 1, 1e-8)
+    assert abs_max(npy(out), want) <= OUT_TOL32
+    d = torch.randn(out.shape, generator=torch.Generator().manual_seed(3))
+    g = gfb.backward(tape, d.cuda())
+    dlx, dly, dhx = O.joint_backward_nchw(lr_x.double().numpy(), lr_y.double().numpy(),
+                                          hr_x.double().numpy(), d.double().numpy(), 1, 1e-8)
+    assert rel_max(npy(g.d_guide_lo), dlx) <= GRAD_TOL32
+    assert rel_max(npy(g.d_src), dly) <= GRAD_TOL32
+    assert rel_max(npy(g.d_guide_hi), dhx) <= GRAD_TOL32
+
+
+@pytest.mark.parametrize("r", [1, 2, 4, 8])
+def test_cfg3_radius_sweep_vs_oracle(gfb, r):
+    import workloads
+
+    lr_x, lr_y, hr_x = workloads.joint_inputs(2, 3, 512, 512, 4, seed=10 + r)
+    p = gfb.GuidedFilterParams(r, 1e-4)
+    out, _ = gfb.forward_joint(lr_x.cuda(), hr_x.cuda(), lr_y.cuda(), p)
+    want = O.joint_forward_nchw(lr_x.double().numpy(), lr_y.double().numpy(),
+                                hr_x.double().numpy(), r, 1e-4)
+    assert abs_max(npy(out), want) <= OUT_TOL32
+
+
+def test_cfg1_highres_vs_oracle(gfb):
+    import workloads
+
+    guide, src = workloads.highres_inputs(2, 3, 512, 512, seed=1)
+    p = gfb.GuidedFilterParams(8, 1e-2)
+    out, tape = gfb.forward_highres(guide.cuda(), src.cuda(), p)
+    want = O.highres_forward_nchw(guide.double().numpy(), src.double().numpy(), 8, 1e-2)
+    assert abs_max(npy(out), want) <= OUT_TOL32
+    d = torch.randn(out.shape, generator=torch.Generator().manual_seed(4))
+    gr = gfb.backward(tape, d.cuda())
+    dg, ds = O.highres_backward_nchw(guide.double().numpy(), src.double().numpy(),
+                                     d.double().numpy(), 8, 1e-2)
+    assert rel_max(npy(gr.d_src), ds) <= GRAD_TOL32
+    assert rel_max(npy(gr.d_guide_hi), dg) <= GRAD_TOL32
+
+
+def test_cfg1_full_size_forward_vs_oracle(gfb):
+    import workloads
+
+    guide, src = workloads.highres_inputs(4, 3, 2048, 2048, seed=0)
+    p = gfb.GuidedFilterParams(8, 1e-2)
+    out, _ = gfb.forward_highres(guide.cuda(), src.cuda(), p)
+    o = npy(out)
+    for n in range(4):  # oracle per image keeps memory bounded
+        want = O.highres_forward_nchw(guide[n:n + 1].double().numpy(),
+                                      src[n:n + 1].double().numpy(), 8, 1e-2)
+        assert abs_max(o[n:n + 1], want) <= OUT_TOL32, n
+
+
+def test_determinism_bitwise(gfb):
+    import workloads
+
+    lr_x, lr_y, hr_x = [t.cuda() for t in workloads.joint_inputs(2, 3, 256, 320, 4, seed=5)]
+    p = gfb.GuidedFilterParams(2, 1e-4)
+    a, ta = gfb.forward_joint(lr_x, hr_x, lr_y, p)
+    b, _ = gfb.forward_joint(lr_x, hr_x, lr_y, p)
+    assert torch.equal(a, b)
+    d = torch.randn(a.shape, device="cuda", generator=torch.Generator("cuda").manual_seed(1))
+    g1, g2 = gfb.backward(ta, d), gfb.backward(ta, d)
+    for f in ("d_src", "d_guide_lo", "d_guide_hi"):
+        assert torch.equal(getattr(g1, f), getattr(g2, f))
+
+
+def test_autograd_module(gfb):
+    import workloads
+
+    lr_x, lr_y, hr_x = [t.cuda().requires_grad_() for t in
+                        workloads.joint_inputs(1, 3, 128, 128, 4, seed=6)]
+    m = gfb.FastGuidedFilter(1, 1e-4)
+    out = m(lr_x, lr_y, hr_x)
+    d = torch.randn_like(out)
+    out.backward(d)
+    assert m.last_status.bits() == 0
+    want = O.joint_backward_nchw(lr_x.detach().double().cpu().numpy(),
+                                 lr_y.detach().double().cpu().numpy(),
+                                 hr_x.detach().double().cpu().numpy(),
+                                 d.double().cpu().numpy(), 1, 1e-4)
+    assert rel_max(npy(lr_x.grad), want[0]) <= GRAD_TOL32
+    assert rel_max(npy(lr_y.grad), want[1]) <= GRAD_TOL32
+    assert rel_max(npy(hr_x.grad), want[2]) <= GRAD_TOL32
