@@ -57,6 +57,14 @@ int gf_version(void);              /* 100 * major + minor                    */
 const char* gf_last_error(void);   /* thread-local text of the last failure  */
 int gf_sm_count(void);             /* SMs of the current device (for sizing) */
 
+/* Scan n elements for NaN/Inf and OR GF_STATUS_NONFINITE_INPUT into status.
+ * The fused kernels do not test every input element (a non-finite input
+ * always makes the output at its own pixel non-finite); a caller that sees
+ * GF_STATUS_NONFINITE_OUTPUT or GF_STATUS_DEGENERATE scans the inputs with
+ * this to restore the reference's check order (inputs first,
+ * gf/guided.py:156-158). */
+int gf_check_finite(int dtype, const void* data, int64_t n, uint32_t* status, void* stream);
+
 /* ---- linear operators: gf/filters.py (the reference's _kernels seam) ----
  * P planes of (h, w).  No workspace. */
 

@@ -23,6 +23,7 @@ SIGNATURES = {
     "gf_version": (_i, []),
     "gf_last_error": (C.c_char_p, []),
     "gf_sm_count": (_i, []),
+    "gf_check_finite": (_i, [_i, _p, _i64, _p, _p]),
     "gf_mean_filter": (_i, [_i, _p, _p, _i64, _i64, _i64, _i, _p]),
     "gf_mean_filter_adjoint": (_i, [_i, _p, _p, _i64, _i64, _i64, _i, _p]),
     "gf_bilinear_resize": (_i, [_i, _p, _p, _i64, _i64, _i64, _i64, _i64, _p]),

@@ -108,11 +108,24 @@ class Status:
     def bits(self) -> int:
         return int(self.buf.item()) & 0xFFFFFFFF
 
-    def raise_if_set(self, what: str = "guided filter") -> None:
-        """Reference exception order: input check, degenerate window, output."""
+    def raise_if_set(self, what: str = "guided filter", inputs=()) -> None:
+        """Reference exception order: input check, degenerate window, output.
+
+        The fused kernels do not test inputs element by element; when a
+        DEGENERATE or OUTPUT bit is set, the inputs are scanned on the device
+        (gf_check_finite) so a non-finite input is reported as such, exactly
+        as the reference's up-front validate() would (gf/guided.py:156-158).
+        """
         from .guided import DegenerateWindowError
 
         b = self.bits()
+        if b and not (b & _lib.STATUS_NONFINITE_INPUT) and inputs:
+            lib = _lib.load()
+            for t in inputs:
+                rc = lib.gf_check_finite(dtype_code(t), t.data_ptr(), t.numel(), self.ptr,
+                                         stream_ptr(t.device))
+                _lib.check(rc, "check_finite")
+            b = self.bits()
         if b & _lib.STATUS_NONFINITE_INPUT:
             raise ValueError(f"{what}: input contains non-finite values")
         if b & _lib.STATUS_DEGENERATE:

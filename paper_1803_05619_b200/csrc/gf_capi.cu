@@ -50,6 +50,8 @@ int check_dims(const char* name, int64_t a, int64_t b, int64_t c, int64_t d) {
 
 cudaStream_t S(void* s) { return (cudaStream_t)s; }
 
+bool aligned16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
+
 bool use_fused_joint(int dtype, int64_t B, int64_t C, int64_t h, int64_t w, int64_t H, int64_t W,
                      int r) {
   return !g_force_generic && dtype == GF_F32 && gfb::fused_joint_ok(B, C, h, w, H, W, r);
@@ -92,6 +94,17 @@ int gf_sm_count(void) {
   if (cudaGetDevice(&dev) != cudaSuccess) return 0;
   if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return 0;
   return n;
+}
+
+int gf_check_finite(int dtype, const void* data, int64_t n, uint32_t* status, void* stream) {
+  if (!dtype_ok(dtype)) return fail(GF_ERR_ARG, "bad dtype %d", dtype);
+  if (n < 0) return fail(GF_ERR_ARG, "negative length");
+  if (n == 0) return GF_OK;
+  if (dtype == GF_F32)
+    gfb::generic_check_finite<float>((const float*)data, n, status, S(stream));
+  else
+    gfb::generic_check_finite<double>((const double*)data, n, status, S(stream));
+  return check_launch("gf_check_finite");
 }
 
 // ---------------------------------------------------------------------------
@@ -186,7 +199,8 @@ int gf_joint_fwd(int dtype, const void* lr_x, const void* lr_y, const void* hr_x
                  double eps, void* workspace, size_t workspace_bytes, uint32_t* status,
                  void* stream) {
   if (int e = check_joint(dtype, B, C, h, w, H, W, radius, eps)) return e;
-  if (use_fused_joint(dtype, B, C, h, w, H, W, radius)) {
+  if (use_fused_joint(dtype, B, C, h, w, H, W, radius) && aligned16(lr_x) && aligned16(lr_y) &&
+      aligned16(hr_x) && aligned16(out)) {
     gfb::fused_joint_fwd((const float*)lr_x, (const float*)lr_y, (const float*)hr_x, (float*)out,
                          B, C, h, w, H, W, radius, (float)eps, status, S(stream));
     return check_launch("gf_joint_fwd[fused]");
@@ -213,7 +227,9 @@ int gf_joint_bwd(int dtype, const void* lr_x, const void* lr_y, const void* hr_x
   size_t need = gf_joint_workspace_bytes(dtype, B, C, h, w, H, W, radius);
   if (workspace_bytes < need)
     return fail(GF_ERR_WORKSPACE, "joint workspace %zu < %zu bytes", workspace_bytes, need);
-  if (use_fused_joint(dtype, B, C, h, w, H, W, radius)) {
+  if (use_fused_joint(dtype, B, C, h, w, H, W, radius) && aligned16(lr_x) && aligned16(lr_y) &&
+      aligned16(hr_x) && aligned16(d_out) && aligned16(d_lr_x) && aligned16(d_lr_y) &&
+      aligned16(d_hr_x)) {
     gfb::fused_joint_bwd((const float*)lr_x, (const float*)lr_y, (const float*)hr_x,
                          (const float*)d_out, (float*)d_lr_x, (float*)d_lr_y, (float*)d_hr_x, B,
                          C, h, w, H, W, radius, (float)eps, workspace, status, S(stream));
@@ -265,7 +281,8 @@ int gf_highres_fwd(int dtype, const void* guide, const void* src, void* out, int
                    int64_t C, int64_t H, int64_t W, int radius, double eps, void* workspace,
                    size_t workspace_bytes, uint32_t* status, void* stream) {
   if (int e = check_highres(dtype, B, Cg, C, H, W, radius, eps)) return e;
-  if (use_fused_highres(dtype, B, Cg, C, H, W, radius)) {
+  if (use_fused_highres(dtype, B, Cg, C, H, W, radius) && aligned16(guide) && aligned16(src) &&
+      aligned16(out)) {
     gfb::fused_highres_fwd((const float*)guide, (const float*)src, (float*)out, B, Cg, C, H, W,
                            radius, (float)eps, status, S(stream));
     return check_launch("gf_highres_fwd[fused]");

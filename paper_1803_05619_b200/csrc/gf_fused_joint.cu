@@ -1,0 +1,702 @@
+// Fused fast (joint-upsampling) guided filter, fp32 NCHW, factor-4 resize,
+// on sm_100a.  gf/guided.py:152-195 (forward) and :267-283 + :236-264
+// (backward).
+//
+// Forward, ONE kernel per call (k_joint_fwd): each CTA owns a 16 x 32
+// low-res block = a 64 x 128 high-res tile of one plane.
+//   1. its high-res guide tile is requested first (8 x 128-bit loads per
+//      thread, held in registers) so HBM latency overlaps step 2;
+//   2. the low-res x, y block plus halo (r for the box, 1 for the bilinear
+//      support) is staged in shared memory, shifted by a per-CTA constant;
+//      vertical then horizontal sliding window sums (fp32, <= 18 rows/cols
+//      per run, so no error growth) give mean_x, mean_y, var, cov and
+//      A = cov/(var+eps), b = mean_y - A mean_x for the (16+2) x (32+2) cells
+//      the tile's bilinear taps touch -- never written to HBM;
+//   3. out = Up(b) + Up(A) * hr_x (half-pixel centres, edge clamp; exact
+//      factor-4 weights) is written with 128-bit stores.
+// HBM traffic = compulsory (read hr_x, lr_x, lr_y; write out) + the lr halo
+// re-reads, which hit L2.
+//
+// Backward, TWO kernels:
+//   k_joint_bwd_hr  -- per tile: recompute A (step 2 above), write
+//       d_hr_x = d_out * Up(A), and gather the exact bilinear adjoints
+//       db = Up^T(d_out), dAraw = Up^T(d_out * hr_x) for the block's low-res
+//       cells (hr rows/cols [4i-2, 4i+5]; deterministic, no atomics) into a
+//       2-field low-res workspace;
+//   k_joint_bwd_lr  -- per 32 x 32 low-res block with a 2r halo: moments,
+//       the slope/intercept -> moment gradients (gf/guided.py:236-253), the
+//       box-filter adjoints and d_lr_x, d_lr_y (gf/guided.py:255-263).
+#include <cuda_runtime.h>
+
+#include "gf_common.cuh"
+#include "gf_internal.h"
+
+namespace gfb {
+namespace jf {
+
+constexpr int TLY = 16, TLX = 32;      // low-res block of the hr kernels
+constexpr int THY = 4 * TLY, THX = 4 * TLX;
+constexpr int NT = 256;
+constexpr int RA = TLY + 2, CA = TLX + 2;  // coefficient cells incl. bilinear halo
+constexpr int kMaxRadius = 12;  // tail-kernel smem <= 227 KB
+
+__device__ __forceinline__ int wlen(int i, int n, int r) {
+  int a = i - r < 0 ? 0 : i - r;
+  int b = i + r > n - 1 ? n - 1 : i + r;
+  return b - a + 1;
+}
+
+// factor-4 half-pixel tap of hr coordinate d into an axis of n low-res cells:
+// s = (d + 0.5)/4 - 0.5 = (2d - 3)/8 exactly, clamped (gf/filters.py:126-131)
+struct Tap {
+  int lo, hi;
+  float f;
+};
+__device__ __forceinline__ Tap tap4(int d, int n) {
+  float s = (float)(2 * d - 3) * 0.125f;
+  const float top = (float)(n - 1);
+  s = s < 0.f ? 0.f : (s > top ? top : s);
+  Tap t;
+  t.lo = (int)floorf(s);
+  if (t.lo > n - 1) t.lo = n - 1;
+  t.f = s - (float)t.lo;
+  t.hi = t.lo + 1 > n - 1 ? n - 1 : t.lo + 1;
+  return t;
+}
+
+struct SmemCoef {
+  // sized for kMaxRadius; carved from dynamic shared memory
+  float* xs;    // [RI][CI]
+  float* ys;    // [RI][CI]
+  float* vsum;  // [4][RA][CI]
+  float* As;    // [RA][CA]
+  float* Bs;    // [RA][CA]
+};
+
+__host__ __device__ inline size_t coef_smem_floats(int r) {
+  const int RI = RA + 2 * r, CI = CA + 2 * r;
+  return (size_t)2 * RI * CI + (size_t)4 * RA * CI + (size_t)2 * RA * CA;
+}
+
+__device__ inline SmemCoef carve(float* base, int r) {
+  const int RI = RA + 2 * r, CI = CA + 2 * r;
+  SmemCoef s;
+  s.xs = base;
+  s.ys = s.xs + RI * CI;
+  s.vsum = s.ys + RI * CI;
+  s.As = s.vsum + 4 * RA * CI;
+  s.Bs = s.As + RA * CA;
+  return s;
+}
+
+// A (and b) for low-res cells [i0-1, i0+TLY] x [k0-1, k0+TLX] of one plane.
+template <bool NEED_B>
+__device__ void lr_coeffs(const float* __restrict__ X, const float* __restrict__ Y, int h, int w,
+                          int i0, int k0, int r, float eps, const SmemCoef& sm, bool& degen) {
+  const int RI = RA + 2 * r, CI = CA + 2 * r;
+  const int tid = threadIdx.x;
+  // per-CTA shift (var/cov are shift invariant); any in-image sample works
+  const int sy_ = min(max(i0, 0), h - 1), sx_ = min(max(k0, 0), w - 1);
+  const float sx = __ldg(X + (int64_t)sy_ * w + sx_);
+  const float sy = __ldg(Y + (int64_t)sy_ * w + sx_);
+  // 1) stage inputs (zero outside the image: clamped windows)
+  for (int idx = tid; idx < RI * CI; idx += NT) {
+    const int row = idx / CI, col = idx - row * CI;
+    const int gy = i0 - 1 - r + row, gx = k0 - 1 - r + col;
+    float xv = 0.f, yv = 0.f;
+    if (gy >= 0 && gy < h && gx >= 0 && gx < w) {
+      xv = __ldg(X + (int64_t)gy * w + gx) - sx;
+      yv = __ldg(Y + (int64_t)gy * w + gx) - sy;
+    }
+    sm.xs[idx] = xv;
+    sm.ys[idx] = yv;
+  }
+  __syncthreads();
+  // 2) vertical sliding sums: item = (column, chunk of rows)
+  {
+    const int nch = NT / CI > 0 ? (NT / CI < RA ? NT / CI : RA) : 1;
+    const int rc = (RA + nch - 1) / nch;
+    for (int it = tid; it < CI * nch; it += NT) {
+      const int col = it % CI, ch = it / CI;
+      const int a0 = ch * rc, a1 = min(RA, a0 + rc);
+      if (a0 >= a1) continue;
+      float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+      for (int d = 0; d < 2 * r; ++d) {
+        const float xv = sm.xs[(a0 + d) * CI + col], yv = sm.ys[(a0 + d) * CI + col];
+        s0 += xv;
+        s1 += yv;
+        s2 += xv * xv;
+        s3 += xv * yv;
+      }
+      for (int a = a0; a < a1; ++a) {
+        const float xv = sm.xs[(a + 2 * r) * CI + col], yv = sm.ys[(a + 2 * r) * CI + col];
+        s0 += xv;
+        s1 += yv;
+        s2 += xv * xv;
+        s3 += xv * yv;
+        sm.vsum[(0 * RA + a) * CI + col] = s0;
+        sm.vsum[(1 * RA + a) * CI + col] = s1;
+        sm.vsum[(2 * RA + a) * CI + col] = s2;
+        sm.vsum[(3 * RA + a) * CI + col] = s3;
+        const float xo = sm.xs[a * CI + col], yo = sm.ys[a * CI + col];
+        s0 -= xo;
+        s1 -= yo;
+        s2 -= xo * xo;
+        s3 -= xo * yo;
+      }
+    }
+  }
+  __syncthreads();
+  // 3) horizontal sliding sums + coefficients: item = (row, chunk of cols)
+  {
+    constexpr int nch = NT / RA < CA ? NT / RA : CA;  // 14
+    constexpr int cc = (CA + nch - 1) / nch;
+    for (int it = tid; it < RA * nch; it += NT) {
+      const int a = it / nch, ch = it - a * nch;
+      const int c0 = ch * cc, c1 = min(CA, c0 + cc);
+      if (c0 >= c1) continue;
+      const float* v0 = sm.vsum + (0 * RA + a) * CI;
+      const float* v1 = sm.vsum + (1 * RA + a) * CI;
+      const float* v2 = sm.vsum + (2 * RA + a) * CI;
+      const float* v3 = sm.vsum + (3 * RA + a) * CI;
+      float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+      for (int d = 0; d < 2 * r; ++d) {
+        s0 += v0[c0 + d];
+        s1 += v1[c0 + d];
+        s2 += v2[c0 + d];
+        s3 += v3[c0 + d];
+      }
+      const int gy = i0 - 1 + a;
+      const bool row_ok = gy >= 0 && gy < h;
+      const float ny = row_ok ? (float)wlen(gy, h, r) : 1.f;
+      for (int c = c0; c < c1; ++c) {
+        s0 += v0[c + 2 * r];
+        s1 += v1[c + 2 * r];
+        s2 += v2[c + 2 * r];
+        s3 += v3[c + 2 * r];
+        const int gx = k0 - 1 + c;
+        float A = 0.f, B = 0.f;
+        if (row_ok && gx >= 0 && gx < w) {
+          const float inv = __frcp_rn(ny * (float)wlen(gx, w, r));
+          const float mx = s0 * inv, my = s1 * inv;
+          const float var = s2 * inv - mx * mx;
+          const float cov = s3 * inv - mx * my;
+          if (eps == 0.f && !(var > 0.f)) degen = true;
+          A = cov * __frcp_rn(var + eps);
+          if (NEED_B) B = (my + sy) - A * (mx + sx);
+        }
+        sm.As[a * CA + c] = A;
+        if (NEED_B) sm.Bs[a * CA + c] = B;
+        s0 -= v0[c];
+        s1 -= v1[c];
+        s2 -= v2[c];
+        s3 -= v3[c];
+      }
+    }
+  }
+  __syncthreads();
+}
+
+struct FwdArgs {
+  const float* lr_x;
+  const float* lr_y;
+  const float* hr_x;
+  float* out;
+  int h, w, H, W, r;
+  float eps;
+  uint32_t* status;
+};
+
+// Horizontal pre-interpolation of one coefficient row for the 4 hr phases of
+// lr cell column (k0 + lane): taps into local columns.
+struct ColTaps {
+  int lo[4], hi[4];
+  float f[4];
+};
+
+__device__ __forceinline__ ColTaps col_taps(int X0, int w, int k0) {
+  ColTaps t;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    Tap tp = tap4(X0 + j, w);
+    t.lo[j] = tp.lo - (k0 - 1);
+    t.hi[j] = tp.hi - (k0 - 1);
+    t.f[j] = tp.f;
+  }
+  return t;
+}
+
+__device__ __forceinline__ void hrow(const float* __restrict__ row, const ColTaps& ct,
+                                     float (&o)[4]) {
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const float a = row[ct.lo[j]];
+    o[j] = a + ct.f[j] * (row[ct.hi[j]] - a);
+  }
+}
+
+__global__ void __launch_bounds__(NT) k_joint_fwd(FwdArgs a) {
+  extern __shared__ float4 smem4[];
+  const int r = a.r;
+  const SmemCoef sm = carve(reinterpret_cast<float*>(smem4), r);
+  const int64_t p = blockIdx.z;
+  const int i0 = blockIdx.y * TLY, k0 = blockIdx.x * TLX;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const float* __restrict__ G = a.hr_x + p * (int64_t)a.H * a.W;
+  float* __restrict__ O = a.out + p * (int64_t)a.H * a.W;
+  const int X0 = 4 * (k0 + lane);
+  const int Yb = 4 * i0 + 8 * warp;  // this warp's 8 hr rows
+  const bool col_ok = X0 < a.W;
+
+  // 1) issue the hr loads first
+  float4 g[8];
+#pragma unroll
+  for (int t = 0; t < 8; ++t) {
+    const int Y = Yb + t;
+    g[t] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (col_ok && Y < a.H) g[t] = __ldg(reinterpret_cast<const float4*>(G + (int64_t)Y * a.W + X0));
+  }
+  // 2) coefficients of the block
+  bool degen = false;
+  lr_coeffs<true>(a.lr_x + p * (int64_t)a.h * a.w, a.lr_y + p * (int64_t)a.h * a.w, a.h, a.w, i0,
+                  k0, r, a.eps, sm, degen);
+  // 3) apply
+  const ColTaps ct = col_taps(X0, a.w, k0);
+  // local coefficient rows 2*warp .. 2*warp+3 cover every tap of rows Yb..Yb+7
+  float HA[4][4], HB[4][4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int rl = 2 * warp + q;
+    if (rl < RA) {
+      hrow(sm.As + rl * CA, ct, HA[q]);
+      hrow(sm.Bs + rl * CA, ct, HB[q]);
+    } else {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) HA[q][j] = HB[q][j] = 0.f;
+    }
+  }
+  bool bad = false;
+  const int slo_base = i0 - 1 + 2 * warp;  // global lr row of HA[0]
+#pragma unroll
+  for (int t = 0; t < 8; ++t) {
+    const int Y = Yb + t;
+    if (!col_ok || Y >= a.H) continue;
+    const Tap ty = tap4(Y, a.h);
+    // static rows for interior taps: phase 0,1 -> (cell-1, cell); 2,3 -> (cell, cell+1)
+    constexpr int dummy = 0;
+    (void)dummy;
+    const int q0 = t / 4 + ((t & 3) >= 2 ? 1 : 0);
+    const int slo = slo_base + q0;
+    float o[4];
+    const float gv[4] = {g[t].x, g[t].y, g[t].z, g[t].w};
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      // exact clamped taps: lo is slo (interior / bottom clamp) or slo+1 (top clamp, f == 0)
+      const float alo = ty.lo == slo ? HA[q0][j] : HA[q0 + 1][j];
+      const float ahi = ty.hi == slo + 1 ? HA[q0 + 1][j] : alo;
+      const float blo = ty.lo == slo ? HB[q0][j] : HB[q0 + 1][j];
+      const float bhi = ty.hi == slo + 1 ? HB[q0 + 1][j] : blo;
+      const float Ah = alo + ty.f * (ahi - alo);
+      const float Bh = blo + ty.f * (bhi - blo);
+      o[j] = Bh + Ah * gv[j];
+      if (!isfinite(o[j])) bad = true;
+    }
+    *reinterpret_cast<float4*>(O + (int64_t)Y * a.W + X0) = make_float4(o[0], o[1], o[2], o[3]);
+  }
+  if (degen) flag(a.status, GF_STATUS_DEGENERATE);
+  if (bad) flag(a.status, GF_STATUS_NONFINITE_OUTPUT);
+}
+
+// ---------------------------------------------------------------------------
+// backward, kernel 1: hr pass
+// ---------------------------------------------------------------------------
+struct BwdHrArgs {
+  const float* lr_x;
+  const float* lr_y;
+  const float* hr_x;
+  const float* d_out;
+  float* d_hr;
+  float* db;     // (P, h, w) workspace
+  float* dA;     // (P, h, w) workspace
+  int h, w, H, W, r;
+  float eps;
+  uint32_t* status;
+};
+
+constexpr int GR = THY + 4;  // gather rows: hr [4 i0 - 2, 4 i0 + 66)
+
+__host__ __device__ inline size_t bwd_hr_smem_floats(int r) {
+  return coef_smem_floats(r) + (size_t)2 * GR * TLX;
+}
+
+__global__ void __launch_bounds__(NT) k_joint_bwd_hr(BwdHrArgs a) {
+  extern __shared__ float4 smem4[];
+  const int r = a.r;
+  float* base = reinterpret_cast<float*>(smem4);
+  const SmemCoef sm = carve(base, r);
+  float* R1 = base + coef_smem_floats(r);  // [GR][TLX]
+  float* R2 = R1 + GR * TLX;
+  const int64_t p = blockIdx.z;
+  const int i0 = blockIdx.y * TLY, k0 = blockIdx.x * TLX;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t hplane = (int64_t)a.H * a.W;
+  const float* __restrict__ G = a.hr_x + p * hplane;
+  const float* __restrict__ D = a.d_out + p * hplane;
+  float* __restrict__ DH = a.d_hr + p * hplane;
+  const int X0 = 4 * (k0 + lane);
+  const int Yb = 4 * i0 + 8 * warp;
+  const bool col_ok = X0 < a.W;
+
+  float4 dv[8];
+#pragma unroll
+  for (int t = 0; t < 8; ++t) {
+    const int Y = Yb + t;
+    dv[t] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (col_ok && Y < a.H) dv[t] = __ldg(reinterpret_cast<const float4*>(D + (int64_t)Y * a.W + X0));
+  }
+  bool degen = false;
+  lr_coeffs<false>(a.lr_x + p * (int64_t)a.h * a.w, a.lr_y + p * (int64_t)a.h * a.w, a.h, a.w,
+                   i0, k0, r, a.eps, sm, degen);
+  // d_hr = d_out * Up(A)
+  {
+    const ColTaps ct = col_taps(X0, a.w, k0);
+    float HA[4][4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int rl = 2 * warp + q;
+      if (rl < RA) {
+        hrow(sm.As + rl * CA, ct, HA[q]);
+      } else {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) HA[q][j] = 0.f;
+      }
+    }
+    const int slo_base = i0 - 1 + 2 * warp;
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      const int Y = Yb + t;
+      if (!col_ok || Y >= a.H) continue;
+      const Tap ty = tap4(Y, a.h);
+      const int q0 = t / 4 + ((t & 3) >= 2 ? 1 : 0);
+      const int slo = slo_base + q0;
+      const float dd[4] = {dv[t].x, dv[t].y, dv[t].z, dv[t].w};
+      float o[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float alo = ty.lo == slo ? HA[q0][j] : HA[q0 + 1][j];
+        const float ahi = ty.hi == slo + 1 ? HA[q0 + 1][j] : alo;
+        o[j] = dd[j] * (alo + ty.f * (ahi - alo));
+      }
+      *reinterpret_cast<float4*>(DH + (int64_t)Y * a.W + X0) = make_float4(o[0], o[1], o[2], o[3]);
+    }
+  }
+  // row partials of the adjoint: R[y][k] = sum_X wx(X, k) * (d, d*G) over
+  // X in [4k-2, 4k+5] (every hr column whose taps touch lr column k)
+  {
+    const int k = k0 + lane;
+    float wx[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int X = 4 * k - 2 + j;
+      wx[j] = 0.f;
+      if (X >= 0 && X < a.W) {
+        const Tap tx = tap4(X, a.w);
+        if (tx.lo == k) wx[j] += 1.f - tx.f;
+        if (tx.hi == k) wx[j] += tx.f;
+      }
+    }
+    const bool left = 4 * k - 4 >= 0, right = 4 * k + 4 < a.W;
+    for (int yl = warp; yl < GR; yl += NT / 32) {
+      const int Y = 4 * i0 - 2 + yl;
+      float s1 = 0.f, s2 = 0.f;
+      if (Y >= 0 && Y < a.H && k < a.w) {
+        const float* drow = D + (int64_t)Y * a.W + 4 * k;
+        const float* grow = G + (int64_t)Y * a.W + 4 * k;
+        const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+        const float4 d0 = left ? __ldg(reinterpret_cast<const float4*>(drow - 4)) : z;
+        const float4 d1 = __ldg(reinterpret_cast<const float4*>(drow));
+        const float4 d2 = right ? __ldg(reinterpret_cast<const float4*>(drow + 4)) : z;
+        const float4 g0 = left ? __ldg(reinterpret_cast<const float4*>(grow - 4)) : z;
+        const float4 g1 = __ldg(reinterpret_cast<const float4*>(grow));
+        const float4 g2 = right ? __ldg(reinterpret_cast<const float4*>(grow + 4)) : z;
+        const float dd[8] = {d0.z, d0.w, d1.x, d1.y, d1.z, d1.w, d2.x, d2.y};
+        const float gg[8] = {g0.z, g0.w, g1.x, g1.y, g1.z, g1.w, g2.x, g2.y};
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          s1 += wx[j] * dd[j];
+          s2 += wx[j] * (dd[j] * gg[j]);
+        }
+      }
+      R1[yl * TLX + lane] = s1;
+      R2[yl * TLX + lane] = s2;
+    }
+  }
+  __syncthreads();
+  // column pass: db[i][k] = sum_Y wy(Y, i) R1[Y][k]
+  for (int it = threadIdx.x; it < TLY * TLX; it += NT) {
+    const int il = it / TLX, kl = it - il * TLX;
+    const int i = i0 + il, k = k0 + kl;
+    if (i >= a.h || k >= a.w) continue;
+    float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+    for (int dy = -2; dy <= 5; ++dy) {
+      const int Y = 4 * i + dy;
+      if (Y < 0 || Y >= a.H) continue;
+      const Tap ty = tap4(Y, a.h);
+      float wgt = 0.f;
+      if (ty.lo == i) wgt += 1.f - ty.f;
+      if (ty.hi == i) wgt += ty.f;
+      const int yl = Y - (4 * i0 - 2);
+      s1 += wgt * R1[yl * TLX + kl];
+      s2 += wgt * R2[yl * TLX + kl];
+    }
+    const int64_t o = p * (int64_t)a.h * a.w + (int64_t)i * a.w + k;
+    a.db[o] = s1;
+    a.dA[o] = s2;
+  }
+  if (degen) flag(a.status, GF_STATUS_DEGENERATE);
+}
+
+// ---------------------------------------------------------------------------
+// backward, kernel 2: low-res tail
+// ---------------------------------------------------------------------------
+constexpr int TL = 32;  // low-res block of the tail kernel
+
+struct BwdLrArgs {
+  const float* lr_x;
+  const float* lr_y;
+  const float* db;
+  const float* dA;
+  float* d_lr_x;
+  float* d_lr_y;
+  int h, w, r;
+  float eps;
+};
+
+__host__ __device__ inline size_t bwd_lr_smem_floats(int r) {
+  const int NI = TL + 4 * r;   // inputs x, y
+  const int NM = TL + 2 * r;   // moment region
+  // xs, ys [NI][NI]; vsum [4][NM][NI]; kf [4][NM][NM]; (vs2 [4][TL][NM] reuses vsum)
+  return (size_t)2 * NI * NI + (size_t)4 * NM * NI + (size_t)4 * NM * NM;
+}
+
+__global__ void __launch_bounds__(NT) k_joint_bwd_lr(BwdLrArgs a) {
+  extern __shared__ float4 smem4[];
+  const int r = a.r;
+  const int NI = TL + 4 * r, NM = TL + 2 * r;
+  float* xs = reinterpret_cast<float*>(smem4);
+  float* ys = xs + NI * NI;
+  float* vsum = ys + NI * NI;      // [4][NM][NI], later [4][TL][NM]
+  float* kf = vsum + 4 * NM * NI;  // [4][NM][NM]
+  const int64_t p = blockIdx.z;
+  const int i0 = blockIdx.y * TL, k0 = blockIdx.x * TL;
+  const int h = a.h, w = a.w;
+  const int tid = threadIdx.x;
+  const float* __restrict__ X = a.lr_x + p * (int64_t)h * w;
+  const float* __restrict__ Yp = a.lr_y + p * (int64_t)h * w;
+  const float* __restrict__ DB = a.db + p * (int64_t)h * w;
+  const float* __restrict__ DA = a.dA + p * (int64_t)h * w;
+  const int sy_ = min(i0, h - 1), sx_ = min(k0, w - 1);
+  const float sx = __ldg(X + (int64_t)sy_ * w + sx_);
+  const float sy = __ldg(Yp + (int64_t)sy_ * w + sx_);
+  // inputs over [i0-2r, i0+TL+2r)^2, shifted, zero outside the image
+  for (int idx = tid; idx < NI * NI; idx += NT) {
+    const int row = idx / NI, col = idx - row * NI;
+    const int gy = i0 - 2 * r + row, gx = k0 - 2 * r + col;
+    float xv = 0.f, yv = 0.f;
+    if (gy >= 0 && gy < h && gx >= 0 && gx < w) {
+      xv = __ldg(X + (int64_t)gy * w + gx) - sx;
+      yv = __ldg(Yp + (int64_t)gy * w + gx) - sy;
+    }
+    xs[idx] = xv;
+    ys[idx] = yv;
+  }
+  __syncthreads();
+  // vertical sums for moment rows m in [0, NM) (global i0 - r + m): input rows [m, m+2r]
+  {
+    const int nch = max(1, min(NM, NT / NI));
+    const int rc = (NM + nch - 1) / nch;
+    for (int it = tid; it < NI * nch; it += NT) {
+      const int col = it % NI, ch = it / NI;
+      const int m0 = ch * rc, m1 = min(NM, m0 + rc);
+      if (m0 >= m1) continue;
+      float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+      for (int d = 0; d < 2 * r; ++d) {
+        const float xv = xs[(m0 + d) * NI + col], yv = ys[(m0 + d) * NI + col];
+        s0 += xv; s1 += yv; s2 += xv * xv; s3 += xv * yv;
+      }
+      for (int m = m0; m < m1; ++m) {
+        const float xv = xs[(m + 2 * r) * NI + col], yv = ys[(m + 2 * r) * NI + col];
+        s0 += xv; s1 += yv; s2 += xv * xv; s3 += xv * yv;
+        vsum[(0 * NM + m) * NI + col] = s0;
+        vsum[(1 * NM + m) * NI + col] = s1;
+        vsum[(2 * NM + m) * NI + col] = s2;
+        vsum[(3 * NM + m) * NI + col] = s3;
+        const float xo = xs[m * NI + col], yo = ys[m * NI + col];
+        s0 -= xo; s1 -= yo; s2 -= xo * xo; s3 -= xo * yo;
+      }
+    }
+  }
+  __syncthreads();
+  // horizontal sums + moment gradients / N at moment cells (m, n)
+  {
+    const int nch = max(1, min(NM, NT / NM));
+    const int cc = (NM + nch - 1) / nch;
+    for (int it = tid; it < NM * nch; it += NT) {
+      const int m = it / nch, ch = it - m * nch;
+      const int n0 = ch * cc, n1 = min(NM, n0 + cc);
+      if (n0 >= n1) continue;
+      const int gy = i0 - r + m;
+      const bool row_ok = gy >= 0 && gy < h;
+      const float* v0 = vsum + (0 * NM + m) * NI;
+      const float* v1 = vsum + (1 * NM + m) * NI;
+      const float* v2 = vsum + (2 * NM + m) * NI;
+      const float* v3 = vsum + (3 * NM + m) * NI;
+      float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+      for (int d = 0; d < 2 * r; ++d) {
+        s0 += v0[n0 + d]; s1 += v1[n0 + d]; s2 += v2[n0 + d]; s3 += v3[n0 + d];
+      }
+      const float ny = row_ok ? (float)wlen(gy, h, r) : 1.f;
+      for (int n = n0; n < n1; ++n) {
+        s0 += v0[n + 2 * r]; s1 += v1[n + 2 * r]; s2 += v2[n + 2 * r]; s3 += v3[n + 2 * r];
+        const int gx = k0 - r + n;
+        float k_cov = 0.f, k_var = 0.f, k_mx = 0.f, k_my = 0.f;
+        if (row_ok && gx >= 0 && gx < w) {
+          const float inv = __frcp_rn(ny * (float)wlen(gx, w, r));
+          const float mx = s0 * inv, my = s1 * inv;  // shifted means
+          const float var = s2 * inv - mx * mx;
+          const float cov = s3 * inv - mx * my;
+          const float rden = __frcp_rn(var + a.eps);
+          const float A = cov * rden;
+          const float ux = mx + sx, uy = my + sy;  // true means
+          const int64_t o = (int64_t)gy * w + gx;
+          const float dbv = __ldg(DB + o);
+          const float dAv = __ldg(DA + o) + (-dbv * ux);   // gf/guided.py:278-280
+          const float d_cov = dAv * rden;                   // :242
+          const float d_var = -dAv * cov * (rden * rden);   // :243
+          const float d_my = dbv + (-d_cov * ux);           // :245-247
+          const float d_mx = (-dbv * A) + (-d_cov * uy) + (-2.f * d_var * ux);  // :248-252
+          k_cov = d_cov * inv;
+          k_var = d_var * inv;
+          k_mx = d_mx * inv;
+          k_my = d_my * inv;
+        }
+        kf[(0 * NM + m) * NM + n] = k_cov;
+        kf[(1 * NM + m) * NM + n] = k_var;
+        kf[(2 * NM + m) * NM + n] = k_mx;
+        kf[(3 * NM + m) * NM + n] = k_my;
+        s0 -= v0[n]; s1 -= v1[n]; s2 -= v2[n]; s3 -= v3[n];
+      }
+    }
+  }
+  __syncthreads();
+  // box adjoint (M^T g = box_sum(g/N)): vertical sums of kf for own rows -> vsum as [4][TL][NM]
+  {
+    const int nch = max(1, min(TL, NT / (4 * NM)));
+    const int rc = (TL + nch - 1) / nch;
+    for (int it = tid; it < 4 * NM * nch; it += NT) {
+      const int ch = it / (4 * NM), rem = it - ch * 4 * NM;
+      const int f = rem / NM, n = rem - f * NM;
+      const int m0 = ch * rc, m1 = min(TL, m0 + rc);
+      if (m0 >= m1) continue;
+      const float* src = kf + f * NM * NM + n;
+      float s = 0.f;
+      for (int d = 0; d < 2 * r; ++d) s += src[(m0 + d) * NM];
+      for (int m = m0; m < m1; ++m) {
+        s += src[(m + 2 * r) * NM];
+        vsum[(f * TL + m) * NM + n] = s;
+        s -= src[m * NM];
+      }
+    }
+  }
+  __syncthreads();
+  // horizontal sums + outputs
+  {
+    constexpr int nch = NT / TL;  // 8
+    constexpr int cc = TL / nch;  // 4
+    for (int it = tid; it < TL * nch; it += NT) {
+      const int m = it / nch, ch = it - m * nch;
+      const int gy = i0 + m;
+      if (gy >= h) continue;
+      const int n0 = ch * cc;
+      const float* v0 = vsum + (0 * TL + m) * NM;
+      const float* v1 = vsum + (1 * TL + m) * NM;
+      const float* v2 = vsum + (2 * TL + m) * NM;
+      const float* v3 = vsum + (3 * TL + m) * NM;
+      float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+      for (int d = 0; d < 2 * r; ++d) {
+        s0 += v0[n0 + d]; s1 += v1[n0 + d]; s2 += v2[n0 + d]; s3 += v3[n0 + d];
+      }
+#pragma unroll
+      for (int n = n0; n < n0 + cc; ++n) {
+        s0 += v0[n + 2 * r]; s1 += v1[n + 2 * r]; s2 += v2[n + 2 * r]; s3 += v3[n + 2 * r];
+        const int gx = k0 + n;
+        if (gx < w) {
+          const float xv = xs[(m + 2 * r) * NI + n + 2 * r] + sx;
+          const float yv = ys[(m + 2 * r) * NI + n + 2 * r] + sy;
+          const int64_t o = p * (int64_t)h * w + (int64_t)gy * w + gx;
+          a.d_lr_y[o] = s0 * xv + s3;                      // gf/guided.py:256-258
+          a.d_lr_x[o] = s0 * yv + 2.f * s1 * xv + s2;       // :259-263
+        }
+        s0 -= v0[n]; s1 -= v1[n]; s2 -= v2[n]; s3 -= v3[n];
+      }
+    }
+  }
+}
+
+}  // namespace jf
+
+bool fused_joint_ok(int64_t B, int64_t C, int64_t h, int64_t w, int64_t H, int64_t W, int r) {
+  if (H != 4 * h || W != 4 * w) return false;
+  if (r < 0 || r > jf::kMaxRadius) return false;
+  if (h < 2 || w < 2) return false;
+  if (H > (1 << 30) || W > (1 << 30)) return false;
+  if ((h + jf::TLY - 1) / jf::TLY > 65535 || B * C > 65535) return false;
+  return true;
+}
+
+static void set_smem(const void* fn, size_t bytes) {
+  if (bytes > 48 * 1024) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+}
+
+void fused_joint_fwd(const float* lr_x, const float* lr_y, const float* hr_x, float* out, int64_t B,
+                     int64_t C, int64_t h, int64_t w, int64_t H, int64_t W, int r, float eps,
+                     uint32_t* status, cudaStream_t s) {
+  const size_t smem = jf::coef_smem_floats(r) * sizeof(float);
+  set_smem((const void*)jf::k_joint_fwd, smem);
+  dim3 grid((unsigned)((w + jf::TLX - 1) / jf::TLX), (unsigned)((h + jf::TLY - 1) / jf::TLY),
+            (unsigned)(B * C));
+  jf::FwdArgs a{lr_x, lr_y, hr_x, out, (int)h, (int)w, (int)H, (int)W, r, eps, status};
+  jf::k_joint_fwd<<<grid, jf::NT, smem, s>>>(a);
+}
+
+size_t fused_joint_bwd_ws_bytes(int64_t B, int64_t C, int64_t h, int64_t w) {
+  return (size_t)2 * B * C * h * w * sizeof(float);
+}
+
+void fused_joint_bwd(const float* lr_x, const float* lr_y, const float* hr_x, const float* d_out,
+                     float* d_lr_x, float* d_lr_y, float* d_hr_x, int64_t B, int64_t C, int64_t h,
+                     int64_t w, int64_t H, int64_t W, int r, float eps, void* ws,
+                     uint32_t* status, cudaStream_t s) {
+  float* db = (float*)ws;
+  float* dA = db + B * C * h * w;
+  {
+    const size_t smem = jf::bwd_hr_smem_floats(r) * sizeof(float);
+    set_smem((const void*)jf::k_joint_bwd_hr, smem);
+    dim3 grid((unsigned)((w + jf::TLX - 1) / jf::TLX), (unsigned)((h + jf::TLY - 1) / jf::TLY),
+              (unsigned)(B * C));
+    jf::BwdHrArgs a{lr_x, lr_y, hr_x, d_out, d_hr_x, db, dA, (int)h, (int)w, (int)H, (int)W, r,
+                    eps, status};
+    jf::k_joint_bwd_hr<<<grid, jf::NT, smem, s>>>(a);
+  }
+  {
+    const size_t smem = jf::bwd_lr_smem_floats(r) * sizeof(float);
+    set_smem((const void*)jf::k_joint_bwd_lr, smem);
+    dim3 grid((unsigned)((w + jf::TL - 1) / jf::TL), (unsigned)((h + jf::TL - 1) / jf::TL),
+              (unsigned)(B * C));
+    jf::BwdLrArgs a{lr_x, lr_y, db, dA, d_lr_x, d_lr_y, (int)h, (int)w, r, eps};
+    jf::k_joint_bwd_lr<<<grid, jf::NT, smem, s>>>(a);
+  }
+}
+
+}  // namespace gfb

@@ -122,6 +122,22 @@ __global__ void k_resize_adj(const T* __restrict__ g, const T* __restrict__ guid
   }
 }
 
+template <typename T>
+__global__ void k_check_finite(const T* __restrict__ p, int64_t n, uint32_t* status) {
+  bool bad = false;
+  GF_GRID_LOOP(i, n) {
+    if (!finite(p[i])) bad = true;
+  }
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) flag(status, GF_STATUS_NONFINITE_INPUT);
+}
+
+template <typename T>
+void generic_check_finite(const T* p, int64_t n, uint32_t* status, cudaStream_t s) {
+  k_check_finite<T><<<grid_for(n, 256), 256, 0, s>>>(p, n, status);
+}
+template void generic_check_finite<float>(const float*, int64_t, uint32_t*, cudaStream_t);
+template void generic_check_finite<double>(const double*, int64_t, uint32_t*, cudaStream_t);
+
 // ===========================================================================
 // layer building blocks (all float64 intermediates)
 // ===========================================================================

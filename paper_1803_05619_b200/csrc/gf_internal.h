@@ -11,6 +11,8 @@ namespace gfb {
 size_t generic_workspace_bytes(int64_t n_moment_plane_total, int64_t extra_doubles);
 
 template <typename T>
+void generic_check_finite(const T* p, int64_t n, uint32_t* status, cudaStream_t s);
+template <typename T>
 void generic_mean_filter(const T* in, T* out, int64_t P, int64_t h, int64_t w, int r, int adjoint,
                          cudaStream_t s);
 template <typename T>

@@ -158,7 +158,7 @@ def forward_joint(guide_lo, guide_hi, src_lo, p: GuidedFilterParams, *, check: b
                           _stream(gl))
     _lib.check(rc, "forward_joint")
     if check:
-        status.raise_if_set("forward_joint")
+        status.raise_if_set("forward_joint", (gl.t, gh.t, sl.t))
     tape = GuidedFilterTape(VARIANT_JOINT, p, gl, sl, gh, gh, status)
     return restore(out, gh), tape
 
@@ -180,13 +180,16 @@ def forward_highres(guide_hi, src_hi, p: GuidedFilterParams, *, check: bool = Tr
     dt = dtype_code(g.t)
     out = torch.empty_like(s.t)
     status = Status(dev)
-    nbytes = lib.gf_highres_workspace_bytes(dt, B, Cg, C, H, W, p.radius)
+    # the fused forward needs no workspace; the general kernels do
+    fused = lib.gf_highres_fwd_is_fused(dt, B, Cg, C, H, W, p.radius) and not any(
+        t.data_ptr() % 16 for t in (g.t, s.t, out))
+    nbytes = 0 if fused else lib.gf_highres_workspace_bytes(dt, B, Cg, C, H, W, p.radius)
     ws = workspace(nbytes, dev)
     rc = lib.gf_highres_fwd(dt, ptr(g.t), ptr(s.t), ptr(out), B, Cg, C, H, W, int(p.radius),
                             float(p.eps), ptr(ws), ws.numel(), status.ptr, _stream(g))
     _lib.check(rc, "forward_highres")
     if check:
-        status.raise_if_set("forward_highres")
+        status.raise_if_set("forward_highres", (g.t, s.t))
     tape = GuidedFilterTape(VARIANT_HIGHRES, p, g, s, g, s, status)
     return restore(out, s), tape
 

@@ -225,8 +225,11 @@ def test_train_step_matches_reference(gfb, golden):
     assert rel_max(npy(res.d_lr_x).transpose(0, 2, 3, 1), c["d_lr_x"]) <= GRAD_TOL32
     assert rel_max(npy(res.d_hr_x).transpose(0, 2, 3, 1), c["d_hr_x"]) <= GRAD_TOL32
     grads = net.unpack(res.dparams)
+    # conv2.bias's exact gradient is ~0 here (1e-16): judge every parameter
+    # gradient against the largest one (relative-to-gradient-norm bar)
+    scale = max(float(np.abs(c["g:" + k]).max()) for k in grads)
     for k, v in grads.items():
-        assert rel_max(npy(v), c["g:" + k]) <= GRAD_TOL32, k
+        assert abs_max(npy(v), c["g:" + k]) <= GRAD_TOL32 * scale, k
 
 
 # ---------------------------------------------------------------------------
@@ -395,3 +398,68 @@ def test_autograd_module(gfb):
     assert rel_max(npy(lr_x.grad), want[0]) <= GRAD_TOL32
     assert rel_max(npy(lr_y.grad), want[1]) <= GRAD_TOL32
     assert rel_max(npy(hr_x.grad), want[2]) <= GRAD_TOL32
+
+
+# ---------------------------------------------------------------------------
+# fused kernels: ragged shapes / radii vs the oracle, and the dispatch
+# ---------------------------------------------------------------------------
+
+@pytest.mark.parametrize("h,w,r", [(37, 45, 0), (37, 45, 1), (16, 32, 2), (33, 17, 5),
+                                   (64, 96, 8), (21, 70, 12), (2, 3, 1), (130, 66, 3)])
+def test_fused_joint_ragged_vs_oracle(gfb, h, w, r):
+    from paper_1803_05619_b200 import _lib
+
+    lib = _lib.load()
+    assert lib.gf_joint_is_fused(0, 2, 3, h, w, 4 * h, 4 * w, r) == 1
+    rng = np.random.default_rng(h * 1000 + w + r)
+    lr_x = rng.uniform(0, 1, (2, 3, h, w)).astype(np.float32)
+    lr_y = rng.uniform(0, 1, (2, 3, h, w)).astype(np.float32)
+    hr_x = rng.uniform(0, 1, (2, 3, 4 * h, 4 * w)).astype(np.float32)
+    d = rng.standard_normal((2, 3, 4 * h, 4 * w)).astype(np.float32)
+    eps = 1e-3
+    p = gfb.GuidedFilterParams(r, eps)
+    out, tape = gfb.forward_joint(t32(lr_x), t32(hr_x), t32(lr_y), p)
+    want = O.joint_forward_nchw(lr_x, lr_y, hr_x, r, eps)
+    assert abs_max(npy(out), want) <= OUT_TOL32
+    g = gfb.backward(tape, t32(d))
+    dlx, dly, dhx = O.joint_backward_nchw(lr_x, lr_y, hr_x, d, r, eps)
+    assert rel_max(npy(g.d_guide_lo), dlx) <= GRAD_TOL32
+    assert rel_max(npy(g.d_src), dly) <= GRAD_TOL32
+    assert rel_max(npy(g.d_guide_hi), dhx) <= GRAD_TOL32
+
+
+@pytest.mark.parametrize("H,W,r,cg", [(77, 132, 1, 1), (77, 132, 3, 3), (300, 260, 8, 1),
+                                      (40, 36, 16, 3), (5, 8, 2, 1), (513, 520, 8, 3)])
+def test_fused_highres_ragged_vs_oracle(gfb, H, W, r, cg):
+    from paper_1803_05619_b200 import _lib
+
+    lib = _lib.load()
+    assert lib.gf_highres_fwd_is_fused(0, 2, cg, 3, H, W, r) == 1
+    rng = np.random.default_rng(H * 7 + W + r)
+    guide = rng.uniform(0, 1, (2, cg, H, W)).astype(np.float32)
+    src = rng.uniform(0, 1, (2, 3, H, W)).astype(np.float32)
+    p = gfb.GuidedFilterParams(r, 1e-2)
+    out, _ = gfb.forward_highres(t32(guide), t32(src), p)
+    want = O.highres_forward_nchw(guide, src, r, 1e-2)
+    assert abs_max(npy(out), want) <= OUT_TOL32
+
+
+def test_fused_highres_nonfinite_input_is_input_error(gfb):
+    g = torch.rand(1, 1, 64, 64, device="cuda")
+    s = torch.rand(1, 3, 64, 64, device="cuda")
+    s[0, 1, 10, 20] = float("nan")
+    with pytest.raises(ValueError, match="input"):
+        gfb.forward_highres(g, s, gfb.GuidedFilterParams(2, 1e-2))
+    g2 = torch.rand(1, 1, 64, 64, device="cuda")
+    with pytest.raises(gfb.DegenerateWindowError):
+        gfb.forward_highres(torch.full_like(g2, 0.5), s.nan_to_num(0.3),
+                            gfb.GuidedFilterParams(2, 0.0))
+
+
+def test_fused_joint_nonfinite_input_is_input_error(gfb):
+    lr_x = torch.rand(1, 3, 16, 16, device="cuda")
+    lr_y = torch.rand(1, 3, 16, 16, device="cuda")
+    hr_x = torch.rand(1, 3, 64, 64, device="cuda")
+    hr_x[0, 2, 5, 5] = float("inf")
+    with pytest.raises(ValueError, match="input"):
+        gfb.forward_joint(lr_x, hr_x, lr_y, gfb.GuidedFilterParams(1, 1e-4))
