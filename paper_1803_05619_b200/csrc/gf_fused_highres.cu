@@ -14,15 +14,16 @@
 //   H2  horizontal sums (runs of K2=4), Ah = M(A), bh = M(b),
 //       out = Ah*G + bh with 128-bit loads of G and 128-bit stores of out.
 //
+// Shared-memory rows read by the sliding runs are stored with one pad word
+// every K columns, so the lanes of a warp (one run each, stride K) hit
+// distinct banks.  The radius is a template parameter (1..16) so every
+// window loop is unrolled.
+//
 // Windows are clamped to the image and normalised by the true count
 // N = ny*nx (gf/filters.py:82-103): out-of-image rows/columns contribute 0.
 // g and s are shifted by a per-CTA constant (var/cov are shift invariant) to
 // keep the fp32 sums small; running sums restart for every segment, so their
 // rounding error is bounded by the segment length, not the image size.
-//
-// Arithmetic per output pixel is ~150 instructions: this kernel is balanced
-// between the SM issue rate and HBM (28 compulsory bytes/pixel for a 1-channel
-// guide); see DESIGN.md.
 #include <cuda_runtime.h>
 
 #include "gf_common.cuh"
@@ -35,34 +36,37 @@ constexpr int R = 8;     // rows per batch
 constexpr int TX = 256;  // output columns per work item
 constexpr int K1 = 8;    // H1 run length
 constexpr int K2 = 4;    // H2 run length (one float4)
-constexpr int kMaxRadius = 16;  // nt = 256 + 4r <= 320 threads, 2 CTAs/SM
+constexpr int kMaxRadius = 16;  // nt = 256 + 4r <= 320 threads
 
-struct Geo {
-  int r, W1, W2, nq1, vsw, ring, ringw, nt;
-  size_t smem_bytes;
-};
-
-__host__ __device__ inline Geo geometry(int r) {
-  Geo g;
-  g.r = r;
-  g.W2 = TX + 2 * r;                  // coefficient columns
-  g.nq1 = (g.W2 + K1 - 1) / K1;       // H1 runs per row
-  g.vsw = g.nq1 * K1 + 2 * r;         // vs row width (>= TX + 4r, zero padded)
-  g.W1 = TX + 4 * r;                  // real input columns
-  g.ring = 2 * r + 1 + R;             // coefficient rows kept
-  g.ringw = g.nq1 * K1;               // ring row width (>= W2)
-  g.nt = ((g.vsw > g.ringw ? g.vsw : g.ringw) + 31) / 32 * 32;
-  g.smem_bytes = sizeof(float) * ((size_t)R * 4 * g.vsw + (size_t)g.ring * 2 * g.ringw +
-                                  (size_t)R * 2 * (TX + 2 * r));
-  return g;
+// padded position of column x in a row read by runs of length K
+template <int K>
+__host__ __device__ constexpr int padpos(int x) {
+  return x + x / K;
 }
+
+template <int RAD>
+struct Geo {
+  static constexpr int W2 = TX + 2 * RAD;              // coefficient columns
+  static constexpr int nq1 = (W2 + K1 - 1) / K1;       // H1 runs per row
+  static constexpr int vsw = nq1 * K1 + 2 * RAD;       // vs columns (>= TX + 4r)
+  static constexpr int vsp = padpos<K1>(vsw) + 1;      // padded vs row pitch
+  static constexpr int W1 = TX + 4 * RAD;              // real input columns
+  static constexpr int ring = 2 * RAD + 1 + R;         // coefficient rows kept
+  static constexpr int ringw = nq1 * K1;               // >= W2
+  static constexpr int ringp = padpos<K1>(ringw) + 1;  // padded ring pitch
+  static constexpr int v2p = padpos<K2>(W2) + 1;       // padded vs2 pitch
+  static constexpr int nt = ((vsw > ringw ? vsw : ringw) + 31) / 32 * 32;
+  static constexpr size_t smem_floats =
+      (size_t)R * 4 * vsp + (size_t)ring * 2 * ringp + (size_t)R * 2 * v2p;
+  static constexpr size_t smem_bytes = smem_floats * sizeof(float);
+};
 
 struct Args {
   const float* guide;
   const float* src;
   float* out;
   int64_t C, Cg, H, W;
-  int r, TY, strips, segs;
+  int TY, strips, segs;
   float eps;
   uint32_t* status;
 };
@@ -73,17 +77,19 @@ __device__ __forceinline__ int wlen(int i, int n, int r) {
   return b - a + 1;
 }
 
+template <int RAD>
 __global__ void __launch_bounds__(320, 2) k_highres_fused(Args a) {
+  using GG = Geo<RAD>;
+  constexpr int r = RAD;
   extern __shared__ float4 smem4[];
   float* smem = reinterpret_cast<float*>(smem4);
-  const Geo geo = geometry(a.r);
-  const int r = a.r;
   const int H = (int)a.H, W = (int)a.W;
-  const int tid = threadIdx.x, nt = blockDim.x;
+  const int tid = threadIdx.x;
+  constexpr int nt = GG::nt;
 
-  float* vs = smem;                                // [R][4][vsw]
-  float* ring = vs + R * 4 * geo.vsw;              // [ring][2][ringw]
-  float* vs2 = ring + geo.ring * 2 * geo.ringw;    // [R][2][W2]
+  float* vs = smem;                              // [R][4][vsp]      (padded by K1)
+  float* ring = vs + R * 4 * GG::vsp;            // [ring][2][ringp] (padded by K1)
+  float* vs2 = ring + GG::ring * 2 * GG::ringp;  // [R][2][v2p]      (padded by K2)
 
   // work item: plane fastest (the C planes sharing a guide run together)
   int64_t item = blockIdx.x;
@@ -104,21 +110,23 @@ __global__ void __launch_bounds__(320, 2) k_highres_fused(Args a) {
 
   const float sG = __ldg(G + (int64_t)y0 * W + x0);
   const float sS = __ldg(S + (int64_t)y0 * W + x0);
+  const float eps = a.eps;
 
-  for (int i = tid; i < geo.ring * 2 * geo.ringw; i += nt) ring[i] = 0.f;
+  for (int i = tid; i < GG::ring * 2 * GG::ringp; i += nt) ring[i] = 0.f;
 
   // ---- level-1 column state: thread = input column xi -------------------
   const int xi = tid;
   const int gx = x0 - 2 * r + xi;
-  const bool col_ok = xi < geo.W1 && gx >= 0 && gx < W;
+  const bool col_ok = xi < GG::W1 && gx >= 0 && gx < W;
+  const int vpos = padpos<K1>(xi);
   float s_g = 0.f, s_gg = 0.f, s_s = 0.f, s_gs = 0.f;
-  const int ya0 = y0 - r;                  // first coefficient row
-  const int nrows = (yend - y0) + 2 * r;   // coefficient rows of this item
-  const int first_add = y0 - 2 * r;        // first input row ever added
+  const int ya0 = y0 - r;                 // first coefficient row
+  const int nrows = (yend - y0) + 2 * r;  // coefficient rows of this item
+  const int first_add = y0 - 2 * r;       // first input row ever added
   if (col_ok) {
     for (int y = max(first_add, 0); y < min(y0, H); ++y) {
-      float g = __ldg(G + (int64_t)y * W + gx) - sG;
-      float s = __ldg(S + (int64_t)y * W + gx) - sS;
+      const float g = __ldg(G + (int64_t)y * W + gx) - sG;
+      const float s = __ldg(S + (int64_t)y * W + gx) - sS;
       s_g += g;
       s_gg += g * g;
       s_s += s;
@@ -127,11 +135,15 @@ __global__ void __launch_bounds__(320, 2) k_highres_fused(Args a) {
   }
   // ---- level-2 column state: thread = coefficient column ----------------
   float a_sum = 0.f, b_sum = 0.f;
+  const int rpos = padpos<K1>(tid);
+  const int v2pos = padpos<K2>(tid);
   bool bad = false, degen = false;
+  int ring_new = 0;                     // ring slot of coefficient row `base`
+  int ring_old = GG::ring - 2 * r - 1;  // slot of row base - 2r - 1 (mod ring)
 
   for (int base = 0; base < nrows; base += R) {
     // ------------------------------ V1 --------------------------------
-    if (xi < geo.vsw) {
+    if (xi < GG::vsw) {
       float ge[R], se[R], gl[R], sl[R];
 #pragma unroll
       for (int j = 0; j < R; ++j) {
@@ -155,85 +167,95 @@ __global__ void __launch_bounds__(320, 2) k_highres_fused(Args a) {
         s_gg += ge[j] * ge[j] - gl[j] * gl[j];
         s_s += se[j] - sl[j];
         s_gs += ge[j] * se[j] - gl[j] * sl[j];
-        float* row = vs + j * 4 * geo.vsw;
-        row[xi] = col_ok ? s_g : 0.f;
-        row[geo.vsw + xi] = col_ok ? s_gg : 0.f;
-        row[2 * geo.vsw + xi] = col_ok ? s_s : 0.f;
-        row[3 * geo.vsw + xi] = col_ok ? s_gs : 0.f;
+        float* row = vs + j * 4 * GG::vsp + vpos;
+        row[0] = col_ok ? s_g : 0.f;
+        row[GG::vsp] = col_ok ? s_gg : 0.f;
+        row[2 * GG::vsp] = col_ok ? s_s : 0.f;
+        row[3 * GG::vsp] = col_ok ? s_gs : 0.f;
       }
     }
     __syncthreads();
 
     // ------------------------------ H1 --------------------------------
-    for (int it = tid; it < R * geo.nq1; it += nt) {
-      const int j = it / geo.nq1, q = it - j * geo.nq1;
+    for (int it = tid; it < R * GG::nq1; it += nt) {
+      const int j = it / GG::nq1, q = it - j * GG::nq1;
       if (base + j >= nrows) continue;
       const int ya = ya0 + base + j;
       const int xa0 = q * K1;
-      float* rrow = ring + ((base + j) % geo.ring) * 2 * geo.ringw;
-      const bool row_ok = ya >= 0 && ya < H;
-      if (!row_ok) {
+      int slot = ring_new + j;
+      if (slot >= GG::ring) slot -= GG::ring;
+      float* rrow = ring + slot * 2 * GG::ringp + q * (K1 + 1);
+      if (ya < 0 || ya >= H) {
 #pragma unroll
-        for (int k = 0; k < K1; ++k) rrow[xa0 + k] = rrow[geo.ringw + xa0 + k] = 0.f;
+        for (int k = 0; k < K1; ++k) rrow[k] = rrow[GG::ringp + k] = 0.f;
         continue;
       }
-      const float* v = vs + j * 4 * geo.vsw + xa0;
-      float sg = 0.f, sgg = 0.f, ss = 0.f, sgs = 0.f;
-      for (int d = 0; d < 2 * r; ++d) {
-        sg += v[d];
-        sgg += v[geo.vsw + d];
-        ss += v[2 * geo.vsw + d];
-        sgs += v[3 * geo.vsw + d];
+      // run window: vs columns [xa0, xa0 + K1 + 2r) at padded positions;
+      // one field at a time keeps the live window to K1 + 2r registers
+      const float* v = vs + j * 4 * GG::vsp;
+      float hs[4][K1];
+#pragma unroll
+      for (int f = 0; f < 4; ++f) {
+        float w[K1 + 2 * r];
+#pragma unroll
+        for (int d = 0; d < K1 + 2 * r; ++d) w[d] = v[f * GG::vsp + padpos<K1>(xa0 + d)];
+        float acc = 0.f;
+#pragma unroll
+        for (int d = 0; d < 2 * r; ++d) acc += w[d];
+#pragma unroll
+        for (int k = 0; k < K1; ++k) {
+          acc += w[k + 2 * r];
+          hs[f][k] = acc;
+          acc -= w[k];
+        }
       }
       const float ny = (float)wlen(ya, H, r);
 #pragma unroll
       for (int k = 0; k < K1; ++k) {
-        const int d = k + 2 * r;
-        sg += v[d];
-        sgg += v[geo.vsw + d];
-        ss += v[2 * geo.vsw + d];
-        sgs += v[3 * geo.vsw + d];
+        const float sg = hs[0][k], sgg = hs[1][k], ss = hs[2][k], sgs = hs[3][k];
         const int gxa = x0 - r + xa0 + k;
         float A = 0.f, B = 0.f;
-        if (xa0 + k < geo.W2 && gxa >= 0 && gxa < W) {
+        if (xa0 + k < GG::W2 && gxa >= 0 && gxa < W) {
           const float inv = __frcp_rn(ny * (float)wlen(gxa, W, r));
           const float mg = sg * inv, ms = ss * inv;
           const float var = sgg * inv - mg * mg;
           const float cov = sgs * inv - mg * ms;
-          if (a.eps == 0.f && !(var > 0.f)) degen = true;
-          A = cov * __frcp_rn(var + a.eps);
+          if (eps == 0.f && !(var > 0.f)) degen = true;
+          A = cov * __frcp_rn(var + eps);
           B = (ms + sS) - A * (mg + sG);
         }
-        rrow[xa0 + k] = A;
-        rrow[geo.ringw + xa0 + k] = B;
-        sg -= v[k];
-        sgg -= v[geo.vsw + k];
-        ss -= v[2 * geo.vsw + k];
-        sgs -= v[3 * geo.vsw + k];
+        rrow[k] = A;
+        rrow[GG::ringp + k] = B;
       }
     }
     __syncthreads();
 
     // ------------------------------ V2 --------------------------------
-    if (tid < geo.W2) {
+    if (tid < GG::W2) {
 #pragma unroll
       for (int j = 0; j < R; ++j) {
         const int loc = base + j;
         if (loc < nrows) {
-          const float* rn = ring + (loc % geo.ring) * 2 * geo.ringw;
-          a_sum += rn[tid];
-          b_sum += rn[geo.ringw + tid];
-          const int old = loc - 2 * r - 1;
-          if (old >= 0) {
-            const float* ro = ring + (old % geo.ring) * 2 * geo.ringw;
-            a_sum -= ro[tid];
-            b_sum -= ro[geo.ringw + tid];
+          int sn = ring_new + j, so = ring_old + j;
+          if (sn >= GG::ring) sn -= GG::ring;
+          if (so >= GG::ring) so -= GG::ring;
+          const float* rn = ring + sn * 2 * GG::ringp + rpos;
+          a_sum += rn[0];
+          b_sum += rn[GG::ringp];
+          if (loc - 2 * r - 1 >= 0) {
+            const float* ro = ring + so * 2 * GG::ringp + rpos;
+            a_sum -= ro[0];
+            b_sum -= ro[GG::ringp];
           }
         }
-        vs2[j * 2 * geo.W2 + tid] = a_sum;
-        vs2[j * 2 * geo.W2 + geo.W2 + tid] = b_sum;
+        vs2[j * 2 * GG::v2p + v2pos] = a_sum;
+        vs2[j * 2 * GG::v2p + GG::v2p + v2pos] = b_sum;
       }
     }
+    ring_new += R;
+    if (ring_new >= GG::ring) ring_new -= GG::ring;
+    ring_old += R;
+    if (ring_old >= GG::ring) ring_old -= GG::ring;
     __syncthreads();
 
     // ------------------------------ H2 --------------------------------
@@ -245,37 +267,80 @@ __global__ void __launch_bounds__(320, 2) k_highres_fused(Args a) {
       const int xo0 = q * K2;
       const int gxo = x0 + xo0;
       if (gxo >= W) continue;
-      const float* va = vs2 + j * 2 * geo.W2 + xo0;
-      const float* vb = va + geo.W2;
+      const float4 g4 = __ldg(reinterpret_cast<const float4*>(G + (int64_t)yo * W + gxo));
+      const float* va = vs2 + j * 2 * GG::v2p;
+      const float* vb = va + GG::v2p;
+      float wa[K2 + 2 * r], wb[K2 + 2 * r];
+#pragma unroll
+      for (int d = 0; d < K2 + 2 * r; ++d) {
+        const int pp = padpos<K2>(xo0 + d);
+        wa[d] = va[pp];
+        wb[d] = vb[pp];
+      }
       float sa = 0.f, sb = 0.f;
+#pragma unroll
       for (int d = 0; d < 2 * r; ++d) {
-        sa += va[d];
-        sb += vb[d];
+        sa += wa[d];
+        sb += wb[d];
       }
       const float ny = (float)wlen(yo, H, r);
-      const float4 g4 = __ldg(reinterpret_cast<const float4*>(G + (int64_t)yo * W + gxo));
       const float gv[4] = {g4.x, g4.y, g4.z, g4.w};
       float ov[4];
 #pragma unroll
       for (int k = 0; k < K2; ++k) {
-        sa += va[k + 2 * r];
-        sb += vb[k + 2 * r];
+        sa += wa[k + 2 * r];
+        sb += wb[k + 2 * r];
         const float inv = __frcp_rn(ny * (float)wlen(gxo + k, W, r));
         ov[k] = (sa * inv) * gv[k] + sb * inv;
         if (!isfinite(ov[k])) bad = true;
-        sa -= va[k];
-        sb -= vb[k];
+        sa -= wa[k];
+        sb -= wb[k];
       }
-      *reinterpret_cast<float4*>(O + (int64_t)yo * W + gxo) = make_float4(ov[0], ov[1], ov[2], ov[3]);
+      *reinterpret_cast<float4*>(O + (int64_t)yo * W + gxo) =
+          make_float4(ov[0], ov[1], ov[2], ov[3]);
     }
-    // the next batch's V1 only touches vs (last read in H1, before a barrier)
-    // and H1 writes ring rows no V2 of this batch reads
+    // next batch: V1 writes vs (last read by H1, before the V2 barrier); H1
+    // writes ring rows this batch's V2 no longer needs; V2 writes vs2 only
+    // after the next H1 barrier.
   }
   // Non-finite inputs are not tested per element here: they always poison
   // the output at their own pixel, so the host (gf_check_finite) classifies
   // an OUTPUT flag as an input error when the inputs are non-finite.
   if (degen) flag(a.status, GF_STATUS_DEGENERATE);
   if (bad) flag(a.status, GF_STATUS_NONFINITE_OUTPUT);
+}
+
+struct Launch {
+  const void* fn;
+  int nt;
+  size_t smem;
+};
+
+template <int RAD>
+Launch launch_info() {
+  return {(const void*)k_highres_fused<RAD>, Geo<RAD>::nt, Geo<RAD>::smem_bytes};
+}
+
+Launch pick(int r) {
+  switch (r) {
+    case 1: return launch_info<1>();
+    case 2: return launch_info<2>();
+    case 3: return launch_info<3>();
+    case 4: return launch_info<4>();
+    case 5: return launch_info<5>();
+    case 6: return launch_info<6>();
+    case 7: return launch_info<7>();
+    case 8: return launch_info<8>();
+    case 9: return launch_info<9>();
+    case 10: return launch_info<10>();
+    case 11: return launch_info<11>();
+    case 12: return launch_info<12>();
+    case 13: return launch_info<13>();
+    case 14: return launch_info<14>();
+    case 15: return launch_info<15>();
+    case 16: return launch_info<16>();
+    default: return {nullptr, 0, 0};
+  }
 }
 
 }  // namespace hrf
@@ -285,53 +350,50 @@ bool fused_highres_fwd_ok(int64_t B, int64_t Cg, int64_t C, int64_t H, int64_t W
   if (W % 4 != 0 || W < 4 || H < 1) return false;
   if (H > (1 << 30) || W > (1 << 30) || H * W > ((int64_t)1 << 40)) return false;
   if (Cg != 1 && Cg != C) return false;
-  if (hrf::geometry(r).smem_bytes > 227 * 1024) return false;
+  if (hrf::pick(r).smem > 227 * 1024) return false;
   return B >= 1 && C >= 1;
 }
 
 void fused_highres_fwd(const float* guide, const float* src, float* out, int64_t B, int64_t Cg,
                        int64_t C, int64_t H, int64_t W, int r, float eps, uint32_t* status,
                        cudaStream_t s) {
-  const hrf::Geo geo = hrf::geometry(r);
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(hrf::k_highres_fused, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         227 * 1024);
-    configured = true;
-  }
-  // resident CTAs per SM for this radius (cached: the query costs microseconds)
-  static int cached_r = -1, cached_per_sm = 1, cached_sms = 148;
-  if (cached_r != r) {
+  const hrf::Launch L = hrf::pick(r);
+  // per-radius launch configuration, cached (the queries cost microseconds)
+  static int per_sm_cache[hrf::kMaxRadius + 1] = {0};
+  static int sms = 0;
+  if (per_sm_cache[r] == 0) {
     int dev = 0;
     cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&cached_sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&cached_per_sm, hrf::k_highres_fused, geo.nt,
-                                                  geo.smem_bytes);
-    if (cached_per_sm < 1) cached_per_sm = 1;
-    cached_r = r;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaFuncSetAttribute(L.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.smem);
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, L.fn, L.nt, L.smem);
+    per_sm_cache[r] = per_sm < 1 ? 1 : per_sm;
   }
-  const int sms = cached_sms, per_sm = cached_per_sm;
   const int64_t strips = (W + hrf::TX - 1) / hrf::TX;
   const int64_t planes = B * C;
-  const int64_t slots = (int64_t)sms * per_sm;
-  // segments per column: fill whole waves, keep segments <= 512 rows so the
-  // running-sum rounding stays bounded
-  int64_t segs = (slots + planes * strips - 1) / (planes * strips);
-  if (segs < 1) segs = 1;
-  int64_t min_segs = (H + 511) / 512;
-  if (segs < min_segs) {
-    // round up to a whole number of waves
-    int64_t items = planes * strips * min_segs;
-    int64_t waves = (items + slots - 1) / slots;
-    segs = (waves * slots + planes * strips - 1) / (planes * strips);
+  const int64_t slots = (int64_t)sms * per_sm_cache[r];
+  // choose the row segmentation: minimise waves x (rows per item incl. the
+  // 4r warm-up rows), with segments of at most 1024 rows (bounded rounding)
+  int64_t best_segs = 1;
+  double best_cost = 1e300;
+  const int64_t max_segs = H / (2 * r + 1) > 0 ? H / (2 * r + 1) : 1;
+  for (int64_t sg = (H + 1023) / 1024; sg <= max_segs && sg <= 4096; ++sg) {
+    const int64_t ty = (H + sg - 1) / sg;
+    const int64_t items = planes * strips * ((H + ty - 1) / ty);
+    const int64_t waves = (items + slots - 1) / slots;
+    const double cost = (double)waves * (double)(ty + 4 * r);
+    if (cost < best_cost * 0.999) {
+      best_cost = cost;
+      best_segs = sg;
+    }
   }
-  if (segs > H) segs = H;
-  int64_t TY = (H + segs - 1) / segs;
-  if (TY < 2 * r + 1 && H > 2 * r + 1) TY = 2 * r + 1;
-  segs = (H + TY - 1) / TY;
-  hrf::Args a{guide, src, out, C, Cg, H, W, r, (int)TY, (int)strips, (int)segs, eps, status};
+  const int64_t TY = (H + best_segs - 1) / best_segs;
+  const int64_t segs = (H + TY - 1) / TY;
+  hrf::Args a{guide, src, out, C, Cg, H, W, (int)TY, (int)strips, (int)segs, eps, status};
   const int64_t grid = planes * strips * segs;
-  hrf::k_highres_fused<<<(unsigned)grid, geo.nt, geo.smem_bytes, s>>>(a);
+  void* args[] = {&a};
+  cudaLaunchKernel(L.fn, dim3((unsigned)grid), dim3(L.nt), args, L.smem, s);
 }
 
 }  // namespace gfb
