@@ -20,6 +20,14 @@ __device__ __forceinline__ bool finite(T v) {
   return isfinite(v);
 }
 
+// One MUFU.RCP (<= 1 ulp): the fp32 kernels' reciprocal of window counts and
+// of var + eps, where the IEEE-rounded __frcp_rn costs a dozen instructions.
+__device__ __forceinline__ float fast_rcp(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
 // ---------------------------------------------------------------------------
 // gf/filters.py:82-93 window_counts: per-axis clamped window length.
 // ---------------------------------------------------------------------------

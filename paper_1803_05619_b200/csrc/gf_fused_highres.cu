@@ -9,15 +9,15 @@
 //       column, registers; the leaving row is re-read from L2)      -> smem vs
 //   H1  horizontal window sums (sliding runs of K1 columns), window means,
 //       var, cov, A = cov/(var+eps), b = mean_s - A*mean_g           -> smem ring
-//   V2  vertical running sums of A and b over the ring of the last
-//       2r+1+R coefficient rows (thread per coefficient column)      -> smem vs2
-//   H2  horizontal sums (runs of K2=4), Ah = M(A), bh = M(b),
+//   V2  vertical running sums of A and b over a ring of the last 2r+1
+//       coefficient rows (thread per coefficient column; the rows leaving
+//       the window are read before H1 overwrites their slots)        -> smem vs2
+//   H2  horizontal sums (runs of K2=8), Ah = M(A), bh = M(b),
 //       out = Ah*G + bh with 128-bit loads of G and 128-bit stores of out.
 //
-// Shared-memory rows read by the sliding runs are stored with one pad word
-// every K columns, so the lanes of a warp (one run each, stride K) hit
-// distinct banks.  The radius is a template parameter (1..16) so every
-// window loop is unrolled.
+// H1/H2 map a warp to 8 rows x 4 runs and every shared row pitch is
+// = 1 (mod 32), so the 32 lanes of a run step hit 32 distinct banks.  The
+// radius is a template parameter (1..16) so every window loop is unrolled.
 //
 // Windows are clamped to the image and normalised by the true count
 // N = ny*nx (gf/filters.py:82-103): out-of-image rows/columns contribute 0.
@@ -35,29 +35,27 @@ namespace hrf {
 constexpr int R = 8;     // rows per batch
 constexpr int TX = 256;  // output columns per work item
 constexpr int K1 = 8;    // H1 run length
-constexpr int K2 = 4;    // H2 run length (one float4)
+constexpr int K2 = 8;    // H2 run length (two float4)
 constexpr int kMaxRadius = 16;  // nt = 256 + 4r <= 320 threads
 
-// padded position of column x in a row read by runs of length K
-template <int K>
-__host__ __device__ constexpr int padpos(int x) {
-  return x + x / K;
-}
+// Row pitches are = 1 (mod 32): a warp's 32 runs (8 rows x 4 runs of 8
+// columns) then touch 32 distinct banks at every step of the run.
+__host__ __device__ constexpr int pitch1(int n) { return n + ((33 - n % 32) % 32); }
 
 template <int RAD>
 struct Geo {
-  static constexpr int W2 = TX + 2 * RAD;              // coefficient columns
-  static constexpr int nq1 = (W2 + K1 - 1) / K1;       // H1 runs per row
-  static constexpr int vsw = nq1 * K1 + 2 * RAD;       // vs columns (>= TX + 4r)
-  static constexpr int vsp = padpos<K1>(vsw) + 1;      // padded vs row pitch
-  static constexpr int W1 = TX + 4 * RAD;              // real input columns
-  static constexpr int ring = 2 * RAD + 1 + R;         // coefficient rows kept
-  static constexpr int ringw = nq1 * K1;               // >= W2
-  static constexpr int ringp = padpos<K1>(ringw) + 1;  // padded ring pitch
-  static constexpr int v2p = padpos<K2>(W2) + 1;       // padded vs2 pitch
+  static constexpr int W2 = TX + 2 * RAD;          // coefficient columns
+  static constexpr int nq1 = (W2 + K1 - 1) / K1;   // H1 runs per row
+  static constexpr int vsw = nq1 * K1 + 2 * RAD;   // vs columns (>= TX + 4r)
+  static constexpr int P1 = pitch1(vsw);
+  static constexpr int W1 = TX + 4 * RAD;          // real input columns
+  static constexpr int ringN = 2 * RAD + 1;        // coefficient rows kept
+  static constexpr int ringw = nq1 * K1;           // >= W2
+  static constexpr int Pr = pitch1(ringw);
+  static constexpr int P2 = pitch1(W2);
   static constexpr int nt = ((vsw > ringw ? vsw : ringw) + 31) / 32 * 32;
   static constexpr size_t smem_floats =
-      (size_t)R * 4 * vsp + (size_t)ring * 2 * ringp + (size_t)R * 2 * v2p;
+      (size_t)4 * R * P1 + (size_t)2 * ringN * Pr + (size_t)2 * R * P2;
   static constexpr size_t smem_bytes = smem_floats * sizeof(float);
 };
 
@@ -84,12 +82,12 @@ __global__ void __launch_bounds__(320, 2) k_highres_fused(Args a) {
   extern __shared__ float4 smem4[];
   float* smem = reinterpret_cast<float*>(smem4);
   const int H = (int)a.H, W = (int)a.W;
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr int nt = GG::nt;
 
-  float* vs = smem;                              // [R][4][vsp]      (padded by K1)
-  float* ring = vs + R * 4 * GG::vsp;            // [ring][2][ringp] (padded by K1)
-  float* vs2 = ring + GG::ring * 2 * GG::ringp;  // [R][2][v2p]      (padded by K2)
+  float* vs = smem;                        // [4 fields][R rows][P1]
+  float* ring = vs + 4 * R * GG::P1;       // [2 fields][ringN slots][Pr]
+  float* vs2 = ring + 2 * GG::ringN * GG::Pr;  // [2 fields][R rows][P2]
 
   // work item: plane fastest (the C planes sharing a guide run together)
   int64_t item = blockIdx.x;
@@ -112,13 +110,12 @@ __global__ void __launch_bounds__(320, 2) k_highres_fused(Args a) {
   const float sS = __ldg(S + (int64_t)y0 * W + x0);
   const float eps = a.eps;
 
-  for (int i = tid; i < GG::ring * 2 * GG::ringp; i += nt) ring[i] = 0.f;
+  for (int i = tid; i < 2 * GG::ringN * GG::Pr; i += nt) ring[i] = 0.f;
 
   // ---- level-1 column state: thread = input column xi -------------------
   const int xi = tid;
   const int gx = x0 - 2 * r + xi;
   const bool col_ok = xi < GG::W1 && gx >= 0 && gx < W;
-  const int vpos = padpos<K1>(xi);
   float s_g = 0.f, s_gg = 0.f, s_s = 0.f, s_gs = 0.f;
   const int ya0 = y0 - r;                 // first coefficient row
   const int nrows = (yend - y0) + 2 * r;  // coefficient rows of this item
@@ -135,14 +132,25 @@ __global__ void __launch_bounds__(320, 2) k_highres_fused(Args a) {
   }
   // ---- level-2 column state: thread = coefficient column ----------------
   float a_sum = 0.f, b_sum = 0.f;
-  const int rpos = padpos<K1>(tid);
-  const int v2pos = padpos<K2>(tid);
   bool bad = false, degen = false;
-  int ring_new = 0;                     // ring slot of coefficient row `base`
-  int ring_old = GG::ring - 2 * r - 1;  // slot of row base - 2r - 1 (mod ring)
+  int ring_new = 0;  // ring slot of coefficient row `base` (mod 2r+1)
+
+  // run mapping shared by H1 and H2: lane -> (row j = lane % 8, run q)
+  const int jl = lane & 7;
+  const int ql = lane >> 3;
 
   for (int base = 0; base < nrows; base += R) {
-    // ------------------------------ V1 --------------------------------
+    // --------------------- V1 (+ V2 old-row prefetch) ------------------
+    float old_a[R], old_b[R];
+    if (tid < GG::W2) {
+#pragma unroll
+      for (int j = 0; j < R; ++j) {
+        int sl = ring_new + j;
+        if (sl >= GG::ringN) sl -= GG::ringN;
+        old_a[j] = ring[sl * GG::Pr + tid];
+        old_b[j] = ring[(GG::ringN + sl) * GG::Pr + tid];
+      }
+    }
     if (xi < GG::vsw) {
       float ge[R], se[R], gl[R], sl[R];
 #pragma unroll
@@ -167,38 +175,38 @@ __global__ void __launch_bounds__(320, 2) k_highres_fused(Args a) {
         s_gg += ge[j] * ge[j] - gl[j] * gl[j];
         s_s += se[j] - sl[j];
         s_gs += ge[j] * se[j] - gl[j] * sl[j];
-        float* row = vs + j * 4 * GG::vsp + vpos;
-        row[0] = col_ok ? s_g : 0.f;
-        row[GG::vsp] = col_ok ? s_gg : 0.f;
-        row[2 * GG::vsp] = col_ok ? s_s : 0.f;
-        row[3 * GG::vsp] = col_ok ? s_gs : 0.f;
+        vs[(0 * R + j) * GG::P1 + xi] = col_ok ? s_g : 0.f;
+        vs[(1 * R + j) * GG::P1 + xi] = col_ok ? s_gg : 0.f;
+        vs[(2 * R + j) * GG::P1 + xi] = col_ok ? s_s : 0.f;
+        vs[(3 * R + j) * GG::P1 + xi] = col_ok ? s_gs : 0.f;
       }
     }
     __syncthreads();
 
     // ------------------------------ H1 --------------------------------
-    for (int it = tid; it < R * GG::nq1; it += nt) {
-      const int j = it / GG::nq1, q = it - j * GG::nq1;
-      if (base + j >= nrows) continue;
+    // chunk = warp-sized group of 8 rows x 4 runs
+    for (int ch = warp; ch * 4 < GG::nq1; ch += nt / 32) {
+      const int j = jl, q = ch * 4 + ql;
+      if (q >= GG::nq1 || base + j >= nrows) continue;
       const int ya = ya0 + base + j;
       const int xa0 = q * K1;
       int slot = ring_new + j;
-      if (slot >= GG::ring) slot -= GG::ring;
-      float* rrow = ring + slot * 2 * GG::ringp + q * (K1 + 1);
+      if (slot >= GG::ringN) slot -= GG::ringN;
+      float* ra = ring + slot * GG::Pr + xa0;
+      float* rb = ring + (GG::ringN + slot) * GG::Pr + xa0;
       if (ya < 0 || ya >= H) {
 #pragma unroll
-        for (int k = 0; k < K1; ++k) rrow[k] = rrow[GG::ringp + k] = 0.f;
+        for (int k = 0; k < K1; ++k) ra[k] = rb[k] = 0.f;
         continue;
       }
-      // run window: vs columns [xa0, xa0 + K1 + 2r) at padded positions;
       // one field at a time keeps the live window to K1 + 2r registers
-      const float* v = vs + j * 4 * GG::vsp;
       float hs[4][K1];
 #pragma unroll
       for (int f = 0; f < 4; ++f) {
+        const float* v = vs + (f * R + j) * GG::P1 + xa0;
         float w[K1 + 2 * r];
 #pragma unroll
-        for (int d = 0; d < K1 + 2 * r; ++d) w[d] = v[f * GG::vsp + padpos<K1>(xa0 + d)];
+        for (int d = 0; d < K1 + 2 * r; ++d) w[d] = v[d];
         float acc = 0.f;
 #pragma unroll
         for (int d = 0; d < 2 * r; ++d) acc += w[d];
@@ -212,20 +220,19 @@ __global__ void __launch_bounds__(320, 2) k_highres_fused(Args a) {
       const float ny = (float)wlen(ya, H, r);
 #pragma unroll
       for (int k = 0; k < K1; ++k) {
-        const float sg = hs[0][k], sgg = hs[1][k], ss = hs[2][k], sgs = hs[3][k];
         const int gxa = x0 - r + xa0 + k;
         float A = 0.f, B = 0.f;
         if (xa0 + k < GG::W2 && gxa >= 0 && gxa < W) {
-          const float inv = __frcp_rn(ny * (float)wlen(gxa, W, r));
-          const float mg = sg * inv, ms = ss * inv;
-          const float var = sgg * inv - mg * mg;
-          const float cov = sgs * inv - mg * ms;
+          const float inv = fast_rcp(ny * (float)wlen(gxa, W, r));
+          const float mg = hs[0][k] * inv, ms = hs[2][k] * inv;
+          const float var = hs[1][k] * inv - mg * mg;
+          const float cov = hs[3][k] * inv - mg * ms;
           if (eps == 0.f && !(var > 0.f)) degen = true;
-          A = cov * __frcp_rn(var + eps);
+          A = cov * fast_rcp(var + eps);
           B = (ms + sS) - A * (mg + sG);
         }
-        rrow[k] = A;
-        rrow[GG::ringp + k] = B;
+        ra[k] = A;
+        rb[k] = B;
       }
     }
     __syncthreads();
@@ -234,74 +241,69 @@ __global__ void __launch_bounds__(320, 2) k_highres_fused(Args a) {
     if (tid < GG::W2) {
 #pragma unroll
       for (int j = 0; j < R; ++j) {
-        const int loc = base + j;
-        if (loc < nrows) {
-          int sn = ring_new + j, so = ring_old + j;
-          if (sn >= GG::ring) sn -= GG::ring;
-          if (so >= GG::ring) so -= GG::ring;
-          const float* rn = ring + sn * 2 * GG::ringp + rpos;
-          a_sum += rn[0];
-          b_sum += rn[GG::ringp];
-          if (loc - 2 * r - 1 >= 0) {
-            const float* ro = ring + so * 2 * GG::ringp + rpos;
-            a_sum -= ro[0];
-            b_sum -= ro[GG::ringp];
-          }
+        if (base + j < nrows) {
+          int sn = ring_new + j;
+          if (sn >= GG::ringN) sn -= GG::ringN;
+          a_sum += ring[sn * GG::Pr + tid] - old_a[j];
+          b_sum += ring[(GG::ringN + sn) * GG::Pr + tid] - old_b[j];
         }
-        vs2[j * 2 * GG::v2p + v2pos] = a_sum;
-        vs2[j * 2 * GG::v2p + GG::v2p + v2pos] = b_sum;
+        vs2[(0 * R + j) * GG::P2 + tid] = a_sum;
+        vs2[(1 * R + j) * GG::P2 + tid] = b_sum;
       }
     }
     ring_new += R;
-    if (ring_new >= GG::ring) ring_new -= GG::ring;
-    ring_old += R;
-    if (ring_old >= GG::ring) ring_old -= GG::ring;
+    while (ring_new >= GG::ringN) ring_new -= GG::ringN;
     __syncthreads();
 
     // ------------------------------ H2 --------------------------------
-    constexpr int nq2 = TX / K2;
-    for (int it = tid; it < R * nq2; it += nt) {
-      const int j = it / nq2, q = it - j * nq2;
+    constexpr int nq2 = TX / K2;  // 32 runs per row
+    for (int ch = warp; ch * 4 < nq2; ch += nt / 32) {
+      const int j = jl, q = ch * 4 + ql;
       const int yo = y0 + base + j - 2 * r;
       if (yo < y0 || yo >= yend) continue;
       const int xo0 = q * K2;
       const int gxo = x0 + xo0;
       if (gxo >= W) continue;
-      const float4 g4 = __ldg(reinterpret_cast<const float4*>(G + (int64_t)yo * W + gxo));
-      const float* va = vs2 + j * 2 * GG::v2p;
-      const float* vb = va + GG::v2p;
-      float wa[K2 + 2 * r], wb[K2 + 2 * r];
+      const float* grow = G + (int64_t)yo * W + gxo;
+      const bool two = gxo + 4 < W;
+      const float4 g0 = __ldg(reinterpret_cast<const float4*>(grow));
+      const float4 g1 = two ? __ldg(reinterpret_cast<const float4*>(grow + 4))
+                            : make_float4(0.f, 0.f, 0.f, 0.f);
+      const float gv[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
+      float ha[K2], hb[K2];
 #pragma unroll
-      for (int d = 0; d < K2 + 2 * r; ++d) {
-        const int pp = padpos<K2>(xo0 + d);
-        wa[d] = va[pp];
-        wb[d] = vb[pp];
-      }
-      float sa = 0.f, sb = 0.f;
+      for (int f = 0; f < 2; ++f) {
+        const float* v = vs2 + (f * R + j) * GG::P2 + xo0;
+        float w[K2 + 2 * r];
 #pragma unroll
-      for (int d = 0; d < 2 * r; ++d) {
-        sa += wa[d];
-        sb += wb[d];
+        for (int d = 0; d < K2 + 2 * r; ++d) w[d] = v[d];
+        float acc = 0.f;
+#pragma unroll
+        for (int d = 0; d < 2 * r; ++d) acc += w[d];
+#pragma unroll
+        for (int k = 0; k < K2; ++k) {
+          acc += w[k + 2 * r];
+          (f == 0 ? ha : hb)[k] = acc;
+          acc -= w[k];
+        }
       }
       const float ny = (float)wlen(yo, H, r);
-      const float gv[4] = {g4.x, g4.y, g4.z, g4.w};
-      float ov[4];
+      float ov[K2];
 #pragma unroll
       for (int k = 0; k < K2; ++k) {
-        sa += wa[k + 2 * r];
-        sb += wb[k + 2 * r];
-        const float inv = __frcp_rn(ny * (float)wlen(gxo + k, W, r));
-        ov[k] = (sa * inv) * gv[k] + sb * inv;
-        if (!isfinite(ov[k])) bad = true;
-        sa -= wa[k];
-        sb -= wb[k];
+        const float inv = fast_rcp(ny * (float)wlen(gxo + k, W, r));
+        ov[k] = (ha[k] * inv) * gv[k] + hb[k] * inv;
+        if (k < 4 || two) {
+          if (!isfinite(ov[k])) bad = true;
+        }
       }
-      *reinterpret_cast<float4*>(O + (int64_t)yo * W + gxo) =
-          make_float4(ov[0], ov[1], ov[2], ov[3]);
+      float* orow = O + (int64_t)yo * W + gxo;
+      *reinterpret_cast<float4*>(orow) = make_float4(ov[0], ov[1], ov[2], ov[3]);
+      if (two) *reinterpret_cast<float4*>(orow + 4) = make_float4(ov[4], ov[5], ov[6], ov[7]);
     }
-    // next batch: V1 writes vs (last read by H1, before the V2 barrier); H1
-    // writes ring rows this batch's V2 no longer needs; V2 writes vs2 only
-    // after the next H1 barrier.
+    // next batch: V1 writes vs (last read by H1, before the V2 barrier) and
+    // reads ring slots H1 wrote before that barrier; V2 writes vs2 only after
+    // the next H1 barrier.
   }
   // Non-finite inputs are not tested per element here: they always poison
   // the output at their own pixel, so the host (gf_check_finite) classifies

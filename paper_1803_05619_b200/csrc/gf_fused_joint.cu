@@ -177,12 +177,12 @@ __device__ void lr_coeffs(const float* __restrict__ X, const float* __restrict__
         const int gx = k0 - 1 + c;
         float A = 0.f, B = 0.f;
         if (row_ok && gx >= 0 && gx < w) {
-          const float inv = __frcp_rn(ny * (float)wlen(gx, w, r));
+          const float inv = fast_rcp(ny * (float)wlen(gx, w, r));
           const float mx = s0 * inv, my = s1 * inv;
           const float var = s2 * inv - mx * mx;
           const float cov = s3 * inv - mx * my;
           if (eps == 0.f && !(var > 0.f)) degen = true;
-          A = cov * __frcp_rn(var + eps);
+          A = cov * fast_rcp(var + eps);
           if (NEED_B) B = (my + sy) - A * (mx + sx);
         }
         sm.As[a * CA + c] = A;
@@ -562,11 +562,11 @@ __global__ void __launch_bounds__(NT) k_joint_bwd_lr(BwdLrArgs a) {
         const int gx = k0 - r + n;
         float k_cov = 0.f, k_var = 0.f, k_mx = 0.f, k_my = 0.f;
         if (row_ok && gx >= 0 && gx < w) {
-          const float inv = __frcp_rn(ny * (float)wlen(gx, w, r));
+          const float inv = fast_rcp(ny * (float)wlen(gx, w, r));
           const float mx = s0 * inv, my = s1 * inv;  // shifted means
           const float var = s2 * inv - mx * mx;
           const float cov = s3 * inv - mx * my;
-          const float rden = __frcp_rn(var + a.eps);
+          const float rden = fast_rcp(var + a.eps);
           const float A = cov * rden;
           const float ux = mx + sx, uy = my + sy;  // true means
           const int64_t o = (int64_t)gy * w + gx;
