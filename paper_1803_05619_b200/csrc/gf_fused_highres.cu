@@ -9,8 +9,8 @@
 //       column, registers; the leaving row is re-read from L2)      -> smem vs
 //   H1  horizontal window sums (sliding runs of K1 columns), window means,
 //       var, cov, A = cov/(var+eps), b = mean_s - A*mean_g           -> smem ring
-//   V2  vertical running sums of A and b over a ring of the last 2r+1
-//       coefficient rows (thread per coefficient column; the rows leaving
+//   V2  vertical running sums of A and b over a ring of the last
+//       max(2r+1, R) coefficient rows (thread per coefficient column; the rows leaving
 //       the window are read before H1 overwrites their slots)        -> smem vs2
 //   H2  horizontal sums (runs of K2=8), Ah = M(A), bh = M(b),
 //       out = Ah*G + bh with 128-bit loads of G and 128-bit stores of out.
@@ -38,9 +38,9 @@ constexpr int K1 = 8;    // H1 run length
 constexpr int K2 = 8;    // H2 run length (two float4)
 constexpr int kMaxRadius = 16;  // nt = 256 + 4r <= 320 threads
 
-// Row pitches are = 1 (mod 32): a warp's 32 runs (8 rows x 4 runs of 8
+// Row pitches are = 1 (mod 8): a warp's 32 runs (8 rows x 4 runs of 8
 // columns) then touch 32 distinct banks at every step of the run.
-__host__ __device__ constexpr int pitch1(int n) { return n + ((33 - n % 32) % 32); }
+__host__ __device__ constexpr int pitch1(int n) { return n + ((9 - n % 8) % 8); }
 
 template <int RAD>
 struct Geo {
@@ -49,15 +49,27 @@ struct Geo {
   static constexpr int vsw = nq1 * K1 + 2 * RAD;   // vs columns (>= TX + 4r)
   static constexpr int P1 = pitch1(vsw);
   static constexpr int W1 = TX + 4 * RAD;          // real input columns
-  static constexpr int ringN = 2 * RAD + 1;        // coefficient rows kept
+  static constexpr int ringN = 2 * RAD + 1 > R ? 2 * RAD + 1 : R;  // coefficient rows kept
   static constexpr int ringw = nq1 * K1;           // >= W2
   static constexpr int Pr = pitch1(ringw);
   static constexpr int P2 = pitch1(W2);
+  // cp.async staging of the entering input rows: 16-byte chunks covering
+  // [x0 - PADL, x0 + TX + PADL) with PADL = 2r rounded up to 4
+  static constexpr int PADL = (2 * RAD + 3) / 4 * 4;
+  static constexpr int SW = TX + 2 * PADL;
   static constexpr int nt = ((vsw > ringw ? vsw : ringw) + 31) / 32 * 32;
-  static constexpr size_t smem_floats =
-      (size_t)4 * R * P1 + (size_t)2 * ringN * Pr + (size_t)2 * R * P2;
+  static constexpr size_t smem_floats = (size_t)4 * R * P1 + (size_t)2 * ringN * Pr +
+                                        (size_t)2 * R * P2 + (size_t)2 * R * SW;
   static constexpr size_t smem_bytes = smem_floats * sizeof(float);
 };
+
+__device__ __forceinline__ void cp_async16(float* dst, const float* src, bool valid) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  const int n = valid ? 16 : 0;  // 0 -> zero fill, nothing read
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(d), "l"(src), "r"(n));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n"); }
 
 struct Args {
   const float* guide;
@@ -88,6 +100,7 @@ __global__ void __launch_bounds__(320, 2) k_highres_fused(Args a) {
   float* vs = smem;                        // [4 fields][R rows][P1]
   float* ring = vs + 4 * R * GG::P1;       // [2 fields][ringN slots][Pr]
   float* vs2 = ring + 2 * GG::ringN * GG::Pr;  // [2 fields][R rows][P2]
+  float* stg = vs2 + 2 * R * GG::P2;           // [2 fields][R rows][SW]
 
   // work item: plane fastest (the C planes sharing a guide run together)
   int64_t item = blockIdx.x;
@@ -112,14 +125,34 @@ __global__ void __launch_bounds__(320, 2) k_highres_fused(Args a) {
 
   for (int i = tid; i < 2 * GG::ringN * GG::Pr; i += nt) ring[i] = 0.f;
 
+  const int ya0 = y0 - r;                 // first coefficient row
+  const int nrows = (yend - y0) + 2 * r;  // coefficient rows of this item
+  const int first_add = y0 - 2 * r;       // first input row ever added
+
+  // asynchronous copy of the R entering input rows of the batch at `bb`
+  // (input rows ya0 + bb + j + r) into stg; out-of-image chunks zero-fill
+  auto prefetch = [&](int bb) {
+    constexpr int chunks = GG::SW / 4;
+    for (int idx = tid; idx < 2 * R * chunks; idx += nt) {
+      const int f = idx / (R * chunks);
+      const int rem = idx - f * R * chunks;
+      const int j = rem / chunks, cc = rem - j * chunks;
+      const int e = ya0 + bb + j + r;
+      const int col = x0 - GG::PADL + 4 * cc;
+      const bool ok = bb + j < nrows && e >= 0 && e < H && col >= 0 && col < W;
+      const float* src = (f == 0 ? G : S) + (ok ? (int64_t)e * W + col : 0);
+      cp_async16(stg + (f * R + j) * GG::SW + 4 * cc, src, ok);
+    }
+    cp_async_commit();
+  };
+  prefetch(0);
+
   // ---- level-1 column state: thread = input column xi -------------------
   const int xi = tid;
   const int gx = x0 - 2 * r + xi;
   const bool col_ok = xi < GG::W1 && gx >= 0 && gx < W;
+  const int spos = xi + GG::PADL - 2 * r;  // column of xi in stg
   float s_g = 0.f, s_gg = 0.f, s_s = 0.f, s_gs = 0.f;
-  const int ya0 = y0 - r;                 // first coefficient row
-  const int nrows = (yend - y0) + 2 * r;  // coefficient rows of this item
-  const int first_add = y0 - 2 * r;       // first input row ever added
   if (col_ok) {
     for (int y = max(first_add, 0); y < min(y0, H); ++y) {
       const float g = __ldg(G + (int64_t)y * W + gx) - sG;
@@ -133,7 +166,8 @@ __global__ void __launch_bounds__(320, 2) k_highres_fused(Args a) {
   // ---- level-2 column state: thread = coefficient column ----------------
   float a_sum = 0.f, b_sum = 0.f;
   bool bad = false, degen = false;
-  int ring_new = 0;  // ring slot of coefficient row `base` (mod 2r+1)
+  int ring_new = 0;  // ring slot of coefficient row `base`
+  int ring_old = ((-(2 * r + 1)) % GG::ringN + GG::ringN) % GG::ringN;  // row base-2r-1
 
   // run mapping shared by H1 and H2: lane -> (row j = lane % 8, run q)
   const int jl = lane & 7;
@@ -145,12 +179,14 @@ __global__ void __launch_bounds__(320, 2) k_highres_fused(Args a) {
     if (tid < GG::W2) {
 #pragma unroll
       for (int j = 0; j < R; ++j) {
-        int sl = ring_new + j;
+        int sl = ring_old + j;
         if (sl >= GG::ringN) sl -= GG::ringN;
         old_a[j] = ring[sl * GG::Pr + tid];
         old_b[j] = ring[(GG::ringN + sl) * GG::Pr + tid];
       }
     }
+    cp_async_wait_all();
+    __syncthreads();  // stg complete and visible to every thread
     if (xi < GG::vsw) {
       float ge[R], se[R], gl[R], sl[R];
 #pragma unroll
@@ -160,8 +196,8 @@ __global__ void __launch_bounds__(320, 2) k_highres_fused(Args a) {
         ge[j] = se[j] = gl[j] = sl[j] = 0.f;
         if (col_ok && base + j < nrows) {
           if (e >= 0 && e < H) {
-            ge[j] = __ldg(G + (int64_t)e * W + gx) - sG;
-            se[j] = __ldg(S + (int64_t)e * W + gx) - sS;
+            ge[j] = stg[j * GG::SW + spos] - sG;
+            se[j] = stg[(R + j) * GG::SW + spos] - sS;
           }
           if (l >= first_add && l >= 0 && l < H) {
             gl[j] = __ldg(G + (int64_t)l * W + gx) - sG;
@@ -182,6 +218,9 @@ __global__ void __launch_bounds__(320, 2) k_highres_fused(Args a) {
       }
     }
     __syncthreads();
+
+    // the next batch's entering rows stream in while H1/V2/H2 compute
+    if (base + R < nrows) prefetch(base + R);
 
     // ------------------------------ H1 --------------------------------
     // chunk = warp-sized group of 8 rows x 4 runs
@@ -253,6 +292,8 @@ __global__ void __launch_bounds__(320, 2) k_highres_fused(Args a) {
     }
     ring_new += R;
     while (ring_new >= GG::ringN) ring_new -= GG::ringN;
+    ring_old += R;
+    while (ring_old >= GG::ringN) ring_old -= GG::ringN;
     __syncthreads();
 
     // ------------------------------ H2 --------------------------------
