@@ -16,7 +16,7 @@
 //       out = Ah*G + bh with 128-bit loads of G and 128-bit stores of out.
 //
 // H1/H2 map a warp to 8 rows x 4 runs and every shared row pitch is
-// = 1 (mod 32), so the 32 lanes of a run step hit 32 distinct banks.  The
+// = 1 (mod 8), so the 32 lanes of a run step hit 32 distinct banks.  The
 // radius is a template parameter (1..16) so every window loop is unrolled.
 //
 // Windows are clamped to the image and normalised by the true count
@@ -97,10 +97,10 @@ __global__ void __launch_bounds__(320, 2) k_highres_fused(Args a) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr int nt = GG::nt;
 
-  float* vs = smem;                        // [4 fields][R rows][P1]
-  float* ring = vs + 4 * R * GG::P1;       // [2 fields][ringN slots][Pr]
+  float* stg = smem;                        // [2 fields][R rows][SW] (16-B aligned for cp.async)
+  float* vs = stg + 2 * R * GG::SW;         // [4 fields][R rows][P1]
+  float* ring = vs + 4 * R * GG::P1;        // [2 fields][ringN slots][Pr]
   float* vs2 = ring + 2 * GG::ringN * GG::Pr;  // [2 fields][R rows][P2]
-  float* stg = vs2 + 2 * R * GG::P2;           // [2 fields][R rows][SW]
 
   // work item: plane fastest (the C planes sharing a guide run together)
   int64_t item = blockIdx.x;
