@@ -5,19 +5,24 @@
 // output rows).  A CTA walks its segment top to bottom in batches of R rows
 // and keeps every intermediate on chip:
 //
-//   V1  vertical running window sums of g, g^2, s, g*s (thread per input
-//       column, registers; the leaving row is re-read from L2)      -> smem vs
-//   H1  horizontal window sums (sliding runs of K1 columns), window means,
-//       var, cov, A = cov/(var+eps), b = mean_s - A*mean_g           -> smem ring
-//   V2  vertical running sums of A and b over a ring of the last
-//       max(2r+1, R) coefficient rows (thread per coefficient column; the rows leaving
-//       the window are read before H1 overwrites their slots)        -> smem vs2
-//   H2  horizontal sums (runs of K2=8), Ah = M(A), bh = M(b),
-//       out = Ah*G + bh with 128-bit loads of G and 128-bit stores of out.
+//   stage  the batch's R entering input rows stream into shared memory with
+//          cp.async one batch ahead (zero-filled outside the image)
+//   V1     vertical running window sums of g, g^2, s, g*s, four columns per
+//          thread (the rows leaving the window are re-read from L2 with
+//          128-bit loads)                                         -> smem vs
+//   H1     horizontal window sums (runs of 8 columns), window means, var,
+//          cov, A = cov/(var+eps), b = mean_s - A*mean_g           -> smem ring
+//   V2     vertical running sums of A and b over the ring of the last
+//          max(2r+1, R) coefficient rows, four columns per thread; the
+//          leaving rows are subtracted before H1 overwrites them  -> smem vs2
+//   H2     horizontal sums (runs of 8), Ah = M(A), bh = M(b), out = Ah*G + bh
+//          with 128-bit loads of G and 128-bit stores of out.
 //
-// H1/H2 map a warp to 8 rows x 4 runs and every shared row pitch is
-// = 1 (mod 8), so the 32 lanes of a run step hit 32 distinct banks.  The
-// radius is a template parameter (1..16) so every window loop is unrolled.
+// Every shared row is 16-byte aligned with a pitch = 4 (mod 32) words: the
+// 8 lanes of a quarter warp (8 rows of one run) then read 8 distinct bank
+// quads with 128-bit loads.  The radius is a template parameter (1..16) so
+// every window loop is unrolled; runs that lie inside the image use the
+// constant 1/(2r+1) column normaliser.
 //
 // Windows are clamped to the image and normalised by the true count
 // N = ny*nx (gf/filters.py:82-103): out-of-image rows/columns contribute 0.
@@ -34,32 +39,33 @@ namespace hrf {
 
 constexpr int R = 8;     // rows per batch
 constexpr int TX = 256;  // output columns per work item
-constexpr int K1 = 8;    // H1 run length
-constexpr int K2 = 8;    // H2 run length (two float4)
-constexpr int kMaxRadius = 16;  // nt = 256 + 4r <= 320 threads
+constexpr int KR = 8;    // run length of H1 and H2
+constexpr int kMaxRadius = 16;
 
-// Row pitches are = 1 (mod 8): a warp's 32 runs (8 rows x 4 runs of 8
-// columns) then touch 32 distinct banks at every step of the run.
-__host__ __device__ constexpr int pitch1(int n) { return n + ((9 - n % 8) % 8); }
+__host__ __device__ constexpr int up4(int n) { return (n + 3) / 4 * 4; }
+// smallest p >= n with p = 4 (mod 32)
+__host__ __device__ constexpr int pitch4(int n) { return n + ((36 - n % 32) % 32); }
+__host__ __device__ constexpr int cmax(int a, int b) { return a > b ? a : b; }
 
 template <int RAD>
 struct Geo {
-  static constexpr int W2 = TX + 2 * RAD;          // coefficient columns
-  static constexpr int nq1 = (W2 + K1 - 1) / K1;   // H1 runs per row
-  static constexpr int vsw = nq1 * K1 + 2 * RAD;   // vs columns (>= TX + 4r)
-  static constexpr int P1 = pitch1(vsw);
-  static constexpr int W1 = TX + 4 * RAD;          // real input columns
-  static constexpr int ringN = 2 * RAD + 1 > R ? 2 * RAD + 1 : R;  // coefficient rows kept
-  static constexpr int ringw = nq1 * K1;           // >= W2
-  static constexpr int Pr = pitch1(ringw);
-  static constexpr int P2 = pitch1(W2);
-  // cp.async staging of the entering input rows: 16-byte chunks covering
-  // [x0 - PADL, x0 + TX + PADL) with PADL = 2r rounded up to 4
-  static constexpr int PADL = (2 * RAD + 3) / 4 * 4;
-  static constexpr int SW = TX + 2 * PADL;
-  static constexpr int nt = ((vsw > ringw ? vsw : ringw) + 31) / 32 * 32;
-  static constexpr size_t smem_floats = (size_t)4 * R * P1 + (size_t)2 * ringN * Pr +
-                                        (size_t)2 * R * P2 + (size_t)2 * R * SW;
+  static constexpr int W2 = TX + 2 * RAD;                 // coefficient columns
+  static constexpr int nq1 = (W2 + KR - 1) / KR;          // H1 runs per row
+  static constexpr int PADL = up4(2 * RAD);               // staged columns left of x0
+  static constexpr int off = PADL - 2 * RAD;              // vs col of a window start
+  static constexpr int nv1 = (off + 2 * RAD + KR + 3) / 4;  // float4s per H1 run window
+  static constexpr int VW = up4(cmax(TX + 2 * PADL, (nq1 - 1) * KR + 4 * nv1));  // V1 columns
+  static constexpr int P1 = pitch4(VW);
+  static constexpr int ringN = cmax(2 * RAD + 1, R);
+  static constexpr int ringw = nq1 * KR;                  // >= W2
+  static constexpr int Pr = pitch4(ringw);
+  static constexpr int nv2 = (2 * RAD + KR + 3) / 4;      // float4s per H2 run window
+  static constexpr int v2w = up4(cmax(ringw, TX - KR + 4 * nv2));
+  static constexpr int P2 = pitch4(v2w);
+  static constexpr int nt = 32 * cmax(cmax((nq1 + 3) / 4, TX / KR / 4),
+                                      cmax((VW / 4 + 31) / 32, (v2w / 4 + 31) / 32));
+  static constexpr size_t smem_floats = (size_t)2 * R * VW + (size_t)4 * R * P1 +
+                                        (size_t)2 * ringN * Pr + (size_t)2 * R * P2;
   static constexpr size_t smem_bytes = smem_floats * sizeof(float);
 };
 
@@ -70,6 +76,13 @@ __device__ __forceinline__ void cp_async16(float* dst, const float* src, bool va
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n"); }
+
+__device__ __forceinline__ float4 lds4(const float* p) {
+  return *reinterpret_cast<const float4*>(p);
+}
+__device__ __forceinline__ void sts4(float* p, float a, float b, float c, float d) {
+  *reinterpret_cast<float4*>(p) = make_float4(a, b, c, d);
+}
 
 struct Args {
   const float* guide;
@@ -91,16 +104,14 @@ template <int RAD>
 __global__ void __launch_bounds__(320, 2) k_highres_fused(Args a) {
   using GG = Geo<RAD>;
   constexpr int r = RAD;
+  constexpr int nt = GG::nt;
   extern __shared__ float4 smem4[];
-  float* smem = reinterpret_cast<float*>(smem4);
+  float* stg = reinterpret_cast<float*>(smem4);  // [2 fields][R][VW]
+  float* vs = stg + 2 * R * GG::VW;              // [4 fields][R][P1]
+  float* ring = vs + 4 * R * GG::P1;             // [2 fields][ringN][Pr]
+  float* vs2 = ring + 2 * GG::ringN * GG::Pr;    // [2 fields][R][P2]
   const int H = (int)a.H, W = (int)a.W;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  constexpr int nt = GG::nt;
-
-  float* stg = smem;                        // [2 fields][R rows][SW] (16-B aligned for cp.async)
-  float* vs = stg + 2 * R * GG::SW;         // [4 fields][R rows][P1]
-  float* ring = vs + 4 * R * GG::P1;        // [2 fields][ringN slots][Pr]
-  float* vs2 = ring + 2 * GG::ringN * GG::Pr;  // [2 fields][R rows][P2]
 
   // work item: plane fastest (the C planes sharing a guide run together)
   int64_t item = blockIdx.x;
@@ -118,191 +129,245 @@ __global__ void __launch_bounds__(320, 2) k_highres_fused(Args a) {
   const float* __restrict__ G = a.guide + (a.Cg == a.C ? b * a.C + c : b * a.Cg) * plane;
   const float* __restrict__ S = a.src + (b * a.C + c) * plane;
   float* __restrict__ O = a.out + (b * a.C + c) * plane;
-
   const float sG = __ldg(G + (int64_t)y0 * W + x0);
   const float sS = __ldg(S + (int64_t)y0 * W + x0);
   const float eps = a.eps;
+  constexpr float inv_full = 1.0f / (float)(2 * r + 1);
 
   for (int i = tid; i < 2 * GG::ringN * GG::Pr; i += nt) ring[i] = 0.f;
 
   const int ya0 = y0 - r;                 // first coefficient row
   const int nrows = (yend - y0) + 2 * r;  // coefficient rows of this item
   const int first_add = y0 - 2 * r;       // first input row ever added
+  const int xs0 = x0 - GG::PADL;          // global column of vs/stg column 0
 
-  // asynchronous copy of the R entering input rows of the batch at `bb`
-  // (input rows ya0 + bb + j + r) into stg; out-of-image chunks zero-fill
+  // cp.async of the R entering input rows of the batch at bb (rows ya + r)
   auto prefetch = [&](int bb) {
-    constexpr int chunks = GG::SW / 4;
+    constexpr int chunks = GG::VW / 4;
     for (int idx = tid; idx < 2 * R * chunks; idx += nt) {
       const int f = idx / (R * chunks);
       const int rem = idx - f * R * chunks;
       const int j = rem / chunks, cc = rem - j * chunks;
       const int e = ya0 + bb + j + r;
-      const int col = x0 - GG::PADL + 4 * cc;
+      const int col = xs0 + 4 * cc;
       const bool ok = bb + j < nrows && e >= 0 && e < H && col >= 0 && col < W;
       const float* src = (f == 0 ? G : S) + (ok ? (int64_t)e * W + col : 0);
-      cp_async16(stg + (f * R + j) * GG::SW + 4 * cc, src, ok);
+      cp_async16(stg + (f * R + j) * GG::VW + 4 * cc, src, ok);
     }
     cp_async_commit();
   };
   prefetch(0);
 
-  // ---- level-1 column state: thread = input column xi -------------------
-  const int xi = tid;
-  const int gx = x0 - 2 * r + xi;
-  const bool col_ok = xi < GG::W1 && gx >= 0 && gx < W;
-  const int spos = xi + GG::PADL - 2 * r;  // column of xi in stg
-  float s_g = 0.f, s_gg = 0.f, s_s = 0.f, s_gs = 0.f;
+  // ---- level-1 state: thread t < VW/4 owns vs columns 4t..4t+3 ----------
+  const bool v1 = tid < GG::VW / 4;
+  const int gx4 = xs0 + 4 * tid;
+  const bool col_ok = v1 && gx4 >= 0 && gx4 < W;  // W % 4 == 0: all 4 or none
+  float s_g[4] = {0.f, 0.f, 0.f, 0.f}, s_gg[4] = {0.f, 0.f, 0.f, 0.f};
+  float s_s[4] = {0.f, 0.f, 0.f, 0.f}, s_gs[4] = {0.f, 0.f, 0.f, 0.f};
   if (col_ok) {
     for (int y = max(first_add, 0); y < min(y0, H); ++y) {
-      const float g = __ldg(G + (int64_t)y * W + gx) - sG;
-      const float s = __ldg(S + (int64_t)y * W + gx) - sS;
-      s_g += g;
-      s_gg += g * g;
-      s_s += s;
-      s_gs += g * s;
+      const float4 g4 = __ldg(reinterpret_cast<const float4*>(G + (int64_t)y * W + gx4));
+      const float4 v4 = __ldg(reinterpret_cast<const float4*>(S + (int64_t)y * W + gx4));
+      const float gg[4] = {g4.x - sG, g4.y - sG, g4.z - sG, g4.w - sG};
+      const float ss[4] = {v4.x - sS, v4.y - sS, v4.z - sS, v4.w - sS};
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        s_g[k] += gg[k];
+        s_gg[k] += gg[k] * gg[k];
+        s_s[k] += ss[k];
+        s_gs[k] += gg[k] * ss[k];
+      }
     }
   }
-  // ---- level-2 column state: thread = coefficient column ----------------
-  float a_sum = 0.f, b_sum = 0.f;
+  // ---- level-2 state: thread t < v2w/4 owns coefficient columns 4t..4t+3
+  const bool v2 = tid < GG::v2w / 4;
+  const bool v2ring = tid < GG::ringw / 4;
+  float a_sum[4] = {0.f, 0.f, 0.f, 0.f}, b_sum[4] = {0.f, 0.f, 0.f, 0.f};
   bool bad = false, degen = false;
-  int ring_new = 0;  // ring slot of coefficient row `base`
-  int ring_old = ((-(2 * r + 1)) % GG::ringN + GG::ringN) % GG::ringN;  // row base-2r-1
-
-  // run mapping shared by H1 and H2: lane -> (row j = lane % 8, run q)
-  const int jl = lane & 7;
-  const int ql = lane >> 3;
+  int ring_new = 0;                                   // slot of coefficient row `base`
+  int ring_old = GG::ringN - (2 * r + 1) % GG::ringN;  // slot of row base - 2r - 1
+  if (ring_old == GG::ringN) ring_old = 0;
+  const int jl = lane & 7;   // run mapping of H1/H2: row
+  const int ql = lane >> 3;  //                       run within the warp's chunk
 
   for (int base = 0; base < nrows; base += R) {
-    // --------------------- V1 (+ V2 old-row prefetch) ------------------
-    float old_a[R], old_b[R];
-    if (tid < GG::W2) {
+    cp_async_wait_all();
+    __syncthreads();  // stg landed; the previous batch's H2 is done with vs2
+
+    // ---- V2 (part 1): subtract the leaving coefficient rows while their
+    //      ring slots still hold them: vs2[j] = sum - sum_{i<=j} old_i
+    if (v2) {
+      float pa[4] = {a_sum[0], a_sum[1], a_sum[2], a_sum[3]};
+      float pb[4] = {b_sum[0], b_sum[1], b_sum[2], b_sum[3]};
 #pragma unroll
       for (int j = 0; j < R; ++j) {
-        int sl = ring_old + j;
-        if (sl >= GG::ringN) sl -= GG::ringN;
-        old_a[j] = ring[sl * GG::Pr + tid];
-        old_b[j] = ring[(GG::ringN + sl) * GG::Pr + tid];
+        if (v2ring && base + j - 2 * r - 1 >= 0) {
+          int so = ring_old + j;
+          if (so >= GG::ringN) so -= GG::ringN;
+          const float4 oa = lds4(ring + so * GG::Pr + 4 * tid);
+          const float4 ob = lds4(ring + (GG::ringN + so) * GG::Pr + 4 * tid);
+          pa[0] -= oa.x; pa[1] -= oa.y; pa[2] -= oa.z; pa[3] -= oa.w;
+          pb[0] -= ob.x; pb[1] -= ob.y; pb[2] -= ob.z; pb[3] -= ob.w;
+        }
+        sts4(vs2 + j * GG::P2 + 4 * tid, pa[0], pa[1], pa[2], pa[3]);
+        sts4(vs2 + (R + j) * GG::P2 + 4 * tid, pb[0], pb[1], pb[2], pb[3]);
       }
     }
-    cp_async_wait_all();
-    __syncthreads();  // stg complete and visible to every thread
-    if (xi < GG::vsw) {
-      float ge[R], se[R], gl[R], sl[R];
+
+    // ---- V1 -----------------------------------------------------------
+    if (v1) {
 #pragma unroll
-      for (int j = 0; j < R; ++j) {
-        const int ya = ya0 + base + j;
-        const int e = ya + r, l = ya - r - 1;
-        ge[j] = se[j] = gl[j] = sl[j] = 0.f;
-        if (col_ok && base + j < nrows) {
-          if (e >= 0 && e < H) {
-            ge[j] = stg[j * GG::SW + spos] - sG;
-            se[j] = stg[(R + j) * GG::SW + spos] - sS;
-          }
-          if (l >= first_add && l >= 0 && l < H) {
-            gl[j] = __ldg(G + (int64_t)l * W + gx) - sG;
-            sl[j] = __ldg(S + (int64_t)l * W + gx) - sS;
+      for (int half = 0; half < 2; ++half) {
+        float4 gl[R / 2], sl[R / 2];
+#pragma unroll
+        for (int jj = 0; jj < R / 2; ++jj) {
+          const int j = half * (R / 2) + jj;
+          const int l = ya0 + base + j - r - 1;
+          gl[jj] = sl[jj] = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (col_ok && base + j < nrows && l >= first_add && l >= 0 && l < H) {
+            gl[jj] = __ldg(reinterpret_cast<const float4*>(G + (int64_t)l * W + gx4));
+            sl[jj] = __ldg(reinterpret_cast<const float4*>(S + (int64_t)l * W + gx4));
           }
         }
-      }
 #pragma unroll
-      for (int j = 0; j < R; ++j) {
-        s_g += ge[j] - gl[j];
-        s_gg += ge[j] * ge[j] - gl[j] * gl[j];
-        s_s += se[j] - sl[j];
-        s_gs += ge[j] * se[j] - gl[j] * sl[j];
-        vs[(0 * R + j) * GG::P1 + xi] = col_ok ? s_g : 0.f;
-        vs[(1 * R + j) * GG::P1 + xi] = col_ok ? s_gg : 0.f;
-        vs[(2 * R + j) * GG::P1 + xi] = col_ok ? s_s : 0.f;
-        vs[(3 * R + j) * GG::P1 + xi] = col_ok ? s_gs : 0.f;
+        for (int jj = 0; jj < R / 2; ++jj) {
+          const int j = half * (R / 2) + jj;
+          const int e = ya0 + base + j + r;
+          const int l = ya0 + base + j - r - 1;
+          const bool e_ok = col_ok && base + j < nrows && e >= 0 && e < H;
+          const bool l_ok = col_ok && base + j < nrows && l >= first_add && l >= 0 && l < H;
+          const float4 ge4 = lds4(stg + j * GG::VW + 4 * tid);
+          const float4 se4 = lds4(stg + (R + j) * GG::VW + 4 * tid);
+          const float ge[4] = {ge4.x - sG, ge4.y - sG, ge4.z - sG, ge4.w - sG};
+          const float se[4] = {se4.x - sS, se4.y - sS, se4.z - sS, se4.w - sS};
+          const float go[4] = {gl[jj].x - sG, gl[jj].y - sG, gl[jj].z - sG, gl[jj].w - sG};
+          const float so[4] = {sl[jj].x - sS, sl[jj].y - sS, sl[jj].z - sS, sl[jj].w - sS};
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const float gn = e_ok ? ge[k] : 0.f, sn = e_ok ? se[k] : 0.f;
+            const float gq = l_ok ? go[k] : 0.f, sq = l_ok ? so[k] : 0.f;
+            s_g[k] += gn - gq;
+            s_gg[k] += gn * gn - gq * gq;
+            s_s[k] += sn - sq;
+            s_gs[k] += gn * sn - gq * sq;
+          }
+          const float m = col_ok ? 1.f : 0.f;
+          sts4(vs + (0 * R + j) * GG::P1 + 4 * tid, m * s_g[0], m * s_g[1], m * s_g[2], m * s_g[3]);
+          sts4(vs + (1 * R + j) * GG::P1 + 4 * tid, m * s_gg[0], m * s_gg[1], m * s_gg[2],
+               m * s_gg[3]);
+          sts4(vs + (2 * R + j) * GG::P1 + 4 * tid, m * s_s[0], m * s_s[1], m * s_s[2], m * s_s[3]);
+          sts4(vs + (3 * R + j) * GG::P1 + 4 * tid, m * s_gs[0], m * s_gs[1], m * s_gs[2],
+               m * s_gs[3]);
+        }
       }
     }
-    __syncthreads();
+    __syncthreads();  // vs complete; stg consumed
 
     // the next batch's entering rows stream in while H1/V2/H2 compute
     if (base + R < nrows) prefetch(base + R);
 
-    // ------------------------------ H1 --------------------------------
-    // chunk = warp-sized group of 8 rows x 4 runs
+    // ---- H1 -----------------------------------------------------------
     for (int ch = warp; ch * 4 < GG::nq1; ch += nt / 32) {
       const int j = jl, q = ch * 4 + ql;
       if (q >= GG::nq1 || base + j >= nrows) continue;
       const int ya = ya0 + base + j;
-      const int xa0 = q * K1;
+      const int xa0 = q * KR;
       int slot = ring_new + j;
       if (slot >= GG::ringN) slot -= GG::ringN;
       float* ra = ring + slot * GG::Pr + xa0;
       float* rb = ring + (GG::ringN + slot) * GG::Pr + xa0;
       if (ya < 0 || ya >= H) {
-#pragma unroll
-        for (int k = 0; k < K1; ++k) ra[k] = rb[k] = 0.f;
+        sts4(ra, 0.f, 0.f, 0.f, 0.f);
+        sts4(ra + 4, 0.f, 0.f, 0.f, 0.f);
+        sts4(rb, 0.f, 0.f, 0.f, 0.f);
+        sts4(rb + 4, 0.f, 0.f, 0.f, 0.f);
         continue;
       }
-      // one field at a time keeps the live window to K1 + 2r registers
-      float hs[4][K1];
+      float hs[4][KR];
 #pragma unroll
       for (int f = 0; f < 4; ++f) {
         const float* v = vs + (f * R + j) * GG::P1 + xa0;
-        float w[K1 + 2 * r];
+        float w[4 * GG::nv1];
 #pragma unroll
-        for (int d = 0; d < K1 + 2 * r; ++d) w[d] = v[d];
+        for (int m = 0; m < GG::nv1; ++m) {
+          const float4 t4 = lds4(v + 4 * m);
+          w[4 * m] = t4.x;
+          w[4 * m + 1] = t4.y;
+          w[4 * m + 2] = t4.z;
+          w[4 * m + 3] = t4.w;
+        }
         float acc = 0.f;
 #pragma unroll
-        for (int d = 0; d < 2 * r; ++d) acc += w[d];
+        for (int d = 0; d < 2 * r; ++d) acc += w[GG::off + d];
 #pragma unroll
-        for (int k = 0; k < K1; ++k) {
-          acc += w[k + 2 * r];
+        for (int k = 0; k < KR; ++k) {
+          acc += w[GG::off + k + 2 * r];
           hs[f][k] = acc;
-          acc -= w[k];
+          acc -= w[GG::off + k];
         }
       }
-      const float ny = (float)wlen(ya, H, r);
+      const float iny = fast_rcp((float)wlen(ya, H, r));
+      const int gxa0 = x0 - r + xa0;  // global column of the run's first coefficient
+      const bool interior = gxa0 >= r && gxa0 + KR - 1 + r <= W - 1 && xa0 + KR <= GG::W2;
+      float A[KR], B[KR];
 #pragma unroll
-      for (int k = 0; k < K1; ++k) {
-        const int gxa = x0 - r + xa0 + k;
-        float A = 0.f, B = 0.f;
-        if (xa0 + k < GG::W2 && gxa >= 0 && gxa < W) {
-          const float inv = fast_rcp(ny * (float)wlen(gxa, W, r));
-          const float mg = hs[0][k] * inv, ms = hs[2][k] * inv;
-          const float var = hs[1][k] * inv - mg * mg;
-          const float cov = hs[3][k] * inv - mg * ms;
-          if (eps == 0.f && !(var > 0.f)) degen = true;
-          A = cov * fast_rcp(var + eps);
-          B = (ms + sS) - A * (mg + sG);
-        }
-        ra[k] = A;
-        rb[k] = B;
+      for (int k = 0; k < KR; ++k) {
+        const int gxa = gxa0 + k;
+        const bool ok = interior || (xa0 + k < GG::W2 && gxa >= 0 && gxa < W);
+        const float inv = interior ? iny * inv_full
+                                   : iny * fast_rcp((float)wlen(gxa, W, r));
+        const float mg = hs[0][k] * inv, ms = hs[2][k] * inv;
+        const float var = hs[1][k] * inv - mg * mg;
+        const float cov = hs[3][k] * inv - mg * ms;
+        if (ok && eps == 0.f && !(var > 0.f)) degen = true;
+        const float Ak = cov * fast_rcp(var + eps);
+        A[k] = ok ? Ak : 0.f;
+        B[k] = ok ? (ms + sS) - Ak * (mg + sG) : 0.f;
       }
+      sts4(ra, A[0], A[1], A[2], A[3]);
+      sts4(ra + 4, A[4], A[5], A[6], A[7]);
+      sts4(rb, B[0], B[1], B[2], B[3]);
+      sts4(rb + 4, B[4], B[5], B[6], B[7]);
     }
-    __syncthreads();
+    __syncthreads();  // ring rows of this batch complete
 
-    // ------------------------------ V2 --------------------------------
-    if (tid < GG::W2) {
+    // ---- V2 (part 2): add the entering coefficient rows ----------------
+    if (v2) {
+      float na[4] = {0.f, 0.f, 0.f, 0.f}, nb[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
       for (int j = 0; j < R; ++j) {
-        if (base + j < nrows) {
+        if (v2ring && base + j < nrows) {
           int sn = ring_new + j;
           if (sn >= GG::ringN) sn -= GG::ringN;
-          a_sum += ring[sn * GG::Pr + tid] - old_a[j];
-          b_sum += ring[(GG::ringN + sn) * GG::Pr + tid] - old_b[j];
+          const float4 xa = lds4(ring + sn * GG::Pr + 4 * tid);
+          const float4 xb = lds4(ring + (GG::ringN + sn) * GG::Pr + 4 * tid);
+          na[0] += xa.x; na[1] += xa.y; na[2] += xa.z; na[3] += xa.w;
+          nb[0] += xb.x; nb[1] += xb.y; nb[2] += xb.z; nb[3] += xb.w;
         }
-        vs2[(0 * R + j) * GG::P2 + tid] = a_sum;
-        vs2[(1 * R + j) * GG::P2 + tid] = b_sum;
+        float* pa = vs2 + j * GG::P2 + 4 * tid;
+        float* pb = vs2 + (R + j) * GG::P2 + 4 * tid;
+        const float4 oa = lds4(pa), ob = lds4(pb);
+        a_sum[0] = oa.x + na[0]; a_sum[1] = oa.y + na[1];
+        a_sum[2] = oa.z + na[2]; a_sum[3] = oa.w + na[3];
+        b_sum[0] = ob.x + nb[0]; b_sum[1] = ob.y + nb[1];
+        b_sum[2] = ob.z + nb[2]; b_sum[3] = ob.w + nb[3];
+        sts4(pa, a_sum[0], a_sum[1], a_sum[2], a_sum[3]);
+        sts4(pb, b_sum[0], b_sum[1], b_sum[2], b_sum[3]);
       }
     }
     ring_new += R;
     while (ring_new >= GG::ringN) ring_new -= GG::ringN;
     ring_old += R;
     while (ring_old >= GG::ringN) ring_old -= GG::ringN;
-    __syncthreads();
+    __syncthreads();  // vs2 complete
 
-    // ------------------------------ H2 --------------------------------
-    constexpr int nq2 = TX / K2;  // 32 runs per row
+    // ---- H2 -----------------------------------------------------------
+    constexpr int nq2 = TX / KR;
     for (int ch = warp; ch * 4 < nq2; ch += nt / 32) {
       const int j = jl, q = ch * 4 + ql;
       const int yo = y0 + base + j - 2 * r;
       if (yo < y0 || yo >= yend) continue;
-      const int xo0 = q * K2;
+      const int xo0 = q * KR;
       const int gxo = x0 + xo0;
       if (gxo >= W) continue;
       const float* grow = G + (int64_t)yo * W + gxo;
@@ -311,40 +376,43 @@ __global__ void __launch_bounds__(320, 2) k_highres_fused(Args a) {
       const float4 g1 = two ? __ldg(reinterpret_cast<const float4*>(grow + 4))
                             : make_float4(0.f, 0.f, 0.f, 0.f);
       const float gv[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
-      float ha[K2], hb[K2];
+      float hs[2][KR];
 #pragma unroll
       for (int f = 0; f < 2; ++f) {
         const float* v = vs2 + (f * R + j) * GG::P2 + xo0;
-        float w[K2 + 2 * r];
+        float w[4 * GG::nv2];
 #pragma unroll
-        for (int d = 0; d < K2 + 2 * r; ++d) w[d] = v[d];
+        for (int m = 0; m < GG::nv2; ++m) {
+          const float4 t4 = lds4(v + 4 * m);
+          w[4 * m] = t4.x;
+          w[4 * m + 1] = t4.y;
+          w[4 * m + 2] = t4.z;
+          w[4 * m + 3] = t4.w;
+        }
         float acc = 0.f;
 #pragma unroll
         for (int d = 0; d < 2 * r; ++d) acc += w[d];
 #pragma unroll
-        for (int k = 0; k < K2; ++k) {
+        for (int k = 0; k < KR; ++k) {
           acc += w[k + 2 * r];
-          (f == 0 ? ha : hb)[k] = acc;
+          hs[f][k] = acc;
           acc -= w[k];
         }
       }
-      const float ny = (float)wlen(yo, H, r);
-      float ov[K2];
+      const float iny = fast_rcp((float)wlen(yo, H, r));
+      const bool interior = gxo >= r && gxo + KR - 1 + r <= W - 1;
+      float ov[KR];
 #pragma unroll
-      for (int k = 0; k < K2; ++k) {
-        const float inv = fast_rcp(ny * (float)wlen(gxo + k, W, r));
-        ov[k] = (ha[k] * inv) * gv[k] + hb[k] * inv;
-        if (k < 4 || two) {
-          if (!isfinite(ov[k])) bad = true;
-        }
+      for (int k = 0; k < KR; ++k) {
+        const float inv = interior ? iny * inv_full
+                                   : iny * fast_rcp((float)wlen(gxo + k, W, r));
+        ov[k] = (hs[0][k] * inv) * gv[k] + hs[1][k] * inv;
+        if ((k < 4 || two) && !isfinite(ov[k])) bad = true;
       }
       float* orow = O + (int64_t)yo * W + gxo;
       *reinterpret_cast<float4*>(orow) = make_float4(ov[0], ov[1], ov[2], ov[3]);
       if (two) *reinterpret_cast<float4*>(orow + 4) = make_float4(ov[4], ov[5], ov[6], ov[7]);
     }
-    // next batch: V1 writes vs (last read by H1, before the V2 barrier) and
-    // reads ring slots H1 wrote before that barrier; V2 writes vs2 only after
-    // the next H1 barrier.
   }
   // Non-finite inputs are not tested per element here: they always poison
   // the output at their own pixel, so the host (gf_check_finite) classifies
