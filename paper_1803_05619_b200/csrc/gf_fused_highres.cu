@@ -63,7 +63,7 @@ struct Geo {
   static constexpr int v2w = up4(cmax(ringw, TX - KR + 4 * nv2));
   static constexpr int P2 = pitch4(v2w);
   static constexpr int nt = 32 * cmax(cmax((nq1 + 3) / 4, TX / KR / 4),
-                                      cmax((VW / 4 + 31) / 32, (v2w / 4 + 31) / 32));
+                                      cmax((VW / 2 + 31) / 32, (v2w / 2 + 31) / 32));
   static constexpr size_t smem_floats = (size_t)2 * R * VW + (size_t)4 * R * P1 +
                                         (size_t)2 * ringN * Pr + (size_t)2 * R * P2;
   static constexpr size_t smem_bytes = smem_floats * sizeof(float);
@@ -158,31 +158,46 @@ __global__ void __launch_bounds__(320, 2) k_highres_fused(Args a) {
   };
   prefetch(0);
 
-  // ---- level-1 state: thread t < VW/4 owns vs columns 4t..4t+3 ----------
-  const bool v1 = tid < GG::VW / 4;
-  const int gx4 = xs0 + 4 * tid;
+  // ---- level-1 state: V1T threads per field group; group 0 keeps the guide
+  //      sums (g, g^2), group 1 the source sums (s, g*s); thread owns vs
+  //      columns 4t..4t+3 of its group
+  constexpr int V1T = GG::VW / 4;
+  const int grp = tid < V1T ? 0 : 1;
+  const int t4 = tid - grp * V1T;
+  const bool v1 = tid < 2 * V1T;
+  const int gx4 = xs0 + 4 * t4;
   const bool col_ok = v1 && gx4 >= 0 && gx4 < W;  // W % 4 == 0: all 4 or none
-  float s_g[4] = {0.f, 0.f, 0.f, 0.f}, s_gg[4] = {0.f, 0.f, 0.f, 0.f};
-  float s_s[4] = {0.f, 0.f, 0.f, 0.f}, s_gs[4] = {0.f, 0.f, 0.f, 0.f};
+  const bool cols_in = xs0 >= 0 && xs0 + GG::VW <= W;  // CTA-uniform
+  float sA[4] = {0.f, 0.f, 0.f, 0.f}, sB[4] = {0.f, 0.f, 0.f, 0.f};
   if (col_ok) {
     for (int y = max(first_add, 0); y < min(y0, H); ++y) {
       const float4 g4 = __ldg(reinterpret_cast<const float4*>(G + (int64_t)y * W + gx4));
-      const float4 v4 = __ldg(reinterpret_cast<const float4*>(S + (int64_t)y * W + gx4));
       const float gg[4] = {g4.x - sG, g4.y - sG, g4.z - sG, g4.w - sG};
-      const float ss[4] = {v4.x - sS, v4.y - sS, v4.z - sS, v4.w - sS};
+      if (grp == 0) {
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        s_g[k] += gg[k];
-        s_gg[k] += gg[k] * gg[k];
-        s_s[k] += ss[k];
-        s_gs[k] += gg[k] * ss[k];
+        for (int k = 0; k < 4; ++k) {
+          sA[k] += gg[k];
+          sB[k] += gg[k] * gg[k];
+        }
+      } else {
+        const float4 v4 = __ldg(reinterpret_cast<const float4*>(S + (int64_t)y * W + gx4));
+        const float ss[4] = {v4.x - sS, v4.y - sS, v4.z - sS, v4.w - sS};
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          sA[k] += ss[k];
+          sB[k] += gg[k] * ss[k];
+        }
       }
     }
   }
-  // ---- level-2 state: thread t < v2w/4 owns coefficient columns 4t..4t+3
-  const bool v2 = tid < GG::v2w / 4;
-  const bool v2ring = tid < GG::ringw / 4;
-  float a_sum[4] = {0.f, 0.f, 0.f, 0.f}, b_sum[4] = {0.f, 0.f, 0.f, 0.f};
+  // ---- level-2 state: V2T threads per coefficient field (A, then b); a
+  //      thread owns coefficient columns 4u..4u+3 of its field
+  constexpr int V2T = GG::v2w / 4;
+  const int fld = tid < V2T ? 0 : 1;
+  const int u4 = tid - fld * V2T;
+  const bool v2 = tid < 2 * V2T;
+  const bool v2ring = v2 && u4 < GG::ringw / 4;
+  float c_sum[4] = {0.f, 0.f, 0.f, 0.f};
   bool bad = false, degen = false;
   int ring_new = 0;                                   // slot of coefficient row `base`
   int ring_old = GG::ringN - (2 * r + 1) % GG::ringN;  // slot of row base - 2r - 1
@@ -197,25 +212,29 @@ __global__ void __launch_bounds__(320, 2) k_highres_fused(Args a) {
     // ---- V2 (part 1): subtract the leaving coefficient rows while their
     //      ring slots still hold them: vs2[j] = sum - sum_{i<=j} old_i
     if (v2) {
-      float pa[4] = {a_sum[0], a_sum[1], a_sum[2], a_sum[3]};
-      float pb[4] = {b_sum[0], b_sum[1], b_sum[2], b_sum[3]};
+      float pc[4] = {c_sum[0], c_sum[1], c_sum[2], c_sum[3]};
+      const float* rf = ring + fld * GG::ringN * GG::Pr + 4 * u4;
+      float* vf = vs2 + fld * R * GG::P2 + 4 * u4;
 #pragma unroll
       for (int j = 0; j < R; ++j) {
-        if (v2ring && base + j - 2 * r - 1 >= 0) {
+        // rows leaving for j >= 2r+1 belong to this batch: part 2 handles them
+        if (j < 2 * r + 1 && v2ring && base + j - 2 * r - 1 >= 0) {
           int so = ring_old + j;
           if (so >= GG::ringN) so -= GG::ringN;
-          const float4 oa = lds4(ring + so * GG::Pr + 4 * tid);
-          const float4 ob = lds4(ring + (GG::ringN + so) * GG::Pr + 4 * tid);
-          pa[0] -= oa.x; pa[1] -= oa.y; pa[2] -= oa.z; pa[3] -= oa.w;
-          pb[0] -= ob.x; pb[1] -= ob.y; pb[2] -= ob.z; pb[3] -= ob.w;
+          const float4 o = lds4(rf + so * GG::Pr);
+          pc[0] -= o.x; pc[1] -= o.y; pc[2] -= o.z; pc[3] -= o.w;
         }
-        sts4(vs2 + j * GG::P2 + 4 * tid, pa[0], pa[1], pa[2], pa[3]);
-        sts4(vs2 + (R + j) * GG::P2 + 4 * tid, pb[0], pb[1], pb[2], pb[3]);
+        sts4(vf + j * GG::P2, pc[0], pc[1], pc[2], pc[3]);
       }
     }
 
     // ---- V1 -----------------------------------------------------------
     if (v1) {
+      // uniform fast path: every row and column of the batch inside the image
+      const bool fast = cols_in && base + R <= nrows && ya0 + base - r - 1 >= max(first_add, 0) &&
+                        ya0 + base + R - 1 + r < H;
+      float* out0 = vs + (2 * grp + 0) * R * GG::P1 + 4 * t4;
+      float* out1 = vs + (2 * grp + 1) * R * GG::P1 + 4 * t4;
 #pragma unroll
       for (int half = 0; half < 2; ++half) {
         float4 gl[R / 2], sl[R / 2];
@@ -223,41 +242,55 @@ __global__ void __launch_bounds__(320, 2) k_highres_fused(Args a) {
         for (int jj = 0; jj < R / 2; ++jj) {
           const int j = half * (R / 2) + jj;
           const int l = ya0 + base + j - r - 1;
+          const bool l_ok = fast || (col_ok && base + j < nrows && l >= first_add && l >= 0 && l < H);
           gl[jj] = sl[jj] = make_float4(0.f, 0.f, 0.f, 0.f);
-          if (col_ok && base + j < nrows && l >= first_add && l >= 0 && l < H) {
+          if (l_ok) {
             gl[jj] = __ldg(reinterpret_cast<const float4*>(G + (int64_t)l * W + gx4));
-            sl[jj] = __ldg(reinterpret_cast<const float4*>(S + (int64_t)l * W + gx4));
+            if (grp) sl[jj] = __ldg(reinterpret_cast<const float4*>(S + (int64_t)l * W + gx4));
           }
         }
 #pragma unroll
         for (int jj = 0; jj < R / 2; ++jj) {
           const int j = half * (R / 2) + jj;
-          const int e = ya0 + base + j + r;
-          const int l = ya0 + base + j - r - 1;
-          const bool e_ok = col_ok && base + j < nrows && e >= 0 && e < H;
-          const bool l_ok = col_ok && base + j < nrows && l >= first_add && l >= 0 && l < H;
-          const float4 ge4 = lds4(stg + j * GG::VW + 4 * tid);
-          const float4 se4 = lds4(stg + (R + j) * GG::VW + 4 * tid);
-          const float ge[4] = {ge4.x - sG, ge4.y - sG, ge4.z - sG, ge4.w - sG};
-          const float se[4] = {se4.x - sS, se4.y - sS, se4.z - sS, se4.w - sS};
-          const float go[4] = {gl[jj].x - sG, gl[jj].y - sG, gl[jj].z - sG, gl[jj].w - sG};
-          const float so[4] = {sl[jj].x - sS, sl[jj].y - sS, sl[jj].z - sS, sl[jj].w - sS};
+          const float4 ge4 = lds4(stg + j * GG::VW + 4 * t4);
+          float gn[4] = {ge4.x - sG, ge4.y - sG, ge4.z - sG, ge4.w - sG};
+          float gq[4] = {gl[jj].x - sG, gl[jj].y - sG, gl[jj].z - sG, gl[jj].w - sG};
+          float sn[4] = {0.f, 0.f, 0.f, 0.f}, sq[4] = {0.f, 0.f, 0.f, 0.f};
+          if (grp) {
+            const float4 se4 = lds4(stg + (R + j) * GG::VW + 4 * t4);
+            sn[0] = se4.x - sS; sn[1] = se4.y - sS; sn[2] = se4.z - sS; sn[3] = se4.w - sS;
+            sq[0] = sl[jj].x - sS; sq[1] = sl[jj].y - sS;
+            sq[2] = sl[jj].z - sS; sq[3] = sl[jj].w - sS;
+          }
+          if (!fast) {  // edge batch: zero the out-of-image contributions
+            const int e = ya0 + base + j + r;
+            const int l = ya0 + base + j - r - 1;
+            const bool e_ok = col_ok && base + j < nrows && e >= 0 && e < H;
+            const bool l_ok = col_ok && base + j < nrows && l >= first_add && l >= 0 && l < H;
 #pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            const float gn = e_ok ? ge[k] : 0.f, sn = e_ok ? se[k] : 0.f;
-            const float gq = l_ok ? go[k] : 0.f, sq = l_ok ? so[k] : 0.f;
-            s_g[k] += gn - gq;
-            s_gg[k] += gn * gn - gq * gq;
-            s_s[k] += sn - sq;
-            s_gs[k] += gn * sn - gq * sq;
+            for (int k = 0; k < 4; ++k) {
+              gn[k] = e_ok ? gn[k] : 0.f;
+              sn[k] = e_ok ? sn[k] : 0.f;
+              gq[k] = l_ok ? gq[k] : 0.f;
+              sq[k] = l_ok ? sq[k] : 0.f;
+            }
+          }
+          if (grp == 0) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              sA[k] += gn[k] - gq[k];
+              sB[k] += gn[k] * gn[k] - gq[k] * gq[k];
+            }
+          } else {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              sA[k] += sn[k] - sq[k];
+              sB[k] += gn[k] * sn[k] - gq[k] * sq[k];
+            }
           }
           const float m = col_ok ? 1.f : 0.f;
-          sts4(vs + (0 * R + j) * GG::P1 + 4 * tid, m * s_g[0], m * s_g[1], m * s_g[2], m * s_g[3]);
-          sts4(vs + (1 * R + j) * GG::P1 + 4 * tid, m * s_gg[0], m * s_gg[1], m * s_gg[2],
-               m * s_gg[3]);
-          sts4(vs + (2 * R + j) * GG::P1 + 4 * tid, m * s_s[0], m * s_s[1], m * s_s[2], m * s_s[3]);
-          sts4(vs + (3 * R + j) * GG::P1 + 4 * tid, m * s_gs[0], m * s_gs[1], m * s_gs[2],
-               m * s_gs[3]);
+          sts4(out0 + j * GG::P1, m * sA[0], m * sA[1], m * sA[2], m * sA[3]);
+          sts4(out1 + j * GG::P1, m * sB[0], m * sB[1], m * sB[2], m * sB[3]);
         }
       }
     }
@@ -310,19 +343,31 @@ __global__ void __launch_bounds__(320, 2) k_highres_fused(Args a) {
       const int gxa0 = x0 - r + xa0;  // global column of the run's first coefficient
       const bool interior = gxa0 >= r && gxa0 + KR - 1 + r <= W - 1 && xa0 + KR <= GG::W2;
       float A[KR], B[KR];
+      if (interior) {  // warp-uniform except at strip edges
+        const float inv = iny * inv_full;
 #pragma unroll
-      for (int k = 0; k < KR; ++k) {
-        const int gxa = gxa0 + k;
-        const bool ok = interior || (xa0 + k < GG::W2 && gxa >= 0 && gxa < W);
-        const float inv = interior ? iny * inv_full
-                                   : iny * fast_rcp((float)wlen(gxa, W, r));
-        const float mg = hs[0][k] * inv, ms = hs[2][k] * inv;
-        const float var = hs[1][k] * inv - mg * mg;
-        const float cov = hs[3][k] * inv - mg * ms;
-        if (ok && eps == 0.f && !(var > 0.f)) degen = true;
-        const float Ak = cov * fast_rcp(var + eps);
-        A[k] = ok ? Ak : 0.f;
-        B[k] = ok ? (ms + sS) - Ak * (mg + sG) : 0.f;
+        for (int k = 0; k < KR; ++k) {
+          const float mg = hs[0][k] * inv, ms = hs[2][k] * inv;
+          const float var = hs[1][k] * inv - mg * mg;
+          const float cov = hs[3][k] * inv - mg * ms;
+          if (eps == 0.f && !(var > 0.f)) degen = true;
+          A[k] = cov * fast_rcp(var + eps);
+          B[k] = (ms + sS) - A[k] * (mg + sG);
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < KR; ++k) {
+          const int gxa = gxa0 + k;
+          const bool ok = xa0 + k < GG::W2 && gxa >= 0 && gxa < W;
+          const float inv = iny * fast_rcp((float)wlen(gxa, W, r));
+          const float mg = hs[0][k] * inv, ms = hs[2][k] * inv;
+          const float var = hs[1][k] * inv - mg * mg;
+          const float cov = hs[3][k] * inv - mg * ms;
+          if (ok && eps == 0.f && !(var > 0.f)) degen = true;
+          const float Ak = cov * fast_rcp(var + eps);
+          A[k] = ok ? Ak : 0.f;
+          B[k] = ok ? (ms + sS) - Ak * (mg + sG) : 0.f;
+        }
       }
       sts4(ra, A[0], A[1], A[2], A[3]);
       sts4(ra + 4, A[4], A[5], A[6], A[7]);
@@ -333,26 +378,27 @@ __global__ void __launch_bounds__(320, 2) k_highres_fused(Args a) {
 
     // ---- V2 (part 2): add the entering coefficient rows ----------------
     if (v2) {
-      float na[4] = {0.f, 0.f, 0.f, 0.f}, nb[4] = {0.f, 0.f, 0.f, 0.f};
+      float nc[4] = {0.f, 0.f, 0.f, 0.f};
+      const float* rf = ring + fld * GG::ringN * GG::Pr + 4 * u4;
+      float* vf = vs2 + fld * R * GG::P2 + 4 * u4;
 #pragma unroll
       for (int j = 0; j < R; ++j) {
         if (v2ring && base + j < nrows) {
           int sn = ring_new + j;
           if (sn >= GG::ringN) sn -= GG::ringN;
-          const float4 xa = lds4(ring + sn * GG::Pr + 4 * tid);
-          const float4 xb = lds4(ring + (GG::ringN + sn) * GG::Pr + 4 * tid);
-          na[0] += xa.x; na[1] += xa.y; na[2] += xa.z; na[3] += xa.w;
-          nb[0] += xb.x; nb[1] += xb.y; nb[2] += xb.z; nb[3] += xb.w;
+          const float4 x = lds4(rf + sn * GG::Pr);
+          nc[0] += x.x; nc[1] += x.y; nc[2] += x.z; nc[3] += x.w;
+          if (j >= 2 * r + 1) {  // leaving row added earlier in this batch (r small)
+            int so = ring_new + j - 2 * r - 1;
+            if (so >= GG::ringN) so -= GG::ringN;
+            const float4 o = lds4(rf + so * GG::Pr);
+            nc[0] -= o.x; nc[1] -= o.y; nc[2] -= o.z; nc[3] -= o.w;
+          }
         }
-        float* pa = vs2 + j * GG::P2 + 4 * tid;
-        float* pb = vs2 + (R + j) * GG::P2 + 4 * tid;
-        const float4 oa = lds4(pa), ob = lds4(pb);
-        a_sum[0] = oa.x + na[0]; a_sum[1] = oa.y + na[1];
-        a_sum[2] = oa.z + na[2]; a_sum[3] = oa.w + na[3];
-        b_sum[0] = ob.x + nb[0]; b_sum[1] = ob.y + nb[1];
-        b_sum[2] = ob.z + nb[2]; b_sum[3] = ob.w + nb[3];
-        sts4(pa, a_sum[0], a_sum[1], a_sum[2], a_sum[3]);
-        sts4(pb, b_sum[0], b_sum[1], b_sum[2], b_sum[3]);
+        const float4 pv = lds4(vf + j * GG::P2);
+        c_sum[0] = pv.x + nc[0]; c_sum[1] = pv.y + nc[1];
+        c_sum[2] = pv.z + nc[2]; c_sum[3] = pv.w + nc[3];
+        sts4(vf + j * GG::P2, c_sum[0], c_sum[1], c_sum[2], c_sum[3]);
       }
     }
     ring_new += R;
