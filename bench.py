@@ -42,6 +42,8 @@ sys.path.insert(0, ROOT)
 
 METRIC = "guided-filter output Mpix/s (fwd, fwd+bwd) and % of HBM roofline"
 
+from paper_1803_05619_b200.sharding import batch_shard, row_bands  # noqa: E402
+
 
 # ---------------------------------------------------------------------------
 # workload descriptions
@@ -162,7 +164,7 @@ class OursStep:
     """Device-resident inputs; one step = one C-ABI layer call (plus, for the
     training config, the full pipeline)."""
 
-    def __init__(self, c, device, seed):
+    def __init__(self, c, device, seed, rank=0, world=1):
         import torch
 
         import workloads
@@ -189,11 +191,28 @@ class OursStep:
             self.launches = 1 if fused else 17
         else:
             f = c["factor"]
+            self.scaling = c.get("scaling", "weak")
+            if c.get("shard") == "batch":  # config 4a: the batch is split over ranks
+                b0, b1 = batch_shard(B, world, rank)
+                B = b1 - b0
             lr_x, lr_y, hr_x = workloads.joint_inputs(B, C, H, H, f, seed=seed, device=device)
+            self.B, self.H, self.W = B, H, H
+            self.pixels = B * H * H
+            if c.get("shard") == "rows":  # config 4b: row bands with the backward halo
+                band = row_bands(H // f, world, c["r"], factor=f, backward=True)[rank]
+                lo, hi = band.crop_lo, band.crop_hi
+                Hlo, Hhi = band.hr_crop
+                lr_x = lr_x[:, :, lo:hi].contiguous()
+                lr_y = lr_y[:, :, lo:hi].contiguous()
+                hr_x = hr_x[:, :, Hlo:Hhi].contiguous()
+                self.H = Hhi - Hlo
+                A0, A1 = band.hr_owned
+                self.pixels = B * (A1 - A0) * H  # owned output rows only
+                torch.cuda.empty_cache()
             self.inputs = [lr_x, lr_y, hr_x]
-            self.h = H // f
+            self.h, self.w = self.H // f, self.W // f
             self.out = torch.empty_like(hr_x)
-            nb = self.lib.gf_joint_workspace_bytes(0, B, C, self.h, self.h, H, H, c["r"])
+            nb = self.lib.gf_joint_workspace_bytes(0, B, C, self.h, self.w, self.H, self.W, c["r"])
             self.ws = torch.empty(max(nb, 16), dtype=torch.uint8, device=device)
             if kind in ("joint_fwd_bwd", "train_step"):
                 self.d_out = torch.randn(hr_x.shape, generator=g).to(device)
@@ -209,11 +228,13 @@ class OursStep:
                                            rng=np.random.default_rng(seed), device=device)
                 self.target = workloads.affine_target(hr_x).contiguous()
                 self.params = gfb.GuidedFilterParams(c["r"], c["eps"])
-            fused = self.lib.gf_joint_is_fused(0, B, C, self.h, self.h, H, H, c["r"])
+            fused = self.lib.gf_joint_is_fused(0, B, C, self.h, self.w, self.H, self.W, c["r"])
             fwd = 1 if fused else 12
-            bwd = 3 if fused else 26
+            bwd = 2 if fused else 26
+            # train step: 2 x (stats, norm, fwd) guidance, GF fwd, mse (2), GF bwd,
+            # 2 x (stats, norm, bwd1, sum1, dx, dw1, final) guidance backward
             self.launches = {"joint_fwd": fwd, "joint_fwd_bwd": fwd + bwd,
-                             "train_step": 2 * 3 + fwd + 2 + bwd + 2 * 8}[kind]
+                             "train_step": 2 * 3 + fwd + 2 + bwd + 2 * 7}[kind]
 
     def step(self):
         c, L = self.c, self.lib
@@ -226,16 +247,17 @@ class OursStep:
             assert rc == 0, L.gf_last_error()
         elif self.kind in ("joint_fwd", "joint_fwd_bwd"):
             lx, ly, hx = self.inputs
-            h = self.h
+            B, h, w, Hh, Ww = self.B, self.h, self.w, self.H, self.W
             rc = L.gf_joint_fwd(0, lx.data_ptr(), ly.data_ptr(), hx.data_ptr(),
-                                self.out.data_ptr(), B, C, h, h, H, H, r, eps, self.ws.data_ptr(),
-                                self.ws.numel(), self.status.data_ptr(), self.sp)
+                                self.out.data_ptr(), B, C, h, w, Hh, Ww, r, eps,
+                                self.ws.data_ptr(), self.ws.numel(), self.status.data_ptr(),
+                                self.sp)
             assert rc == 0, L.gf_last_error()
             if self.kind == "joint_fwd_bwd":
                 rc = L.gf_joint_bwd(0, lx.data_ptr(), ly.data_ptr(), hx.data_ptr(),
                                     self.d_out.data_ptr(), self.d_lr_x.data_ptr(),
-                                    self.d_lr_y.data_ptr(), self.d_hr_x.data_ptr(), B, C, h, h, H,
-                                    H, r, eps, self.ws.data_ptr(), self.ws.numel(),
+                                    self.d_lr_y.data_ptr(), self.d_hr_x.data_ptr(), B, C, h, w,
+                                    Hh, Ww, r, eps, self.ws.data_ptr(), self.ws.numel(),
                                     self.status.data_ptr(), self.sp)
                 assert rc == 0, L.gf_last_error()
         else:  # train_step
@@ -378,8 +400,9 @@ def run_reference(args, c, rank, world):
 
 def config_block(args, c, world):
     B, C, H = c["batch"], c["channels"], c["hr"]
-    blk = {"workload": f"{args.config}: {c['kind']}", "batch_per_gpu": B, "channels": C,
-           "hr": [H, H], "radius": c["r"], "eps": c["eps"], "parallelism": f"batch-shard x{world}"}
+    blk = {"workload": f"{args.config}: {c['kind']}",
+           "batch_per_gpu": (B if not c.get("shard") else f"{B} split over {world}"), "channels": C,
+           "hr": [H, H], "radius": c["r"], "eps": c["eps"], "parallelism": (f"row-bands x{world} (lr halo max(2r,r+1))" if c.get("shard") == "rows" else f"batch-shard x{world}")}
     if c["kind"] == "highres_fwd":
         blk["guide_channels"] = 1
     else:
@@ -431,7 +454,8 @@ def main():
 
         dist.init_process_group("nccl", device_id=device)
 
-    st = OursStep(c, device, seed=args.seed + 1000 * rank)
+    st = OursStep(c, device, seed=args.seed + (0 if c.get("shard") else 1000 * rank), rank=rank,
+                  world=world)
     flush = None
     if algorithmic_bytes(c) <= 2.5 * 126e6:
         flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=device)
@@ -474,7 +498,13 @@ def main():
         ms = float(t.item())
     assert int(st.status.item()) == 0, f"status bits {int(st.status.item())}"
 
-    px = st.pixels * world
+    if c.get("shard"):  # strong scaling: the ranks split one fixed workload
+        t = torch.tensor([float(st.pixels)], device=device, dtype=torch.float64)
+        if dist:
+            dist.all_reduce(t)
+        px = float(t.item())
+    else:
+        px = st.pixels * world
     value = px / (ms * 1e-3) / 1e6
 
     e2e = None
@@ -494,7 +524,8 @@ def main():
         return
 
     peak, peak_kind = measured_peak()
-    alg = algorithmic_bytes(c)
+    # the dominant kernels process this rank's share of the workload
+    alg = int(algorithmic_bytes(c) * st.pixels / (c["batch"] * c["hr"] * c["hr"]))
     achieved = alg / (ms * 1e-3) / 1e9
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "traffic": ncu_traffic(args.config),
@@ -511,7 +542,8 @@ def main():
     line = {
         "metric": METRIC, "value": round(value, 3), "unit": "Mpix/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 5),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "higher_is_better": True, "scaling": "strong" if c.get("shard") else "weak",
+        "vs_baseline": None, "dtype": "f32",
         "data": "synthetic (seeded; BASELINE.json shapes and distributions, workloads.py)",
         "config": config_block(args, c, world),
         "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,

@@ -120,7 +120,7 @@ CONFIGS = {
                  hidden=15),
     "cfg3": dict(kind="joint_fwd", batch=16, channels=3, hr=4096, factor=4, r=8, eps=1e-4),
     "cfg4a": dict(kind="joint_fwd_bwd", batch=64, channels=3, hr=3072, factor=4, r=2,
-                  eps=1e-4),
+                  eps=1e-4, shard="batch"),
     "cfg4b": dict(kind="joint_fwd_bwd", batch=1, channels=3, hr=16384, factor=4, r=2,
-                  eps=1e-4),
+                  eps=1e-4, shard="rows"),
 }
