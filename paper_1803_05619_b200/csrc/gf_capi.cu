@@ -327,12 +327,12 @@ int64_t gn_param_count(int64_t Cin, int64_t Cout, int64_t hidden) {
 
 size_t gn_workspace_bytes(int dtype, int64_t B, int64_t Cin, int64_t Cout, int64_t hidden,
                           int64_t H, int64_t W) {
-  (void)dtype;
-  (void)Cin;
-  (void)Cout;
-  (void)H;
-  (void)W;
-  return gfb::gn_ws_bytes(B, hidden);
+  size_t gen = gfb::gn_ws_bytes(B, hidden);
+  if (dtype == GF_F32 && gfb::gn_fast_ok(Cin, Cout, hidden, H * W)) {
+    size_t fast = gfb::gn_fast_ws_bytes(B, hidden);
+    return fast > gen ? fast : gen;
+  }
+  return gen;
 }
 
 static int check_gn(int dtype, int64_t B, int64_t Cin, int64_t Cout, int64_t hidden, int64_t H,
@@ -342,7 +342,7 @@ static int check_gn(int dtype, int64_t B, int64_t Cin, int64_t Cout, int64_t hid
   if (!gfb::gn_supported(Cin, Cout, hidden))
     return fail(GF_ERR_UNSUPPORTED, "guidance net limits: Cin<=4, Cout<=4, hidden<=64 (got %lld, %lld, %lld)",
                 (long long)Cin, (long long)Cout, (long long)hidden);
-  size_t need = gfb::gn_ws_bytes(B, hidden);
+  size_t need = gn_workspace_bytes(dtype, B, Cin, Cout, hidden, H, W);
   if (ws_bytes < need) return fail(GF_ERR_WORKSPACE, "gn workspace %zu < %zu bytes", ws_bytes, need);
   return GF_OK;
 }
@@ -351,6 +351,12 @@ int gn_forward(int dtype, const void* x, void* y, const void* params, int64_t B,
                int64_t Cout, int64_t hidden, int64_t H, int64_t W, void* workspace,
                size_t workspace_bytes, uint32_t* status, void* stream) {
   if (int e = check_gn(dtype, B, Cin, Cout, hidden, H, W, workspace_bytes)) return e;
+  if (!g_force_generic && dtype == GF_F32 && gfb::gn_fast_ok(Cin, Cout, hidden, H * W) &&
+      aligned16(x) && aligned16(y)) {
+    gfb::gn_fast_forward((const float*)x, (float*)y, (const float*)params, B, hidden, H * W,
+                         workspace, status, S(stream));
+    return check_launch("gn_forward[fused]");
+  }
   if (dtype == GF_F32)
     gfb::gn_forward_impl<float>((const float*)x, (float*)y, (const float*)params, B, Cin, Cout,
                                 hidden, H * W, workspace, status, S(stream));
@@ -365,6 +371,13 @@ int gn_backward(int dtype, const void* x, const void* dy, void* dx, void* dparam
                 int64_t H, int64_t W, void* workspace, size_t workspace_bytes, uint32_t* status,
                 void* stream) {
   if (int e = check_gn(dtype, B, Cin, Cout, hidden, H, W, workspace_bytes)) return e;
+  if (!g_force_generic && dtype == GF_F32 && gfb::gn_fast_ok(Cin, Cout, hidden, H * W) &&
+      aligned16(x) && aligned16(dy) && aligned16(dx)) {
+    gfb::gn_fast_backward((const float*)x, (const float*)dy, (float*)dx, (float*)dparams,
+                          accumulate, (const float*)params, B, hidden, H * W, workspace, status,
+                          S(stream));
+    return check_launch("gn_backward[fused]");
+  }
   if (dtype == GF_F32)
     gfb::gn_backward_impl<float>((const float*)x, (const float*)dy, (float*)dx, (float*)dparams,
                                  accumulate, (const float*)params, B, Cin, Cout, hidden, H * W,

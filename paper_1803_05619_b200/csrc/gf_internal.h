@@ -72,3 +72,14 @@ void fused_joint_bwd(const float* lr_x, const float* lr_y, const float* hr_x, co
                      uint32_t* status, cudaStream_t s);
 
 }  // namespace gfb
+
+namespace gfb {
+// fused fp32 guidance net (Cin = Cout = 3, hidden in {4, 8, 15, 16})
+bool gn_fast_ok(int64_t Cin, int64_t Cout, int64_t hidden, int64_t HW);
+size_t gn_fast_ws_bytes(int64_t B, int64_t hidden);
+void gn_fast_forward(const float* x, float* y, const float* params, int64_t B, int64_t hidden,
+                     int64_t HW, void* ws, uint32_t* status, cudaStream_t s);
+void gn_fast_backward(const float* x, const float* dy, float* dx, float* dparams, int accumulate,
+                      const float* params, int64_t B, int64_t hidden, int64_t HW, void* ws,
+                      uint32_t* status, cudaStream_t s);
+}  // namespace gfb

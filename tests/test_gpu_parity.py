@@ -468,3 +468,47 @@ def test_fused_joint_nonfinite_input_is_input_error(gfb):
     hr_x[0, 2, 5, 5] = float("inf")
     with pytest.raises(ValueError, match="input"):
         gfb.forward_joint(lr_x, hr_x, lr_y, gfb.GuidedFilterParams(1, 1e-4))
+
+
+@pytest.mark.parametrize("hidden", [4, 8, 15, 16])
+def test_fused_guidance_net_vs_oracle(gfb, hidden):
+    from paper_1803_05619_b200 import _lib
+
+    rng = np.random.default_rng(hidden)
+    params = O.guidance_init(3, 3, hidden, rng)
+    params["norm.norm_gain"] = np.array([0.6])
+    params["norm.gain"] = np.array([0.9])
+    params["conv2.bias"] = rng.uniform(-0.1, 0.1, 3)
+    params = {k: np.asarray(v, np.float32).astype(np.float64) for k, v in params.items()}
+    B, H, W = 2, 48, 64
+    x = rng.uniform(0, 1, (B, 3, H, W)).astype(np.float32)
+    dy = rng.standard_normal((B, 3, H, W)).astype(np.float32)
+    net = gfb.GuidanceNet(3, 3, hidden=hidden)
+    net.load_parameters(params)
+    y, tape = net.forward(t32(x))
+    dx, grads = net.backward(tape, t32(dy))
+    want_y, want_dx = [], []
+    want_g = {k: 0.0 for k in params}
+    for n in range(B):
+        xh = x[n].transpose(1, 2, 0).astype(np.float64)
+        yy, tp = O.guidance_forward(params, xh)
+        dxx, gg = O.guidance_backward(params, tp, dy[n].transpose(1, 2, 0).astype(np.float64))
+        want_y.append(yy.transpose(2, 0, 1))
+        want_dx.append(dxx.transpose(2, 0, 1))
+        for k in gg:
+            want_g[k] = want_g[k] + gg[k]
+    assert abs_max(npy(y), np.stack(want_y)) <= 1e-5
+    assert rel_max(npy(dx), np.stack(want_dx)) <= GRAD_TOL32
+    scale = max(float(np.abs(v).max()) for v in want_g.values())
+    for k, v in grads.items():
+        assert abs_max(npy(v), want_g[k]) <= GRAD_TOL32 * scale, k
+    # the general kernels agree with the fused ones
+    lib = _lib.load()
+    old = lib.gf_force_generic(1)
+    try:
+        y2, tape2 = net.forward(t32(x))
+        dx2, _ = net.backward(tape2, t32(dy))
+    finally:
+        lib.gf_force_generic(old)
+    assert abs_max(npy(y2), npy(y)) <= 1e-5
+    assert rel_max(npy(dx2), npy(dx)) <= GRAD_TOL32
