@@ -316,6 +316,27 @@ __global__ void k_mse(const T* __restrict__ out, const T* __restrict__ tgt, T* _
   block_reduce_store<1>(acc, partials + b * gridDim.x + blockIdx.x);
 }
 
+// fp32 fast path: 128-bit accesses, fp32 per-thread sums (a few hundred
+// elements each), float64 across threads and blocks
+__global__ void k_mse4(const float* __restrict__ out, const float* __restrict__ tgt,
+                       float* __restrict__ d_out, double* __restrict__ partials, int64_t per_image,
+                       float scale2) {
+  const int64_t b = blockIdx.y;
+  const float4* o4 = reinterpret_cast<const float4*>(out + b * per_image);
+  const float4* t4 = reinterpret_cast<const float4*>(tgt + b * per_image);
+  float4* d4 = reinterpret_cast<float4*>(d_out + b * per_image);
+  float s = 0.f;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < per_image / 4;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const float4 o = __ldg(o4 + i), t = __ldg(t4 + i);
+    const float e0 = o.x - t.x, e1 = o.y - t.y, e2 = o.z - t.z, e3 = o.w - t.w;
+    s = fmaf(e0, e0, fmaf(e1, e1, fmaf(e2, e2, fmaf(e3, e3, s))));
+    d4[i] = make_float4(scale2 * e0, scale2 * e1, scale2 * e2, scale2 * e3);
+  }
+  double acc[1] = {(double)s};
+  block_reduce_store<1>(acc, partials + b * gridDim.x + blockIdx.x);
+}
+
 __global__ void k_mse_final(const double* __restrict__ partials, double* __restrict__ loss,
                             int64_t B, int nblk, double per_image) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
@@ -391,7 +412,7 @@ void gn_backward_impl(const T* x, const T* dy, T* dx, T* dparams, int accumulate
   k_gn_final<T><<<1, 256, 0, s>>>(S1, pw1, dparams, accumulate, d, kGnBlocks);
 }
 
-constexpr int kMseBlocks = 64;
+constexpr int kMseBlocks = 256;  // per image
 
 size_t mse_ws_bytes(int64_t B) { return (size_t)B * kMseBlocks * sizeof(double); }
 
@@ -400,8 +421,15 @@ void mse_impl(const T* out, const T* tgt, T* d_out, double* loss, int64_t B, int
               void* ws, cudaStream_t s) {
   double* partials = (double*)ws;
   double scale = 1.0 / (double)per_image / (double)B;
-  k_mse<T><<<dim3(kMseBlocks, (unsigned)B), kGnThreads, 0, s>>>(out, tgt, d_out, partials,
-                                                                 per_image, scale);
+  if (sizeof(T) == 4 && per_image % 4 == 0 && ((uintptr_t)out & 15) == 0 &&
+      ((uintptr_t)tgt & 15) == 0 && ((uintptr_t)d_out & 15) == 0) {
+    k_mse4<<<dim3(kMseBlocks, (unsigned)B), kGnThreads, 0, s>>>(
+        (const float*)out, (const float*)tgt, (float*)d_out, partials, per_image,
+        (float)(2.0 * scale));
+  } else {
+    k_mse<T><<<dim3(kMseBlocks, (unsigned)B), kGnThreads, 0, s>>>(out, tgt, d_out, partials,
+                                                                   per_image, scale);
+  }
   k_mse_final<<<1, 32, 0, s>>>(partials, loss, B, kMseBlocks, (double)per_image);
 }
 

@@ -117,11 +117,14 @@ __global__ void k_prep(const double* __restrict__ part, const float* __restrict_
                        float* __restrict__ fold, int64_t HW, int nblk) {
   const int b = blockIdx.x;
   const int j = threadIdx.x;
+  __shared__ double S[9];
+  if (j < 9) {  // one thread per statistic, fixed block order
+    double s = 0.0;
+    for (int k = 0; k < nblk; ++k) s += part[((int64_t)b * nblk + k) * 9 + j];
+    S[j] = s;
+  }
+  __syncthreads();
   if (j >= HID) return;
-  double S[9];
-  for (int v = 0; v < 9; ++v) S[v] = 0.0;
-  for (int k = 0; k < nblk; ++k)
-    for (int v = 0; v < 9; ++v) S[v] += part[((int64_t)b * nblk + k) * 9 + v];
   const double N = (double)HW;
   const double m[3] = {S[0] / N, S[1] / N, S[2] / N};
   const int ix[3][3] = {{3, 4, 5}, {4, 6, 7}, {5, 7, 8}};
@@ -385,6 +388,17 @@ __global__ void __launch_bounds__(NT) k_bwd_b(const float* __restrict__ x,
   reduce_store<NV>(fa, part + (b * gridDim.x + blockIdx.x) * NV);
 }
 
+// ---- per-image dW1 sums of the pass-B partials (fixed block order) --------
+template <int HID>
+__global__ void k_fin_b(const double* __restrict__ partb, double* __restrict__ pbi, int nblk) {
+  const int64_t b = blockIdx.x;
+  const int v = threadIdx.x;
+  if (v >= HID * CI) return;
+  double s = 0.0;
+  for (int k = 0; k < nblk; ++k) s += partb[(b * nblk + k) * (HID * CI) + v];
+  pbi[b * (HID * CI) + v] = s;
+}
+
 // ---- final parameter gradients (one block; fixed order over images) -------
 template <int HID>
 __global__ void k_fin_params(const double* __restrict__ gsum, const double* __restrict__ partb,
@@ -393,8 +407,7 @@ __global__ void k_fin_params(const double* __restrict__ gsum, const double* __re
   for (int idx = threadIdx.x; idx < P<HID>::count; idx += blockDim.x) {
     double s = 0.0;
     if (idx < HID * CI) {
-      for (int64_t b = 0; b < B; ++b)
-        for (int k = 0; k < nblk; ++k) s += partb[(b * nblk + k) * (HID * CI) + idx];
+      for (int64_t b = 0; b < B; ++b) s += partb[b * (HID * CI) + idx];  // per-image sums
     } else if (idx == P<HID>::gain) {
       for (int64_t b = 0; b < B; ++b) s += gsum[b * GS + CO * HID + CO];
     } else if (idx == P<HID>::ng) {
@@ -461,7 +474,9 @@ void backward(const float* x, const float* dy, float* dx, float* dparams, int ac
   k_bwd_a<HID><<<grid, NT, 0, s>>>(x, dy, params, fold, pa, HW);
   k_fin_a<HID><<<(unsigned)B, 128, 0, s>>>(pa, params, fold, coef, gsum, HW, kBlocks);
   k_bwd_b<HID><<<grid, NT, 0, s>>>(x, dy, dx, params, fold, coef, pb, HW);
-  k_fin_params<HID><<<1, 128, 0, s>>>(gsum, pb, dparams, accumulate, B, kBlocks);
+  // per-image dW1 sums land in `stats` (free after prep), then the batch sum
+  k_fin_b<HID><<<(unsigned)B, 64, 0, s>>>(pb, stats, kBlocks);
+  k_fin_params<HID><<<1, 128, 0, s>>>(gsum, stats, dparams, accumulate, B, kBlocks);
 }
 
 }  // namespace gnf

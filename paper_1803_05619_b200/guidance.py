@@ -96,6 +96,18 @@ class GuidanceNet:
             v = params[k]
             v = torch.as_tensor(np.asarray(v) if not isinstance(v, torch.Tensor) else v)
             self.flat[sl] = v.to(self.device, torch.float64).reshape(-1)
+        self._cast = {}
+
+    def _params_as(self, dtype):
+        """Packed parameters in the compute dtype, cast once per load."""
+        if dtype == torch.float64:
+            return self.flat
+        cache = self.__dict__.setdefault("_cast", {})
+        key = (dtype, self.flat._version)  # in-place edits of parameters() bump it
+        if key not in cache:
+            cache.clear()
+            cache[key] = self.flat.to(dtype)
+        return cache[key]
 
     def _check_x(self, im: Img, n_ch: int, what: str):
         if im.shape[1] != n_ch:
@@ -107,7 +119,7 @@ class GuidanceNet:
         B, _, H, W = im.shape
         lib = _lib.load()
         dt = dtype_code(im.t)
-        params = self.flat.to(im.t.dtype)
+        params = self._params_as(im.t.dtype)
         y = torch.empty((B, self.out_ch, H, W), dtype=im.t.dtype, device=self.device)
         status = Status(self.device)
         ws = workspace(lib.gn_workspace_bytes(dt, B, self.in_ch, self.out_ch, self.hidden, H, W),
@@ -132,7 +144,7 @@ class GuidanceNet:
             raise ValueError(f"dy shape {d.shape} does not match output {(B, self.out_ch, H, W)}")
         lib = _lib.load()
         dt = dtype_code(im.t)
-        params = self.flat.to(im.t.dtype)
+        params = self._params_as(im.t.dtype)
         dx = torch.empty_like(im.t)
         if dparams is None:
             dparams = torch.zeros(self.param_count(), dtype=im.t.dtype, device=self.device)
