@@ -339,14 +339,25 @@ __global__ void k_mse4(const float* __restrict__ out, const float* __restrict__ 
 
 __global__ void k_mse_final(const double* __restrict__ partials, double* __restrict__ loss,
                             int64_t B, int nblk, double per_image) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  // one warp per image sums its block partials (fixed lane order), then
+  // thread 0 adds the images in order
+  __shared__ double img[32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   double total = 0.0;
-  for (int64_t b = 0; b < B; ++b) {
-    double s = 0.0;
-    for (int k = 0; k < nblk; ++k) s += partials[b * nblk + k];
-    total += (s / per_image) / (double)B;
+  for (int64_t b0 = 0; b0 < B; b0 += 32) {
+    const int64_t b = b0 + warp;
+    if (warp < 32 && b < B) {
+      double s = 0.0;
+      for (int k = lane; k < nblk; k += 32) s += partials[b * nblk + k];
+      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+      if (lane == 0) img[warp] = s;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0)
+      for (int64_t k = 0; k < 32 && b0 + k < B; ++k) total += (img[k] / per_image) / (double)B;
+    __syncthreads();
   }
-  *loss = total;
+  if (threadIdx.x == 0) *loss = total;
 }
 
 // ===========================================================================
@@ -430,7 +441,7 @@ void mse_impl(const T* out, const T* tgt, T* d_out, double* loss, int64_t B, int
     k_mse<T><<<dim3(kMseBlocks, (unsigned)B), kGnThreads, 0, s>>>(out, tgt, d_out, partials,
                                                                    per_image, scale);
   }
-  k_mse_final<<<1, 32, 0, s>>>(partials, loss, B, kMseBlocks, (double)per_image);
+  k_mse_final<<<1, 1024, 0, s>>>(partials, loss, B, kMseBlocks, (double)per_image);
 }
 
 #define GN_INST(T)                                                                            \
