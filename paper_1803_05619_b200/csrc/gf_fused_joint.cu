@@ -90,9 +90,10 @@ __device__ inline SmemCoef carve(float* base, int r) {
 }
 
 // A (and b) for low-res cells [i0-1, i0+TLY] x [k0-1, k0+TLX] of one plane.
-template <bool NEED_B>
+template <int RAD, bool NEED_B>
 __device__ void lr_coeffs(const float* __restrict__ X, const float* __restrict__ Y, int h, int w,
-                          int i0, int k0, int r, float eps, const SmemCoef& sm, bool& degen) {
+                          int i0, int k0, float eps, const SmemCoef& sm, bool& degen) {
+  constexpr int r = RAD;
   const int RI = RA + 2 * r, CI = CA + 2 * r;
   const int tid = threadIdx.x;
   // per-CTA shift (var/cov are shift invariant); any in-image sample works
@@ -235,9 +236,10 @@ __device__ __forceinline__ void hrow(const float* __restrict__ row, const ColTap
   }
 }
 
+template <int RAD>
 __global__ void __launch_bounds__(NT) k_joint_fwd(FwdArgs a) {
   extern __shared__ float4 smem4[];
-  const int r = a.r;
+  constexpr int r = RAD;
   const SmemCoef sm = carve(reinterpret_cast<float*>(smem4), r);
   const int64_t p = blockIdx.z;
   const int i0 = blockIdx.y * TLY, k0 = blockIdx.x * TLX;
@@ -258,8 +260,8 @@ __global__ void __launch_bounds__(NT) k_joint_fwd(FwdArgs a) {
   }
   // 2) coefficients of the block
   bool degen = false;
-  lr_coeffs<true>(a.lr_x + p * (int64_t)a.h * a.w, a.lr_y + p * (int64_t)a.h * a.w, a.h, a.w, i0,
-                  k0, r, a.eps, sm, degen);
+  lr_coeffs<RAD, true>(a.lr_x + p * (int64_t)a.h * a.w, a.lr_y + p * (int64_t)a.h * a.w, a.h, a.w, i0,
+                  k0, a.eps, sm, degen);
   // 3) apply
   const ColTaps ct = col_taps(X0, a.w, k0);
   // local coefficient rows 2*warp .. 2*warp+3 cover every tap of rows Yb..Yb+7
@@ -329,9 +331,10 @@ __host__ __device__ inline size_t bwd_hr_smem_floats(int r) {
   return coef_smem_floats(r) + (size_t)2 * GR * TLX;
 }
 
+template <int RAD>
 __global__ void __launch_bounds__(NT) k_joint_bwd_hr(BwdHrArgs a) {
   extern __shared__ float4 smem4[];
-  const int r = a.r;
+  constexpr int r = RAD;
   float* base = reinterpret_cast<float*>(smem4);
   const SmemCoef sm = carve(base, r);
   float* R1 = base + coef_smem_floats(r);  // [GR][TLX]
@@ -355,8 +358,8 @@ __global__ void __launch_bounds__(NT) k_joint_bwd_hr(BwdHrArgs a) {
     if (col_ok && Y < a.H) dv[t] = __ldg(reinterpret_cast<const float4*>(D + (int64_t)Y * a.W + X0));
   }
   bool degen = false;
-  lr_coeffs<false>(a.lr_x + p * (int64_t)a.h * a.w, a.lr_y + p * (int64_t)a.h * a.w, a.h, a.w,
-                   i0, k0, r, a.eps, sm, degen);
+  lr_coeffs<RAD, false>(a.lr_x + p * (int64_t)a.h * a.w, a.lr_y + p * (int64_t)a.h * a.w, a.h, a.w,
+                   i0, k0, a.eps, sm, degen);
   // d_hr = d_out * Up(A)
   {
     const ColTaps ct = col_taps(X0, a.w, k0);
@@ -480,9 +483,10 @@ __host__ __device__ inline size_t bwd_lr_smem_floats(int r) {
   return (size_t)2 * NI * NI + (size_t)4 * NM * NI + (size_t)4 * NM * NM;
 }
 
+template <int RAD>
 __global__ void __launch_bounds__(NT) k_joint_bwd_lr(BwdLrArgs a) {
   extern __shared__ float4 smem4[];
-  const int r = a.r;
+  constexpr int r = RAD;
   const int NI = TL + 4 * r, NM = TL + 2 * r;
   float* xs = reinterpret_cast<float*>(smem4);
   float* ys = xs + NI * NI;
@@ -659,15 +663,52 @@ static void set_smem(const void* fn, size_t bytes) {
   if (bytes > 48 * 1024) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
 }
 
+// kernels are instantiated per radius (0..kMaxRadius) so window loops unroll
+struct JointFns {
+  const void* fwd;
+  const void* bwd_hr;
+  const void* bwd_lr;
+};
+
+template <int RAD>
+static JointFns joint_fns() {
+  return {(const void*)jf::k_joint_fwd<RAD>, (const void*)jf::k_joint_bwd_hr<RAD>,
+          (const void*)jf::k_joint_bwd_lr<RAD>};
+}
+
+static JointFns pick_joint(int r) {
+  switch (r) {
+    case 0: return joint_fns<0>();
+    case 1: return joint_fns<1>();
+    case 2: return joint_fns<2>();
+    case 3: return joint_fns<3>();
+    case 4: return joint_fns<4>();
+    case 5: return joint_fns<5>();
+    case 6: return joint_fns<6>();
+    case 7: return joint_fns<7>();
+    case 8: return joint_fns<8>();
+    case 9: return joint_fns<9>();
+    case 10: return joint_fns<10>();
+    case 11: return joint_fns<11>();
+    default: return joint_fns<12>();
+  }
+}
+
+static void launch(const void* fn, dim3 grid, size_t smem, cudaStream_t s, void* arg) {
+  void* args[] = {arg};
+  cudaLaunchKernel(fn, grid, dim3(jf::NT), args, smem, s);
+}
+
 void fused_joint_fwd(const float* lr_x, const float* lr_y, const float* hr_x, float* out, int64_t B,
                      int64_t C, int64_t h, int64_t w, int64_t H, int64_t W, int r, float eps,
                      uint32_t* status, cudaStream_t s) {
+  const JointFns fns = pick_joint(r);
   const size_t smem = jf::coef_smem_floats(r) * sizeof(float);
-  set_smem((const void*)jf::k_joint_fwd, smem);
+  set_smem(fns.fwd, smem);
   dim3 grid((unsigned)((w + jf::TLX - 1) / jf::TLX), (unsigned)((h + jf::TLY - 1) / jf::TLY),
             (unsigned)(B * C));
   jf::FwdArgs a{lr_x, lr_y, hr_x, out, (int)h, (int)w, (int)H, (int)W, r, eps, status};
-  jf::k_joint_fwd<<<grid, jf::NT, smem, s>>>(a);
+  launch(fns.fwd, grid, smem, s, &a);
 }
 
 size_t fused_joint_bwd_ws_bytes(int64_t B, int64_t C, int64_t h, int64_t w) {
@@ -680,22 +721,23 @@ void fused_joint_bwd(const float* lr_x, const float* lr_y, const float* hr_x, co
                      uint32_t* status, cudaStream_t s) {
   float* db = (float*)ws;
   float* dA = db + B * C * h * w;
+  const JointFns fns = pick_joint(r);
   {
     const size_t smem = jf::bwd_hr_smem_floats(r) * sizeof(float);
-    set_smem((const void*)jf::k_joint_bwd_hr, smem);
+    set_smem(fns.bwd_hr, smem);
     dim3 grid((unsigned)((w + jf::TLX - 1) / jf::TLX), (unsigned)((h + jf::TLY - 1) / jf::TLY),
               (unsigned)(B * C));
     jf::BwdHrArgs a{lr_x, lr_y, hr_x, d_out, d_hr_x, db, dA, (int)h, (int)w, (int)H, (int)W, r,
                     eps, status};
-    jf::k_joint_bwd_hr<<<grid, jf::NT, smem, s>>>(a);
+    launch(fns.bwd_hr, grid, smem, s, &a);
   }
   {
     const size_t smem = jf::bwd_lr_smem_floats(r) * sizeof(float);
-    set_smem((const void*)jf::k_joint_bwd_lr, smem);
+    set_smem(fns.bwd_lr, smem);
     dim3 grid((unsigned)((w + jf::TL - 1) / jf::TL), (unsigned)((h + jf::TL - 1) / jf::TL),
               (unsigned)(B * C));
     jf::BwdLrArgs a{lr_x, lr_y, db, dA, d_lr_x, d_lr_y, (int)h, (int)w, r, eps};
-    jf::k_joint_bwd_lr<<<grid, jf::NT, smem, s>>>(a);
+    launch(fns.bwd_lr, grid, smem, s, &a);
   }
 }
 
