@@ -63,7 +63,7 @@ struct Geo {
   static constexpr int v2w = up4(cmax(ringw, TX - KR + 4 * nv2));
   static constexpr int P2 = pitch4(v2w);
   static constexpr int nt = 32 * cmax(cmax((nq1 + 3) / 4, TX / KR / 4),
-                                      cmax((VW + 31) / 32, (v2w / 2 + 31) / 32));
+                                      cmax((VW / 2 + 31) / 32, (v2w / 2 + 31) / 32));
   static constexpr size_t smem_floats = (size_t)2 * R * VW + (size_t)4 * R * P1 +
                                         (size_t)2 * ringN * Pr + (size_t)2 * R * P2;
   static constexpr size_t smem_bytes = smem_floats * sizeof(float);
@@ -158,30 +158,36 @@ __global__ void __launch_bounds__(320, 2) k_highres_fused(Args a) {
   };
   prefetch(0);
 
-  // ---- level-1 state: V1T threads per field (g, g^2, s, g*s); a thread owns
-  //      vs columns 4t..4t+3 of its field, so the whole CTA shares V1
+  // ---- level-1 state: V1T threads per field group; group 0 keeps the guide
+  //      sums (g, g^2), group 1 the source sums (s, g*s); thread owns vs
+  //      columns 4t..4t+3 of its group
   constexpr int V1T = GG::VW / 4;
-  const int fld1 = tid / V1T;  // 0: g, 1: g^2, 2: s, 3: g*s (4+: idle in V1)
-  const int t4 = tid - fld1 * V1T;
-  const bool v1 = fld1 < 4;
-  const bool needG = fld1 != 2, needS = fld1 >= 2;
+  const int grp = tid < V1T ? 0 : 1;
+  const int t4 = tid - grp * V1T;
+  const bool v1 = tid < 2 * V1T;
   const int gx4 = xs0 + 4 * t4;
   const bool col_ok = v1 && gx4 >= 0 && gx4 < W;  // W % 4 == 0: all 4 or none
   const bool cols_in = xs0 >= 0 && xs0 + GG::VW <= W;  // CTA-uniform
-  // field value of one pixel from its shifted guide / source values
-  auto fv = [&](float g, float s) {
-    return fld1 == 0 ? g : fld1 == 1 ? g * g : fld1 == 2 ? s : g * s;
-  };
-  float sA[4] = {0.f, 0.f, 0.f, 0.f};
+  float sA[4] = {0.f, 0.f, 0.f, 0.f}, sB[4] = {0.f, 0.f, 0.f, 0.f};
   if (col_ok) {
     for (int y = max(first_add, 0); y < min(y0, H); ++y) {
-      float4 g4 = make_float4(0.f, 0.f, 0.f, 0.f), v4 = g4;
-      if (needG) g4 = __ldg(reinterpret_cast<const float4*>(G + (int64_t)y * W + gx4));
-      if (needS) v4 = __ldg(reinterpret_cast<const float4*>(S + (int64_t)y * W + gx4));
-      sA[0] += fv(g4.x - sG, v4.x - sS);
-      sA[1] += fv(g4.y - sG, v4.y - sS);
-      sA[2] += fv(g4.z - sG, v4.z - sS);
-      sA[3] += fv(g4.w - sG, v4.w - sS);
+      const float4 g4 = __ldg(reinterpret_cast<const float4*>(G + (int64_t)y * W + gx4));
+      const float gg[4] = {g4.x - sG, g4.y - sG, g4.z - sG, g4.w - sG};
+      if (grp == 0) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          sA[k] += gg[k];
+          sB[k] += gg[k] * gg[k];
+        }
+      } else {
+        const float4 v4 = __ldg(reinterpret_cast<const float4*>(S + (int64_t)y * W + gx4));
+        const float ss[4] = {v4.x - sS, v4.y - sS, v4.z - sS, v4.w - sS};
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          sA[k] += ss[k];
+          sB[k] += gg[k] * ss[k];
+        }
+      }
     }
   }
   // ---- level-2 state: V2T threads per coefficient field (A, then b); a
@@ -227,43 +233,65 @@ __global__ void __launch_bounds__(320, 2) k_highres_fused(Args a) {
       // uniform fast path: every row and column of the batch inside the image
       const bool fast = cols_in && base + R <= nrows && ya0 + base - r - 1 >= max(first_add, 0) &&
                         ya0 + base + R - 1 + r < H;
-      float* out0 = vs + fld1 * R * GG::P1 + 4 * t4;
-      const float m = col_ok ? 1.f : 0.f;
-      // leaving rows (L2) for all R rows first, then the running update
-      float4 gl[R], sl[R];
+      float* out0 = vs + (2 * grp + 0) * R * GG::P1 + 4 * t4;
+      float* out1 = vs + (2 * grp + 1) * R * GG::P1 + 4 * t4;
 #pragma unroll
-      for (int j = 0; j < R; ++j) {
-        const int l = ya0 + base + j - r - 1;
-        const bool l_ok = fast || (col_ok && base + j < nrows && l >= first_add && l >= 0 && l < H);
-        gl[j] = sl[j] = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (l_ok) {
-          if (needG) gl[j] = __ldg(reinterpret_cast<const float4*>(G + (int64_t)l * W + gx4));
-          if (needS) sl[j] = __ldg(reinterpret_cast<const float4*>(S + (int64_t)l * W + gx4));
-        }
-      }
+      for (int half = 0; half < 2; ++half) {
+        float4 gl[R / 2], sl[R / 2];
 #pragma unroll
-      for (int j = 0; j < R; ++j) {
-        float4 ge4 = make_float4(0.f, 0.f, 0.f, 0.f), se4 = ge4;
-        if (needG) ge4 = lds4(stg + j * GG::VW + 4 * t4);
-        if (needS) se4 = lds4(stg + (R + j) * GG::VW + 4 * t4);
-        float en[4] = {fv(ge4.x - sG, se4.x - sS), fv(ge4.y - sG, se4.y - sS),
-                       fv(ge4.z - sG, se4.z - sS), fv(ge4.w - sG, se4.w - sS)};
-        float lv[4] = {fv(gl[j].x - sG, sl[j].x - sS), fv(gl[j].y - sG, sl[j].y - sS),
-                       fv(gl[j].z - sG, sl[j].z - sS), fv(gl[j].w - sG, sl[j].w - sS)};
-        if (!fast) {  // edge batch: zero the out-of-image contributions
-          const int e = ya0 + base + j + r;
+        for (int jj = 0; jj < R / 2; ++jj) {
+          const int j = half * (R / 2) + jj;
           const int l = ya0 + base + j - r - 1;
-          const bool e_ok = col_ok && base + j < nrows && e >= 0 && e < H;
-          const bool l_ok = col_ok && base + j < nrows && l >= first_add && l >= 0 && l < H;
-#pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            en[k] = e_ok ? en[k] : 0.f;
-            lv[k] = l_ok ? lv[k] : 0.f;
+          const bool l_ok = fast || (col_ok && base + j < nrows && l >= first_add && l >= 0 && l < H);
+          gl[jj] = sl[jj] = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (l_ok) {
+            gl[jj] = __ldg(reinterpret_cast<const float4*>(G + (int64_t)l * W + gx4));
+            if (grp) sl[jj] = __ldg(reinterpret_cast<const float4*>(S + (int64_t)l * W + gx4));
           }
         }
 #pragma unroll
-        for (int k = 0; k < 4; ++k) sA[k] += en[k] - lv[k];
-        sts4(out0 + j * GG::P1, m * sA[0], m * sA[1], m * sA[2], m * sA[3]);
+        for (int jj = 0; jj < R / 2; ++jj) {
+          const int j = half * (R / 2) + jj;
+          const float4 ge4 = lds4(stg + j * GG::VW + 4 * t4);
+          float gn[4] = {ge4.x - sG, ge4.y - sG, ge4.z - sG, ge4.w - sG};
+          float gq[4] = {gl[jj].x - sG, gl[jj].y - sG, gl[jj].z - sG, gl[jj].w - sG};
+          float sn[4] = {0.f, 0.f, 0.f, 0.f}, sq[4] = {0.f, 0.f, 0.f, 0.f};
+          if (grp) {
+            const float4 se4 = lds4(stg + (R + j) * GG::VW + 4 * t4);
+            sn[0] = se4.x - sS; sn[1] = se4.y - sS; sn[2] = se4.z - sS; sn[3] = se4.w - sS;
+            sq[0] = sl[jj].x - sS; sq[1] = sl[jj].y - sS;
+            sq[2] = sl[jj].z - sS; sq[3] = sl[jj].w - sS;
+          }
+          if (!fast) {  // edge batch: zero the out-of-image contributions
+            const int e = ya0 + base + j + r;
+            const int l = ya0 + base + j - r - 1;
+            const bool e_ok = col_ok && base + j < nrows && e >= 0 && e < H;
+            const bool l_ok = col_ok && base + j < nrows && l >= first_add && l >= 0 && l < H;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              gn[k] = e_ok ? gn[k] : 0.f;
+              sn[k] = e_ok ? sn[k] : 0.f;
+              gq[k] = l_ok ? gq[k] : 0.f;
+              sq[k] = l_ok ? sq[k] : 0.f;
+            }
+          }
+          if (grp == 0) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              sA[k] += gn[k] - gq[k];
+              sB[k] += gn[k] * gn[k] - gq[k] * gq[k];
+            }
+          } else {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              sA[k] += sn[k] - sq[k];
+              sB[k] += gn[k] * sn[k] - gq[k] * sq[k];
+            }
+          }
+          const float m = col_ok ? 1.f : 0.f;
+          sts4(out0 + j * GG::P1, m * sA[0], m * sA[1], m * sA[2], m * sA[3]);
+          sts4(out1 + j * GG::P1, m * sB[0], m * sB[1], m * sB[2], m * sB[3]);
+        }
       }
     }
     __syncthreads();  // vs complete; stg consumed
