@@ -144,15 +144,30 @@ __global__ void __launch_bounds__(320, 2) k_highres_fused(Args a) {
   // cp.async of the R entering input rows of the batch at bb (rows ya + r)
   auto prefetch = [&](int bb) {
     constexpr int chunks = GG::VW / 4;
-    for (int idx = tid; idx < 2 * R * chunks; idx += nt) {
-      const int f = idx / (R * chunks);
-      const int rem = idx - f * R * chunks;
-      const int j = rem / chunks, cc = rem - j * chunks;
-      const int e = ya0 + bb + j + r;
-      const int col = xs0 + 4 * cc;
-      const bool ok = bb + j < nrows && e >= 0 && e < H && col >= 0 && col < W;
-      const float* src = (f == 0 ? G : S) + (ok ? (int64_t)e * W + col : 0);
-      cp_async16(stg + (f * R + j) * GG::VW + 4 * cc, src, ok);
+    const int e0 = ya0 + bb + r;  // first entering row of the batch
+    const bool all_in = xs0 >= 0 && xs0 + GG::VW <= W && bb + R <= nrows && e0 >= 0 &&
+                        e0 + R <= H;  // uniform
+    if (all_in) {
+      const float* gb = G + (int64_t)e0 * W + xs0;
+      const float* sb = S + (int64_t)e0 * W + xs0;
+      for (int idx = tid; idx < 2 * R * chunks; idx += nt) {
+        const int f = idx / (R * chunks);
+        const int rem = idx - f * R * chunks;
+        const int j = rem / chunks, cc = rem - j * chunks;
+        cp_async16(stg + (f * R + j) * GG::VW + 4 * cc, (f == 0 ? gb : sb) + j * W + 4 * cc,
+                   true);
+      }
+    } else {
+      for (int idx = tid; idx < 2 * R * chunks; idx += nt) {
+        const int f = idx / (R * chunks);
+        const int rem = idx - f * R * chunks;
+        const int j = rem / chunks, cc = rem - j * chunks;
+        const int e = e0 + j;
+        const int col = xs0 + 4 * cc;
+        const bool ok = bb + j < nrows && e >= 0 && e < H && col >= 0 && col < W;
+        const float* src = (f == 0 ? G : S) + (ok ? (int64_t)e * W + col : 0);
+        cp_async16(stg + (f * R + j) * GG::VW + 4 * cc, src, ok);
+      }
     }
     cp_async_commit();
   };
@@ -229,10 +244,56 @@ __global__ void __launch_bounds__(320, 2) k_highres_fused(Args a) {
     }
 
     // ---- V1 -----------------------------------------------------------
-    if (v1) {
-      // uniform fast path: every row and column of the batch inside the image
-      const bool fast = cols_in && base + R <= nrows && ya0 + base - r - 1 >= max(first_add, 0) &&
-                        ya0 + base + R - 1 + r < H;
+    // uniform fast path: every row and column of the batch inside the image
+    const bool fast = cols_in && base + R <= nrows && ya0 + base - r - 1 >= max(first_add, 0) &&
+                      ya0 + base + R - 1 + r < H;
+    if (v1 && fast) {
+      // no predicates: leaving rows straight from L2, entering rows from stg
+      float* out0 = vs + (2 * grp + 0) * R * GG::P1 + 4 * t4;
+      float* out1 = vs + (2 * grp + 1) * R * GG::P1 + 4 * t4;
+      const float* gl_p = G + (int64_t)(ya0 + base - r - 1) * W + gx4;
+      const float* sl_p = S + (int64_t)(ya0 + base - r - 1) * W + gx4;
+      const float* ge_p = stg + 4 * t4;
+      const float* se_p = stg + R * GG::VW + 4 * t4;
+      float4 gl[R], sl[R];
+#pragma unroll
+      for (int j = 0; j < R; ++j) {
+        gl[j] = __ldg(reinterpret_cast<const float4*>(gl_p + (int64_t)j * W));
+        if (grp) sl[j] = __ldg(reinterpret_cast<const float4*>(sl_p + (int64_t)j * W));
+      }
+      if (grp == 0) {
+#pragma unroll
+        for (int j = 0; j < R; ++j) {
+          const float4 e = lds4(ge_p + j * GG::VW);
+          const float gn[4] = {e.x - sG, e.y - sG, e.z - sG, e.w - sG};
+          const float gq[4] = {gl[j].x - sG, gl[j].y - sG, gl[j].z - sG, gl[j].w - sG};
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            sA[k] += gn[k] - gq[k];
+            sB[k] += fmaf(gn[k], gn[k], -gq[k] * gq[k]);
+          }
+          sts4(out0 + j * GG::P1, sA[0], sA[1], sA[2], sA[3]);
+          sts4(out1 + j * GG::P1, sB[0], sB[1], sB[2], sB[3]);
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < R; ++j) {
+          const float4 e = lds4(ge_p + j * GG::VW);
+          const float4 f = lds4(se_p + j * GG::VW);
+          const float gn[4] = {e.x - sG, e.y - sG, e.z - sG, e.w - sG};
+          const float sn[4] = {f.x - sS, f.y - sS, f.z - sS, f.w - sS};
+          const float gq[4] = {gl[j].x - sG, gl[j].y - sG, gl[j].z - sG, gl[j].w - sG};
+          const float sq[4] = {sl[j].x - sS, sl[j].y - sS, sl[j].z - sS, sl[j].w - sS};
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            sA[k] += sn[k] - sq[k];
+            sB[k] += fmaf(gn[k], sn[k], -gq[k] * sq[k]);
+          }
+          sts4(out0 + j * GG::P1, sA[0], sA[1], sA[2], sA[3]);
+          sts4(out1 + j * GG::P1, sB[0], sB[1], sB[2], sB[3]);
+        }
+      }
+    } else if (v1) {
       float* out0 = vs + (2 * grp + 0) * R * GG::P1 + 4 * t4;
       float* out1 = vs + (2 * grp + 1) * R * GG::P1 + 4 * t4;
 #pragma unroll
