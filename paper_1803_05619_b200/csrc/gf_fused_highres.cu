@@ -33,6 +33,7 @@
 
 #include "gf_common.cuh"
 #include "gf_internal.h"
+#include "gf_tma.cuh"
 
 namespace gfb {
 namespace hrf {
@@ -64,9 +65,14 @@ struct Geo {
   static constexpr int P2 = pitch4(v2w);
   static constexpr int nt = 32 * cmax(cmax((nq1 + 3) / 4, TX / KR / 4),
                                       cmax((VW / 2 + 31) / 32, (v2w / 2 + 31) / 32));
-  static constexpr size_t smem_floats = (size_t)2 * R * VW + (size_t)4 * R * P1 +
-                                        (size_t)2 * ringN * Pr + (size_t)2 * R * P2;
+  // TMA boxes of the staged rows: NB boxes of BX columns (box dims <= 256)
+  static constexpr int NB = (VW + 255) / 256;
+  static constexpr int BX = up4((VW + NB - 1) / NB);
+  static constexpr int SWF = NB * BX;  // staged columns per field (>= VW)
+  static constexpr size_t smem_floats = (size_t)2 * R * SWF + (size_t)4 * R * P1 +
+                                        (size_t)2 * ringN * Pr + (size_t)2 * R * P2 + 4;
   static constexpr size_t smem_bytes = smem_floats * sizeof(float);
+  static constexpr uint32_t tx_bytes = 2u * NB * R * BX * 4u;
 };
 
 __device__ __forceinline__ void cp_async16(float* dst, const float* src, bool valid) {
@@ -100,16 +106,26 @@ __device__ __forceinline__ int wlen(int i, int n, int r) {
   return b - a + 1;
 }
 
+// staged column c of row j of field f: boxes of BX columns, dense rows
+template <typename GG>
+__device__ __forceinline__ int stg_idx(int f, int j, int c) {
+  const int box = c / GG::BX;
+  return ((f * GG::NB + box) * R + j) * GG::BX + (c - box * GG::BX);
+}
+
 template <int RAD>
-__global__ void __launch_bounds__(320, 2) k_highres_fused(Args a) {
+__global__ void __launch_bounds__(320, 2)
+    k_highres_fused(const __grid_constant__ CUtensorMap tmG,
+                    const __grid_constant__ CUtensorMap tmS, Args a) {
   using GG = Geo<RAD>;
   constexpr int r = RAD;
   constexpr int nt = GG::nt;
-  extern __shared__ float4 smem4[];
-  float* stg = reinterpret_cast<float*>(smem4);  // [2 fields][R][VW]
-  float* vs = stg + 2 * R * GG::VW;              // [4 fields][R][P1]
+  extern __shared__ __align__(128) float4 smem4[];
+  float* stg = reinterpret_cast<float*>(smem4);  // [2 fields][NB][R][BX] (TMA boxes)
+  float* vs = stg + 2 * R * GG::SWF;             // [4 fields][R][P1]
   float* ring = vs + 4 * R * GG::P1;             // [2 fields][ringN][Pr]
   float* vs2 = ring + 2 * GG::ringN * GG::Pr;    // [2 fields][R][P2]
+  uint64_t* bar = reinterpret_cast<uint64_t*>(vs2 + 2 * R * GG::P2);
   const int H = (int)a.H, W = (int)a.W;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 
@@ -141,35 +157,24 @@ __global__ void __launch_bounds__(320, 2) k_highres_fused(Args a) {
   const int first_add = y0 - 2 * r;       // first input row ever added
   const int xs0 = x0 - GG::PADL;          // global column of vs/stg column 0
 
-  // cp.async of the R entering input rows of the batch at bb (rows ya + r)
+  // TMA of the R entering input rows of the batch at bb (rows ya0+bb+r ...);
+  // out-of-image box elements are zero-filled by the hardware
+  const int zG = (int)(a.Cg == a.C ? b * a.C + c : b * a.Cg);
+  const int zS = (int)(b * a.C + c);
+  if (tid == 0) tma::mbar_init(bar, 1);
+  __syncthreads();
+  uint32_t phase = 0;
   auto prefetch = [&](int bb) {
-    constexpr int chunks = GG::VW / 4;
-    const int e0 = ya0 + bb + r;  // first entering row of the batch
-    const bool all_in = xs0 >= 0 && xs0 + GG::VW <= W && bb + R <= nrows && e0 >= 0 &&
-                        e0 + R <= H;  // uniform
-    if (all_in) {
-      const float* gb = G + (int64_t)e0 * W + xs0;
-      const float* sb = S + (int64_t)e0 * W + xs0;
-      for (int idx = tid; idx < 2 * R * chunks; idx += nt) {
-        const int f = idx / (R * chunks);
-        const int rem = idx - f * R * chunks;
-        const int j = rem / chunks, cc = rem - j * chunks;
-        cp_async16(stg + (f * R + j) * GG::VW + 4 * cc, (f == 0 ? gb : sb) + j * W + 4 * cc,
-                   true);
-      }
-    } else {
-      for (int idx = tid; idx < 2 * R * chunks; idx += nt) {
-        const int f = idx / (R * chunks);
-        const int rem = idx - f * R * chunks;
-        const int j = rem / chunks, cc = rem - j * chunks;
-        const int e = e0 + j;
-        const int col = xs0 + 4 * cc;
-        const bool ok = bb + j < nrows && e >= 0 && e < H && col >= 0 && col < W;
-        const float* src = (f == 0 ? G : S) + (ok ? (int64_t)e * W + col : 0);
-        cp_async16(stg + (f * R + j) * GG::VW + 4 * cc, src, ok);
+    if (tid == 0) {
+      tma::fence_proxy_async();
+      tma::mbar_arrive_expect_tx(bar, GG::tx_bytes);
+      const int e0 = ya0 + bb + r;
+#pragma unroll
+      for (int box = 0; box < GG::NB; ++box) {
+        tma::load_3d(stg + (0 * GG::NB + box) * R * GG::BX, &tmG, xs0 + box * GG::BX, e0, zG, bar);
+        tma::load_3d(stg + (1 * GG::NB + box) * R * GG::BX, &tmS, xs0 + box * GG::BX, e0, zS, bar);
       }
     }
-    cp_async_commit();
   };
   prefetch(0);
 
@@ -221,8 +226,9 @@ __global__ void __launch_bounds__(320, 2) k_highres_fused(Args a) {
   const int ql = lane >> 3;  //                       run within the warp's chunk
 
   for (int base = 0; base < nrows; base += R) {
-    cp_async_wait_all();
-    __syncthreads();  // stg landed; the previous batch's H2 is done with vs2
+    tma::mbar_wait(bar, phase);  // this batch's rows landed in stg
+    phase ^= 1u;
+    __syncthreads();  // ... and the previous batch's H2 is done with vs2
 
     // ---- V2 (part 1): subtract the leaving coefficient rows while their
     //      ring slots still hold them: vs2[j] = sum - sum_{i<=j} old_i
@@ -253,8 +259,8 @@ __global__ void __launch_bounds__(320, 2) k_highres_fused(Args a) {
       float* out1 = vs + (2 * grp + 1) * R * GG::P1 + 4 * t4;
       const float* gl_p = G + (int64_t)(ya0 + base - r - 1) * W + gx4;
       const float* sl_p = S + (int64_t)(ya0 + base - r - 1) * W + gx4;
-      const float* ge_p = stg + 4 * t4;
-      const float* se_p = stg + R * GG::VW + 4 * t4;
+      const float* ge_p = stg + stg_idx<GG>(0, 0, 4 * t4);
+      const float* se_p = stg + stg_idx<GG>(1, 0, 4 * t4);
       float4 gl[R], sl[R];
 #pragma unroll
       for (int j = 0; j < R; ++j) {
@@ -264,7 +270,7 @@ __global__ void __launch_bounds__(320, 2) k_highres_fused(Args a) {
       if (grp == 0) {
 #pragma unroll
         for (int j = 0; j < R; ++j) {
-          const float4 e = lds4(ge_p + j * GG::VW);
+          const float4 e = lds4(ge_p + j * GG::BX);
           const float gn[4] = {e.x - sG, e.y - sG, e.z - sG, e.w - sG};
           const float gq[4] = {gl[j].x - sG, gl[j].y - sG, gl[j].z - sG, gl[j].w - sG};
 #pragma unroll
@@ -278,8 +284,8 @@ __global__ void __launch_bounds__(320, 2) k_highres_fused(Args a) {
       } else {
 #pragma unroll
         for (int j = 0; j < R; ++j) {
-          const float4 e = lds4(ge_p + j * GG::VW);
-          const float4 f = lds4(se_p + j * GG::VW);
+          const float4 e = lds4(ge_p + j * GG::BX);
+          const float4 f = lds4(se_p + j * GG::BX);
           const float gn[4] = {e.x - sG, e.y - sG, e.z - sG, e.w - sG};
           const float sn[4] = {f.x - sS, f.y - sS, f.z - sS, f.w - sS};
           const float gq[4] = {gl[j].x - sG, gl[j].y - sG, gl[j].z - sG, gl[j].w - sG};
@@ -313,12 +319,12 @@ __global__ void __launch_bounds__(320, 2) k_highres_fused(Args a) {
 #pragma unroll
         for (int jj = 0; jj < R / 2; ++jj) {
           const int j = half * (R / 2) + jj;
-          const float4 ge4 = lds4(stg + j * GG::VW + 4 * t4);
+          const float4 ge4 = lds4(stg + stg_idx<GG>(0, j, 4 * t4));
           float gn[4] = {ge4.x - sG, ge4.y - sG, ge4.z - sG, ge4.w - sG};
           float gq[4] = {gl[jj].x - sG, gl[jj].y - sG, gl[jj].z - sG, gl[jj].w - sG};
           float sn[4] = {0.f, 0.f, 0.f, 0.f}, sq[4] = {0.f, 0.f, 0.f, 0.f};
           if (grp) {
-            const float4 se4 = lds4(stg + (R + j) * GG::VW + 4 * t4);
+            const float4 se4 = lds4(stg + stg_idx<GG>(1, j, 4 * t4));
             sn[0] = se4.x - sS; sn[1] = se4.y - sS; sn[2] = se4.z - sS; sn[3] = se4.w - sS;
             sq[0] = sl[jj].x - sS; sq[1] = sl[jj].y - sS;
             sq[2] = sl[jj].z - sS; sq[3] = sl[jj].w - sS;
@@ -532,11 +538,12 @@ struct Launch {
   const void* fn;
   int nt;
   size_t smem;
+  int box_w;  // TMA box width of the staged rows
 };
 
 template <int RAD>
 Launch launch_info() {
-  return {(const void*)k_highres_fused<RAD>, Geo<RAD>::nt, Geo<RAD>::smem_bytes};
+  return {(const void*)k_highres_fused<RAD>, Geo<RAD>::nt, Geo<RAD>::smem_bytes, Geo<RAD>::BX};
 }
 
 Launch pick(int r) {
@@ -610,7 +617,14 @@ void fused_highres_fwd(const float* guide, const float* src, float* out, int64_t
   const int64_t segs = (H + TY - 1) / TY;
   hrf::Args a{guide, src, out, C, Cg, H, W, (int)TY, (int)strips, (int)segs, eps, status};
   const int64_t grid = planes * strips * segs;
-  void* args[] = {&a};
+  CUtensorMap tmG, tmS;
+  if (!tma::make_plane_map(&tmG, guide, W, H, B * Cg, L.box_w, hrf::R) ||
+      !tma::make_plane_map(&tmS, src, W, H, B * C, L.box_w, hrf::R)) {
+    // surfaces as a launch error through the C ABI's cudaGetLastError check
+    cudaLaunchKernel(L.fn, dim3(0), dim3(0), nullptr, 0, s);
+    return;
+  }
+  void* args[] = {&tmG, &tmS, &a};
   cudaLaunchKernel(L.fn, dim3((unsigned)grid), dim3(L.nt), args, L.smem, s);
 }
 
