@@ -57,15 +57,14 @@ struct Geo {
   static constexpr int nv1 = (off + 2 * RAD + KR + 3) / 4;  // float4s per H1 run window
   static constexpr int VW = up4(cmax(TX + 2 * PADL, (nq1 - 1) * KR + 4 * nv1));  // V1 columns
   static constexpr int P1 = pitch4(VW);
-  static constexpr int ringN = 2 * RAD + 1 + R;  // H1(k) must not overwrite what V2(k) reads
+  static constexpr int ringN = cmax(2 * RAD + 1, R);
   static constexpr int ringw = nq1 * KR;                  // >= W2
   static constexpr int Pr = pitch4(ringw);
   static constexpr int nv2 = (2 * RAD + KR + 3) / 4;      // float4s per H2 run window
   static constexpr int v2w = up4(cmax(ringw, TX - KR + 4 * nv2));
   static constexpr int P2 = pitch4(v2w);
-  // phase B: H1 warps + H2 warps side by side; phase A: V1 then V2 threads
-  static constexpr int nt = 32 * cmax((nq1 + 3) / 4 + TX / KR / 4,
-                                      (VW / 2 + 31) / 32 + (v2w / 2 + 31) / 32);
+  static constexpr int nt = 32 * cmax(cmax((nq1 + 3) / 4, TX / KR / 4),
+                                      cmax((VW / 2 + 31) / 32, (v2w / 2 + 31) / 32));
   // TMA boxes of the staged rows: NB boxes of BX columns (box dims <= 256)
   static constexpr int NB = (VW + 255) / 256;
   static constexpr int BX = up4((VW + NB - 1) / NB);
@@ -115,7 +114,7 @@ __device__ __forceinline__ int stg_idx(int f, int j, int c) {
 }
 
 template <int RAD>
-__global__ void __launch_bounds__(640, 1)
+__global__ void __launch_bounds__(320, 2)
     k_highres_fused(const __grid_constant__ CUtensorMap tmG,
                     const __grid_constant__ CUtensorMap tmS, Args a) {
   using GG = Geo<RAD>;
@@ -211,185 +210,166 @@ __global__ void __launch_bounds__(640, 1)
       }
     }
   }
-  // ---- level-2 state: V2 threads (from V2O on) own coefficient columns
-  //      4u..4u+3 of one field (A, then b)
+  // ---- level-2 state: V2T threads per coefficient field (A, then b); a
+  //      thread owns coefficient columns 4u..4u+3 of its field
   constexpr int V2T = GG::v2w / 4;
-  constexpr int V2O = (2 * V1T + 31) / 32 * 32;
-  const int tv = tid - V2O;
-  const int fld = tv < V2T ? 0 : 1;
-  const int u4 = tv - fld * V2T;
-  const bool v2 = tv >= 0 && tv < 2 * V2T;
+  const int fld = tid < V2T ? 0 : 1;
+  const int u4 = tid - fld * V2T;
+  const bool v2 = tid < 2 * V2T;
   const bool v2ring = v2 && u4 < GG::ringw / 4;
   float c_sum[4] = {0.f, 0.f, 0.f, 0.f};
   bool bad = false, degen = false;
-  int ring_new = 0;  // ring slot of coefficient row `base`
+  int ring_new = 0;                                   // slot of coefficient row `base`
+  int ring_old = GG::ringN - (2 * r + 1) % GG::ringN;  // slot of row base - 2r - 1
+  if (ring_old == GG::ringN) ring_old = 0;
   const int jl = lane & 7;   // run mapping of H1/H2: row
   const int ql = lane >> 3;  //                       run within the warp's chunk
-  constexpr int NCH1 = (GG::nq1 + 3) / 4;  // H1 warps; H2 warps follow
 
-  // Software pipeline, two barriers per batch: iteration `base` runs
-  //   phase A: V1(batch base) || V2(batch base - R)
-  //   phase B: H1(batch base) || H2(batch base - R)
-  // One extra iteration drains V2/H2 of the last batch.
-  for (int base = 0; base < nrows + R; base += R) {
-    const bool cur = base < nrows;  // uniform
-    const int pb = base - R;
-    const bool prev = pb >= 0;
-    if (cur) {
-      tma::mbar_wait(bar, phase);  // this batch's rows landed in stg
-      phase ^= 1u;
-    }
-    __syncthreads();  // phase B of the previous iteration is done with vs, vs2
+  for (int base = 0; base < nrows; base += R) {
+    tma::mbar_wait(bar, phase);  // this batch's rows landed in stg
+    phase ^= 1u;
+    __syncthreads();  // ... and the previous batch's H2 is done with vs2
 
-    // ================= phase A =================
-    if (cur) {
-      // ---- V1 -----------------------------------------------------------
-      // uniform fast path: every row and column of the batch inside the image
-      const bool fast = cols_in && base + R <= nrows && ya0 + base - r - 1 >= max(first_add, 0) &&
-                        ya0 + base + R - 1 + r < H;
-      if (v1 && fast) {
-        // no predicates: leaving rows straight from L2, entering rows from stg
-        float* out0 = vs + (2 * grp + 0) * R * GG::P1 + 4 * t4;
-        float* out1 = vs + (2 * grp + 1) * R * GG::P1 + 4 * t4;
-        const float* gl_p = G + (int64_t)(ya0 + base - r - 1) * W + gx4;
-        const float* sl_p = S + (int64_t)(ya0 + base - r - 1) * W + gx4;
-        const float* ge_p = stg + stg_idx<GG>(0, 0, 4 * t4);
-        const float* se_p = stg + stg_idx<GG>(1, 0, 4 * t4);
-        float4 gl[R], sl[R];
-  #pragma unroll
-        for (int j = 0; j < R; ++j) {
-          gl[j] = __ldg(reinterpret_cast<const float4*>(gl_p + (int64_t)j * W));
-          if (grp) sl[j] = __ldg(reinterpret_cast<const float4*>(sl_p + (int64_t)j * W));
-        }
-        if (grp == 0) {
-  #pragma unroll
-          for (int j = 0; j < R; ++j) {
-            const float4 e = lds4(ge_p + j * GG::BX);
-            const float gn[4] = {e.x - sG, e.y - sG, e.z - sG, e.w - sG};
-            const float gq[4] = {gl[j].x - sG, gl[j].y - sG, gl[j].z - sG, gl[j].w - sG};
-  #pragma unroll
-            for (int k = 0; k < 4; ++k) {
-              sA[k] += gn[k] - gq[k];
-              sB[k] += fmaf(gn[k], gn[k], -gq[k] * gq[k]);
-            }
-            sts4(out0 + j * GG::P1, sA[0], sA[1], sA[2], sA[3]);
-            sts4(out1 + j * GG::P1, sB[0], sB[1], sB[2], sB[3]);
-          }
-        } else {
-  #pragma unroll
-          for (int j = 0; j < R; ++j) {
-            const float4 e = lds4(ge_p + j * GG::BX);
-            const float4 f = lds4(se_p + j * GG::BX);
-            const float gn[4] = {e.x - sG, e.y - sG, e.z - sG, e.w - sG};
-            const float sn[4] = {f.x - sS, f.y - sS, f.z - sS, f.w - sS};
-            const float gq[4] = {gl[j].x - sG, gl[j].y - sG, gl[j].z - sG, gl[j].w - sG};
-            const float sq[4] = {sl[j].x - sS, sl[j].y - sS, sl[j].z - sS, sl[j].w - sS};
-  #pragma unroll
-            for (int k = 0; k < 4; ++k) {
-              sA[k] += sn[k] - sq[k];
-              sB[k] += fmaf(gn[k], sn[k], -gq[k] * sq[k]);
-            }
-            sts4(out0 + j * GG::P1, sA[0], sA[1], sA[2], sA[3]);
-            sts4(out1 + j * GG::P1, sB[0], sB[1], sB[2], sB[3]);
-          }
-        }
-      } else if (v1) {
-        float* out0 = vs + (2 * grp + 0) * R * GG::P1 + 4 * t4;
-        float* out1 = vs + (2 * grp + 1) * R * GG::P1 + 4 * t4;
-  #pragma unroll
-        for (int half = 0; half < 2; ++half) {
-          float4 gl[R / 2], sl[R / 2];
-  #pragma unroll
-          for (int jj = 0; jj < R / 2; ++jj) {
-            const int j = half * (R / 2) + jj;
-            const int l = ya0 + base + j - r - 1;
-            const bool l_ok = fast || (col_ok && base + j < nrows && l >= first_add && l >= 0 && l < H);
-            gl[jj] = sl[jj] = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (l_ok) {
-              gl[jj] = __ldg(reinterpret_cast<const float4*>(G + (int64_t)l * W + gx4));
-              if (grp) sl[jj] = __ldg(reinterpret_cast<const float4*>(S + (int64_t)l * W + gx4));
-            }
-          }
-  #pragma unroll
-          for (int jj = 0; jj < R / 2; ++jj) {
-            const int j = half * (R / 2) + jj;
-            const float4 ge4 = lds4(stg + stg_idx<GG>(0, j, 4 * t4));
-            float gn[4] = {ge4.x - sG, ge4.y - sG, ge4.z - sG, ge4.w - sG};
-            float gq[4] = {gl[jj].x - sG, gl[jj].y - sG, gl[jj].z - sG, gl[jj].w - sG};
-            float sn[4] = {0.f, 0.f, 0.f, 0.f}, sq[4] = {0.f, 0.f, 0.f, 0.f};
-            if (grp) {
-              const float4 se4 = lds4(stg + stg_idx<GG>(1, j, 4 * t4));
-              sn[0] = se4.x - sS; sn[1] = se4.y - sS; sn[2] = se4.z - sS; sn[3] = se4.w - sS;
-              sq[0] = sl[jj].x - sS; sq[1] = sl[jj].y - sS;
-              sq[2] = sl[jj].z - sS; sq[3] = sl[jj].w - sS;
-            }
-            if (!fast) {  // edge batch: zero the out-of-image contributions
-              const int e = ya0 + base + j + r;
-              const int l = ya0 + base + j - r - 1;
-              const bool e_ok = col_ok && base + j < nrows && e >= 0 && e < H;
-              const bool l_ok = col_ok && base + j < nrows && l >= first_add && l >= 0 && l < H;
-  #pragma unroll
-              for (int k = 0; k < 4; ++k) {
-                gn[k] = e_ok ? gn[k] : 0.f;
-                sn[k] = e_ok ? sn[k] : 0.f;
-                gq[k] = l_ok ? gq[k] : 0.f;
-                sq[k] = l_ok ? sq[k] : 0.f;
-              }
-            }
-            if (grp == 0) {
-  #pragma unroll
-              for (int k = 0; k < 4; ++k) {
-                sA[k] += gn[k] - gq[k];
-                sB[k] += gn[k] * gn[k] - gq[k] * gq[k];
-              }
-            } else {
-  #pragma unroll
-              for (int k = 0; k < 4; ++k) {
-                sA[k] += sn[k] - sq[k];
-                sB[k] += gn[k] * sn[k] - gq[k] * sq[k];
-              }
-            }
-            const float m = col_ok ? 1.f : 0.f;
-            sts4(out0 + j * GG::P1, m * sA[0], m * sA[1], m * sA[2], m * sA[3]);
-            sts4(out1 + j * GG::P1, m * sB[0], m * sB[1], m * sB[2], m * sB[3]);
-          }
-        }
-      }
-    }
-    // ---- V2 of the previous batch: add its coefficient rows, subtract the
-    //      rows leaving the 2r+1 window (slot of row pb+j-2r-1 == slot of
-    //      row base+j, which H1 only overwrites in phase B)
-    if (prev && v2) {
+    // ---- V2 (part 1): subtract the leaving coefficient rows while their
+    //      ring slots still hold them: vs2[j] = sum - sum_{i<=j} old_i
+    if (v2) {
+      float pc[4] = {c_sum[0], c_sum[1], c_sum[2], c_sum[3]};
       const float* rf = ring + fld * GG::ringN * GG::Pr + 4 * u4;
       float* vf = vs2 + fld * R * GG::P2 + 4 * u4;
 #pragma unroll
       for (int j = 0; j < R; ++j) {
-        if (v2ring && pb + j < nrows) {
-          int sn = ring_new + 2 * r + 1 + j;
-          if (sn >= GG::ringN) sn -= GG::ringN;
-          const float4 x = lds4(rf + sn * GG::Pr);
-          c_sum[0] += x.x; c_sum[1] += x.y; c_sum[2] += x.z; c_sum[3] += x.w;
-          if (pb + j - 2 * r - 1 >= 0) {
-            int so = ring_new + j;
-            if (so >= GG::ringN) so -= GG::ringN;
-            const float4 o = lds4(rf + so * GG::Pr);
-            c_sum[0] -= o.x; c_sum[1] -= o.y; c_sum[2] -= o.z; c_sum[3] -= o.w;
-          }
+        // rows leaving for j >= 2r+1 belong to this batch: part 2 handles them
+        if (j < 2 * r + 1 && v2ring && base + j - 2 * r - 1 >= 0) {
+          int so = ring_old + j;
+          if (so >= GG::ringN) so -= GG::ringN;
+          const float4 o = lds4(rf + so * GG::Pr);
+          pc[0] -= o.x; pc[1] -= o.y; pc[2] -= o.z; pc[3] -= o.w;
         }
-        sts4(vf + j * GG::P2, c_sum[0], c_sum[1], c_sum[2], c_sum[3]);
+        sts4(vf + j * GG::P2, pc[0], pc[1], pc[2], pc[3]);
       }
     }
-    __syncthreads();  // vs (this batch) and vs2 (previous batch) complete
 
-    // the next batch's entering rows stream in while phase B computes
-    if (cur && base + R < nrows) prefetch(base + R);
+    // ---- V1 -----------------------------------------------------------
+    // uniform fast path: every row and column of the batch inside the image
+    const bool fast = cols_in && base + R <= nrows && ya0 + base - r - 1 >= max(first_add, 0) &&
+                      ya0 + base + R - 1 + r < H;
+    if (v1 && fast) {
+      // no predicates: leaving rows straight from L2, entering rows from stg
+      float* out0 = vs + (2 * grp + 0) * R * GG::P1 + 4 * t4;
+      float* out1 = vs + (2 * grp + 1) * R * GG::P1 + 4 * t4;
+      const float* gl_p = G + (int64_t)(ya0 + base - r - 1) * W + gx4;
+      const float* sl_p = S + (int64_t)(ya0 + base - r - 1) * W + gx4;
+      const float* ge_p = stg + stg_idx<GG>(0, 0, 4 * t4);
+      const float* se_p = stg + stg_idx<GG>(1, 0, 4 * t4);
+      float4 gl[R], sl[R];
+#pragma unroll
+      for (int j = 0; j < R; ++j) {
+        gl[j] = __ldg(reinterpret_cast<const float4*>(gl_p + (int64_t)j * W));
+        if (grp) sl[j] = __ldg(reinterpret_cast<const float4*>(sl_p + (int64_t)j * W));
+      }
+      if (grp == 0) {
+#pragma unroll
+        for (int j = 0; j < R; ++j) {
+          const float4 e = lds4(ge_p + j * GG::BX);
+          const float gn[4] = {e.x - sG, e.y - sG, e.z - sG, e.w - sG};
+          const float gq[4] = {gl[j].x - sG, gl[j].y - sG, gl[j].z - sG, gl[j].w - sG};
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            sA[k] += gn[k] - gq[k];
+            sB[k] += fmaf(gn[k], gn[k], -gq[k] * gq[k]);
+          }
+          sts4(out0 + j * GG::P1, sA[0], sA[1], sA[2], sA[3]);
+          sts4(out1 + j * GG::P1, sB[0], sB[1], sB[2], sB[3]);
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < R; ++j) {
+          const float4 e = lds4(ge_p + j * GG::BX);
+          const float4 f = lds4(se_p + j * GG::BX);
+          const float gn[4] = {e.x - sG, e.y - sG, e.z - sG, e.w - sG};
+          const float sn[4] = {f.x - sS, f.y - sS, f.z - sS, f.w - sS};
+          const float gq[4] = {gl[j].x - sG, gl[j].y - sG, gl[j].z - sG, gl[j].w - sG};
+          const float sq[4] = {sl[j].x - sS, sl[j].y - sS, sl[j].z - sS, sl[j].w - sS};
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            sA[k] += sn[k] - sq[k];
+            sB[k] += fmaf(gn[k], sn[k], -gq[k] * sq[k]);
+          }
+          sts4(out0 + j * GG::P1, sA[0], sA[1], sA[2], sA[3]);
+          sts4(out1 + j * GG::P1, sB[0], sB[1], sB[2], sB[3]);
+        }
+      }
+    } else if (v1) {
+      float* out0 = vs + (2 * grp + 0) * R * GG::P1 + 4 * t4;
+      float* out1 = vs + (2 * grp + 1) * R * GG::P1 + 4 * t4;
+#pragma unroll
+      for (int half = 0; half < 2; ++half) {
+        float4 gl[R / 2], sl[R / 2];
+#pragma unroll
+        for (int jj = 0; jj < R / 2; ++jj) {
+          const int j = half * (R / 2) + jj;
+          const int l = ya0 + base + j - r - 1;
+          const bool l_ok = fast || (col_ok && base + j < nrows && l >= first_add && l >= 0 && l < H);
+          gl[jj] = sl[jj] = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (l_ok) {
+            gl[jj] = __ldg(reinterpret_cast<const float4*>(G + (int64_t)l * W + gx4));
+            if (grp) sl[jj] = __ldg(reinterpret_cast<const float4*>(S + (int64_t)l * W + gx4));
+          }
+        }
+#pragma unroll
+        for (int jj = 0; jj < R / 2; ++jj) {
+          const int j = half * (R / 2) + jj;
+          const float4 ge4 = lds4(stg + stg_idx<GG>(0, j, 4 * t4));
+          float gn[4] = {ge4.x - sG, ge4.y - sG, ge4.z - sG, ge4.w - sG};
+          float gq[4] = {gl[jj].x - sG, gl[jj].y - sG, gl[jj].z - sG, gl[jj].w - sG};
+          float sn[4] = {0.f, 0.f, 0.f, 0.f}, sq[4] = {0.f, 0.f, 0.f, 0.f};
+          if (grp) {
+            const float4 se4 = lds4(stg + stg_idx<GG>(1, j, 4 * t4));
+            sn[0] = se4.x - sS; sn[1] = se4.y - sS; sn[2] = se4.z - sS; sn[3] = se4.w - sS;
+            sq[0] = sl[jj].x - sS; sq[1] = sl[jj].y - sS;
+            sq[2] = sl[jj].z - sS; sq[3] = sl[jj].w - sS;
+          }
+          if (!fast) {  // edge batch: zero the out-of-image contributions
+            const int e = ya0 + base + j + r;
+            const int l = ya0 + base + j - r - 1;
+            const bool e_ok = col_ok && base + j < nrows && e >= 0 && e < H;
+            const bool l_ok = col_ok && base + j < nrows && l >= first_add && l >= 0 && l < H;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              gn[k] = e_ok ? gn[k] : 0.f;
+              sn[k] = e_ok ? sn[k] : 0.f;
+              gq[k] = l_ok ? gq[k] : 0.f;
+              sq[k] = l_ok ? sq[k] : 0.f;
+            }
+          }
+          if (grp == 0) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              sA[k] += gn[k] - gq[k];
+              sB[k] += gn[k] * gn[k] - gq[k] * gq[k];
+            }
+          } else {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              sA[k] += sn[k] - sq[k];
+              sB[k] += gn[k] * sn[k] - gq[k] * sq[k];
+            }
+          }
+          const float m = col_ok ? 1.f : 0.f;
+          sts4(out0 + j * GG::P1, m * sA[0], m * sA[1], m * sA[2], m * sA[3]);
+          sts4(out1 + j * GG::P1, m * sB[0], m * sB[1], m * sB[2], m * sB[3]);
+        }
+      }
+    }
+    __syncthreads();  // vs complete; stg consumed
 
-    // ================= phase B =================
+    // the next batch's entering rows stream in while H1/V2/H2 compute
+    if (base + R < nrows) prefetch(base + R);
+
     // ---- H1 -----------------------------------------------------------
-    if (cur && warp < NCH1) {
-      const int ch = warp;
+    for (int ch = warp; ch * 4 < GG::nq1; ch += nt / 32) {
       const int j = jl, q = ch * 4 + ql;
-      if (q < GG::nq1 && base + j < nrows) {
+      if (q >= GG::nq1 || base + j >= nrows) continue;
       const int ya = ya0 + base + j;
       const int xa0 = q * KR;
       int slot = ring_new + j;
@@ -401,7 +381,8 @@ __global__ void __launch_bounds__(640, 1)
         sts4(ra + 4, 0.f, 0.f, 0.f, 0.f);
         sts4(rb, 0.f, 0.f, 0.f, 0.f);
         sts4(rb + 4, 0.f, 0.f, 0.f, 0.f);
-      } else {
+        continue;
+      }
       float hs[4][KR];
 #pragma unroll
       for (int f = 0; f < 4; ++f) {
@@ -460,17 +441,48 @@ __global__ void __launch_bounds__(640, 1)
       sts4(rb, B[0], B[1], B[2], B[3]);
       sts4(rb + 4, B[4], B[5], B[6], B[7]);
     }
+    __syncthreads();  // ring rows of this batch complete
+
+    // ---- V2 (part 2): add the entering coefficient rows ----------------
+    if (v2) {
+      float nc[4] = {0.f, 0.f, 0.f, 0.f};
+      const float* rf = ring + fld * GG::ringN * GG::Pr + 4 * u4;
+      float* vf = vs2 + fld * R * GG::P2 + 4 * u4;
+#pragma unroll
+      for (int j = 0; j < R; ++j) {
+        if (v2ring && base + j < nrows) {
+          int sn = ring_new + j;
+          if (sn >= GG::ringN) sn -= GG::ringN;
+          const float4 x = lds4(rf + sn * GG::Pr);
+          nc[0] += x.x; nc[1] += x.y; nc[2] += x.z; nc[3] += x.w;
+          if (j >= 2 * r + 1) {  // leaving row added earlier in this batch (r small)
+            int so = ring_new + j - 2 * r - 1;
+            if (so >= GG::ringN) so -= GG::ringN;
+            const float4 o = lds4(rf + so * GG::Pr);
+            nc[0] -= o.x; nc[1] -= o.y; nc[2] -= o.z; nc[3] -= o.w;
+          }
+        }
+        const float4 pv = lds4(vf + j * GG::P2);
+        c_sum[0] = pv.x + nc[0]; c_sum[1] = pv.y + nc[1];
+        c_sum[2] = pv.z + nc[2]; c_sum[3] = pv.w + nc[3];
+        sts4(vf + j * GG::P2, c_sum[0], c_sum[1], c_sum[2], c_sum[3]);
+      }
     }
-    }
+    ring_new += R;
+    while (ring_new >= GG::ringN) ring_new -= GG::ringN;
+    ring_old += R;
+    while (ring_old >= GG::ringN) ring_old -= GG::ringN;
+    __syncthreads();  // vs2 complete
 
     // ---- H2 -----------------------------------------------------------
-    if (prev && warp >= NCH1) {
-      const int ch = warp - NCH1;
+    constexpr int nq2 = TX / KR;
+    for (int ch = warp; ch * 4 < nq2; ch += nt / 32) {
       const int j = jl, q = ch * 4 + ql;
-      const int yo = y0 + pb + j - 2 * r;
-      if (yo >= y0 && yo < yend && x0 + q * KR < W) {
+      const int yo = y0 + base + j - 2 * r;
+      if (yo < y0 || yo >= yend) continue;
       const int xo0 = q * KR;
       const int gxo = x0 + xo0;
+      if (gxo >= W) continue;
       const float* grow = G + (int64_t)yo * W + gxo;
       const bool two = gxo + 4 < W;
       const float4 g0 = __ldg(reinterpret_cast<const float4*>(grow));
@@ -513,11 +525,7 @@ __global__ void __launch_bounds__(640, 1)
       float* orow = O + (int64_t)yo * W + gxo;
       *reinterpret_cast<float4*>(orow) = make_float4(ov[0], ov[1], ov[2], ov[3]);
       if (two) *reinterpret_cast<float4*>(orow + 4) = make_float4(ov[4], ov[5], ov[6], ov[7]);
-      }
     }
-
-    ring_new += R;
-    while (ring_new >= GG::ringN) ring_new -= GG::ringN;
   }
   // Non-finite inputs are not tested per element here: they always poison
   // the output at their own pixel, so the host (gf_check_finite) classifies
