@@ -2,27 +2,29 @@
 // NCHW on sm_100a: ONE kernel reads guide and src once and writes out once.
 //
 // Work item = (plane, column strip of TX output columns, row segment of TY
-// output rows).  A CTA walks its segment top to bottom in batches of R rows
-// and keeps every intermediate on chip:
+// output rows).  A CTA streams its segment top to bottom in batches of R
+// coefficient rows.  Two kinds of work alternate, separated by the only two
+// CTA barriers of a batch:
 //
-//   stage  the batch's R entering input rows stream into shared memory with
-//          cp.async one batch ahead (zero-filled outside the image)
-//   V1     vertical running window sums of g, g^2, s, g*s, four columns per
-//          thread (the rows leaving the window are re-read from L2 with
-//          128-bit loads)                                         -> smem vs
-//   H1     horizontal window sums (runs of 8 columns), window means, var,
-//          cov, A = cov/(var+eps), b = mean_s - A*mean_g           -> smem ring
-//   V2     vertical running sums of A and b over the ring of the last
-//          max(2r+1, R) coefficient rows, four columns per thread; the
-//          leaving rows are subtracted before H1 overwrites them  -> smem vs2
-//   H2     horizontal sums (runs of 8), Ah = M(A), bh = M(b), out = Ah*G + bh
-//          with 128-bit loads of G and 128-bit stores of out.
+//   column phase X(k)   one thread per column, every thread busy
+//     V1(k)    vertical running window sums of g, g^2, s, g*s for batch k
+//              (entering rows from the TMA-staged rows, leaving rows re-read
+//              from L2)                                          -> smem vs
+//     V2(k-1)  vertical running sums of the coefficient rows A, b of batch
+//              k-1 (entering rows and the leaving rows of batch k are read
+//              from the coefficient ring before H1(k) overwrites them) -> vs2
+//   run phase Y(k)      one thread per (row, run of K columns)
+//     H1(k)    horizontal window sums of the 4 fields streamed over a run of
+//              K=16 columns, A = cov/(var+eps), b = mean_s - A mean_g
+//                                                        -> coefficient ring
+//     H2(k-1)  horizontal sums of A, b streamed over a run, out = Ah*G + bh,
+//              128-bit loads of G and stores of out
 //
-// Every shared row is 16-byte aligned with a pitch = 4 (mod 32) words: the
-// 8 lanes of a quarter warp (8 rows of one run) then read 8 distinct bank
-// quads with 128-bit loads.  The radius is a template parameter (1..16) so
-// every window loop is unrolled; runs that lie inside the image use the
-// constant 1/(2r+1) column normaliser.
+// The TMA load of the next batch's entering rows (cp.async.bulk.tensor,
+// zero-filled outside the image) is issued at the start of Y(k) and lands
+// while Y(k) computes.  Run-phase reads are 128-bit and conflict free: the 8
+// lanes of a quarter warp are 8 rows of one run and every row pitch is 4 mod
+// 32 words; column-phase accesses are consecutive words.
 //
 // Windows are clamped to the image and normalised by the true count
 // N = ny*nx (gf/filters.py:82-103): out-of-image rows/columns contribute 0.
@@ -38,56 +40,99 @@
 namespace gfb {
 namespace hrf {
 
-constexpr int R = 8;     // rows per batch
+constexpr int R = 8;     // coefficient rows per batch (= lanes per run group)
 constexpr int TX = 256;  // output columns per work item
-constexpr int KR = 8;    // run length of H1 and H2
+constexpr int K = 16;    // run length of H1 and H2
 constexpr int kMaxRadius = 16;
 
 __host__ __device__ constexpr int up4(int n) { return (n + 3) / 4 * 4; }
 // smallest p >= n with p = 4 (mod 32)
 __host__ __device__ constexpr int pitch4(int n) { return n + ((36 - n % 32) % 32); }
 __host__ __device__ constexpr int cmax(int a, int b) { return a > b ? a : b; }
+__host__ __device__ constexpr int cdiv(int a, int b) { return (a + b - 1) / b; }
 
 template <int RAD>
 struct Geo {
-  static constexpr int W2 = TX + 2 * RAD;                 // coefficient columns
-  static constexpr int nq1 = (W2 + KR - 1) / KR;          // H1 runs per row
-  static constexpr int PADL = up4(2 * RAD);               // staged columns left of x0
-  static constexpr int off = PADL - 2 * RAD;              // vs col of a window start
-  static constexpr int nv1 = (off + 2 * RAD + KR + 3) / 4;  // float4s per H1 run window
-  static constexpr int VW = up4(cmax(TX + 2 * PADL, (nq1 - 1) * KR + 4 * nv1));  // V1 columns
+  static constexpr int W2 = TX + 2 * RAD;  // coefficient columns
+  static constexpr int nq1 = cdiv(W2, K);  // H1 runs per row
+  static constexpr int nq2 = TX / K;       // H2 runs per row
+  static constexpr int RW = nq1 * K;       // ring row width (>= W2)
+  // vs column c <-> image column x0 - PADL + c (16-byte aligned TMA boxes); the
+  // window of coefficient column a starts at vs column a + off
+  static constexpr int PADL = up4(2 * RAD);
+  static constexpr int off = PADL - 2 * RAD;  // 0 or 2
+  static constexpr int VW = up4(cmax(TX + 2 * PADL, RW + PADL));  // V1 columns
   static constexpr int P1 = pitch4(VW);
   static constexpr int ringN = cmax(2 * RAD + 1, R);
-  static constexpr int ringw = nq1 * KR;                  // >= W2
-  static constexpr int Pr = pitch4(ringw);
-  static constexpr int nv2 = (2 * RAD + KR + 3) / 4;      // float4s per H2 run window
-  static constexpr int v2w = up4(cmax(ringw, TX - KR + 4 * nv2));
-  static constexpr int P2 = pitch4(v2w);
-  static constexpr int nt = 32 * cmax(cmax((nq1 + 3) / 4, TX / KR / 4),
-                                      cmax((VW / 2 + 31) / 32, (v2w / 2 + 31) / 32));
+  static constexpr int Pr = pitch4(RW);
+  static constexpr int P2 = pitch4(W2);
+  static constexpr int h1w = cdiv(nq1, 4);  // warps of H1 (4 runs x 8 rows each)
+  static constexpr int h2w = nq2 / 4;       // warps of H2
+  static constexpr int nt = 32 * cmax(cdiv(cmax(VW, W2), 32), h1w + h2w);
   // TMA boxes of the staged rows: NB boxes of BX columns (box dims <= 256)
-  static constexpr int NB = (VW + 255) / 256;
-  static constexpr int BX = up4((VW + NB - 1) / NB);
+  static constexpr int NB = cdiv(VW, 256);
+  static constexpr int BX = up4(cdiv(VW, NB));
   static constexpr int SWF = NB * BX;  // staged columns per field (>= VW)
   static constexpr size_t smem_floats = (size_t)2 * R * SWF + (size_t)4 * R * P1 +
                                         (size_t)2 * ringN * Pr + (size_t)2 * R * P2 + 4;
   static constexpr size_t smem_bytes = smem_floats * sizeof(float);
   static constexpr uint32_t tx_bytes = 2u * NB * R * BX * 4u;
+  static constexpr int min_blocks = smem_bytes <= 112 * 1024 ? 2 : 1;
+  // float4 window chunks at offset 2r from an aligned run start are aligned
+  // when 2r = 0 mod 4 (else two 8-byte halves)
+  static constexpr bool A4 = (2 * RAD) % 4 == 0;
 };
-
-__device__ __forceinline__ void cp_async16(float* dst, const float* src, bool valid) {
-  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
-  const int n = valid ? 16 : 0;  // 0 -> zero fill, nothing read
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(d), "l"(src), "r"(n));
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n"); }
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n"); }
 
 __device__ __forceinline__ float4 lds4(const float* p) {
   return *reinterpret_cast<const float4*>(p);
 }
+template <bool A4>
+__device__ __forceinline__ float4 lds4u(const float* p) {
+  if constexpr (A4) {
+    return *reinterpret_cast<const float4*>(p);
+  } else {  // 8-byte aligned
+    const float2 a = *reinterpret_cast<const float2*>(p);
+    const float2 b = *reinterpret_cast<const float2*>(p + 2);
+    return make_float4(a.x, a.y, b.x, b.y);
+  }
+}
 __device__ __forceinline__ void sts4(float* p, float a, float b, float c, float d) {
   *reinterpret_cast<float4*>(p) = make_float4(a, b, c, d);
+}
+
+// sum of p[0 .. N-1], N even; p 16-byte aligned, or 8-byte aligned with
+// (N - 2) = 0 mod 4 when HEAD2
+template <int N, bool HEAD2 = false>
+__device__ __forceinline__ float window_sum(const float* p) {
+  float acc = 0.f;
+  if constexpr (HEAD2) {
+    const float2 v = *reinterpret_cast<const float2*>(p);
+    acc += v.x;
+    acc += v.y;
+#pragma unroll
+    for (int c = 2; c + 4 <= N; c += 4) {
+      const float4 w = lds4(p + c);
+      acc += w.x;
+      acc += w.y;
+      acc += w.z;
+      acc += w.w;
+    }
+    return acc;
+  }
+#pragma unroll
+  for (int c = 0; c + 4 <= N; c += 4) {
+    const float4 v = lds4(p + c);
+    acc += v.x;
+    acc += v.y;
+    acc += v.z;
+    acc += v.w;
+  }
+  if constexpr (N % 4 == 2) {
+    const float2 v = *reinterpret_cast<const float2*>(p + (N / 4) * 4);
+    acc += v.x;
+    acc += v.y;
+  }
+  return acc;
 }
 
 struct Args {
@@ -106,25 +151,18 @@ __device__ __forceinline__ int wlen(int i, int n, int r) {
   return b - a + 1;
 }
 
-// staged column c of row j of field f: boxes of BX columns, dense rows
-template <typename GG>
-__device__ __forceinline__ int stg_idx(int f, int j, int c) {
-  const int box = c / GG::BX;
-  return ((f * GG::NB + box) * R + j) * GG::BX + (c - box * GG::BX);
-}
-
 template <int RAD>
-__global__ void __launch_bounds__(320, 2)
+__global__ void __launch_bounds__(Geo<RAD>::nt, Geo<RAD>::min_blocks)
     k_highres_fused(const __grid_constant__ CUtensorMap tmG,
                     const __grid_constant__ CUtensorMap tmS, Args a) {
   using GG = Geo<RAD>;
   constexpr int r = RAD;
-  constexpr int nt = GG::nt;
+  constexpr int ringN = GG::ringN;
   extern __shared__ __align__(128) float4 smem4[];
   float* stg = reinterpret_cast<float*>(smem4);  // [2 fields][NB][R][BX] (TMA boxes)
   float* vs = stg + 2 * R * GG::SWF;             // [4 fields][R][P1]
   float* ring = vs + 4 * R * GG::P1;             // [2 fields][ringN][Pr]
-  float* vs2 = ring + 2 * GG::ringN * GG::Pr;    // [2 fields][R][P2]
+  float* vs2 = ring + 2 * ringN * GG::Pr;        // [2 fields][R][P2]
   uint64_t* bar = reinterpret_cast<uint64_t*>(vs2 + 2 * R * GG::P2);
   const int H = (int)a.H, W = (int)a.W;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -142,7 +180,8 @@ __global__ void __launch_bounds__(320, 2)
   if (y0 >= H) return;
   const int yend = min(y0 + a.TY, H);
   const int64_t plane = (int64_t)H * W;
-  const float* __restrict__ G = a.guide + (a.Cg == a.C ? b * a.C + c : b * a.Cg) * plane;
+  const int64_t gplane = a.Cg == a.C ? b * a.C + c : b * a.Cg;
+  const float* __restrict__ G = a.guide + gplane * plane;
   const float* __restrict__ S = a.src + (b * a.C + c) * plane;
   float* __restrict__ O = a.out + (b * a.C + c) * plane;
   const float sG = __ldg(G + (int64_t)y0 * W + x0);
@@ -150,382 +189,292 @@ __global__ void __launch_bounds__(320, 2)
   const float eps = a.eps;
   constexpr float inv_full = 1.0f / (float)(2 * r + 1);
 
-  for (int i = tid; i < 2 * GG::ringN * GG::Pr; i += nt) ring[i] = 0.f;
-
-  const int ya0 = y0 - r;                 // first coefficient row
+  const int ya0 = y0 - r;                 // image row of coefficient row 0
   const int nrows = (yend - y0) + 2 * r;  // coefficient rows of this item
+  const int nb = (nrows + R - 1) / R;     // batches
   const int first_add = y0 - 2 * r;       // first input row ever added
-  const int xs0 = x0 - GG::PADL;          // global column of vs/stg column 0
+  const int xs0 = x0 - GG::PADL;          // image column of vs / stg column 0
 
-  // TMA of the R entering input rows of the batch at bb (rows ya0+bb+r ...);
-  // out-of-image box elements are zero-filled by the hardware
-  const int zG = (int)(a.Cg == a.C ? b * a.C + c : b * a.Cg);
-  const int zS = (int)(b * a.C + c);
   if (tid == 0) tma::mbar_init(bar, 1);
   __syncthreads();
   uint32_t phase = 0;
-  auto prefetch = [&](int bb) {
+  // TMA of the R entering input rows of batch k (image rows ya0 + kR + r ...)
+  auto prefetch = [&](int k) {
     if (tid == 0) {
       tma::fence_proxy_async();
       tma::mbar_arrive_expect_tx(bar, GG::tx_bytes);
-      const int e0 = ya0 + bb + r;
+      const int e0 = ya0 + k * R + r;
 #pragma unroll
       for (int box = 0; box < GG::NB; ++box) {
-        tma::load_3d(stg + (0 * GG::NB + box) * R * GG::BX, &tmG, xs0 + box * GG::BX, e0, zG, bar);
-        tma::load_3d(stg + (1 * GG::NB + box) * R * GG::BX, &tmS, xs0 + box * GG::BX, e0, zS, bar);
+        tma::load_3d(stg + (0 * GG::NB + box) * R * GG::BX, &tmG, xs0 + box * GG::BX, e0,
+                     (int)gplane, bar);
+        tma::load_3d(stg + (1 * GG::NB + box) * R * GG::BX, &tmS, xs0 + box * GG::BX, e0,
+                     (int)(b * a.C + c), bar);
       }
     }
   };
   prefetch(0);
 
-  // ---- level-1 state: V1T threads per field group; group 0 keeps the guide
-  //      sums (g, g^2), group 1 the source sums (s, g*s); thread owns vs
-  //      columns 4t..4t+3 of its group
-  constexpr int V1T = GG::VW / 4;
-  const int grp = tid < V1T ? 0 : 1;
-  const int t4 = tid - grp * V1T;
-  const bool v1 = tid < 2 * V1T;
-  const int gx4 = xs0 + 4 * t4;
-  const bool col_ok = v1 && gx4 >= 0 && gx4 < W;  // W % 4 == 0: all 4 or none
-  const bool cols_in = xs0 >= 0 && xs0 + GG::VW <= W;  // CTA-uniform
-  float sA[4] = {0.f, 0.f, 0.f, 0.f}, sB[4] = {0.f, 0.f, 0.f, 0.f};
+  // ---- column-phase state: thread owns vs column `tid` (V1) and
+  //      coefficient column `tid` (V2)
+  const bool v1 = tid < GG::VW;
+  const int gx = xs0 + tid;
+  const bool col_ok = v1 && gx >= 0 && gx < W;
+  const int sbox = tid / GG::BX;
+  const float* st_g = stg + sbox * R * GG::BX + (tid - sbox * GG::BX);
+  const float* st_s = st_g + GG::NB * R * GG::BX;
+  float sI = 0.f, sII = 0.f, sP = 0.f, sIP = 0.f;
   if (col_ok) {
-    for (int y = max(first_add, 0); y < min(y0, H); ++y) {
-      const float4 g4 = __ldg(reinterpret_cast<const float4*>(G + (int64_t)y * W + gx4));
-      const float gg[4] = {g4.x - sG, g4.y - sG, g4.z - sG, g4.w - sG};
-      if (grp == 0) {
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          sA[k] += gg[k];
-          sB[k] += gg[k] * gg[k];
-        }
-      } else {
-        const float4 v4 = __ldg(reinterpret_cast<const float4*>(S + (int64_t)y * W + gx4));
-        const float ss[4] = {v4.x - sS, v4.y - sS, v4.z - sS, v4.w - sS};
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          sA[k] += ss[k];
-          sB[k] += gg[k] * ss[k];
-        }
-      }
+    for (int y = max(first_add, 0); y < y0; ++y) {
+      const float gv = __ldg(G + (int64_t)y * W + gx) - sG;
+      const float pv = __ldg(S + (int64_t)y * W + gx) - sS;
+      sI += gv;
+      sII = fmaf(gv, gv, sII);
+      sP += pv;
+      sIP = fmaf(gv, pv, sIP);
     }
   }
-  // ---- level-2 state: V2T threads per coefficient field (A, then b); a
-  //      thread owns coefficient columns 4u..4u+3 of its field
-  constexpr int V2T = GG::v2w / 4;
-  const int fld = tid < V2T ? 0 : 1;
-  const int u4 = tid - fld * V2T;
-  const bool v2 = tid < 2 * V2T;
-  const bool v2ring = v2 && u4 < GG::ringw / 4;
-  float c_sum[4] = {0.f, 0.f, 0.f, 0.f};
+  const bool v2 = tid < GG::W2;
+  float cA = 0.f, cB = 0.f;  // level-2 sums at the end of the last finished batch
+  float pA[R], pB[R];        // running sums minus the leaving rows (pre-subtracted)
+#pragma unroll
+  for (int j = 0; j < R; ++j) pA[j] = pB[j] = 0.f;
+  int s_cur = 0;                                      // ring slot of coefficient row kR
+  int s_prev = ringN - (R % ringN);                   // ... of row (k-1)R
+  if (s_prev == ringN) s_prev = 0;
+  int s_old = ringN - ((2 * r + 1) % ringN);          // ... of row kR - 2r - 1
+  if (s_old == ringN) s_old = 0;
   bool bad = false, degen = false;
-  int ring_new = 0;                                   // slot of coefficient row `base`
-  int ring_old = GG::ringN - (2 * r + 1) % GG::ringN;  // slot of row base - 2r - 1
-  if (ring_old == GG::ringN) ring_old = 0;
-  const int jl = lane & 7;   // run mapping of H1/H2: row
-  const int ql = lane >> 3;  //                       run within the warp's chunk
 
-  for (int base = 0; base < nrows; base += R) {
-    tma::mbar_wait(bar, phase);  // this batch's rows landed in stg
-    phase ^= 1u;
-    __syncthreads();  // ... and the previous batch's H2 is done with vs2
-
-    // ---- V2 (part 1): subtract the leaving coefficient rows while their
-    //      ring slots still hold them: vs2[j] = sum - sum_{i<=j} old_i
-    if (v2) {
-      float pc[4] = {c_sum[0], c_sum[1], c_sum[2], c_sum[3]};
-      const float* rf = ring + fld * GG::ringN * GG::Pr + 4 * u4;
-      float* vf = vs2 + fld * R * GG::P2 + 4 * u4;
-#pragma unroll
-      for (int j = 0; j < R; ++j) {
-        // rows leaving for j >= 2r+1 belong to this batch: part 2 handles them
-        if (j < 2 * r + 1 && v2ring && base + j - 2 * r - 1 >= 0) {
-          int so = ring_old + j;
-          if (so >= GG::ringN) so -= GG::ringN;
-          const float4 o = lds4(rf + so * GG::Pr);
-          pc[0] -= o.x; pc[1] -= o.y; pc[2] -= o.z; pc[3] -= o.w;
-        }
-        sts4(vf + j * GG::P2, pc[0], pc[1], pc[2], pc[3]);
-      }
+  for (int k = 0; k <= nb; ++k) {
+    const int base = k * R;
+    if (k < nb) {
+      tma::mbar_wait(bar, phase);  // batch k's entering rows landed in stg
+      phase ^= 1u;
     }
 
-    // ---- V1 -----------------------------------------------------------
-    // uniform fast path: every row and column of the batch inside the image
-    const bool fast = cols_in && base + R <= nrows && ya0 + base - r - 1 >= max(first_add, 0) &&
-                      ya0 + base + R - 1 + r < H;
-    if (v1 && fast) {
-      // no predicates: leaving rows straight from L2, entering rows from stg
-      float* out0 = vs + (2 * grp + 0) * R * GG::P1 + 4 * t4;
-      float* out1 = vs + (2 * grp + 1) * R * GG::P1 + 4 * t4;
-      const float* gl_p = G + (int64_t)(ya0 + base - r - 1) * W + gx4;
-      const float* sl_p = S + (int64_t)(ya0 + base - r - 1) * W + gx4;
-      const float* ge_p = stg + stg_idx<GG>(0, 0, 4 * t4);
-      const float* se_p = stg + stg_idx<GG>(1, 0, 4 * t4);
-      float4 gl[R], sl[R];
+    // ================= column phase X(k) =================================
+    if (k < nb && v1) {
+      float* o = vs + tid;
+      const int l0 = ya0 + base - r - 1;  // leaving image row of row 0
+      const bool rows_fast = base + R <= nrows && l0 >= max(first_add, 0) &&
+                             ya0 + base + R - 1 + r < H;
+      if (rows_fast) {
+        if (col_ok) {
+          float lg[R], ls[R];
+          const float* gl = G + (int64_t)l0 * W + gx;
+          const float* sl = S + (int64_t)l0 * W + gx;
 #pragma unroll
-      for (int j = 0; j < R; ++j) {
-        gl[j] = __ldg(reinterpret_cast<const float4*>(gl_p + (int64_t)j * W));
-        if (grp) sl[j] = __ldg(reinterpret_cast<const float4*>(sl_p + (int64_t)j * W));
-      }
-      if (grp == 0) {
+          for (int j = 0; j < R; ++j) {
+            lg[j] = __ldg(gl + (int64_t)j * W);
+            ls[j] = __ldg(sl + (int64_t)j * W);
+          }
+#pragma unroll
+          for (int j = 0; j < R; ++j) {
+            const float eg = st_g[j * GG::BX] - sG, es = st_s[j * GG::BX] - sS;
+            const float qg = lg[j] - sG, qs = ls[j] - sS;
+            sI += eg - qg;
+            sII = fmaf(eg, eg, sII);
+            sII = fmaf(-qg, qg, sII);
+            sP += es - qs;
+            sIP = fmaf(eg, es, sIP);
+            sIP = fmaf(-qg, qs, sIP);
+            o[(0 * R + j) * GG::P1] = sI;
+            o[(1 * R + j) * GG::P1] = sII;
+            o[(2 * R + j) * GG::P1] = sP;
+            o[(3 * R + j) * GG::P1] = sIP;
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < R; ++j) {
+            o[(0 * R + j) * GG::P1] = 0.f;
+            o[(1 * R + j) * GG::P1] = 0.f;
+            o[(2 * R + j) * GG::P1] = 0.f;
+            o[(3 * R + j) * GG::P1] = 0.f;
+          }
+        }
+      } else {  // top / bottom batches: per-row predicates
 #pragma unroll
         for (int j = 0; j < R; ++j) {
-          const float4 e = lds4(ge_p + j * GG::BX);
-          const float gn[4] = {e.x - sG, e.y - sG, e.z - sG, e.w - sG};
-          const float gq[4] = {gl[j].x - sG, gl[j].y - sG, gl[j].z - sG, gl[j].w - sG};
-#pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            sA[k] += gn[k] - gq[k];
-            sB[k] += fmaf(gn[k], gn[k], -gq[k] * gq[k]);
+          const int i = base + j;
+          const int e = ya0 + i + r, l = e - 2 * r - 1;
+          const bool in_i = i < nrows;
+          const bool e_ok = col_ok && in_i && e >= 0 && e < H;
+          const bool l_ok = col_ok && in_i && l >= first_add && l >= 0 && l < H;
+          float eg = 0.f, es = 0.f, qg = 0.f, qs = 0.f;
+          if (e_ok) {
+            eg = st_g[j * GG::BX] - sG;
+            es = st_s[j * GG::BX] - sS;
           }
-          sts4(out0 + j * GG::P1, sA[0], sA[1], sA[2], sA[3]);
-          sts4(out1 + j * GG::P1, sB[0], sB[1], sB[2], sB[3]);
-        }
-      } else {
-#pragma unroll
-        for (int j = 0; j < R; ++j) {
-          const float4 e = lds4(ge_p + j * GG::BX);
-          const float4 f = lds4(se_p + j * GG::BX);
-          const float gn[4] = {e.x - sG, e.y - sG, e.z - sG, e.w - sG};
-          const float sn[4] = {f.x - sS, f.y - sS, f.z - sS, f.w - sS};
-          const float gq[4] = {gl[j].x - sG, gl[j].y - sG, gl[j].z - sG, gl[j].w - sG};
-          const float sq[4] = {sl[j].x - sS, sl[j].y - sS, sl[j].z - sS, sl[j].w - sS};
-#pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            sA[k] += sn[k] - sq[k];
-            sB[k] += fmaf(gn[k], sn[k], -gq[k] * sq[k]);
-          }
-          sts4(out0 + j * GG::P1, sA[0], sA[1], sA[2], sA[3]);
-          sts4(out1 + j * GG::P1, sB[0], sB[1], sB[2], sB[3]);
-        }
-      }
-    } else if (v1) {
-      float* out0 = vs + (2 * grp + 0) * R * GG::P1 + 4 * t4;
-      float* out1 = vs + (2 * grp + 1) * R * GG::P1 + 4 * t4;
-#pragma unroll
-      for (int half = 0; half < 2; ++half) {
-        float4 gl[R / 2], sl[R / 2];
-#pragma unroll
-        for (int jj = 0; jj < R / 2; ++jj) {
-          const int j = half * (R / 2) + jj;
-          const int l = ya0 + base + j - r - 1;
-          const bool l_ok = fast || (col_ok && base + j < nrows && l >= first_add && l >= 0 && l < H);
-          gl[jj] = sl[jj] = make_float4(0.f, 0.f, 0.f, 0.f);
           if (l_ok) {
-            gl[jj] = __ldg(reinterpret_cast<const float4*>(G + (int64_t)l * W + gx4));
-            if (grp) sl[jj] = __ldg(reinterpret_cast<const float4*>(S + (int64_t)l * W + gx4));
+            qg = __ldg(G + (int64_t)l * W + gx) - sG;
+            qs = __ldg(S + (int64_t)l * W + gx) - sS;
           }
-        }
-#pragma unroll
-        for (int jj = 0; jj < R / 2; ++jj) {
-          const int j = half * (R / 2) + jj;
-          const float4 ge4 = lds4(stg + stg_idx<GG>(0, j, 4 * t4));
-          float gn[4] = {ge4.x - sG, ge4.y - sG, ge4.z - sG, ge4.w - sG};
-          float gq[4] = {gl[jj].x - sG, gl[jj].y - sG, gl[jj].z - sG, gl[jj].w - sG};
-          float sn[4] = {0.f, 0.f, 0.f, 0.f}, sq[4] = {0.f, 0.f, 0.f, 0.f};
-          if (grp) {
-            const float4 se4 = lds4(stg + stg_idx<GG>(1, j, 4 * t4));
-            sn[0] = se4.x - sS; sn[1] = se4.y - sS; sn[2] = se4.z - sS; sn[3] = se4.w - sS;
-            sq[0] = sl[jj].x - sS; sq[1] = sl[jj].y - sS;
-            sq[2] = sl[jj].z - sS; sq[3] = sl[jj].w - sS;
-          }
-          if (!fast) {  // edge batch: zero the out-of-image contributions
-            const int e = ya0 + base + j + r;
-            const int l = ya0 + base + j - r - 1;
-            const bool e_ok = col_ok && base + j < nrows && e >= 0 && e < H;
-            const bool l_ok = col_ok && base + j < nrows && l >= first_add && l >= 0 && l < H;
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-              gn[k] = e_ok ? gn[k] : 0.f;
-              sn[k] = e_ok ? sn[k] : 0.f;
-              gq[k] = l_ok ? gq[k] : 0.f;
-              sq[k] = l_ok ? sq[k] : 0.f;
-            }
-          }
-          if (grp == 0) {
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-              sA[k] += gn[k] - gq[k];
-              sB[k] += gn[k] * gn[k] - gq[k] * gq[k];
-            }
-          } else {
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-              sA[k] += sn[k] - sq[k];
-              sB[k] += gn[k] * sn[k] - gq[k] * sq[k];
-            }
-          }
-          const float m = col_ok ? 1.f : 0.f;
-          sts4(out0 + j * GG::P1, m * sA[0], m * sA[1], m * sA[2], m * sA[3]);
-          sts4(out1 + j * GG::P1, m * sB[0], m * sB[1], m * sB[2], m * sB[3]);
+          sI += eg - qg;
+          sII = fmaf(eg, eg, sII);
+          sII = fmaf(-qg, qg, sII);
+          sP += es - qs;
+          sIP = fmaf(eg, es, sIP);
+          sIP = fmaf(-qg, qs, sIP);
+          o[(0 * R + j) * GG::P1] = sI;
+          o[(1 * R + j) * GG::P1] = sII;
+          o[(2 * R + j) * GG::P1] = sP;
+          o[(3 * R + j) * GG::P1] = sIP;
         }
       }
     }
-    __syncthreads();  // vs complete; stg consumed
-
-    // the next batch's entering rows stream in while H1/V2/H2 compute
-    if (base + R < nrows) prefetch(base + R);
-
-    // ---- H1 -----------------------------------------------------------
-    for (int ch = warp; ch * 4 < GG::nq1; ch += nt / 32) {
-      const int j = jl, q = ch * 4 + ql;
-      if (q >= GG::nq1 || base + j >= nrows) continue;
-      const int ya = ya0 + base + j;
-      const int xa0 = q * KR;
-      int slot = ring_new + j;
-      if (slot >= GG::ringN) slot -= GG::ringN;
-      float* ra = ring + slot * GG::Pr + xa0;
-      float* rb = ring + (GG::ringN + slot) * GG::Pr + xa0;
-      if (ya < 0 || ya >= H) {
-        sts4(ra, 0.f, 0.f, 0.f, 0.f);
-        sts4(ra + 4, 0.f, 0.f, 0.f, 0.f);
-        sts4(rb, 0.f, 0.f, 0.f, 0.f);
-        sts4(rb + 4, 0.f, 0.f, 0.f, 0.f);
-        continue;
-      }
-      float hs[4][KR];
-#pragma unroll
-      for (int f = 0; f < 4; ++f) {
-        const float* v = vs + (f * R + j) * GG::P1 + xa0;
-        float w[4 * GG::nv1];
-#pragma unroll
-        for (int m = 0; m < GG::nv1; ++m) {
-          const float4 t4 = lds4(v + 4 * m);
-          w[4 * m] = t4.x;
-          w[4 * m + 1] = t4.y;
-          w[4 * m + 2] = t4.z;
-          w[4 * m + 3] = t4.w;
-        }
-        float acc = 0.f;
-#pragma unroll
-        for (int d = 0; d < 2 * r; ++d) acc += w[GG::off + d];
-#pragma unroll
-        for (int k = 0; k < KR; ++k) {
-          acc += w[GG::off + k + 2 * r];
-          hs[f][k] = acc;
-          acc -= w[GG::off + k];
-        }
-      }
-      const float iny = fast_rcp((float)wlen(ya, H, r));
-      const int gxa0 = x0 - r + xa0;  // global column of the run's first coefficient
-      const bool interior = gxa0 >= r && gxa0 + KR - 1 + r <= W - 1 && xa0 + KR <= GG::W2;
-      float A[KR], B[KR];
-      if (interior) {  // warp-uniform except at strip edges
-        const float inv = iny * inv_full;
-#pragma unroll
-        for (int k = 0; k < KR; ++k) {
-          const float mg = hs[0][k] * inv, ms = hs[2][k] * inv;
-          const float var = hs[1][k] * inv - mg * mg;
-          const float cov = hs[3][k] * inv - mg * ms;
-          if (eps == 0.f && !(var > 0.f)) degen = true;
-          A[k] = cov * fast_rcp(var + eps);
-          B[k] = (ms + sS) - A[k] * (mg + sG);
-        }
-      } else {
-#pragma unroll
-        for (int k = 0; k < KR; ++k) {
-          const int gxa = gxa0 + k;
-          const bool ok = xa0 + k < GG::W2 && gxa >= 0 && gxa < W;
-          const float inv = iny * fast_rcp((float)wlen(gxa, W, r));
-          const float mg = hs[0][k] * inv, ms = hs[2][k] * inv;
-          const float var = hs[1][k] * inv - mg * mg;
-          const float cov = hs[3][k] * inv - mg * ms;
-          if (ok && eps == 0.f && !(var > 0.f)) degen = true;
-          const float Ak = cov * fast_rcp(var + eps);
-          A[k] = ok ? Ak : 0.f;
-          B[k] = ok ? (ms + sS) - Ak * (mg + sG) : 0.f;
-        }
-      }
-      sts4(ra, A[0], A[1], A[2], A[3]);
-      sts4(ra + 4, A[4], A[5], A[6], A[7]);
-      sts4(rb, B[0], B[1], B[2], B[3]);
-      sts4(rb + 4, B[4], B[5], B[6], B[7]);
-    }
-    __syncthreads();  // ring rows of this batch complete
-
-    // ---- V2 (part 2): add the entering coefficient rows ----------------
     if (v2) {
-      float nc[4] = {0.f, 0.f, 0.f, 0.f};
-      const float* rf = ring + fld * GG::ringN * GG::Pr + 4 * u4;
-      float* vf = vs2 + fld * R * GG::P2 + 4 * u4;
+      const float* rA = ring + tid;
+      const float* rB = ring + ringN * GG::Pr + tid;
+      if (k >= 1) {  // V2(k-1): add batch k-1's coefficient rows -> vs2
+        const int bb = base - R;
+        float nA = 0.f, nB = 0.f;
 #pragma unroll
-      for (int j = 0; j < R; ++j) {
-        if (v2ring && base + j < nrows) {
-          int sn = ring_new + j;
-          if (sn >= GG::ringN) sn -= GG::ringN;
-          const float4 x = lds4(rf + sn * GG::Pr);
-          nc[0] += x.x; nc[1] += x.y; nc[2] += x.z; nc[3] += x.w;
-          if (j >= 2 * r + 1) {  // leaving row added earlier in this batch (r small)
-            int so = ring_new + j - 2 * r - 1;
-            if (so >= GG::ringN) so -= GG::ringN;
-            const float4 o = lds4(rf + so * GG::Pr);
-            nc[0] -= o.x; nc[1] -= o.y; nc[2] -= o.z; nc[3] -= o.w;
+        for (int j = 0; j < R; ++j) {
+          if (bb + j < nrows) {
+            int s = s_prev + j;
+            if (s >= ringN) s -= ringN;
+            nA += rA[s * GG::Pr];
+            nB += rB[s * GG::Pr];
+            if (j >= 2 * r + 1) {  // leaving row inside this batch (small r)
+              int so = s - (2 * r + 1);
+              if (so < 0) so += ringN;
+              nA -= rA[so * GG::Pr];
+              nB -= rB[so * GG::Pr];
+            }
+          }
+          vs2[j * GG::P2 + tid] = pA[j] + nA;
+          vs2[(R + j) * GG::P2 + tid] = pB[j] + nB;
+        }
+        cA = pA[R - 1] + nA;
+        cB = pB[R - 1] + nB;
+      }
+      if (k < nb) {  // pre-subtract batch k's leaving rows before H1(k) overwrites them
+        float qa = cA, qb = cB;
+#pragma unroll
+        for (int j = 0; j < R; ++j) {
+          if (j < 2 * r + 1 && base + j - 2 * r - 1 >= 0) {
+            int so = s_old + j;
+            if (so >= ringN) so -= ringN;
+            qa -= rA[so * GG::Pr];
+            qb -= rB[so * GG::Pr];
+          }
+          pA[j] = qa;
+          pB[j] = qb;
+        }
+      }
+    }
+    __syncthreads();  // vs, vs2 complete; stg and the leaving ring rows consumed
+
+    // ================= run phase Y(k) ====================================
+    if (k + 1 < nb) prefetch(k + 1);
+    const int j = lane & 7;
+    if (warp < GG::h1w) {
+      // ---- H1(k): coefficient row base+j, columns [qK, qK+K) ---------------
+      const int q = warp * 4 + (lane >> 3);
+      const int i = base + j;
+      if (k < nb && q < GG::nq1 && i < nrows) {
+        const int ya = ya0 + i;
+        int s = s_cur + j;
+        if (s >= ringN) s -= ringN;
+        float* ra = ring + s * GG::Pr + q * K;
+        float* rb = ring + (ringN + s) * GG::Pr + q * K;
+        if (ya < 0 || ya >= H) {
+#pragma unroll
+          for (int m = 0; m < K / 4; ++m) {
+            sts4(ra + 4 * m, 0.f, 0.f, 0.f, 0.f);
+            sts4(rb + 4 * m, 0.f, 0.f, 0.f, 0.f);
+          }
+        } else {
+          const float* v = vs + j * GG::P1 + q * K + GG::off;  // field f at + f*R*P1
+          float acc[4];
+#pragma unroll
+          for (int f = 0; f < 4; ++f)
+            acc[f] = window_sum<2 * r, GG::off != 0>(v + f * R * GG::P1);
+          const float iny = fast_rcp((float)wlen(ya, H, r));
+          const int gxa0 = x0 - r + q * K;  // image column of the run's first coefficient
+          const bool interior = gxa0 >= r && gxa0 + K - 1 + r <= W - 1 && q * K + K <= GG::W2;
+          const float inv_i = iny * inv_full;
+#pragma unroll
+          for (int m = 0; m < K / 4; ++m) {
+            float h[4][4];
+#pragma unroll
+            for (int f = 0; f < 4; ++f) {
+              const float* vf = v + f * R * GG::P1 + 4 * m;
+              const float4 e = lds4(vf + 2 * r);            // vs column q*K + PADL + 4m
+              const float4 l = lds4u<GG::off == 0>(vf);
+              acc[f] += e.x; h[f][0] = acc[f]; acc[f] -= l.x;
+              acc[f] += e.y; h[f][1] = acc[f]; acc[f] -= l.y;
+              acc[f] += e.z; h[f][2] = acc[f]; acc[f] -= l.z;
+              acc[f] += e.w; h[f][3] = acc[f]; acc[f] -= l.w;
+            }
+            float A[4], B[4];
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+              const int gxa = gxa0 + 4 * m + t;
+              const bool ok = interior || (q * K + 4 * m + t < GG::W2 && gxa >= 0 && gxa < W);
+              const float inv = interior ? inv_i : iny * fast_rcp((float)wlen(gxa, W, r));
+              const float mg = h[0][t] * inv, ms = h[2][t] * inv;
+              const float var = fmaf(h[1][t], inv, -mg * mg);
+              const float cov = fmaf(h[3][t], inv, -mg * ms);
+              if (ok && eps == 0.f && !(var > 0.f)) degen = true;
+              const float At = cov * fast_rcp(var + eps);
+              A[t] = ok ? At : 0.f;
+              B[t] = ok ? fmaf(-At, mg + sG, ms + sS) : 0.f;
+            }
+            sts4(ra + 4 * m, A[0], A[1], A[2], A[3]);
+            sts4(rb + 4 * m, B[0], B[1], B[2], B[3]);
           }
         }
-        const float4 pv = lds4(vf + j * GG::P2);
-        c_sum[0] = pv.x + nc[0]; c_sum[1] = pv.y + nc[1];
-        c_sum[2] = pv.z + nc[2]; c_sum[3] = pv.w + nc[3];
-        sts4(vf + j * GG::P2, c_sum[0], c_sum[1], c_sum[2], c_sum[3]);
       }
-    }
-    ring_new += R;
-    while (ring_new >= GG::ringN) ring_new -= GG::ringN;
-    ring_old += R;
-    while (ring_old >= GG::ringN) ring_old -= GG::ringN;
-    __syncthreads();  // vs2 complete
-
-    // ---- H2 -----------------------------------------------------------
-    constexpr int nq2 = TX / KR;
-    for (int ch = warp; ch * 4 < nq2; ch += nt / 32) {
-      const int j = jl, q = ch * 4 + ql;
-      const int yo = y0 + base + j - 2 * r;
-      if (yo < y0 || yo >= yend) continue;
-      const int xo0 = q * KR;
-      const int gxo = x0 + xo0;
-      if (gxo >= W) continue;
-      const float* grow = G + (int64_t)yo * W + gxo;
-      const bool two = gxo + 4 < W;
-      const float4 g0 = __ldg(reinterpret_cast<const float4*>(grow));
-      const float4 g1 = two ? __ldg(reinterpret_cast<const float4*>(grow + 4))
-                            : make_float4(0.f, 0.f, 0.f, 0.f);
-      const float gv[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
-      float hs[2][KR];
+    } else if (warp < GG::h1w + GG::h2w) {
+      // ---- H2(k-1): output row of coefficient row base-R+j, columns [qK, qK+K)
+      const int q = (warp - GG::h1w) * 4 + (lane >> 3);
+      const int yo = y0 - 2 * r + base - R + j;
+      const int gxo0 = x0 + q * K;
+      if (k >= 1 && yo >= y0 && yo < yend && gxo0 < W) {
+        const float* vA = vs2 + j * GG::P2 + q * K;
+        const float* vB = vs2 + (R + j) * GG::P2 + q * K;
+        float accA = window_sum<2 * r>(vA), accB = window_sum<2 * r>(vB);
+        const float iny = fast_rcp((float)wlen(yo, H, r));
+        const bool interior = gxo0 >= r && gxo0 + K - 1 + r <= W - 1;
+        const float inv_i = iny * inv_full;
+        const float* grow = G + (int64_t)yo * W + gxo0;
+        float* orow = O + (int64_t)yo * W + gxo0;
 #pragma unroll
-      for (int f = 0; f < 2; ++f) {
-        const float* v = vs2 + (f * R + j) * GG::P2 + xo0;
-        float w[4 * GG::nv2];
+        for (int m = 0; m < K / 4; ++m) {
+          if (gxo0 + 4 * m >= W) break;  // W % 4 == 0: a float4 is all in or all out
+          const float4 g4 = __ldg(reinterpret_cast<const float4*>(grow + 4 * m));
+          const float4 eA = lds4u<GG::A4>(vA + 4 * m + 2 * r), lA = lds4(vA + 4 * m);
+          const float4 eB = lds4u<GG::A4>(vB + 4 * m + 2 * r), lB = lds4(vB + 4 * m);
+          float hA[4], hB[4];
+          accA += eA.x; hA[0] = accA; accA -= lA.x;
+          accA += eA.y; hA[1] = accA; accA -= lA.y;
+          accA += eA.z; hA[2] = accA; accA -= lA.z;
+          accA += eA.w; hA[3] = accA; accA -= lA.w;
+          accB += eB.x; hB[0] = accB; accB -= lB.x;
+          accB += eB.y; hB[1] = accB; accB -= lB.y;
+          accB += eB.z; hB[2] = accB; accB -= lB.z;
+          accB += eB.w; hB[3] = accB; accB -= lB.w;
+          const float gv[4] = {g4.x, g4.y, g4.z, g4.w};
+          float ov[4];
 #pragma unroll
-        for (int m = 0; m < GG::nv2; ++m) {
-          const float4 t4 = lds4(v + 4 * m);
-          w[4 * m] = t4.x;
-          w[4 * m + 1] = t4.y;
-          w[4 * m + 2] = t4.z;
-          w[4 * m + 3] = t4.w;
-        }
-        float acc = 0.f;
-#pragma unroll
-        for (int d = 0; d < 2 * r; ++d) acc += w[d];
-#pragma unroll
-        for (int k = 0; k < KR; ++k) {
-          acc += w[k + 2 * r];
-          hs[f][k] = acc;
-          acc -= w[k];
+          for (int t = 0; t < 4; ++t) {
+            const float inv =
+                interior ? inv_i : iny * fast_rcp((float)wlen(gxo0 + 4 * m + t, W, r));
+            ov[t] = fmaf(hA[t], gv[t], hB[t]) * inv;
+            if (!isfinite(ov[t])) bad = true;
+          }
+          *reinterpret_cast<float4*>(orow + 4 * m) = make_float4(ov[0], ov[1], ov[2], ov[3]);
         }
       }
-      const float iny = fast_rcp((float)wlen(yo, H, r));
-      const bool interior = gxo >= r && gxo + KR - 1 + r <= W - 1;
-      float ov[KR];
-#pragma unroll
-      for (int k = 0; k < KR; ++k) {
-        const float inv = interior ? iny * inv_full
-                                   : iny * fast_rcp((float)wlen(gxo + k, W, r));
-        ov[k] = (hs[0][k] * inv) * gv[k] + hs[1][k] * inv;
-        if ((k < 4 || two) && !isfinite(ov[k])) bad = true;
-      }
-      float* orow = O + (int64_t)yo * W + gxo;
-      *reinterpret_cast<float4*>(orow) = make_float4(ov[0], ov[1], ov[2], ov[3]);
-      if (two) *reinterpret_cast<float4*>(orow + 4) = make_float4(ov[4], ov[5], ov[6], ov[7]);
     }
+    s_prev = s_cur;
+    s_cur += R;
+    if (s_cur >= ringN) s_cur -= ringN;
+    s_old += R;
+    if (s_old >= ringN) s_old -= ringN;
+    __syncthreads();  // ring rows of batch k and the outputs of batch k-1 done
   }
   // Non-finite inputs are not tested per element here: they always poison
   // the output at their own pixel, so the host (gf_check_finite) classifies
@@ -564,7 +513,7 @@ Launch pick(int r) {
     case 14: return launch_info<14>();
     case 15: return launch_info<15>();
     case 16: return launch_info<16>();
-    default: return {nullptr, 0, 0};
+    default: return {nullptr, 0, 0, 0};
   }
 }
 
@@ -574,6 +523,7 @@ bool fused_highres_fwd_ok(int64_t B, int64_t Cg, int64_t C, int64_t H, int64_t W
   if (r < 1 || r > hrf::kMaxRadius) return false;
   if (W % 4 != 0 || W < 4 || H < 1) return false;
   if (H > (1 << 30) || W > (1 << 30) || H * W > ((int64_t)1 << 40)) return false;
+  if (B * C > (1 << 30)) return false;  // TMA plane coordinate is a 32-bit int
   if (Cg != 1 && Cg != C) return false;
   if (hrf::pick(r).smem > 227 * 1024) return false;
   return B >= 1 && C >= 1;
