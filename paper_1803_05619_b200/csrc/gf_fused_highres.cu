@@ -1,36 +1,41 @@
 // Fused full-resolution guided filter forward (gf/guided.py:198-233) for fp32
 // NCHW on sm_100a: ONE kernel reads guide and src once and writes out once.
 //
-// Work item = (plane, column strip of TX output columns, row segment of TY
-// output rows).  A CTA streams its segment top to bottom in batches of R
-// coefficient rows.  Two kinds of work alternate, separated by the only two
-// CTA barriers of a batch:
+// Work item = rows of (plane, column strip of tx <= 224 output columns); the
+// rows of all strips are cut into equal chunks, one per CTA.  A CTA streams
+// each piece of its chunk top to bottom in batches of R coefficient rows.
+// Two kinds of work alternate, separated by the only two CTA barriers of a
+// batch:
 //
-//   column phase X(k)   one thread per column, every thread busy
-//     V1(k)    vertical running window sums of g, g^2, s, g*s for batch k
-//              (entering rows from the TMA-staged rows, leaving rows re-read
-//              from L2)                                          -> smem vs
-//     V2(k-1)  vertical running sums of the coefficient rows A, b of batch
-//              k-1 (entering rows and the leaving rows of batch k are read
-//              from the coefficient ring before H1(k) overwrites them) -> vs2
-//   run phase Y(k)      one thread per (row, run of K columns)
-//     H1(k)    horizontal window sums of the 4 fields streamed over a run of
-//              K=16 columns, A = cov/(var+eps), b = mean_s - A mean_g
-//                                                        -> coefficient ring
-//     H2(k-1)  horizontal sums of A, b streamed over a run, out = Ah*G + bh,
-//              128-bit loads of G and stores of out
+//   column phase X(k)   every thread owns one column
+//     V1(k)    vertical running window sums of (g, s) and (g^2, g*s) for
+//              batch k (entering rows from the TMA-staged rows, leaving rows
+//              re-read from L2)                                   -> smem vs
+//     V2(k-1)  vertical running sums of the coefficient rows (A, b') of
+//              batch k-1; the leaving rows of batch k are read from the
+//              coefficient ring before H1(k) overwrites them       -> vs2
+//   run phase Y(k)      every thread: H1(k) on one (row, run of K=8 columns),
+//                       then H2(k-1) on one (row, run)
+//     H1(k)    horizontal window sums streamed over the run, A = cov/(var+eps),
+//              b' = mean_s - A mean_g (shifted means)      -> coefficient ring
+//     H2(k-1)  horizontal sums of (A, b') streamed over the run,
+//              out = (Ah*(G - sG) + b'h)/N + sS, 128-bit loads of G and
+//              stores of out
 //
-// The TMA load of the next batch's entering rows (cp.async.bulk.tensor,
-// zero-filled outside the image) is issued at the start of Y(k) and lands
-// while Y(k) computes.  Run-phase reads are 128-bit and conflict free: the 8
-// lanes of a quarter warp are 8 rows of one run and every row pitch is 4 mod
-// 32 words; column-phase accesses are consecutive words.
+// Arithmetic is on fp32 PAIRS (sm_100 FADD2 / FFMA2 / FMUL2): every column,
+// window and coefficient carries two fields side by side -- (s_g, s_s) and
+// (s_gg, s_gs) at level 1, (A, b') at level 2 -- so one instruction updates
+// both, and the shared-memory rows interleave the pair (128-bit loads fetch
+// two columns).  The entering rows arrive by TMA (cp.async.bulk.tensor,
+// zero-filled outside the image) into two stages: the load of batch k+2 is
+// issued at the start of Y(k), into the stage X(k) just consumed.
 //
 // Windows are clamped to the image and normalised by the true count
 // N = ny*nx (gf/filters.py:82-103): out-of-image rows/columns contribute 0.
-// g and s are shifted by a per-CTA constant (var/cov are shift invariant) to
-// keep the fp32 sums small; running sums restart for every segment, so their
-// rounding error is bounded by the segment length, not the image size.
+// g and s are shifted by a per-piece constant (sG, sS; var/cov are shift
+// invariant) to keep the fp32 sums small; b' is the shifted intercept and the
+// shift returns in the output.  Running sums restart for every piece, so
+// their rounding error is bounded by the piece length (<= 1024 rows).
 #include <cuda_runtime.h>
 
 #include "gf_common.cuh"
@@ -41,8 +46,8 @@ namespace gfb {
 namespace hrf {
 
 constexpr int R = 8;     // coefficient rows per batch (= lanes per run group)
-constexpr int TX = 256;  // output columns per work item
-constexpr int K = 16;    // run length of H1 and H2
+constexpr int NT = 256;  // threads: one vs column each in the column phase
+constexpr int K = 8;     // run length of H1 and H2
 constexpr int kMaxRadius = 16;
 
 __host__ __device__ constexpr int up4(int n) { return (n + 3) / 4 * 4; }
@@ -50,97 +55,81 @@ __host__ __device__ constexpr int up4(int n) { return (n + 3) / 4 * 4; }
 __host__ __device__ constexpr int pitch4(int n) { return n + ((36 - n % 32) % 32); }
 __host__ __device__ constexpr int cmax(int a, int b) { return a > b ? a : b; }
 __host__ __device__ constexpr int cdiv(int a, int b) { return (a + b - 1) / b; }
+// widest strip (multiple of K) whose vs columns and H1 reads fit NT columns
+__host__ __device__ constexpr int tx_max(int r) {
+  const int padl = up4(2 * r);
+  int t = NT;
+  while (t >= K && !(t + 2 * padl <= NT && cdiv(t + 2 * r, K) * K + padl <= NT)) t -= K;
+  return t;
+}
 
 template <int RAD>
 struct Geo {
-  static constexpr int W2 = TX + 2 * RAD;  // coefficient columns
-  static constexpr int nq1 = cdiv(W2, K);  // H1 runs per row
-  static constexpr int nq2 = TX / K;       // H2 runs per row
-  static constexpr int RW = nq1 * K;       // ring row width (>= W2)
   // vs column c <-> image column x0 - PADL + c (16-byte aligned TMA boxes); the
   // window of coefficient column a starts at vs column a + off
   static constexpr int PADL = up4(2 * RAD);
   static constexpr int off = PADL - 2 * RAD;  // 0 or 2
-  static constexpr int VW = up4(cmax(TX + 2 * PADL, RW + PADL));  // V1 columns
-  static constexpr int P1 = pitch4(VW);
+  static constexpr int TXM = tx_max(RAD);     // strip width bound (runtime tx <= TXM)
+  static constexpr int W2M = TXM + 2 * RAD;   // coefficient columns bound
+  static constexpr int RWM = cdiv(W2M, K) * K;
+  static constexpr int PV = pitch4(2 * NT);   // vs rows: NT column pairs
   static constexpr int ringN = cmax(2 * RAD + 1, R);
-  static constexpr int Pr = pitch4(RW);
-  static constexpr int P2 = pitch4(W2);
-  static constexpr int h1w = cdiv(nq1, 4);  // warps of H1 (4 runs x 8 rows each)
-  static constexpr int h2w = nq2 / 4;       // warps of H2
-  static constexpr int nt = 32 * cmax(cdiv(cmax(VW, W2), 32), h1w + h2w);
-  // TMA boxes of the staged rows: NB boxes of BX columns (box dims <= 256)
-  static constexpr int NB = cdiv(VW, 256);
-  static constexpr int BX = up4(cdiv(VW, NB));
-  static constexpr int SWF = NB * BX;  // staged columns per field (>= VW)
-  static constexpr size_t smem_floats = (size_t)2 * R * SWF + (size_t)4 * R * P1 +
-                                        (size_t)2 * ringN * Pr + (size_t)2 * R * P2 + 4;
+  static constexpr int PR = pitch4(2 * RWM);  // ring rows: (A, b') pairs
+  static constexpr int P2 = pitch4(2 * W2M);  // vs2 rows: (A, b') sums
+  static constexpr size_t smem_floats = (size_t)2 * 2 * R * NT + (size_t)2 * R * PV +
+                                        (size_t)ringN * PR + (size_t)R * P2 + 4;
   static constexpr size_t smem_bytes = smem_floats * sizeof(float);
-  static constexpr uint32_t tx_bytes = 2u * NB * R * BX * 4u;
-  static constexpr int min_blocks = smem_bytes <= 112 * 1024 ? 2 : 1;
-  // float4 window chunks at offset 2r from an aligned run start are aligned
-  // when 2r = 0 mod 4 (else two 8-byte halves)
-  static constexpr bool A4 = (2 * RAD) % 4 == 0;
+  static constexpr uint32_t tx_bytes = 2u * R * NT * 4u;
+  static constexpr int min_blocks = smem_bytes <= 113 * 1024 ? 2 : 1;
 };
 
-__device__ __forceinline__ float4 lds4(const float* p) {
-  return *reinterpret_cast<const float4*>(p);
+// ---- fp32 pair arithmetic (FADD2 / FMUL2 / FFMA2) -------------------------
+typedef unsigned long long u64;
+__device__ __forceinline__ u64 pk(float a, float b) {
+  u64 r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
 }
-template <bool A4>
-__device__ __forceinline__ float4 lds4u(const float* p) {
-  if constexpr (A4) {
-    return *reinterpret_cast<const float4*>(p);
-  } else {  // 8-byte aligned
-    const float2 a = *reinterpret_cast<const float2*>(p);
-    const float2 b = *reinterpret_cast<const float2*>(p + 2);
-    return make_float4(a.x, a.y, b.x, b.y);
-  }
+__device__ __forceinline__ float lo(u64 v) {
+  return __uint_as_float((unsigned)(v & 0xffffffffull));
 }
-__device__ __forceinline__ void sts4(float* p, float a, float b, float c, float d) {
-  *reinterpret_cast<float4*>(p) = make_float4(a, b, c, d);
+__device__ __forceinline__ float hi(u64 v) { return __uint_as_float((unsigned)(v >> 32)); }
+__device__ __forceinline__ u64 add2(u64 a, u64 b) {
+  u64 r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
 }
+__device__ __forceinline__ u64 sub2(u64 a, u64 b) {
+  u64 r;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ u64 mul2(u64 a, u64 b) {
+  u64 r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ u64 fma2(u64 a, u64 b, u64 c) {
+  u64 r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+__device__ __forceinline__ u64 lds2(const float* p) { return *reinterpret_cast<const u64*>(p); }
+__device__ __forceinline__ ulonglong2 lds22(const float* p) {
+  return *reinterpret_cast<const ulonglong2*>(p);
+}
+__device__ __forceinline__ void sts2(float* p, u64 v) { *reinterpret_cast<u64*>(p) = v; }
 
-// sum of p[0 .. N-1], N even; p 16-byte aligned, or 8-byte aligned with
-// (N - 2) = 0 mod 4 when HEAD2
-template <int N, bool HEAD2 = false>
-__device__ __forceinline__ float window_sum(const float* p) {
-  float acc = 0.f;
-  if constexpr (HEAD2) {
-    const float2 v = *reinterpret_cast<const float2*>(p);
-    acc += v.x;
-    acc += v.y;
-#pragma unroll
-    for (int c = 2; c + 4 <= N; c += 4) {
-      const float4 w = lds4(p + c);
-      acc += w.x;
-      acc += w.y;
-      acc += w.z;
-      acc += w.w;
-    }
-    return acc;
-  }
-#pragma unroll
-  for (int c = 0; c + 4 <= N; c += 4) {
-    const float4 v = lds4(p + c);
-    acc += v.x;
-    acc += v.y;
-    acc += v.z;
-    acc += v.w;
-  }
-  if constexpr (N % 4 == 2) {
-    const float2 v = *reinterpret_cast<const float2*>(p + (N / 4) * 4);
-    acc += v.x;
-    acc += v.y;
-  }
-  return acc;
-}
+// CTA barrier 0
+__device__ __forceinline__ void cta_sync() { asm volatile("bar.sync 0;\n" ::: "memory"); }
 
 struct Args {
   const float* guide;
   const float* src;
   float* out;
   int64_t C, Cg, H, W;
-  int TY, strips, segs;
+  int tx, strips;
+  int64_t U, chunk;  // rows of all (image, strip) columns; rows per CTA
   float eps;
   uint32_t* status;
 };
@@ -151,348 +140,385 @@ __device__ __forceinline__ int wlen(int i, int n, int r) {
   return b - a + 1;
 }
 
+// sum of the N2 pairs p[0..N2) (16-byte aligned, N2 even)
+template <int N2>
+__device__ __forceinline__ u64 window_sum(const float* p) {
+  u64 acc = 0;
+#pragma unroll
+  for (int c = 0; c < N2; c += 2) {
+    const ulonglong2 v = lds22(p + 2 * c);
+    acc = add2(acc, v.x);
+    acc = add2(acc, v.y);
+  }
+  return acc;
+}
+
+// H1 on one run: (g, s) and (gg, gs) window sums streamed over K coefficient
+// columns -> (A, b') pairs into the ring row `ra`.
+template <int RAD, bool INTERIOR>
+__device__ __forceinline__ void h1_run(const float* vA, const float* vB, float* ra, float iny,
+                                       int gxa0, int w2_left, int W, float eps, float& vmin) {
+  constexpr int r = RAD;
+  u64 accA = window_sum<2 * r>(vA), accB = window_sum<2 * r>(vB);
+  const float inv_i = iny * (1.0f / (float)(2 * r + 1));
+#pragma unroll
+  for (int m = 0; m < K; m += 2) {
+    const ulonglong2 eA = lds22(vA + 2 * (m + 2 * r)), lA = lds22(vA + 2 * m);
+    const ulonglong2 eB = lds22(vB + 2 * (m + 2 * r)), lB = lds22(vB + 2 * m);
+    u64 hA[2], hB[2];
+    accA = add2(accA, eA.x); hA[0] = accA; accA = sub2(accA, lA.x);
+    accB = add2(accB, eB.x); hB[0] = accB; accB = sub2(accB, lB.x);
+    accA = add2(accA, eA.y); hA[1] = accA; accA = sub2(accA, lA.y);
+    accB = add2(accB, eB.y); hB[1] = accB; accB = sub2(accB, lB.y);
+    float cf[4];
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {
+      float inv = inv_i;
+      bool ok = true;
+      if constexpr (!INTERIOR) {
+        const int gxa = gxa0 + m + t;
+        ok = m + t < w2_left && gxa >= 0 && gxa < W;
+        inv = iny * fast_rcp((float)wlen(gxa, W, r));
+      }
+      const u64 inv2 = pk(inv, inv);
+      const u64 mA = mul2(hA[t], inv2);  // (mean g, mean s)
+      const u64 mB = mul2(hB[t], inv2);  // (mean gg, mean gs)
+      const float mg = lo(mA);
+      const u64 vc = fma2(pk(-mg, -mg), mA, mB);  // (var, cov)
+      const float var = lo(vc);
+      if (ok) vmin = fminf(vmin, var);
+      const float At = hi(vc) * fast_rcp(var + eps);
+      cf[2 * t] = ok ? At : 0.f;
+      cf[2 * t + 1] = ok ? fmaf(-At, mg, hi(mA)) : 0.f;
+    }
+    *reinterpret_cast<float4*>(ra + 2 * m) = make_float4(cf[0], cf[1], cf[2], cf[3]);
+  }
+}
+
+// H2 on one run: window sums of (A, b') streamed over K output columns,
+// out = (Ah*(G - sG) + b'h)/N + sS with 128-bit loads of G and stores of out
+template <int RAD, bool INTERIOR>
+__device__ __forceinline__ void h2_run(const float* v, const float* grow, float* orow,
+                                       float iny, int gxo0, int W, float sG, float sS,
+                                       float& chk) {
+  constexpr int r = RAD;
+  u64 acc = window_sum<2 * r>(v);
+  const float inv_i = iny * (1.0f / (float)(2 * r + 1));
+#pragma unroll
+  for (int m = 0; m < K; m += 4) {
+    if (!INTERIOR && gxo0 + m >= W) break;  // W % 4 == 0: a float4 is all in or out
+    const float4 g4 = __ldg(reinterpret_cast<const float4*>(grow + m));
+    const ulonglong2 e0 = lds22(v + 2 * (m + 2 * r)), l0 = lds22(v + 2 * m);
+    const ulonglong2 e1 = lds22(v + 2 * (m + 2 + 2 * r)), l1 = lds22(v + 2 * (m + 2));
+    u64 h[4];
+    acc = add2(acc, e0.x); h[0] = acc; acc = sub2(acc, l0.x);
+    acc = add2(acc, e0.y); h[1] = acc; acc = sub2(acc, l0.y);
+    acc = add2(acc, e1.x); h[2] = acc; acc = sub2(acc, l1.x);
+    acc = add2(acc, e1.y); h[3] = acc; acc = sub2(acc, l1.y);
+    const float gv[4] = {g4.x, g4.y, g4.z, g4.w};
+    float ov[4];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      float inv = inv_i;
+      if constexpr (!INTERIOR) inv = iny * fast_rcp((float)wlen(gxo0 + m + t, W, r));
+      ov[t] = fmaf(fmaf(lo(h[t]), gv[t] - sG, hi(h[t])), inv, sS);
+      chk += ov[t] - ov[t];  // NaN iff some output is not finite
+    }
+    *reinterpret_cast<float4*>(orow + m) = make_float4(ov[0], ov[1], ov[2], ov[3]);
+  }
+}
+
 template <int RAD>
-__global__ void __launch_bounds__(Geo<RAD>::nt, Geo<RAD>::min_blocks)
+__global__ void __launch_bounds__(NT, Geo<RAD>::min_blocks)
     k_highres_fused(const __grid_constant__ CUtensorMap tmG,
                     const __grid_constant__ CUtensorMap tmS, Args a) {
   using GG = Geo<RAD>;
   constexpr int r = RAD;
   constexpr int ringN = GG::ringN;
+  constexpr int PR = GG::PR;
   extern __shared__ __align__(128) float4 smem4[];
-  float* stg = reinterpret_cast<float*>(smem4);  // [2 fields][NB][R][BX] (TMA boxes)
-  float* vs = stg + 2 * R * GG::SWF;             // [4 fields][R][P1]
-  float* ring = vs + 4 * R * GG::P1;             // [2 fields][ringN][Pr]
-  float* vs2 = ring + 2 * ringN * GG::Pr;        // [2 fields][R][P2]
-  uint64_t* bar = reinterpret_cast<uint64_t*>(vs2 + 2 * R * GG::P2);
+  float* stg = reinterpret_cast<float*>(smem4);  // [2 stages][2 fields][R][NT] (TMA)
+  float* vsA = stg + 2 * 2 * R * NT;             // [R][PV] (s_g, s_s) pairs
+  float* vsB = vsA + R * GG::PV;                 // [R][PV] (s_gg, s_gs) pairs
+  float* ring = vsB + R * GG::PV;                // [ringN][PR] (A, b') pairs
+  float* vs2 = ring + ringN * PR;                // [R][P2] (A, b') vertical sums
+  uint64_t* bar = reinterpret_cast<uint64_t*>(vs2 + R * GG::P2);  // [2 stages]
   const int H = (int)a.H, W = (int)a.W;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 
-  // work item: plane fastest (the C planes sharing a guide run together)
-  int64_t item = blockIdx.x;
-  const int c = (int)(item % a.C);
-  item /= a.C;
-  const int strip = (int)(item % a.strips);
-  item /= a.strips;
-  const int seg = (int)(item % a.segs);
-  const int64_t b = item / a.segs;
-  const int x0 = strip * TX;
-  const int y0 = seg * a.TY;
-  if (y0 >= H) return;
-  const int yend = min(y0 + a.TY, H);
+  // Work: the rows of all (image, strip) columns of channel c, laid end to
+  // end (u = (b*strips + strip)*H + y), cut into equal chunks; the C
+  // channels of a chunk are consecutive CTAs so they share the guide in L2.
+  // A chunk may cover the tail of one column and the head of the next: each
+  // such piece is streamed separately (its own 4r warm-up rows).
+  const int c = (int)(blockIdx.x % a.C);
+  const int64_t chunk_id = blockIdx.x / a.C;
+  const int64_t u_lo = chunk_id * a.chunk;
+  const int64_t u_hi = min(u_lo + a.chunk, a.U);
+  const int tx = a.tx;
+  const int W2 = tx + 2 * r;  // coefficient columns of a strip
   const int64_t plane = (int64_t)H * W;
-  const int64_t gplane = a.Cg == a.C ? b * a.C + c : b * a.Cg;
-  const float* __restrict__ G = a.guide + gplane * plane;
-  const float* __restrict__ S = a.src + (b * a.C + c) * plane;
-  float* __restrict__ O = a.out + (b * a.C + c) * plane;
-  const float sG = __ldg(G + (int64_t)y0 * W + x0);
-  const float sS = __ldg(S + (int64_t)y0 * W + x0);
   const float eps = a.eps;
-  constexpr float inv_full = 1.0f / (float)(2 * r + 1);
-
-  const int ya0 = y0 - r;                 // image row of coefficient row 0
-  const int nrows = (yend - y0) + 2 * r;  // coefficient rows of this item
-  const int nb = (nrows + R - 1) / R;     // batches
-  const int first_add = y0 - 2 * r;       // first input row ever added
-  const int xs0 = x0 - GG::PADL;          // image column of vs / stg column 0
-
-  if (tid == 0) tma::mbar_init(bar, 1);
-  __syncthreads();
-  uint32_t phase = 0;
-  // TMA of the R entering input rows of batch k (image rows ya0 + kR + r ...)
-  auto prefetch = [&](int k) {
-    if (tid == 0) {
-      tma::fence_proxy_async();
-      tma::mbar_arrive_expect_tx(bar, GG::tx_bytes);
-      const int e0 = ya0 + k * R + r;
-#pragma unroll
-      for (int box = 0; box < GG::NB; ++box) {
-        tma::load_3d(stg + (0 * GG::NB + box) * R * GG::BX, &tmG, xs0 + box * GG::BX, e0,
-                     (int)gplane, bar);
-        tma::load_3d(stg + (1 * GG::NB + box) * R * GG::BX, &tmS, xs0 + box * GG::BX, e0,
-                     (int)(b * a.C + c), bar);
-      }
-    }
-  };
-  prefetch(0);
-
-  // ---- column-phase state: thread owns vs column `tid` (V1) and
-  //      coefficient column `tid` (V2)
-  const bool v1 = tid < GG::VW;
-  const int gx = xs0 + tid;
-  const bool col_ok = v1 && gx >= 0 && gx < W;
-  const int sbox = tid / GG::BX;
-  const float* st_g = stg + sbox * R * GG::BX + (tid - sbox * GG::BX);
-  const float* st_s = st_g + GG::NB * R * GG::BX;
-  float sI = 0.f, sII = 0.f, sP = 0.f, sIP = 0.f;
-  if (col_ok) {
-    for (int y = max(first_add, 0); y < y0; ++y) {
-      const float gv = __ldg(G + (int64_t)y * W + gx) - sG;
-      const float pv = __ldg(S + (int64_t)y * W + gx) - sS;
-      sI += gv;
-      sII = fmaf(gv, gv, sII);
-      sP += pv;
-      sIP = fmaf(gv, pv, sIP);
-    }
+  float vmin = 1.f, chk = 0.f;
+  uint32_t phases = 0;  // bit s: parity of stage s's next completion
+  if (tid == 0) {
+    tma::mbar_init(bar, 1);
+    tma::mbar_init(bar + 1, 1);
   }
-  const bool v2 = tid < GG::W2;
-  float cA = 0.f, cB = 0.f;  // level-2 sums at the end of the last finished batch
-  float pA[R], pB[R];        // running sums minus the leaving rows (pre-subtracted)
-#pragma unroll
-  for (int j = 0; j < R; ++j) pA[j] = pB[j] = 0.f;
-  int s_cur = 0;                                      // ring slot of coefficient row kR
-  int s_prev = ringN - (R % ringN);                   // ... of row (k-1)R
-  if (s_prev == ringN) s_prev = 0;
-  int s_old = ringN - ((2 * r + 1) % ringN);          // ... of row kR - 2r - 1
-  if (s_old == ringN) s_old = 0;
-  bool bad = false, degen = false;
+  __syncthreads();
 
-  for (int k = 0; k <= nb; ++k) {
-    const int base = k * R;
-    if (k < nb) {
-      tma::mbar_wait(bar, phase);  // batch k's entering rows landed in stg
-      phase ^= 1u;
+  for (int64_t u = u_lo; u < u_hi;) {
+    const int64_t col = u / H;
+    const int y0 = (int)(u - col * H);
+    const int yend = (int)min((int64_t)H, y0 + (u_hi - u));
+    u += yend - y0;
+    const int64_t b = col / a.strips;
+    const int strip = (int)(col - b * a.strips);
+    const int x0 = strip * tx;
+    const int64_t gplane = a.Cg == a.C ? b * a.C + c : b * a.Cg;
+    const int64_t splane = b * a.C + c;
+    const float* __restrict__ G = a.guide + gplane * plane;
+    const float* __restrict__ S = a.src + splane * plane;
+    float* __restrict__ O = a.out + splane * plane;
+    const float sG = __ldg(G + (int64_t)y0 * W + x0);
+    const float sS = __ldg(S + (int64_t)y0 * W + x0);
+    const u64 SH = pk(sG, sS);
+
+    const int ya0 = y0 - r;                 // image row of coefficient row 0
+    const int nrows = (yend - y0) + 2 * r;  // coefficient rows of this piece
+    const int nb = (nrows + R - 1) / R;     // batches
+    const int first_add = y0 - 2 * r;       // first input row ever added
+    const int xs0 = x0 - GG::PADL;          // image column of vs / stg column 0
+
+    // TMA of the R entering input rows of batch k (image rows ya0 + kR + r ...)
+    // into stage k & 1, two batches ahead of their use
+    auto prefetch = [&](int k) {
+      if (tid == 0) {
+        const int st = k & 1;
+        tma::fence_proxy_async();
+        tma::mbar_arrive_expect_tx(bar + st, GG::tx_bytes);
+        const int e0 = ya0 + k * R + r;
+        float* dst = stg + st * 2 * R * NT;
+        tma::load_3d(dst, &tmG, xs0, e0, (int)gplane, bar + st);
+        tma::load_3d(dst + R * NT, &tmS, xs0, e0, (int)splane, bar + st);
+      }
+    };
+    prefetch(0);
+    if (nb > 1) prefetch(1);
+
+    // ---- column-phase state: V1 on vs column tid, V2 on coefficient column tid
+    const int gx = xs0 + tid;
+    const bool col_ok = gx >= 0 && gx < W;
+    const char* gcb = reinterpret_cast<const char*>(G + gx);  // V1 column pointers
+    const char* scb = reinterpret_cast<const char*>(S + gx);
+    u64 SA = 0, SB = 0;  // (s_g, s_s), (s_gg, s_gs) of the current window
+    if (col_ok) {
+      for (int y = max(first_add, 0); y < y0; ++y) {
+        const u64 e = sub2(pk(__ldg(G + (int64_t)y * W + gx), __ldg(S + (int64_t)y * W + gx)), SH);
+        SA = add2(SA, e);
+        SB = fma2(pk(lo(e), lo(e)), e, SB);
+      }
     }
+    const bool v2 = tid < W2;
+    const float* rr = ring + 2 * tid;  // V2: ring column tid
+    u64 cS = 0;                        // level-2 sums at the end of the last batch
+    u64 pS[R];                         // running sums minus the leaving rows
+#pragma unroll
+    for (int j = 0; j < R; ++j) pS[j] = 0;
+    int s_cur = 0;                                // ring slot of coefficient row kR
+    int s_prev = ringN - (R % ringN);             // ... of row (k-1)R
+    if (s_prev == ringN) s_prev = 0;
+    int s_old = ringN - ((2 * r + 1) % ringN);    // ... of row kR - 2r - 1
+    if (s_old == ringN) s_old = 0;
+    const int jr = lane & 7;                      // run phase: row of the batch
+    const int q = warp * 4 + (lane >> 3);         // run phase: run
 
-    // ================= column phase X(k) =================================
-    if (k < nb && v1) {
-      float* o = vs + tid;
-      const int l0 = ya0 + base - r - 1;  // leaving image row of row 0
-      const bool rows_fast = base + R <= nrows && l0 >= max(first_add, 0) &&
-                             ya0 + base + R - 1 + r < H;
-      if (rows_fast) {
-        if (col_ok) {
-          float lg[R], ls[R];
-          const float* gl = G + (int64_t)l0 * W + gx;
-          const float* sl = S + (int64_t)l0 * W + gx;
+    for (int k = 0; k <= nb; ++k) {
+      const int base = k * R;
+      // ================= column phase X(k) ===============================
+      if (k < nb) {  // ---- V1(k)
+        const int st = k & 1;
+        float* oA = vsA + 2 * tid;
+        float* oB = vsB + 2 * tid;
+        const float* eg = stg + st * 2 * R * NT + tid;
+        const float* es = eg + R * NT;
+        const int l0 = ya0 + base - r - 1;  // leaving image row of row 0
+        const bool rows_fast = base + R <= nrows && l0 >= max(first_add, 0) &&
+                               ya0 + base + R - 1 + r < H;
+        const bool fastc = rows_fast && col_ok;
+        u64 lq[R];
+        if (fastc) {  // the leaving rows (L2) load while the entering rows land
+          // per-thread column pointers + CTA-uniform byte offsets of the rows
+          const int64_t rowb = (int64_t)l0 * W * 4, strb = (int64_t)W * 4;
 #pragma unroll
           for (int j = 0; j < R; ++j) {
-            lg[j] = __ldg(gl + (int64_t)j * W);
-            ls[j] = __ldg(sl + (int64_t)j * W);
-          }
-#pragma unroll
-          for (int j = 0; j < R; ++j) {
-            const float eg = st_g[j * GG::BX] - sG, es = st_s[j * GG::BX] - sS;
-            const float qg = lg[j] - sG, qs = ls[j] - sS;
-            sI += eg - qg;
-            sII = fmaf(eg, eg, sII);
-            sII = fmaf(-qg, qg, sII);
-            sP += es - qs;
-            sIP = fmaf(eg, es, sIP);
-            sIP = fmaf(-qg, qs, sIP);
-            o[(0 * R + j) * GG::P1] = sI;
-            o[(1 * R + j) * GG::P1] = sII;
-            o[(2 * R + j) * GG::P1] = sP;
-            o[(3 * R + j) * GG::P1] = sIP;
-          }
-        } else {
-#pragma unroll
-          for (int j = 0; j < R; ++j) {
-            o[(0 * R + j) * GG::P1] = 0.f;
-            o[(1 * R + j) * GG::P1] = 0.f;
-            o[(2 * R + j) * GG::P1] = 0.f;
-            o[(3 * R + j) * GG::P1] = 0.f;
+            const int64_t o = rowb + j * strb;
+            lq[j] = pk(__ldg(reinterpret_cast<const float*>(gcb + o)),
+                       __ldg(reinterpret_cast<const float*>(scb + o)));
           }
         }
-      } else {  // top / bottom batches: per-row predicates
+        tma::mbar_wait(bar + st, (phases >> st) & 1u);  // batch k's entering rows landed
+        phases ^= 1u << st;
+        if (fastc) {
+          u64 ev[R];
 #pragma unroll
-        for (int j = 0; j < R; ++j) {
-          const int i = base + j;
-          const int e = ya0 + i + r, l = e - 2 * r - 1;
-          const bool in_i = i < nrows;
-          const bool e_ok = col_ok && in_i && e >= 0 && e < H;
-          const bool l_ok = col_ok && in_i && l >= first_add && l >= 0 && l < H;
-          float eg = 0.f, es = 0.f, qg = 0.f, qs = 0.f;
-          if (e_ok) {
-            eg = st_g[j * GG::BX] - sG;
-            es = st_s[j * GG::BX] - sS;
+          for (int j = 0; j < R; ++j) ev[j] = pk(eg[j * NT], es[j * NT]);
+#pragma unroll
+          for (int j = 0; j < R; ++j) {
+            const u64 e = sub2(ev[j], SH);
+            const u64 qv = sub2(lq[j], SH);
+            SA = add2(SA, sub2(e, qv));
+            SB = fma2(pk(lo(e), lo(e)), e, SB);
+            SB = fma2(pk(-lo(qv), -lo(qv)), qv, SB);
+            sts2(oA + j * GG::PV, SA);
+            sts2(oB + j * GG::PV, SB);
           }
-          if (l_ok) {
-            qg = __ldg(G + (int64_t)l * W + gx) - sG;
-            qs = __ldg(S + (int64_t)l * W + gx) - sS;
+        } else if (!col_ok) {  // column outside the image: its sums stay 0
+#pragma unroll
+          for (int j = 0; j < R; ++j) {
+            sts2(oA + j * GG::PV, 0);
+            sts2(oB + j * GG::PV, 0);
           }
-          sI += eg - qg;
-          sII = fmaf(eg, eg, sII);
-          sII = fmaf(-qg, qg, sII);
-          sP += es - qs;
-          sIP = fmaf(eg, es, sIP);
-          sIP = fmaf(-qg, qs, sIP);
-          o[(0 * R + j) * GG::P1] = sI;
-          o[(1 * R + j) * GG::P1] = sII;
-          o[(2 * R + j) * GG::P1] = sP;
-          o[(3 * R + j) * GG::P1] = sIP;
+        } else {  // top / bottom batches: per-row predicates
+#pragma unroll
+          for (int j = 0; j < R; ++j) {
+            const int i = base + j;
+            const int e_row = ya0 + i + r, l = e_row - 2 * r - 1;
+            const bool in_i = i < nrows;
+            // a skipped row enters / leaves as the shift itself: contributes 0
+            u64 ev = SH, lv = SH;
+            if (in_i && e_row >= 0 && e_row < H) ev = pk(eg[j * NT], es[j * NT]);
+            if (in_i && l >= first_add && l >= 0 && l < H)
+              lv = pk(__ldg(G + (int64_t)l * W + gx), __ldg(S + (int64_t)l * W + gx));
+            const u64 e = sub2(ev, SH), qv = sub2(lv, SH);
+            SA = add2(SA, sub2(e, qv));
+            SB = fma2(pk(lo(e), lo(e)), e, SB);
+            SB = fma2(pk(-lo(qv), -lo(qv)), qv, SB);
+            sts2(oA + j * GG::PV, SA);
+            sts2(oB + j * GG::PV, SB);
+          }
         }
       }
-    }
-    if (v2) {
-      const float* rA = ring + tid;
-      const float* rB = ring + ringN * GG::Pr + tid;
-      if (k >= 1) {  // V2(k-1): add batch k-1's coefficient rows -> vs2
-        const int bb = base - R;
-        float nA = 0.f, nB = 0.f;
+      if (v2) {
+        // ring rows of slots s..s+R-1 (mod ringN): rows j < w at p + j*PR, the
+        // wrapped rows at p + (j - ringN)*PR
+        constexpr int dj = 2 * r + 1;        // row distance of the leaving row
+        constexpr int nl = dj < R ? dj : R;  // rows of a batch whose leaving row is older
+        if (k >= 1) {  // ---- V2(k-1): add batch k-1's coefficient rows -> vs2
+          const int nvalid = nrows - (base - R);
+          const float* fa = rr + s_prev * PR;
+          const float* fw = fa - ringN * PR;
+          const int wF = ringN - s_prev;
+          u64 x[R];
+          if (wF >= R && nvalid >= R) {
 #pragma unroll
-        for (int j = 0; j < R; ++j) {
-          if (bb + j < nrows) {
-            int s = s_prev + j;
-            if (s >= ringN) s -= ringN;
-            nA += rA[s * GG::Pr];
-            nB += rB[s * GG::Pr];
-            if (j >= 2 * r + 1) {  // leaving row inside this batch (small r)
-              int so = s - (2 * r + 1);
-              if (so < 0) so += ringN;
-              nA -= rA[so * GG::Pr];
-              nB -= rB[so * GG::Pr];
+            for (int j = 0; j < R; ++j) x[j] = lds2(fa + j * PR);
+          } else {
+#pragma unroll
+            for (int j = 0; j < R; ++j) {
+              x[j] = 0;
+              if (j < nvalid) x[j] = lds2((j < wF ? fa : fw) + j * PR);
             }
           }
-          vs2[j * GG::P2 + tid] = pA[j] + nA;
-          vs2[(R + j) * GG::P2 + tid] = pB[j] + nB;
-        }
-        cA = pA[R - 1] + nA;
-        cB = pB[R - 1] + nB;
-      }
-      if (k < nb) {  // pre-subtract batch k's leaving rows before H1(k) overwrites them
-        float qa = cA, qb = cB;
+          u64 n = 0;
 #pragma unroll
-        for (int j = 0; j < R; ++j) {
-          if (j < 2 * r + 1 && base + j - 2 * r - 1 >= 0) {
-            int so = s_old + j;
-            if (so >= ringN) so -= ringN;
-            qa -= rA[so * GG::Pr];
-            qb -= rB[so * GG::Pr];
+          for (int j = 0; j < R; ++j) {
+            n = add2(n, x[j]);
+            if (j >= dj) n = sub2(n, x[j - dj]);  // leaving row inside this batch (small r)
+            sts2(vs2 + j * GG::P2 + 2 * tid, add2(pS[j], n));
           }
-          pA[j] = qa;
-          pB[j] = qb;
+          cS = add2(pS[R - 1], n);
+        }
+        if (k < nb) {  // ---- leaving rows of batch k, before H1(k) overwrites them
+          const float* oa = rr + s_old * PR;
+          const float* ow = oa - ringN * PR;
+          const int wO = ringN - s_old;
+          u64 y[nl];
+          if (wO >= nl && base >= dj) {
+#pragma unroll
+            for (int j = 0; j < nl; ++j) y[j] = lds2(oa + j * PR);
+          } else {
+            const int jmin = dj - base;  // rows j >= jmin leave a real row
+#pragma unroll
+            for (int j = 0; j < nl; ++j) {
+              y[j] = 0;
+              if (j >= jmin) y[j] = lds2((j < wO ? oa : ow) + j * PR);
+            }
+          }
+          u64 qs = cS;
+#pragma unroll
+          for (int j = 0; j < R; ++j) {
+            if (j < nl) qs = sub2(qs, y[j]);
+            pS[j] = qs;
+          }
         }
       }
-    }
-    __syncthreads();  // vs, vs2 complete; stg and the leaving ring rows consumed
+      cta_sync();  // vs, vs2 complete; stg and the leaving ring rows consumed
 
-    // ================= run phase Y(k) ====================================
-    if (k + 1 < nb) prefetch(k + 1);
-    const int j = lane & 7;
-    if (warp < GG::h1w) {
-      // ---- H1(k): coefficient row base+j, columns [qK, qK+K) ---------------
-      const int q = warp * 4 + (lane >> 3);
-      const int i = base + j;
-      if (k < nb && q < GG::nq1 && i < nrows) {
-        const int ya = ya0 + i;
-        int s = s_cur + j;
-        if (s >= ringN) s -= ringN;
-        float* ra = ring + s * GG::Pr + q * K;
-        float* rb = ring + (ringN + s) * GG::Pr + q * K;
-        if (ya < 0 || ya >= H) {
+      // ================= run phase Y(k) ==================================
+      if (k + 2 < nb) prefetch(k + 2);  // into the stage X(k) just consumed
+      {  // ---- H1(k): coefficient row base+jr, columns [qK, qK+K)
+        const int i = base + jr;
+        if (k < nb && q * K < W2 && i < nrows) {
+          const int ya = ya0 + i;
+          int s = s_cur + jr;
+          if (s >= ringN) s -= ringN;
+          float* ra = ring + s * PR + 2 * q * K;
+          if (ya < 0 || ya >= H) {
 #pragma unroll
-          for (int m = 0; m < K / 4; ++m) {
-            sts4(ra + 4 * m, 0.f, 0.f, 0.f, 0.f);
-            sts4(rb + 4 * m, 0.f, 0.f, 0.f, 0.f);
-          }
-        } else {
-          const float* v = vs + j * GG::P1 + q * K + GG::off;  // field f at + f*R*P1
-          float acc[4];
-#pragma unroll
-          for (int f = 0; f < 4; ++f)
-            acc[f] = window_sum<2 * r, GG::off != 0>(v + f * R * GG::P1);
-          const float iny = fast_rcp((float)wlen(ya, H, r));
-          const int gxa0 = x0 - r + q * K;  // image column of the run's first coefficient
-          const bool interior = gxa0 >= r && gxa0 + K - 1 + r <= W - 1 && q * K + K <= GG::W2;
-          const float inv_i = iny * inv_full;
-#pragma unroll
-          for (int m = 0; m < K / 4; ++m) {
-            float h[4][4];
-#pragma unroll
-            for (int f = 0; f < 4; ++f) {
-              const float* vf = v + f * R * GG::P1 + 4 * m;
-              const float4 e = lds4(vf + 2 * r);            // vs column q*K + PADL + 4m
-              const float4 l = lds4u<GG::off == 0>(vf);
-              acc[f] += e.x; h[f][0] = acc[f]; acc[f] -= l.x;
-              acc[f] += e.y; h[f][1] = acc[f]; acc[f] -= l.y;
-              acc[f] += e.z; h[f][2] = acc[f]; acc[f] -= l.z;
-              acc[f] += e.w; h[f][3] = acc[f]; acc[f] -= l.w;
-            }
-            float A[4], B[4];
-#pragma unroll
-            for (int t = 0; t < 4; ++t) {
-              const int gxa = gxa0 + 4 * m + t;
-              const bool ok = interior || (q * K + 4 * m + t < GG::W2 && gxa >= 0 && gxa < W);
-              const float inv = interior ? inv_i : iny * fast_rcp((float)wlen(gxa, W, r));
-              const float mg = h[0][t] * inv, ms = h[2][t] * inv;
-              const float var = fmaf(h[1][t], inv, -mg * mg);
-              const float cov = fmaf(h[3][t], inv, -mg * ms);
-              if (ok && eps == 0.f && !(var > 0.f)) degen = true;
-              const float At = cov * fast_rcp(var + eps);
-              A[t] = ok ? At : 0.f;
-              B[t] = ok ? fmaf(-At, mg + sG, ms + sS) : 0.f;
-            }
-            sts4(ra + 4 * m, A[0], A[1], A[2], A[3]);
-            sts4(rb + 4 * m, B[0], B[1], B[2], B[3]);
+            for (int m = 0; m < K; m += 2)
+              *reinterpret_cast<float4*>(ra + 2 * m) = make_float4(0.f, 0.f, 0.f, 0.f);
+          } else {
+            const float* vA = vsA + jr * GG::PV + 2 * (q * K + GG::off);
+            const float* vB = vA + R * GG::PV;
+            const float iny = fast_rcp((float)wlen(ya, H, r));
+            const int gxa0 = x0 - r + q * K;  // image column of the run's first coefficient
+            if (gxa0 >= r && gxa0 + K - 1 + r <= W - 1 && q * K + K <= W2)
+              h1_run<RAD, true>(vA, vB, ra, iny, gxa0, W2 - q * K, W, eps, vmin);
+            else
+              h1_run<RAD, false>(vA, vB, ra, iny, gxa0, W2 - q * K, W, eps, vmin);
           }
         }
       }
-    } else if (warp < GG::h1w + GG::h2w) {
-      // ---- H2(k-1): output row of coefficient row base-R+j, columns [qK, qK+K)
-      const int q = (warp - GG::h1w) * 4 + (lane >> 3);
-      const int yo = y0 - 2 * r + base - R + j;
-      const int gxo0 = x0 + q * K;
-      if (k >= 1 && yo >= y0 && yo < yend && gxo0 < W) {
-        const float* vA = vs2 + j * GG::P2 + q * K;
-        const float* vB = vs2 + (R + j) * GG::P2 + q * K;
-        float accA = window_sum<2 * r>(vA), accB = window_sum<2 * r>(vB);
-        const float iny = fast_rcp((float)wlen(yo, H, r));
-        const bool interior = gxo0 >= r && gxo0 + K - 1 + r <= W - 1;
-        const float inv_i = iny * inv_full;
-        const float* grow = G + (int64_t)yo * W + gxo0;
-        float* orow = O + (int64_t)yo * W + gxo0;
-#pragma unroll
-        for (int m = 0; m < K / 4; ++m) {
-          if (gxo0 + 4 * m >= W) break;  // W % 4 == 0: a float4 is all in or all out
-          const float4 g4 = __ldg(reinterpret_cast<const float4*>(grow + 4 * m));
-          const float4 eA = lds4u<GG::A4>(vA + 4 * m + 2 * r), lA = lds4(vA + 4 * m);
-          const float4 eB = lds4u<GG::A4>(vB + 4 * m + 2 * r), lB = lds4(vB + 4 * m);
-          float hA[4], hB[4];
-          accA += eA.x; hA[0] = accA; accA -= lA.x;
-          accA += eA.y; hA[1] = accA; accA -= lA.y;
-          accA += eA.z; hA[2] = accA; accA -= lA.z;
-          accA += eA.w; hA[3] = accA; accA -= lA.w;
-          accB += eB.x; hB[0] = accB; accB -= lB.x;
-          accB += eB.y; hB[1] = accB; accB -= lB.y;
-          accB += eB.z; hB[2] = accB; accB -= lB.z;
-          accB += eB.w; hB[3] = accB; accB -= lB.w;
-          const float gv[4] = {g4.x, g4.y, g4.z, g4.w};
-          float ov[4];
-#pragma unroll
-          for (int t = 0; t < 4; ++t) {
-            const float inv =
-                interior ? inv_i : iny * fast_rcp((float)wlen(gxo0 + 4 * m + t, W, r));
-            ov[t] = fmaf(hA[t], gv[t], hB[t]) * inv;
-            if (!isfinite(ov[t])) bad = true;
-          }
-          *reinterpret_cast<float4*>(orow + 4 * m) = make_float4(ov[0], ov[1], ov[2], ov[3]);
+      {  // ---- H2(k-1): output row of coefficient row base-R+jr, columns [qK, qK+K)
+        const int yo = y0 - 2 * r + base - R + jr;
+        const int gxo0 = x0 + q * K;
+        if (k >= 1 && q * K < tx && yo >= y0 && yo < yend && gxo0 < W) {
+          const float* v = vs2 + jr * GG::P2 + 2 * q * K;
+          const float iny = fast_rcp((float)wlen(yo, H, r));
+          const float* grow = G + (int64_t)yo * W + gxo0;
+          float* orow = O + (int64_t)yo * W + gxo0;
+          if (gxo0 >= r && gxo0 + K - 1 + r <= W - 1)
+            h2_run<RAD, true>(v, grow, orow, iny, gxo0, W, sG, sS, chk);
+          else
+            h2_run<RAD, false>(v, grow, orow, iny, gxo0, W, sG, sS, chk);
         }
       }
+      s_prev = s_cur;
+      s_cur += R;
+      if (s_cur >= ringN) s_cur -= ringN;
+      s_old += R;
+      if (s_old >= ringN) s_old -= ringN;
+      cta_sync();  // ring rows of batch k and the outputs of batch k-1 done
     }
-    s_prev = s_cur;
-    s_cur += R;
-    if (s_cur >= ringN) s_cur -= ringN;
-    s_old += R;
-    if (s_old >= ringN) s_old -= ringN;
-    __syncthreads();  // ring rows of batch k and the outputs of batch k-1 done
   }
   // Non-finite inputs are not tested per element here: they always poison
   // the output at their own pixel, so the host (gf_check_finite) classifies
   // an OUTPUT flag as an input error when the inputs are non-finite.
-  if (degen) flag(a.status, GF_STATUS_DEGENERATE);
-  if (bad) flag(a.status, GF_STATUS_NONFINITE_OUTPUT);
+  if (eps == 0.f && !(vmin > 0.f)) flag(a.status, GF_STATUS_DEGENERATE);
+  if (chk != 0.f) flag(a.status, GF_STATUS_NONFINITE_OUTPUT);
 }
 
 struct Launch {
   const void* fn;
   int nt;
   size_t smem;
-  int box_w;  // TMA box width of the staged rows
+  int txm;  // widest strip
 };
 
 template <int RAD>
 Launch launch_info() {
-  return {(const void*)k_highres_fused<RAD>, Geo<RAD>::nt, Geo<RAD>::smem_bytes, Geo<RAD>::BX};
+  return {(const void*)k_highres_fused<RAD>, NT, Geo<RAD>::smem_bytes, Geo<RAD>::TXM};
 }
 
 Launch pick(int r) {
@@ -545,31 +571,25 @@ void fused_highres_fwd(const float* guide, const float* src, float* out, int64_t
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, L.fn, L.nt, L.smem);
     per_sm_cache[r] = per_sm < 1 ? 1 : per_sm;
   }
-  const int64_t strips = (W + hrf::TX - 1) / hrf::TX;
-  const int64_t planes = B * C;
+  // strips of equal width (multiple of K, at most the kernel's bound)
+  const int64_t nstrip = (W + L.txm - 1) / L.txm;
+  const int tx = (int)(((W + nstrip - 1) / nstrip + hrf::K - 1) / hrf::K * hrf::K);
+  const int64_t strips = (W + tx - 1) / tx;
   const int64_t slots = (int64_t)sms * per_sm_cache[r];
-  // choose the row segmentation: minimise waves x (rows per item incl. the
-  // 4r warm-up rows), with segments of at most 1024 rows (bounded rounding)
-  int64_t best_segs = 1;
-  double best_cost = 1e300;
-  const int64_t max_segs = H / (2 * r + 1) > 0 ? H / (2 * r + 1) : 1;
-  for (int64_t sg = (H + 1023) / 1024; sg <= max_segs && sg <= 4096; ++sg) {
-    const int64_t ty = (H + sg - 1) / sg;
-    const int64_t items = planes * strips * ((H + ty - 1) / ty);
-    const int64_t waves = (items + slots - 1) / slots;
-    const double cost = (double)waves * (double)(ty + 4 * r);
-    if (cost < best_cost * 0.999) {
-      best_cost = cost;
-      best_segs = sg;
-    }
-  }
-  const int64_t TY = (H + best_segs - 1) / best_segs;
-  const int64_t segs = (H + TY - 1) / TY;
-  hrf::Args a{guide, src, out, C, Cg, H, W, (int)TY, (int)strips, (int)segs, eps, status};
-  const int64_t grid = planes * strips * segs;
+  // balanced chunks of the rows of all (image, strip) columns: one wave of
+  // C x nch CTAs, more waves only to keep a chunk <= 1024 rows (bounded
+  // running-sum rounding); at least 8 rows per chunk
+  const int64_t U = B * strips * H;
+  const int64_t per_wave = slots / C > 0 ? slots / C : 1;
+  const int64_t waves = (U + per_wave * 1024 - 1) / (per_wave * 1024);
+  int64_t chunk = (U + per_wave * waves - 1) / (per_wave * waves);
+  if (chunk < 8) chunk = U < 8 ? U : 8;
+  const int64_t nch = (U + chunk - 1) / chunk;
+  hrf::Args a{guide, src, out, C, Cg, H, W, tx, (int)strips, U, chunk, eps, status};
+  const int64_t grid = nch * C;
   CUtensorMap tmG, tmS;
-  if (!tma::make_plane_map(&tmG, guide, W, H, B * Cg, L.box_w, hrf::R) ||
-      !tma::make_plane_map(&tmS, src, W, H, B * C, L.box_w, hrf::R)) {
+  if (!tma::make_plane_map(&tmG, guide, W, H, B * Cg, hrf::NT, hrf::R) ||
+      !tma::make_plane_map(&tmS, src, W, H, B * C, hrf::NT, hrf::R)) {
     // surfaces as a launch error through the C ABI's cudaGetLastError check
     cudaLaunchKernel(L.fn, dim3(0), dim3(0), nullptr, 0, s);
     return;
