@@ -278,14 +278,18 @@ class OursStep:
         p = gfb.GuidedFilterParams(c["r"], c["eps"])
 
         def one():
-            dev = [t.to(self.device, non_blocking=True) for t in host_in]
+            # forward-only workloads: the host-image entry points (reference call
+            # shape), which overlap copy-in / kernel / copy-out image by image
             if self.kind == "highres_fwd":
-                out, _ = gfb.forward_highres(dev[0], dev[1], p, check=False)
-                res = out
-            elif self.kind == "joint_fwd":
-                out, _ = gfb.forward_joint(dev[0], dev[2], dev[1], p, check=False)
-                res = out
-            elif self.kind == "joint_fwd_bwd":
+                gfb.forward_highres_host(host_in[0], host_in[1], p, out=host_out,
+                                         device=self.device, check=False)
+                return
+            if self.kind == "joint_fwd":
+                gfb.forward_joint_host(host_in[0], host_in[2], host_in[1], p, out=host_out,
+                                       device=self.device, check=False)
+                return
+            dev = [t.to(self.device, non_blocking=True) for t in host_in]
+            if self.kind == "joint_fwd_bwd":
                 out, tape = gfb.forward_joint(dev[0], dev[2], dev[1], p, check=False)
                 gr = gfb.backward(tape, out, check=False)  # d_out = out (<out,out>/2 probe)
                 res = gr.d_guide_hi

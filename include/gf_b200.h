@@ -152,6 +152,29 @@ int gn_backward(int dtype, const void* x, const void* dy, void* dx, void* dparam
                 int64_t hidden, int64_t H, int64_t W, void* workspace, size_t workspace_bytes,
                 uint32_t* status, void* stream);
 
+/* ---- host-buffer entries: the reference's call shape (host images in, host
+ * image out; gf/guided.py:152 guided_filter, :198 guided_filter_full) ----
+ * Synchronous: the calls return when `out` (HOST memory) is written.  The
+ * batch streams through the device one image at a time (copy-in of image
+ * b+1, kernel of image b and copy-out of image b-1 overlap on three streams),
+ * so page-locked host buffers make the call cost ~max(H2D, D2H) of the whole
+ * batch.  `workspace` is DEVICE memory of *_host_workspace_bytes(); `status`
+ * is a HOST uint32 receiving the OR of the GF_STATUS_* bits of all images. */
+size_t gf_highres_host_workspace_bytes(int dtype, int64_t Cg, int64_t C, int64_t H, int64_t W,
+                                       int radius);
+
+int gf_highres_fwd_host(int dtype, const void* guide, const void* src, void* out, int64_t B,
+                        int64_t Cg, int64_t C, int64_t H, int64_t W, int radius, double eps,
+                        void* workspace, size_t workspace_bytes, uint32_t* status);
+
+size_t gf_joint_host_workspace_bytes(int dtype, int64_t C, int64_t h, int64_t w, int64_t H,
+                                     int64_t W, int radius);
+
+int gf_joint_fwd_host(int dtype, const void* lr_x, const void* lr_y, const void* hr_x, void* out,
+                      int64_t B, int64_t C, int64_t h, int64_t w, int64_t H, int64_t W,
+                      int radius, double eps, void* workspace, size_t workspace_bytes,
+                      uint32_t* status);
+
 /* ---- mse_loss: gf/training.py:93-101 (batch-mean variant of config 2) ----
  * loss = mean over the batch of per-image mean((out - target)^2); d_out =
  * 2 (out - target) / (C*H*W) / B.  loss is one device double. */

@@ -21,6 +21,7 @@ from .guidance import GuidanceNet
 from .filters import bilinear_resize, bilinear_resize_adjoint, mean_filter, mean_filter_adjoint
 from .training import affine_target, mse_loss, train_step
 from .nn import FastGuidedFilter, FullResGuidedFilter
+from .host import forward_highres_host, forward_joint_host
 
 __version__ = "0.1.0"
 
@@ -29,5 +30,5 @@ __all__ = [
     "VARIANT_HIGHRES", "VARIANT_JOINT", "backward", "forward_highres", "forward_joint",
     "GuidanceNet", "bilinear_resize", "bilinear_resize_adjoint", "mean_filter",
     "mean_filter_adjoint", "affine_target", "mse_loss", "train_step", "FastGuidedFilter",
-    "FullResGuidedFilter",
+    "FullResGuidedFilter", "forward_highres_host", "forward_joint_host",
 ]

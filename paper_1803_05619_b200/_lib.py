@@ -45,6 +45,12 @@ SIGNATURES = {
                          _sz, _p, _p]),
     "gf_mse_loss": (_i, [_i, _p, _p, _p, _p, _i64, _i64, _i64, _i64, _p, _sz, _p]),
     "gf_mse_workspace_bytes": (_sz, [_i64, _i64, _i64, _i64]),
+    "gf_highres_host_workspace_bytes": (_sz, [_i, _i64, _i64, _i64, _i64, _i]),
+    "gf_highres_fwd_host": (_i, [_i, _p, _p, _p, _i64, _i64, _i64, _i64, _i64, _i, _d, _p, _sz,
+                                 _p]),
+    "gf_joint_host_workspace_bytes": (_sz, [_i, _i64, _i64, _i64, _i64, _i64, _i]),
+    "gf_joint_fwd_host": (_i, [_i, _p, _p, _p, _p, _i64, _i64, _i64, _i64, _i64, _i64, _i, _d,
+                               _p, _sz, _p]),
 }
 
 # test hooks exported by the library but not part of the public header

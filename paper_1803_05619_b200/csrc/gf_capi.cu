@@ -413,3 +413,17 @@ int gf_mse_loss(int dtype, const void* out, const void* target, void* d_out, dou
 }
 
 }  // extern "C"
+
+// checks shared with the host-buffer entries (gf_host.cu)
+namespace gfb {
+int api_check_highres(int dtype, int64_t B, int64_t Cg, int64_t C, int64_t H, int64_t W, int r,
+                      double eps) {
+  return check_highres(dtype, B, Cg, C, H, W, r, eps);
+}
+int api_check_joint(int dtype, int64_t B, int64_t C, int64_t h, int64_t w, int64_t H, int64_t W,
+                    int r, double eps) {
+  return check_joint(dtype, B, C, h, w, H, W, r, eps);
+}
+int api_fail(int code, const char* what) { return fail(code, "%s", what); }
+}  // namespace gfb
+

@@ -82,4 +82,11 @@ void gn_fast_forward(const float* x, float* y, const float* params, int64_t B, i
 void gn_fast_backward(const float* x, const float* dy, float* dx, float* dparams, int accumulate,
                       const float* params, int64_t B, int64_t hidden, int64_t HW, void* ws,
                       uint32_t* status, cudaStream_t s);
+// argument checks / error text of the C ABI (gf_capi.cu), for gf_host.cu
+int api_check_highres(int dtype, int64_t B, int64_t Cg, int64_t C, int64_t H, int64_t W, int r,
+                      double eps);
+int api_check_joint(int dtype, int64_t B, int64_t C, int64_t h, int64_t w, int64_t H, int64_t W,
+                    int r, double eps);
+int api_fail(int code, const char* what);
+
 }  // namespace gfb
