@@ -12,8 +12,8 @@
 //              batch k (entering rows from the TMA-staged rows, leaving rows
 //              re-read from L2)                                   -> smem vs
 //     V2(k-1)  vertical running sums of the coefficient rows (A, b') of
-//              batch k-1; the leaving rows of batch k are read from the
-//              coefficient ring before H1(k) overwrites them       -> vs2
+//              batch k-1: entering and leaving rows both come from the
+//              coefficient ring of 2r+1+R rows                      -> vs2
 //   run phase Y(k)      every thread: H1(k) on one (row, run of K=8 columns),
 //                       then H2(k-1) on one (row, run)
 //     H1(k)    horizontal window sums streamed over the run, A = cov/(var+eps),
@@ -27,8 +27,8 @@
 // (s_gg, s_gs) at level 1, (A, b') at level 2 -- so one instruction updates
 // both, and the shared-memory rows interleave the pair (128-bit loads fetch
 // two columns).  The entering rows arrive by TMA (cp.async.bulk.tensor,
-// zero-filled outside the image) into two stages: the load of batch k+2 is
-// issued at the start of Y(k), into the stage X(k) just consumed.
+// zero-filled outside the image): the load of batch k+NSTAGE is issued at
+// the start of Y(k), into the stage X(k) just consumed.
 //
 // Windows are clamped to the image and normalised by the true count
 // N = ny*nx (gf/filters.py:82-103): out-of-image rows/columns contribute 0.
@@ -49,6 +49,7 @@ constexpr int R = 8;     // coefficient rows per batch (= lanes per run group)
 constexpr int NT = 256;  // threads: one vs column each in the column phase
 constexpr int K = 8;     // run length of H1 and H2
 constexpr int kMaxRadius = 16;
+constexpr int NSTAGE = 1;  // TMA stages of the entering rows
 
 __host__ __device__ constexpr int up4(int n) { return (n + 3) / 4 * 4; }
 // smallest p >= n with p = 4 (mod 32)
@@ -73,10 +74,12 @@ struct Geo {
   static constexpr int W2M = TXM + 2 * RAD;   // coefficient columns bound
   static constexpr int RWM = cdiv(W2M, K) * K;
   static constexpr int PV = pitch4(2 * NT);   // vs rows: NT column pairs
-  static constexpr int ringN = cmax(2 * RAD + 1, R);
+  // coefficient rows kept: the 2r+1 of the level-2 window plus a batch, so V2
+  // reads a batch's entering and leaving rows after H1 wrote the batch
+  static constexpr int ringN = 2 * RAD + 1 + R;
   static constexpr int PR = pitch4(2 * RWM);  // ring rows: (A, b') pairs
   static constexpr int P2 = pitch4(2 * W2M);  // vs2 rows: (A, b') sums
-  static constexpr size_t smem_floats = (size_t)2 * 2 * R * NT + (size_t)2 * R * PV +
+  static constexpr size_t smem_floats = (size_t)NSTAGE * 2 * R * NT + (size_t)2 * R * PV +
                                         (size_t)ringN * PR + (size_t)R * P2 + 4;
   static constexpr size_t smem_bytes = smem_floats * sizeof(float);
   static constexpr uint32_t tx_bytes = 2u * R * NT * 4u;
@@ -237,8 +240,8 @@ __global__ void __launch_bounds__(NT, Geo<RAD>::min_blocks)
   constexpr int ringN = GG::ringN;
   constexpr int PR = GG::PR;
   extern __shared__ __align__(128) float4 smem4[];
-  float* stg = reinterpret_cast<float*>(smem4);  // [2 stages][2 fields][R][NT] (TMA)
-  float* vsA = stg + 2 * 2 * R * NT;             // [R][PV] (s_g, s_s) pairs
+  float* stg = reinterpret_cast<float*>(smem4);  // [NSTAGE][2 fields][R][NT] (TMA)
+  float* vsA = stg + NSTAGE * 2 * R * NT;        // [R][PV] (s_g, s_s) pairs
   float* vsB = vsA + R * GG::PV;                 // [R][PV] (s_gg, s_gs) pairs
   float* ring = vsB + R * GG::PV;                // [ringN][PR] (A, b') pairs
   float* vs2 = ring + ringN * PR;                // [R][P2] (A, b') vertical sums
@@ -291,10 +294,10 @@ __global__ void __launch_bounds__(NT, Geo<RAD>::min_blocks)
     const int xs0 = x0 - GG::PADL;          // image column of vs / stg column 0
 
     // TMA of the R entering input rows of batch k (image rows ya0 + kR + r ...)
-    // into stage k & 1, two batches ahead of their use
+    // into stage k % NSTAGE, NSTAGE batches ahead of their use
     auto prefetch = [&](int k) {
       if (tid == 0) {
-        const int st = k & 1;
+        const int st = k % NSTAGE;
         tma::fence_proxy_async();
         tma::mbar_arrive_expect_tx(bar + st, GG::tx_bytes);
         const int e0 = ya0 + k * R + r;
@@ -303,8 +306,9 @@ __global__ void __launch_bounds__(NT, Geo<RAD>::min_blocks)
         tma::load_3d(dst + R * NT, &tmS, xs0, e0, (int)splane, bar + st);
       }
     };
-    prefetch(0);
-    if (nb > 1) prefetch(1);
+#pragma unroll
+    for (int k = 0; k < NSTAGE; ++k)
+      if (k < nb) prefetch(k);
 
     // ---- column-phase state: V1 on vs column tid, V2 on coefficient column tid
     const int gx = xs0 + tid;
@@ -322,14 +326,10 @@ __global__ void __launch_bounds__(NT, Geo<RAD>::min_blocks)
     const bool v2 = tid < W2;
     const float* rr = ring + 2 * tid;  // V2: ring column tid
     u64 cS = 0;                        // level-2 sums at the end of the last batch
-    u64 pS[R];                         // running sums minus the leaving rows
-#pragma unroll
-    for (int j = 0; j < R; ++j) pS[j] = 0;
-    int s_cur = 0;                                // ring slot of coefficient row kR
-    int s_prev = ringN - (R % ringN);             // ... of row (k-1)R
-    if (s_prev == ringN) s_prev = 0;
-    int s_old = ringN - ((2 * r + 1) % ringN);    // ... of row kR - 2r - 1
-    if (s_old == ringN) s_old = 0;
+    constexpr int dj = 2 * r + 1;      // row distance of a leaving coefficient row
+    int s_cur = 0;                     // ring slot of coefficient row kR
+    int s_prev = ringN - R;            // ... of row (k-1)R
+    int s_lv = ringN - R - dj;         // ... of row (k-1)R - dj (its leaving row)
     const int jr = lane & 7;                      // run phase: row of the batch
     const int q = warp * 4 + (lane >> 3);         // run phase: run
 
@@ -337,7 +337,7 @@ __global__ void __launch_bounds__(NT, Geo<RAD>::min_blocks)
       const int base = k * R;
       // ================= column phase X(k) ===============================
       if (k < nb) {  // ---- V1(k)
-        const int st = k & 1;
+        const int st = k % NSTAGE;
         float* oA = vsA + 2 * tid;
         float* oB = vsB + 2 * tid;
         const float* eg = stg + st * 2 * R * NT + tid;
@@ -399,64 +399,49 @@ __global__ void __launch_bounds__(NT, Geo<RAD>::min_blocks)
           }
         }
       }
-      if (v2) {
-        // ring rows of slots s..s+R-1 (mod ringN): rows j < w at p + j*PR, the
-        // wrapped rows at p + (j - ringN)*PR
-        constexpr int dj = 2 * r + 1;        // row distance of the leaving row
-        constexpr int nl = dj < R ? dj : R;  // rows of a batch whose leaving row is older
-        if (k >= 1) {  // ---- V2(k-1): add batch k-1's coefficient rows -> vs2
-          const int nvalid = nrows - (base - R);
-          const float* fa = rr + s_prev * PR;
-          const float* fw = fa - ringN * PR;
-          const int wF = ringN - s_prev;
-          u64 x[R];
-          if (wF >= R && nvalid >= R) {
-#pragma unroll
-            for (int j = 0; j < R; ++j) x[j] = lds2(fa + j * PR);
-          } else {
-#pragma unroll
-            for (int j = 0; j < R; ++j) {
-              x[j] = 0;
-              if (j < nvalid) x[j] = lds2((j < wF ? fa : fw) + j * PR);
-            }
-          }
-          u64 n = 0;
+      if (v2 && k >= 1) {
+        // ---- V2(k-1): vertical sums of batch k-1's coefficient rows -> vs2.
+        // Ring rows of slots s..s+R-1 (mod ringN): rows j < w at p + j*PR, the
+        // wrapped rows at p + (j - ringN)*PR.
+        const int bb = base - R;             // first coefficient row of batch k-1
+        const int nvalid = nrows - bb;
+        const int jmin = dj - bb;            // rows j >= jmin have a leaving row
+        const float* fa = rr + s_prev * PR;
+        const float* fw = fa - ringN * PR;
+        const int wF = ringN - s_prev;
+        const float* la = rr + s_lv * PR;
+        const float* lw = la - ringN * PR;
+        const int wL = ringN - s_lv;
+        u64 x[R], y[R];
+        if (wF >= R && wL >= R && nvalid >= R && jmin <= 0) {
 #pragma unroll
           for (int j = 0; j < R; ++j) {
-            n = add2(n, x[j]);
-            if (j >= dj) n = sub2(n, x[j - dj]);  // leaving row inside this batch (small r)
-            sts2(vs2 + j * GG::P2 + 2 * tid, add2(pS[j], n));
+            x[j] = lds2(fa + j * PR);
+            y[j] = lds2(la + j * PR);
           }
-          cS = add2(pS[R - 1], n);
-        }
-        if (k < nb) {  // ---- leaving rows of batch k, before H1(k) overwrites them
-          const float* oa = rr + s_old * PR;
-          const float* ow = oa - ringN * PR;
-          const int wO = ringN - s_old;
-          u64 y[nl];
-          if (wO >= nl && base >= dj) {
-#pragma unroll
-            for (int j = 0; j < nl; ++j) y[j] = lds2(oa + j * PR);
-          } else {
-            const int jmin = dj - base;  // rows j >= jmin leave a real row
-#pragma unroll
-            for (int j = 0; j < nl; ++j) {
-              y[j] = 0;
-              if (j >= jmin) y[j] = lds2((j < wO ? oa : ow) + j * PR);
-            }
-          }
-          u64 qs = cS;
+        } else {
 #pragma unroll
           for (int j = 0; j < R; ++j) {
-            if (j < nl) qs = sub2(qs, y[j]);
-            pS[j] = qs;
+            x[j] = 0;
+            y[j] = 0;
+            if (j < nvalid) {
+              x[j] = lds2((j < wF ? fa : fw) + j * PR);
+              if (j >= jmin) y[j] = lds2((j < wL ? la : lw) + j * PR);
+            }
           }
         }
+        u64 c = cS;
+#pragma unroll
+        for (int j = 0; j < R; ++j) {
+          c = add2(c, sub2(x[j], y[j]));
+          sts2(vs2 + j * GG::P2 + 2 * tid, c);
+        }
+        cS = c;
       }
       cta_sync();  // vs, vs2 complete; stg and the leaving ring rows consumed
 
       // ================= run phase Y(k) ==================================
-      if (k + 2 < nb) prefetch(k + 2);  // into the stage X(k) just consumed
+      if (k + NSTAGE < nb) prefetch(k + NSTAGE);  // into the stage X(k) just consumed
       {  // ---- H1(k): coefficient row base+jr, columns [qK, qK+K)
         const int i = base + jr;
         if (k < nb && q * K < W2 && i < nrows) {
@@ -497,8 +482,8 @@ __global__ void __launch_bounds__(NT, Geo<RAD>::min_blocks)
       s_prev = s_cur;
       s_cur += R;
       if (s_cur >= ringN) s_cur -= ringN;
-      s_old += R;
-      if (s_old >= ringN) s_old -= ringN;
+      s_lv += R;
+      if (s_lv >= ringN) s_lv -= ringN;
       cta_sync();  // ring rows of batch k and the outputs of batch k-1 done
     }
   }
