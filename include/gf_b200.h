@@ -175,6 +175,26 @@ int gf_joint_fwd_host(int dtype, const void* lr_x, const void* lr_y, const void*
                       int radius, double eps, void* workspace, size_t workspace_bytes,
                       uint32_t* status);
 
+/* ---- guidance / core net with a k x k dilated first convolution ----
+ * gf/guidance.py:184-224 with ConvLayer(kernel=k, dilation=d) (:52-124):
+ * GuidedUpsampler's low-res core net C_l (gf/training.py:186-207, k = 3).
+ * Same layer chain and packed parameter order as gn_*, with conv1.weight
+ * (hidden, Cin, k, k) row-major: gnk_param_count() values.  kernel odd >= 1,
+ * dilation >= 1, zero "same" padding (k-1)*d/2.  kernel == 1 equals gn_*. */
+int64_t gnk_param_count(int64_t Cin, int64_t Cout, int64_t hidden, int kernel);
+
+size_t gnk_workspace_bytes(int dtype, int64_t B, int64_t Cin, int64_t Cout, int64_t hidden,
+                           int kernel, int64_t H, int64_t W);
+
+int gnk_forward(int dtype, const void* x, void* y, const void* params, int64_t B, int64_t Cin,
+                int64_t Cout, int64_t hidden, int kernel, int dilation, int64_t H, int64_t W,
+                void* workspace, size_t workspace_bytes, uint32_t* status, void* stream);
+
+int gnk_backward(int dtype, const void* x, const void* dy, void* dx, void* dparams,
+                 int accumulate, const void* params, int64_t B, int64_t Cin, int64_t Cout,
+                 int64_t hidden, int kernel, int dilation, int64_t H, int64_t W, void* workspace,
+                 size_t workspace_bytes, uint32_t* status, void* stream);
+
 /* ---- mse_loss: gf/training.py:93-101 (batch-mean variant of config 2) ----
  * loss = mean over the batch of per-image mean((out - target)^2); d_out =
  * 2 (out - target) / (C*H*W) / B.  loss is one device double. */

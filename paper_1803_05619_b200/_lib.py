@@ -45,6 +45,12 @@ SIGNATURES = {
                          _sz, _p, _p]),
     "gf_mse_loss": (_i, [_i, _p, _p, _p, _p, _i64, _i64, _i64, _i64, _p, _sz, _p]),
     "gf_mse_workspace_bytes": (_sz, [_i64, _i64, _i64, _i64]),
+    "gnk_param_count": (_i64, [_i64, _i64, _i64, _i]),
+    "gnk_workspace_bytes": (_sz, [_i, _i64, _i64, _i64, _i64, _i, _i64, _i64]),
+    "gnk_forward": (_i, [_i, _p, _p, _p, _i64, _i64, _i64, _i64, _i, _i, _i64, _i64, _p, _sz, _p,
+                         _p]),
+    "gnk_backward": (_i, [_i, _p, _p, _p, _p, _i, _p, _i64, _i64, _i64, _i64, _i, _i, _i64, _i64,
+                          _p, _sz, _p, _p]),
     "gf_highres_host_workspace_bytes": (_sz, [_i, _i64, _i64, _i64, _i64, _i]),
     "gf_highres_fwd_host": (_i, [_i, _p, _p, _p, _i64, _i64, _i64, _i64, _i64, _i, _d, _p, _sz,
                                  _p]),

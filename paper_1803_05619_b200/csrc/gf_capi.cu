@@ -389,6 +389,67 @@ int gn_backward(int dtype, const void* x, const void* dy, void* dx, void* dparam
   return check_launch("gn_backward");
 }
 
+// ---------------------------------------------------------------------------
+// k x k (dilated) guidance / core net
+// ---------------------------------------------------------------------------
+int64_t gnk_param_count(int64_t Cin, int64_t Cout, int64_t hidden, int kernel) {
+  return hidden * Cin * kernel * kernel + 2 + Cout * hidden + Cout;
+}
+
+size_t gnk_workspace_bytes(int dtype, int64_t B, int64_t Cin, int64_t Cout, int64_t hidden,
+                           int kernel, int64_t H, int64_t W) {
+  return gfb::gnk_ws_bytes_impl(B, Cin, Cout, hidden, kernel, H * W, dtype == GF_F64 ? 8 : 4);
+}
+
+static int check_gnk(int dtype, int64_t B, int64_t Cin, int64_t Cout, int64_t hidden, int kernel,
+                     int dilation, int64_t H, int64_t W, size_t ws_bytes) {
+  if (!dtype_ok(dtype)) return fail(GF_ERR_ARG, "bad dtype %d", dtype);
+  if (int e = check_dims("x", B, Cin, H, W)) return e;
+  // ConvLayer.__init__, gf/guidance.py:62-65
+  if (kernel < 1 || kernel % 2 == 0)
+    return fail(GF_ERR_ARG, "kernel must be odd and >= 1, got %d", kernel);
+  if (dilation < 1) return fail(GF_ERR_ARG, "dilation must be >= 1, got %d", dilation);
+  if (Cout < 1 || hidden < 1)
+    return fail(GF_ERR_ARG, "Cout and hidden must be >= 1 (got %lld, %lld)", (long long)Cout,
+                (long long)hidden);
+  size_t need = gnk_workspace_bytes(dtype, B, Cin, Cout, hidden, kernel, H, W);
+  if (ws_bytes < need) return fail(GF_ERR_WORKSPACE, "gnk workspace %zu < %zu bytes", ws_bytes, need);
+  return GF_OK;
+}
+
+int gnk_forward(int dtype, const void* x, void* y, const void* params, int64_t B, int64_t Cin,
+                int64_t Cout, int64_t hidden, int kernel, int dilation, int64_t H, int64_t W,
+                void* workspace, size_t workspace_bytes, uint32_t* status, void* stream) {
+  if (int e = check_gnk(dtype, B, Cin, Cout, hidden, kernel, dilation, H, W, workspace_bytes))
+    return e;
+  if (dtype == GF_F32)
+    gfb::gnk_forward_impl<float>((const float*)x, (float*)y, (const float*)params, B, Cin, Cout,
+                                 hidden, kernel, dilation, H, W, workspace, status, S(stream));
+  else
+    gfb::gnk_forward_impl<double>((const double*)x, (double*)y, (const double*)params, B, Cin,
+                                  Cout, hidden, kernel, dilation, H, W, workspace, status,
+                                  S(stream));
+  return check_launch("gnk_forward");
+}
+
+int gnk_backward(int dtype, const void* x, const void* dy, void* dx, void* dparams,
+                 int accumulate, const void* params, int64_t B, int64_t Cin, int64_t Cout,
+                 int64_t hidden, int kernel, int dilation, int64_t H, int64_t W, void* workspace,
+                 size_t workspace_bytes, uint32_t* status, void* stream) {
+  if (int e = check_gnk(dtype, B, Cin, Cout, hidden, kernel, dilation, H, W, workspace_bytes))
+    return e;
+  if (dtype == GF_F32)
+    gfb::gnk_backward_impl<float>((const float*)x, (const float*)dy, (float*)dx, (float*)dparams,
+                                  accumulate, (const float*)params, B, Cin, Cout, hidden, kernel,
+                                  dilation, H, W, workspace, status, S(stream));
+  else
+    gfb::gnk_backward_impl<double>((const double*)x, (const double*)dy, (double*)dx,
+                                   (double*)dparams, accumulate, (const double*)params, B, Cin,
+                                   Cout, hidden, kernel, dilation, H, W, workspace, status,
+                                   S(stream));
+  return check_launch("gnk_backward");
+}
+
 size_t gf_mse_workspace_bytes(int64_t B, int64_t C, int64_t H, int64_t W) {
   (void)C;
   (void)H;

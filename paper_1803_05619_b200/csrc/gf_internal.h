@@ -82,6 +82,18 @@ void gn_fast_forward(const float* x, float* y, const float* params, int64_t B, i
 void gn_fast_backward(const float* x, const float* dy, float* dx, float* dparams, int accumulate,
                       const float* params, int64_t B, int64_t hidden, int64_t HW, void* ws,
                       uint32_t* status, cudaStream_t s);
+// guidance / core net with a k x k dilated first conv (gf_guidance_k.cu)
+size_t gnk_ws_bytes_impl(int64_t B, int64_t Cin, int64_t Cout, int64_t hid, int k, int64_t HW,
+                         size_t es);
+template <typename T>
+void gnk_forward_impl(const T* x, T* y, const T* params, int64_t B, int64_t Cin, int64_t Cout,
+                      int64_t hid, int k, int d, int64_t H, int64_t W, void* ws, uint32_t* status,
+                      cudaStream_t s);
+template <typename T>
+void gnk_backward_impl(const T* x, const T* dy, T* dx, T* dparams, int accumulate, const T* params,
+                       int64_t B, int64_t Cin, int64_t Cout, int64_t hid, int k, int d, int64_t H,
+                       int64_t W, void* ws, uint32_t* status, cudaStream_t s);
+
 // argument checks / error text of the C ABI (gf_capi.cu), for gf_host.cu
 int api_check_highres(int dtype, int64_t B, int64_t Cg, int64_t C, int64_t H, int64_t W, int r,
                       double eps);
