@@ -195,6 +195,23 @@ int gnk_backward(int dtype, const void* x, const void* dy, void* dx, void* dpara
                  int64_t hidden, int kernel, int dilation, int64_t H, int64_t W, void* workspace,
                  size_t workspace_bytes, uint32_t* status, void* stream);
 
+/* ---- FixedChannelMeanGuidance (gf/guidance.py:227-255) ----
+ * y (B, Cout, H, W): every channel = mean over the Cin channels of x;
+ * adjoint dx (B, Cin, H, W) = (sum over Cout of dy) / Cin. */
+int gf_channel_mean(int dtype, const void* x, void* y, int64_t B, int64_t Cin, int64_t Cout,
+                    int64_t H, int64_t W, void* stream);
+
+int gf_channel_mean_adjoint(int dtype, const void* dy, void* dx, int64_t B, int64_t Cin,
+                            int64_t Cout, int64_t H, int64_t W, void* stream);
+
+/* ---- adam_step (gf/training.py:66-90) on one packed vector of n values ----
+ * In place: m = b1 m + (1-b1) g; v = b2 v + (1-b2) g^2; p -= lr mhat /
+ * (sqrt(vhat) + 1e-8) with b1 = 0.9, b2 = 0.999 and the bias corrections of
+ * the 1-based step t.  A non-finite gradient sets GF_STATUS_NONFINITE_INPUT
+ * (the reference's TrainingError) and leaves that element unchanged. */
+int gf_adam_step(int dtype, void* params, const void* grads, void* m, void* v, int64_t n,
+                 int step, double lr, uint32_t* status, void* stream);
+
 /* ---- mse_loss: gf/training.py:93-101 (batch-mean variant of config 2) ----
  * loss = mean over the batch of per-image mean((out - target)^2); d_out =
  * 2 (out - target) / (C*H*W) / B.  loss is one device double. */

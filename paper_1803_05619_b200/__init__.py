@@ -17,11 +17,13 @@ from .guided import (
     forward_highres,
     forward_joint,
 )
-from .guidance import GuidanceNet
+from .guidance import FixedChannelMeanGuidance, GuidanceNet
 from .filters import bilinear_resize, bilinear_resize_adjoint, mean_filter, mean_filter_adjoint
 from .training import affine_target, mse_loss, train_step
 from .nn import FastGuidedFilter, FullResGuidedFilter
 from .host import forward_highres_host, forward_joint_host
+from .upsampler import (AdamState, GuidedUpsampler, PipelineTape, TrainConfig, TrainingError,
+                        adam_step, build_model, train)
 
 __version__ = "0.1.0"
 
@@ -31,4 +33,6 @@ __all__ = [
     "GuidanceNet", "bilinear_resize", "bilinear_resize_adjoint", "mean_filter",
     "mean_filter_adjoint", "affine_target", "mse_loss", "train_step", "FastGuidedFilter",
     "FullResGuidedFilter", "forward_highres_host", "forward_joint_host",
+    "FixedChannelMeanGuidance", "AdamState", "GuidedUpsampler", "PipelineTape", "TrainConfig",
+    "TrainingError", "adam_step", "build_model", "train",
 ]

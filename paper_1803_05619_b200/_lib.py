@@ -51,6 +51,9 @@ SIGNATURES = {
                          _p]),
     "gnk_backward": (_i, [_i, _p, _p, _p, _p, _i, _p, _i64, _i64, _i64, _i64, _i, _i, _i64, _i64,
                           _p, _sz, _p, _p]),
+    "gf_channel_mean": (_i, [_i, _p, _p, _i64, _i64, _i64, _i64, _i64, _p]),
+    "gf_channel_mean_adjoint": (_i, [_i, _p, _p, _i64, _i64, _i64, _i64, _i64, _p]),
+    "gf_adam_step": (_i, [_i, _p, _p, _p, _p, _i64, _i, _d, _p, _p]),
     "gf_highres_host_workspace_bytes": (_sz, [_i, _i64, _i64, _i64, _i64, _i]),
     "gf_highres_fwd_host": (_i, [_i, _p, _p, _p, _i64, _i64, _i64, _i64, _i64, _i, _d, _p, _sz,
                                  _p]),

@@ -450,6 +450,52 @@ int gnk_backward(int dtype, const void* x, const void* dy, void* dx, void* dpara
   return check_launch("gnk_backward");
 }
 
+// ---------------------------------------------------------------------------
+// training harness: fixed channel-mean guidance, Adam
+// ---------------------------------------------------------------------------
+int gf_channel_mean(int dtype, const void* x, void* y, int64_t B, int64_t Cin, int64_t Cout,
+                    int64_t H, int64_t W, void* stream) {
+  if (!dtype_ok(dtype)) return fail(GF_ERR_ARG, "bad dtype %d", dtype);
+  if (int e = check_dims("x", B, Cin, H, W)) return e;
+  if (Cout < 1) return fail(GF_ERR_ARG, "Cout must be >= 1, got %lld", (long long)Cout);
+  if (dtype == GF_F32)
+    gfb::chan_mean_impl<float>((const float*)x, (float*)y, B, Cin, Cout, H * W, S(stream));
+  else
+    gfb::chan_mean_impl<double>((const double*)x, (double*)y, B, Cin, Cout, H * W, S(stream));
+  return check_launch("gf_channel_mean");
+}
+
+int gf_channel_mean_adjoint(int dtype, const void* dy, void* dx, int64_t B, int64_t Cin,
+                            int64_t Cout, int64_t H, int64_t W, void* stream) {
+  if (!dtype_ok(dtype)) return fail(GF_ERR_ARG, "bad dtype %d", dtype);
+  if (int e = check_dims("dy", B, Cout, H, W)) return e;
+  if (Cin < 1) return fail(GF_ERR_ARG, "Cin must be >= 1, got %lld", (long long)Cin);
+  if (dtype == GF_F32)
+    gfb::chan_mean_adj_impl<float>((const float*)dy, (float*)dx, B, Cin, Cout, H * W, S(stream));
+  else
+    gfb::chan_mean_adj_impl<double>((const double*)dy, (double*)dx, B, Cin, Cout, H * W,
+                                    S(stream));
+  return check_launch("gf_channel_mean_adjoint");
+}
+
+int gf_adam_step(int dtype, void* params, const void* grads, void* m, void* v, int64_t n, int step,
+                 double lr, uint32_t* status, void* stream) {
+  if (!dtype_ok(dtype)) return fail(GF_ERR_ARG, "bad dtype %d", dtype);
+  if (n < 0) return fail(GF_ERR_ARG, "n must be >= 0");
+  if (step < 1) return fail(GF_ERR_ARG, "step must be >= 1 (1-based), got %d", step);
+  // TrainConfig.__post_init__, gf/training.py:43-45
+  if (!std::isfinite(lr) || lr < 0.0)
+    return fail(GF_ERR_ARG, "learning_rate must be finite and >= 0, got %g", lr);
+  if (n == 0) return GF_OK;
+  if (dtype == GF_F32)
+    gfb::adam_impl<float>((float*)params, (const float*)grads, (float*)m, (float*)v, n, step, lr,
+                          0.9, 0.999, 1e-8, status, S(stream));
+  else
+    gfb::adam_impl<double>((double*)params, (const double*)grads, (double*)m, (double*)v, n, step,
+                           lr, 0.9, 0.999, 1e-8, status, S(stream));
+  return check_launch("gf_adam_step");
+}
+
 size_t gf_mse_workspace_bytes(int64_t B, int64_t C, int64_t H, int64_t W) {
   (void)C;
   (void)H;

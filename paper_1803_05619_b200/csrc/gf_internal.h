@@ -94,6 +94,17 @@ void gnk_backward_impl(const T* x, const T* dy, T* dx, T* dparams, int accumulat
                        int64_t B, int64_t Cin, int64_t Cout, int64_t hid, int k, int d, int64_t H,
                        int64_t W, void* ws, uint32_t* status, cudaStream_t s);
 
+// training harness (gf_train.cu)
+template <typename T>
+void chan_mean_impl(const T* x, T* y, int64_t B, int64_t Cin, int64_t Cout, int64_t HW,
+                    cudaStream_t s);
+template <typename T>
+void chan_mean_adj_impl(const T* dy, T* dx, int64_t B, int64_t Cin, int64_t Cout, int64_t HW,
+                        cudaStream_t s);
+template <typename T>
+void adam_impl(T* p, const T* g, T* m, T* v, int64_t n, int step, double lr, double b1, double b2,
+               double eps, uint32_t* status, cudaStream_t s);
+
 // argument checks / error text of the C ABI (gf_capi.cu), for gf_host.cu
 int api_check_highres(int dtype, int64_t B, int64_t Cg, int64_t C, int64_t H, int64_t W, int r,
                       double eps);

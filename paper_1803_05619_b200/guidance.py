@@ -7,9 +7,11 @@ xavier-uniform; AdaptiveNorm gain=1, norm_gain=0; conv2 bias 0), forward
 (gf/guidance.py:209-214) and backward (gf/guidance.py:216-224).  The whole
 net runs in the sm_100a kernels behind ``gn_forward`` / ``gn_backward``.
 
-Only the 1x1 configuration is on the B200 path (BASELINE config 2: 3 -> 15
--> 3).  ``kernel > 1`` (dilated k x k convs, used only by the reference's
-core net) raises NotImplementedError.
+The 1x1 net (BASELINE config 2: 3 -> 15 -> 3) runs the gn_* kernels (a
+fused fp32 path for the small hidden widths); ``kernel > 1`` (odd, with
+``dilation``, the reference's low-res core net C_l, gf/training.py:186-207)
+runs the gnk_* kernels.  ``FixedChannelMeanGuidance`` mirrors
+gf/guidance.py:227-255.
 """
 
 from __future__ import annotations
@@ -48,17 +50,16 @@ class GuidanceNet:
             raise ValueError(f"kernel must be odd and >= 1, got {kernel}")
         if dilation < 1:
             raise ValueError(f"dilation must be >= 1, got {dilation}")
-        if kernel != 1:
-            raise NotImplementedError("only the 1x1 guidance transform is on the B200 path")
         self.in_ch, self.out_ch, self.hidden = int(in_ch), int(out_ch), int(hidden)
+        self.kernel, self.dilation = int(kernel), int(dilation)
         if device is None:
             device = torch.device("cuda", torch.cuda.current_device())
         self.device = torch.device(device)
         if rng is None:
-            w1 = np.zeros((hidden, in_ch, 1, 1))
+            w1 = np.zeros((hidden, in_ch, kernel, kernel))
             w2 = np.zeros((out_ch, hidden, 1, 1))
         else:
-            w1 = xavier_uniform(rng, hidden, in_ch, 1)
+            w1 = xavier_uniform(rng, hidden, in_ch, kernel)
             w2 = xavier_uniform(rng, out_ch, hidden, 1)
         self.flat = torch.zeros(self.param_count(), dtype=torch.float64, device=self.device)
         self.load_parameters({
@@ -67,13 +68,15 @@ class GuidanceNet:
 
     # packed layout (include/gf_b200.h): w1, gain, norm_gain, w2, b2
     def param_count(self) -> int:
-        return self.hidden * self.in_ch + 2 + self.out_ch * self.hidden + self.out_ch
+        k2 = self.kernel * self.kernel
+        return self.hidden * self.in_ch * k2 + 2 + self.out_ch * self.hidden + self.out_ch
 
     def _slices(self):
-        a = self.hidden * self.in_ch
+        k = self.kernel
+        a = self.hidden * self.in_ch * k * k
         b = a + 2 + self.out_ch * self.hidden
         return {
-            "conv1.weight": (slice(0, a), (self.hidden, self.in_ch, 1, 1)),
+            "conv1.weight": (slice(0, a), (self.hidden, self.in_ch, k, k)),
             "norm.gain": (slice(a, a + 1), (1,)),
             "norm.norm_gain": (slice(a + 1, a + 2), (1,)),
             "conv2.weight": (slice(a + 2, b), (self.out_ch, self.hidden, 1, 1)),
@@ -122,11 +125,18 @@ class GuidanceNet:
         params = self._params_as(im.t.dtype)
         y = torch.empty((B, self.out_ch, H, W), dtype=im.t.dtype, device=self.device)
         status = Status(self.device)
-        ws = workspace(lib.gn_workspace_bytes(dt, B, self.in_ch, self.out_ch, self.hidden, H, W),
-                       self.device)
-        rc = lib.gn_forward(dt, ptr(im.t), ptr(y), ptr(params), B, self.in_ch, self.out_ch,
-                            self.hidden, H, W, ptr(ws), ws.numel(), status.ptr,
-                            stream_ptr(self.device))
+        if self.kernel == 1:
+            ws = workspace(lib.gn_workspace_bytes(dt, B, self.in_ch, self.out_ch, self.hidden, H,
+                                                  W), self.device)
+            rc = lib.gn_forward(dt, ptr(im.t), ptr(y), ptr(params), B, self.in_ch, self.out_ch,
+                                self.hidden, H, W, ptr(ws), ws.numel(), status.ptr,
+                                stream_ptr(self.device))
+        else:
+            ws = workspace(lib.gnk_workspace_bytes(dt, B, self.in_ch, self.out_ch, self.hidden,
+                                                   self.kernel, H, W), self.device)
+            rc = lib.gnk_forward(dt, ptr(im.t), ptr(y), ptr(params), B, self.in_ch, self.out_ch,
+                                 self.hidden, self.kernel, self.dilation, H, W, ptr(ws),
+                                 ws.numel(), status.ptr, stream_ptr(self.device))
         _lib.check(rc, "GuidanceNet.forward")
         if check:
             status.raise_if_set("GuidanceNet.forward")
@@ -149,11 +159,19 @@ class GuidanceNet:
         if dparams is None:
             dparams = torch.zeros(self.param_count(), dtype=im.t.dtype, device=self.device)
         status = Status(self.device)
-        ws = workspace(lib.gn_workspace_bytes(dt, B, self.in_ch, self.out_ch, self.hidden, H, W),
-                       self.device)
-        rc = lib.gn_backward(dt, ptr(im.t), ptr(d.t), ptr(dx), ptr(dparams), int(accumulate),
-                             ptr(params), B, self.in_ch, self.out_ch, self.hidden, H, W,
-                             ptr(ws), ws.numel(), status.ptr, stream_ptr(self.device))
+        if self.kernel == 1:
+            ws = workspace(lib.gn_workspace_bytes(dt, B, self.in_ch, self.out_ch, self.hidden, H,
+                                                  W), self.device)
+            rc = lib.gn_backward(dt, ptr(im.t), ptr(d.t), ptr(dx), ptr(dparams), int(accumulate),
+                                 ptr(params), B, self.in_ch, self.out_ch, self.hidden, H, W,
+                                 ptr(ws), ws.numel(), status.ptr, stream_ptr(self.device))
+        else:
+            ws = workspace(lib.gnk_workspace_bytes(dt, B, self.in_ch, self.out_ch, self.hidden,
+                                                   self.kernel, H, W), self.device)
+            rc = lib.gnk_backward(dt, ptr(im.t), ptr(d.t), ptr(dx), ptr(dparams),
+                                  int(accumulate), ptr(params), B, self.in_ch, self.out_ch,
+                                  self.hidden, self.kernel, self.dilation, H, W, ptr(ws),
+                                  ws.numel(), status.ptr, stream_ptr(self.device))
         _lib.check(rc, "GuidanceNet.backward")
         if check:
             status.raise_if_set("GuidanceNet.backward")
@@ -161,3 +179,50 @@ class GuidanceNet:
         if im.kind == "np_hwc":
             grads = {k: v.double().cpu().numpy() for k, v in grads.items()}
         return restore(dx, im), grads
+
+
+class FixedChannelMeanGuidance:
+    """Parameter-free guidance: channel mean of the input, replicated
+    (gf/guidance.py:227-255).  Same forward/backward surface as GuidanceNet."""
+
+    def __init__(self, in_ch: int, out_ch: int, *, device=None):
+        self.in_ch, self.out_ch = int(in_ch), int(out_ch)
+        if device is None:
+            device = torch.device("cuda", torch.cuda.current_device())
+        self.device = torch.device(device)
+
+    def param_count(self) -> int:
+        return 0
+
+    def parameters(self) -> dict:
+        return {}
+
+    def load_parameters(self, params: dict) -> None:
+        if params:
+            raise ValueError("fixed guidance has no parameters")
+
+    def forward(self, x, *, check: bool = True):
+        im = as_img(x, "x", device=self.device)
+        if im.shape[1] != self.in_ch:
+            raise ValueError(f"expected {self.in_ch} input channels, got {im.shape[1]}")
+        B, _, H, W = im.shape
+        y = torch.empty((B, self.out_ch, H, W), dtype=im.t.dtype, device=self.device)
+        lib = _lib.load()
+        rc = lib.gf_channel_mean(dtype_code(im.t), ptr(im.t), ptr(y), B, self.in_ch, self.out_ch,
+                                 H, W, stream_ptr(self.device))
+        _lib.check(rc, "FixedChannelMeanGuidance.forward")
+        return restore(y, im), GuidanceTape(x=im)
+
+    def backward(self, tape: GuidanceTape, dy, *, dparams=None, accumulate: bool = False,
+                 check: bool = True):
+        d = as_img(dy, "dy", device=self.device)
+        B, _, H, W = tape.x.shape
+        if d.shape != (B, self.out_ch, H, W):
+            raise ValueError(f"dy shape {d.shape} does not match output {(B, self.out_ch, H, W)}")
+        dx = torch.empty_like(tape.x.t)
+        lib = _lib.load()
+        rc = lib.gf_channel_mean_adjoint(dtype_code(d.t), ptr(d.t), ptr(dx), B, self.in_ch,
+                                         self.out_ch, H, W, stream_ptr(self.device))
+        _lib.check(rc, "FixedChannelMeanGuidance.backward")
+        return restore(dx, tape.x), {}
+
