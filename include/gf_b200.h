@@ -155,10 +155,11 @@ int gn_backward(int dtype, const void* x, const void* dy, void* dx, void* dparam
 /* ---- host-buffer entries: the reference's call shape (host images in, host
  * image out; gf/guided.py:152 guided_filter, :198 guided_filter_full) ----
  * Synchronous: the calls return when `out` (HOST memory) is written.  The
- * batch streams through the device one image at a time (copy-in of image
- * b+1, kernel of image b and copy-out of image b-1 overlap on three streams),
- * so page-locked host buffers make the call cost ~max(H2D, D2H) of the whole
- * batch.  `workspace` is DEVICE memory of *_host_workspace_bytes(); `status`
+ * batch streams through the device chunk by chunk -- one plane, or one image
+ * when a 1-channel guide drives C planes (copy-in of chunk b+1, kernel of
+ * chunk b and copy-out of chunk b-1 overlap on three streams kept per host
+ * thread and device), so page-locked host buffers make the call cost
+ * ~max(H2D, D2H) of the whole batch.  `workspace` is DEVICE memory of *_host_workspace_bytes(); `status`
  * is a HOST uint32 receiving the OR of the GF_STATUS_* bits of all images. */
 size_t gf_highres_host_workspace_bytes(int dtype, int64_t Cg, int64_t C, int64_t H, int64_t W,
                                        int radius);
