@@ -156,18 +156,75 @@ __device__ __forceinline__ u64 window_sum(const float* p) {
   return acc;
 }
 
+// ---- run warm-up shared across lanes (r a multiple of 4, K = 8) ------------
+// The window of a run's first output spans the run's own K columns and the
+// next r/4 - 1 runs' columns.  Every lane loads its own K columns once (they
+// are also the values that leave its window) and sums them; the neighbouring
+// runs' sums arrive by shuffle (lane + 8t = same row, run q + t), except for
+// the last runs of a warp, which load them.
+template <int RAD>
+struct Warm {
+  static constexpr bool kShared = RAD % 4 == 0 && RAD >= 4 && K == 8;
+  static constexpr int nS = kShared ? 2 * RAD / K : 0;
+};
+
+struct Own {
+  ulonglong2 c[K / 2];  // this run's K columns (pairs), 2 per 128-bit chunk
+  u64 sum;
+};
+
+__device__ __forceinline__ Own own_chunks(const float* v, bool need) {
+  Own o;
+  o.sum = 0;
+#pragma unroll
+  for (int m = 0; m < K / 2; ++m) {
+    o.c[m] = need ? lds22(v + 4 * m) : make_ulonglong2(0ull, 0ull);
+    o.sum = add2(o.sum, add2(o.c[m].x, o.c[m].y));
+  }
+  return o;
+}
+
+__device__ __forceinline__ u64 chunk_sum(const float* v) {
+  u64 s = 0;
+#pragma unroll
+  for (int m = 0; m < K / 2; ++m) {
+    const ulonglong2 c = lds22(v + 4 * m);
+    s = add2(s, add2(c.x, c.y));
+  }
+  return s;
+}
+
+// sum of the first 2r columns of the run at v (all 32 lanes must call; only
+// lanes with `task` need the result)
+template <int RAD>
+__device__ __forceinline__ u64 shared_warm(const float* v, u64 own_sum, int lane, bool task) {
+  u64 acc = own_sum;
+#pragma unroll
+  for (int t = 1; t < Warm<RAD>::nS; ++t) {
+    u64 nb = __shfl_down_sync(0xffffffffu, own_sum, 8 * t);
+    if ((lane >> 3) + t > 3)  // run q + t belongs to the next warp
+      nb = task ? chunk_sum(v + 2 * K * t) : 0ull;
+    acc = add2(acc, nb);
+  }
+  return acc;
+}
+
 // H1 on one run: (g, s) and (gg, gs) window sums streamed over K coefficient
 // columns -> (A, b') pairs into the ring row `ra`.
 template <int RAD, bool INTERIOR>
 __device__ __forceinline__ void h1_run(const float* vA, const float* vB, float* ra, float iny,
-                                       int gxa0, int w2_left, int W, float eps, float& vmin) {
+                                       int gxa0, int w2_left, int W, float eps, float& vmin,
+                                       u64 warmA, u64 warmB, const Own& oA, const Own& oB) {
   constexpr int r = RAD;
-  u64 accA = window_sum<2 * r>(vA), accB = window_sum<2 * r>(vB);
+  constexpr bool SH = Warm<RAD>::kShared;
+  u64 accA = SH ? warmA : window_sum<2 * r>(vA), accB = SH ? warmB : window_sum<2 * r>(vB);
   const float inv_i = iny * (1.0f / (float)(2 * r + 1));
 #pragma unroll
   for (int m = 0; m < K; m += 2) {
-    const ulonglong2 eA = lds22(vA + 2 * (m + 2 * r)), lA = lds22(vA + 2 * m);
-    const ulonglong2 eB = lds22(vB + 2 * (m + 2 * r)), lB = lds22(vB + 2 * m);
+    const ulonglong2 eA = lds22(vA + 2 * (m + 2 * r));
+    const ulonglong2 eB = lds22(vB + 2 * (m + 2 * r));
+    const ulonglong2 lA = SH ? oA.c[m / 2] : lds22(vA + 2 * m);
+    const ulonglong2 lB = SH ? oB.c[m / 2] : lds22(vB + 2 * m);
     u64 hA[2], hB[2];
     accA = add2(accA, eA.x); hA[0] = accA; accA = sub2(accA, lA.x);
     accB = add2(accB, eB.x); hB[0] = accB; accB = sub2(accB, lB.x);
@@ -203,16 +260,19 @@ __device__ __forceinline__ void h1_run(const float* vA, const float* vB, float* 
 template <int RAD, bool INTERIOR>
 __device__ __forceinline__ void h2_run(const float* v, const float* grow, float* orow,
                                        float iny, int gxo0, int W, float sG, float sS,
-                                       float& chk) {
+                                       float& chk, u64 warm, const Own& o) {
   constexpr int r = RAD;
-  u64 acc = window_sum<2 * r>(v);
+  constexpr bool SH = Warm<RAD>::kShared;
+  u64 acc = SH ? warm : window_sum<2 * r>(v);
   const float inv_i = iny * (1.0f / (float)(2 * r + 1));
 #pragma unroll
   for (int m = 0; m < K; m += 4) {
     if (!INTERIOR && gxo0 + m >= W) break;  // W % 4 == 0: a float4 is all in or out
     const float4 g4 = __ldg(reinterpret_cast<const float4*>(grow + m));
-    const ulonglong2 e0 = lds22(v + 2 * (m + 2 * r)), l0 = lds22(v + 2 * m);
-    const ulonglong2 e1 = lds22(v + 2 * (m + 2 + 2 * r)), l1 = lds22(v + 2 * (m + 2));
+    const ulonglong2 e0 = lds22(v + 2 * (m + 2 * r));
+    const ulonglong2 e1 = lds22(v + 2 * (m + 2 + 2 * r));
+    const ulonglong2 l0 = SH ? o.c[m / 2] : lds22(v + 2 * m);
+    const ulonglong2 l1 = SH ? o.c[m / 2 + 1] : lds22(v + 2 * (m + 2));
     u64 h[4];
     acc = add2(acc, e0.x); h[0] = acc; acc = sub2(acc, l0.x);
     acc = add2(acc, e0.y); h[1] = acc; acc = sub2(acc, l0.y);
@@ -444,7 +504,20 @@ __global__ void __launch_bounds__(NT, Geo<RAD>::min_blocks)
       if (k + NSTAGE < nb) prefetch(k + NSTAGE);  // into the stage X(k) just consumed
       {  // ---- H1(k): coefficient row base+jr, columns [qK, qK+K)
         const int i = base + jr;
-        if (k < nb && q * K < W2 && i < nrows) {
+        const bool task = k < nb && q * K < W2 && i < nrows;
+        const float* vA = vsA + jr * GG::PV + 2 * (q * K + GG::off);
+        const float* vB = vA + R * GG::PV;
+        Own oA, oB;
+        u64 wA = 0, wB = 0;
+        if constexpr (Warm<RAD>::kShared) {  // whole warp: shuffles
+          // runs q - nS + 1 .. q of this row may use this run's columns
+          const bool need = k < nb && q * K < W2 + (Warm<RAD>::nS - 1) * K;
+          oA = own_chunks(vA, need);
+          oB = own_chunks(vB, need);
+          wA = shared_warm<RAD>(vA, oA.sum, lane, task);
+          wB = shared_warm<RAD>(vB, oB.sum, lane, task);
+        }
+        if (task) {
           const int ya = ya0 + i;
           int s = s_cur + jr;
           if (s >= ringN) s -= ringN;
@@ -454,29 +527,36 @@ __global__ void __launch_bounds__(NT, Geo<RAD>::min_blocks)
             for (int m = 0; m < K; m += 2)
               *reinterpret_cast<float4*>(ra + 2 * m) = make_float4(0.f, 0.f, 0.f, 0.f);
           } else {
-            const float* vA = vsA + jr * GG::PV + 2 * (q * K + GG::off);
-            const float* vB = vA + R * GG::PV;
             const float iny = fast_rcp((float)wlen(ya, H, r));
             const int gxa0 = x0 - r + q * K;  // image column of the run's first coefficient
             if (gxa0 >= r && gxa0 + K - 1 + r <= W - 1 && q * K + K <= W2)
-              h1_run<RAD, true>(vA, vB, ra, iny, gxa0, W2 - q * K, W, eps, vmin);
+              h1_run<RAD, true>(vA, vB, ra, iny, gxa0, W2 - q * K, W, eps, vmin, wA, wB, oA, oB);
             else
-              h1_run<RAD, false>(vA, vB, ra, iny, gxa0, W2 - q * K, W, eps, vmin);
+              h1_run<RAD, false>(vA, vB, ra, iny, gxa0, W2 - q * K, W, eps, vmin, wA, wB, oA,
+                                 oB);
           }
         }
       }
       {  // ---- H2(k-1): output row of coefficient row base-R+jr, columns [qK, qK+K)
         const int yo = y0 - 2 * r + base - R + jr;
         const int gxo0 = x0 + q * K;
-        if (k >= 1 && q * K < tx && yo >= y0 && yo < yend && gxo0 < W) {
-          const float* v = vs2 + jr * GG::P2 + 2 * q * K;
+        const bool task = k >= 1 && q * K < tx && yo >= y0 && yo < yend && gxo0 < W;
+        const float* v = vs2 + jr * GG::P2 + 2 * q * K;
+        Own o;
+        u64 w = 0;
+        if constexpr (Warm<RAD>::kShared) {
+          const bool need = k >= 1 && q * K < tx + (Warm<RAD>::nS - 1) * K;
+          o = own_chunks(v, need);
+          w = shared_warm<RAD>(v, o.sum, lane, task);
+        }
+        if (task) {
           const float iny = fast_rcp((float)wlen(yo, H, r));
           const float* grow = G + (int64_t)yo * W + gxo0;
           float* orow = O + (int64_t)yo * W + gxo0;
           if (gxo0 >= r && gxo0 + K - 1 + r <= W - 1)
-            h2_run<RAD, true>(v, grow, orow, iny, gxo0, W, sG, sS, chk);
+            h2_run<RAD, true>(v, grow, orow, iny, gxo0, W, sG, sS, chk, w, o);
           else
-            h2_run<RAD, false>(v, grow, orow, iny, gxo0, W, sG, sS, chk);
+            h2_run<RAD, false>(v, grow, orow, iny, gxo0, W, sG, sS, chk, w, o);
         }
       }
       s_prev = s_cur;
