@@ -237,7 +237,7 @@ __device__ __forceinline__ void hrow(const float* __restrict__ row, const ColTap
 }
 
 template <int RAD>
-__global__ void __launch_bounds__(NT, 3) k_joint_fwd(FwdArgs a) {
+__global__ void __launch_bounds__(NT, (RAD >= 2 && RAD <= 4) ? 4 : 3) k_joint_fwd(FwdArgs a) {
   extern __shared__ float4 smem4[];
   constexpr int r = RAD;
   const SmemCoef sm = carve(reinterpret_cast<float*>(smem4), r);
@@ -332,7 +332,7 @@ __host__ __device__ inline size_t bwd_hr_smem_floats(int r) {
 }
 
 template <int RAD>
-__global__ void __launch_bounds__(NT, 3) k_joint_bwd_hr(BwdHrArgs a) {
+__global__ void __launch_bounds__(NT, 4) k_joint_bwd_hr(BwdHrArgs a) {
   extern __shared__ float4 smem4[];
   constexpr int r = RAD;
   float* base = reinterpret_cast<float*>(smem4);
