@@ -204,8 +204,32 @@ struct A {
                        nv = 2 * HID + CO + CO * HID;
 };
 
+// block reduce of NV float64 values given per thread by get(v) -> out[0..NV)
+template <int NV, class Get>
+__device__ void reduce_store_fn(Get get, double* out) {
+  __shared__ double red[NT / 32][NV];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int v = 0; v < NV; ++v) {
+    double a = (double)get(v);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+    if (lane == 0) red[warp][v] = a;
+  }
+  __syncthreads();
+  for (int v = threadIdx.x; v < NV; v += NT) {
+    double s = 0.0;
+#pragma unroll
+    for (int w = 0; w < NT / 32; ++w) s += red[w][v];
+    out[v] = s;
+  }
+  __syncthreads();
+}
+
+// Two threads (adjacent lanes) per 4-pixel group, each owning half of the
+// hidden units: half the per-thread accumulators, so two CTAs fit an SM.
 template <int HID>
-__global__ void __launch_bounds__(NT) k_bwd_a(const float* __restrict__ x,
+__global__ void __launch_bounds__(NT, 2) k_bwd_a(const float* __restrict__ x,
                                               const float* __restrict__ dy,
                                               const float* __restrict__ params,
                                               const float* __restrict__ fold,
@@ -220,52 +244,78 @@ __global__ void __launch_bounds__(NT) k_bwd_a(const float* __restrict__ x,
   for (int i = threadIdx.x; i < HID; i += NT) sbeta[i] = f[F<HID>::beta + i];
   for (int i = threadIdx.x; i < CO * HID; i += NT) sw2[i] = params[P<HID>::w2 + i];
   __syncthreads();
+  constexpr int JH = (HID + 1) / 2;  // hidden units per thread
+  const int half = threadIdx.x & 1;
+  const int j0 = half * JH;
   // fp32 per-thread sums (a few hundred pixels each), float64 across threads
-  constexpr int NV = A<HID>::nv;
-  float fa[NV];
+  float sd2[JH], sd2h1[JH], sdw2[CO][JH], sdy[CO];
 #pragma unroll
-  for (int v = 0; v < NV; ++v) fa[v] = 0.f;
+  for (int jj = 0; jj < JH; ++jj) {
+    sd2[jj] = sd2h1[jj] = 0.f;
+#pragma unroll
+    for (int o = 0; o < CO; ++o) sdw2[o][jj] = 0.f;
+  }
+#pragma unroll
+  for (int o = 0; o < CO; ++o) sdy[o] = 0.f;
   const int64_t n4 = HW / 4;
-  const int64_t stride = (int64_t)gridDim.x * NT;
-  {
-    for (int64_t i = (int64_t)blockIdx.x * NT + threadIdx.x; i < n4; i += stride) {
-      float xv[CI][4], gv[CO][4];
+  const int64_t stride = (int64_t)gridDim.x * (NT / 2);
+  for (int64_t i = (int64_t)blockIdx.x * (NT / 2) + (threadIdx.x >> 1); i < n4; i += stride) {
+    float xv[CI][4], gv[CO][4];
 #pragma unroll
-      for (int c = 0; c < CI; ++c) {
-        const float4 t = __ldg(reinterpret_cast<const float4*>(x + (b * CI + c) * HW) + i);
-        xv[c][0] = t.x; xv[c][1] = t.y; xv[c][2] = t.z; xv[c][3] = t.w;
-      }
+    for (int c = 0; c < CI; ++c) {
+      const float4 t = __ldg(reinterpret_cast<const float4*>(x + (b * CI + c) * HW) + i);
+      xv[c][0] = t.x; xv[c][1] = t.y; xv[c][2] = t.z; xv[c][3] = t.w;
+    }
 #pragma unroll
-      for (int o = 0; o < CO; ++o) {
-        const float4 t = __ldg(reinterpret_cast<const float4*>(dy + (b * CO + o) * HW) + i);
-        gv[o][0] = t.x; gv[o][1] = t.y; gv[o][2] = t.z; gv[o][3] = t.w;
+    for (int o = 0; o < CO; ++o) {
+      const float4 t = __ldg(reinterpret_cast<const float4*>(dy + (b * CO + o) * HW) + i);
+      gv[o][0] = t.x; gv[o][1] = t.y; gv[o][2] = t.z; gv[o][3] = t.w;
 #pragma unroll
-        for (int q = 0; q < 4; ++q) fa[A<HID>::dy + o] += gv[o][q];
-      }
+      for (int q = 0; q < 4; ++q) sdy[o] += gv[o][q];
+    }
 #pragma unroll
-      for (int j = 0; j < HID; ++j) {
+    for (int jj = 0; jj < JH; ++jj) {
+      const int j = j0 + jj;
+      if (j >= HID) break;  // odd HID: the second half has one unit fewer
+      const float a0 = sw1[j * CI], a1 = sw1[j * CI + 1], a2 = sw1[j * CI + 2];
+      const float f0 = sw1f[j * CI], f1 = sw1f[j * CI + 1], f2 = sw1f[j * CI + 2];
+      const float be = sbeta[j];
+      const float v0 = sw2[0 * HID + j], v1 = sw2[1 * HID + j], v2 = sw2[2 * HID + j];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const float h1 = fmaf(sw1[j * CI + 2], xv[2][q],
-                                fmaf(sw1[j * CI + 1], xv[1][q], sw1[j * CI] * xv[0][q]));
-          const float h2 = fmaf(sw1f[j * CI + 2], xv[2][q],
-                                fmaf(sw1f[j * CI + 1], xv[1][q],
-                                     fmaf(sw1f[j * CI], xv[0][q], sbeta[j])));
-          const bool pos = h2 >= 0.f;
-          const float h3 = pos ? h2 : kLeaky * h2;
-          const float d3 = fmaf(sw2[2 * HID + j], gv[2][q],
-                                fmaf(sw2[1 * HID + j], gv[1][q], sw2[0 * HID + j] * gv[0][q]));
-          const float d2 = pos ? d3 : kLeaky * d3;
-          fa[A<HID>::d2 + j] += d2;
-          fa[A<HID>::d2h1 + j] = fmaf(d2, h1, fa[A<HID>::d2h1 + j]);
+      for (int q = 0; q < 4; ++q) {
+        const float h1 = fmaf(a2, xv[2][q], fmaf(a1, xv[1][q], a0 * xv[0][q]));
+        const float h2 = fmaf(f2, xv[2][q], fmaf(f1, xv[1][q], fmaf(f0, xv[0][q], be)));
+        const bool pos = h2 >= 0.f;
+        const float h3 = pos ? h2 : kLeaky * h2;
+        const float d3 = fmaf(v2, gv[2][q], fmaf(v1, gv[1][q], v0 * gv[0][q]));
+        const float d2 = pos ? d3 : kLeaky * d3;
+        sd2[jj] += d2;
+        sd2h1[jj] = fmaf(d2, h1, sd2h1[jj]);
 #pragma unroll
-          for (int o = 0; o < CO; ++o)
-            fa[A<HID>::dw2 + o * HID + j] = fmaf(gv[o][q], h3, fa[A<HID>::dw2 + o * HID + j]);
-        }
+        for (int o = 0; o < CO; ++o) sdw2[o][jj] = fmaf(gv[o][q], h3, sdw2[o][jj]);
       }
     }
   }
-  reduce_store<NV>(fa, part + (b * gridDim.x + blockIdx.x) * NV);
+  // value v of the A layout from the thread that owns it (0 elsewhere)
+  auto get = [&](int v) -> float {
+    if (v >= A<HID>::dw2) {
+      const int u = v - A<HID>::dw2, o = u / HID, j = u - o * HID;
+      float r = 0.f;
+#pragma unroll
+      for (int jj = 0; jj < JH; ++jj)
+        if (j == j0 + jj) r = sdw2[o][jj];
+      return r;
+    }
+    if (v >= A<HID>::dy) return half == 0 ? sdy[v - A<HID>::dy] : 0.f;
+    const bool h1f = v >= A<HID>::d2h1;
+    const int j = h1f ? v - A<HID>::d2h1 : v;
+    float r = 0.f;
+#pragma unroll
+    for (int jj = 0; jj < JH; ++jj)
+      if (j == j0 + jj) r = h1f ? sd2h1[jj] : sd2[jj];
+    return r;
+  };
+  reduce_store_fn<A<HID>::nv>(get, part + (b * gridDim.x + blockIdx.x) * A<HID>::nv);
 }
 
 // ---- finalize A: per-image constants of dh1 and the W2/b2/gain/ng grads ----
@@ -314,8 +364,10 @@ __global__ void k_fin_a(const double* __restrict__ part, const float* __restrict
 }
 
 // ---- backward pass B: dx and dW1 partials ----------------------------------
+// Two threads (adjacent lanes) per 4-pixel group, each owning half of the
+// hidden units; their dx contributions are summed with one shuffle.
 template <int HID>
-__global__ void __launch_bounds__(NT) k_bwd_b(const float* __restrict__ x,
+__global__ void __launch_bounds__(NT, 2) k_bwd_b(const float* __restrict__ x,
                                               const float* __restrict__ dy,
                                               float* __restrict__ dx,
                                               const float* __restrict__ params,
@@ -338,54 +390,81 @@ __global__ void __launch_bounds__(NT) k_bwd_b(const float* __restrict__ x,
   }
   for (int i = threadIdx.x; i < CO * HID; i += NT) sw2[i] = params[P<HID>::w2 + i];
   __syncthreads();
-  constexpr int NV = HID * CI;
-  float fa[NV];
+  constexpr int JH = (HID + 1) / 2;
+  const int half = threadIdx.x & 1;
+  const int j0 = half * JH;
+  float fa[JH][CI];
 #pragma unroll
-  for (int v = 0; v < NV; ++v) fa[v] = 0.f;
+  for (int jj = 0; jj < JH; ++jj)
+#pragma unroll
+    for (int c = 0; c < CI; ++c) fa[jj][c] = 0.f;
   const int64_t n4 = HW / 4;
-  const int64_t stride = (int64_t)gridDim.x * NT;
-  {
-    for (int64_t i = (int64_t)blockIdx.x * NT + threadIdx.x; i < n4; i += stride) {
-      float xv[CI][4], gv[CO][4], dxv[CI][4];
+  const int64_t stride = (int64_t)gridDim.x * (NT / 2);
+  const int64_t first = (int64_t)blockIdx.x * (NT / 2);
+  // warp-uniform trip count: the dx shuffle below needs every lane
+  const int64_t iters = n4 > first ? (n4 - first + stride - 1) / stride : 0;
+  for (int64_t it = 0; it < iters; ++it) {
+    const int64_t i = first + it * stride + (threadIdx.x >> 1);
+    const bool valid = i < n4;  // a lane pair is valid or invalid together
+    float xv[CI][4], gv[CO][4], dxv[CI][4];
 #pragma unroll
-      for (int c = 0; c < CI; ++c) {
-        const float4 t = __ldg(reinterpret_cast<const float4*>(x + (b * CI + c) * HW) + i);
-        xv[c][0] = t.x; xv[c][1] = t.y; xv[c][2] = t.z; xv[c][3] = t.w;
+    for (int c = 0; c < CI; ++c) {
+      const float4 t = valid ? __ldg(reinterpret_cast<const float4*>(x + (b * CI + c) * HW) + i)
+                             : make_float4(0.f, 0.f, 0.f, 0.f);
+      xv[c][0] = t.x; xv[c][1] = t.y; xv[c][2] = t.z; xv[c][3] = t.w;
 #pragma unroll
-        for (int q = 0; q < 4; ++q) dxv[c][q] = 0.f;
+      for (int q = 0; q < 4; ++q) dxv[c][q] = 0.f;
+    }
+#pragma unroll
+    for (int o = 0; o < CO; ++o) {
+      const float4 t = valid ? __ldg(reinterpret_cast<const float4*>(dy + (b * CO + o) * HW) + i)
+                             : make_float4(0.f, 0.f, 0.f, 0.f);
+      gv[o][0] = t.x; gv[o][1] = t.y; gv[o][2] = t.z; gv[o][3] = t.w;
+    }
+#pragma unroll
+    for (int jj = 0; jj < JH; ++jj) {
+      const int j = j0 + jj;
+      if (j >= HID) break;
+      const float a0 = sw1[j * CI], a1 = sw1[j * CI + 1], a2 = sw1[j * CI + 2];
+      const float f0 = sw1f[j * CI], f1 = sw1f[j * CI + 1], f2 = sw1f[j * CI + 2];
+      const float be = sbeta[j], al = salpha[j], ka = skap[j], la = slam[j];
+      const float v0 = sw2[0 * HID + j], v1 = sw2[1 * HID + j], v2 = sw2[2 * HID + j];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const float h1 = fmaf(a2, xv[2][q], fmaf(a1, xv[1][q], a0 * xv[0][q]));
+        const float h2 = fmaf(f2, xv[2][q], fmaf(f1, xv[1][q], fmaf(f0, xv[0][q], be)));
+        const float d3 = fmaf(v2, gv[2][q], fmaf(v1, gv[1][q], v0 * gv[0][q]));
+        const float d2 = h2 >= 0.f ? d3 : kLeaky * d3;
+        const float dh = fmaf(al, d2, fmaf(la, h1, ka));
+        dxv[0][q] = fmaf(a0, dh, dxv[0][q]);
+        dxv[1][q] = fmaf(a1, dh, dxv[1][q]);
+        dxv[2][q] = fmaf(a2, dh, dxv[2][q]);
+#pragma unroll
+        for (int c = 0; c < CI; ++c) fa[jj][c] = fmaf(dh, xv[c][q], fa[jj][c]);
       }
+    }
 #pragma unroll
-      for (int o = 0; o < CO; ++o) {
-        const float4 t = __ldg(reinterpret_cast<const float4*>(dy + (b * CO + o) * HW) + i);
-        gv[o][0] = t.x; gv[o][1] = t.y; gv[o][2] = t.z; gv[o][3] = t.w;
-      }
+    for (int c = 0; c < CI; ++c)
 #pragma unroll
-      for (int j = 0; j < HID; ++j) {
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const float h1 = fmaf(sw1[j * CI + 2], xv[2][q],
-                                fmaf(sw1[j * CI + 1], xv[1][q], sw1[j * CI] * xv[0][q]));
-          const float h2 = fmaf(sw1f[j * CI + 2], xv[2][q],
-                                fmaf(sw1f[j * CI + 1], xv[1][q],
-                                     fmaf(sw1f[j * CI], xv[0][q], sbeta[j])));
-          const float d3 = fmaf(sw2[2 * HID + j], gv[2][q],
-                                fmaf(sw2[1 * HID + j], gv[1][q], sw2[0 * HID + j] * gv[0][q]));
-          const float d2 = h2 >= 0.f ? d3 : kLeaky * d3;
-          const float dh = fmaf(salpha[j], d2, fmaf(slam[j], h1, skap[j]));
-#pragma unroll
-          for (int c = 0; c < CI; ++c) {
-            dxv[c][q] = fmaf(sw1[j * CI + c], dh, dxv[c][q]);
-            fa[j * CI + c] = fmaf(dh, xv[c][q], fa[j * CI + c]);
-          }
-        }
-      }
+      for (int q = 0; q < 4; ++q) dxv[c][q] += __shfl_xor_sync(0xffffffffu, dxv[c][q], 1);
+    if (valid && half == 0) {
 #pragma unroll
       for (int c = 0; c < CI; ++c)
         reinterpret_cast<float4*>(dx + (b * CI + c) * HW)[i] =
             make_float4(dxv[c][0], dxv[c][1], dxv[c][2], dxv[c][3]);
     }
   }
-  reduce_store<NV>(fa, part + (b * gridDim.x + blockIdx.x) * NV);
+  auto get = [&](int v) -> float {
+    const int j = v / CI, c = v - j * CI;
+    float r = 0.f;
+#pragma unroll
+    for (int jj = 0; jj < JH; ++jj)
+#pragma unroll
+      for (int cc = 0; cc < CI; ++cc)
+        if (j == j0 + jj && c == cc) r = fa[jj][cc];
+    return r;
+  };
+  reduce_store_fn<HID * CI>(get, part + (b * gridDim.x + blockIdx.x) * (HID * CI));
 }
 
 // ---- per-image dW1 sums of the pass-B partials (fixed block order) --------
