@@ -100,17 +100,30 @@ __device__ void lr_coeffs(const float* __restrict__ X, const float* __restrict__
   const int sy_ = min(max(i0, 0), h - 1), sx_ = min(max(k0, 0), w - 1);
   const float sx = __ldg(X + (int64_t)sy_ * w + sx_);
   const float sy = __ldg(Y + (int64_t)sy_ * w + sx_);
-  // 1) stage inputs (zero outside the image: clamped windows)
-  for (int idx = tid; idx < RI * CI; idx += NT) {
-    const int row = idx / CI, col = idx - row * CI;
-    const int gy = i0 - 1 - r + row, gx = k0 - 1 - r + col;
-    float xv = 0.f, yv = 0.f;
-    if (gy >= 0 && gy < h && gx >= 0 && gx < w) {
-      xv = __ldg(X + (int64_t)gy * w + gx) - sx;
-      yv = __ldg(Y + (int64_t)gy * w + gx) - sy;
+  // 1) stage inputs (zero outside the image: clamped windows); every load of
+  //    the block is issued before the first store, so the CTA waits for one
+  //    memory latency, not one per element
+  {
+    constexpr int RIc = RA + 2 * r, CIc = CA + 2 * r;
+    constexpr int NE = (RIc * CIc + NT - 1) / NT;
+    float xv[NE], yv[NE];
+#pragma unroll
+    for (int e = 0; e < NE; ++e) {
+      const int idx = tid + e * NT;
+      const int row = idx / CIc, col = idx - row * CIc;
+      const int gy = i0 - 1 - r + row, gx = k0 - 1 - r + col;
+      const bool ok = idx < RIc * CIc && gy >= 0 && gy < h && gx >= 0 && gx < w;
+      xv[e] = ok ? __ldg(X + (int64_t)gy * w + gx) - sx : 0.f;
+      yv[e] = ok ? __ldg(Y + (int64_t)gy * w + gx) - sy : 0.f;
     }
-    sm.xs[idx] = xv;
-    sm.ys[idx] = yv;
+#pragma unroll
+    for (int e = 0; e < NE; ++e) {
+      const int idx = tid + e * NT;
+      if (idx < RIc * CIc) {
+        sm.xs[idx] = xv[e];
+        sm.ys[idx] = yv[e];
+      }
+    }
   }
   __syncthreads();
   // 2) vertical sliding sums: item = (column, chunk of rows)
@@ -504,16 +517,27 @@ __global__ void __launch_bounds__(NT) k_joint_bwd_lr(BwdLrArgs a) {
   const float sx = __ldg(X + (int64_t)sy_ * w + sx_);
   const float sy = __ldg(Yp + (int64_t)sy_ * w + sx_);
   // inputs over [i0-2r, i0+TL+2r)^2, shifted, zero outside the image
-  for (int idx = tid; idx < NI * NI; idx += NT) {
-    const int row = idx / NI, col = idx - row * NI;
-    const int gy = i0 - 2 * r + row, gx = k0 - 2 * r + col;
-    float xv = 0.f, yv = 0.f;
-    if (gy >= 0 && gy < h && gx >= 0 && gx < w) {
-      xv = __ldg(X + (int64_t)gy * w + gx) - sx;
-      yv = __ldg(Yp + (int64_t)gy * w + gx) - sy;
+  {  // all loads in flight before the first store (one latency per block)
+    constexpr int NIc = TL + 4 * r;
+    constexpr int NE = (NIc * NIc + NT - 1) / NT;
+    float xv[NE], yv[NE];
+#pragma unroll
+    for (int e = 0; e < NE; ++e) {
+      const int idx = tid + e * NT;
+      const int row = idx / NIc, col = idx - row * NIc;
+      const int gy = i0 - 2 * r + row, gx = k0 - 2 * r + col;
+      const bool ok = idx < NIc * NIc && gy >= 0 && gy < h && gx >= 0 && gx < w;
+      xv[e] = ok ? __ldg(X + (int64_t)gy * w + gx) - sx : 0.f;
+      yv[e] = ok ? __ldg(Yp + (int64_t)gy * w + gx) - sy : 0.f;
     }
-    xs[idx] = xv;
-    ys[idx] = yv;
+#pragma unroll
+    for (int e = 0; e < NE; ++e) {
+      const int idx = tid + e * NT;
+      if (idx < NIc * NIc) {
+        xs[idx] = xv[e];
+        ys[idx] = yv[e];
+      }
+    }
   }
   __syncthreads();
   // vertical sums for moment rows m in [0, NM) (global i0 - r + m): input rows [m, m+2r]
