@@ -422,6 +422,7 @@ __global__ void __launch_bounds__(NT, 4) k_joint_bwd_hr(BwdHrArgs a) {
       }
     }
     const bool left = 4 * k - 4 >= 0, right = 4 * k + 4 < a.W;
+#pragma unroll 2
     for (int yl = warp; yl < GR; yl += NT / 32) {
       const int Y = 4 * i0 - 2 + yl;
       float s1 = 0.f, s2 = 0.f;
