@@ -267,8 +267,12 @@ static int check_highres(int dtype, int64_t B, int64_t Cg, int64_t C, int64_t H,
 
 size_t gf_highres_workspace_bytes(int dtype, int64_t B, int64_t Cg, int64_t C, int64_t H,
                                   int64_t W, int radius) {
-  (void)Cg;
-  return gfb::generic_workspace_bytes(B * C * H * W, 0);
+  size_t gen = gfb::generic_workspace_bytes(B * C * H * W, 0);
+  if (dtype == GF_F32 && gfb::fused_highres_bwd_ok(B, Cg, C, H, W, radius)) {
+    size_t fast = gfb::fused_highres_bwd_ws_bytes(B, Cg, C, H, W);
+    return fast > gen ? fast : gen;
+  }
+  return gen;
 }
 
 static size_t highres_fwd_need(int dtype, int64_t B, int64_t Cg, int64_t C, int64_t H, int64_t W,
@@ -307,6 +311,12 @@ int gf_highres_bwd(int dtype, const void* guide, const void* src, const void* d_
   size_t need = gf_highres_workspace_bytes(dtype, B, Cg, C, H, W, radius);
   if (workspace_bytes < need)
     return fail(GF_ERR_WORKSPACE, "highres workspace %zu < %zu bytes", workspace_bytes, need);
+  if (!g_force_generic && dtype == GF_F32 && gfb::fused_highres_bwd_ok(B, Cg, C, H, W, radius)) {
+    gfb::fused_highres_bwd((const float*)guide, (const float*)src, (const float*)d_out,
+                           (float*)d_guide, (float*)d_src, B, Cg, C, H, W, radius, (float)eps,
+                           workspace, status, S(stream));
+    return check_launch("gf_highres_bwd[fused]");
+  }
   if (dtype == GF_F32)
     gfb::generic_highres_bwd<float>((const float*)guide, (const float*)src, (const float*)d_out,
                                      (float*)d_guide, (float*)d_src, B, Cg, C, H, W, radius, eps,

@@ -105,6 +105,13 @@ template <typename T>
 void adam_impl(T* p, const T* g, T* m, T* v, int64_t n, int step, double lr, double b1, double b2,
                double eps, uint32_t* status, cudaStream_t s);
 
+// full-resolution backward, fp32 streaming window sums (gf_fused_highres_bwd.cu)
+bool fused_highres_bwd_ok(int64_t B, int64_t Cg, int64_t C, int64_t H, int64_t W, int r);
+size_t fused_highres_bwd_ws_bytes(int64_t B, int64_t Cg, int64_t C, int64_t H, int64_t W);
+void fused_highres_bwd(const float* guide, const float* src, const float* d_out, float* d_guide,
+                       float* d_src, int64_t B, int64_t Cg, int64_t C, int64_t H, int64_t W, int r,
+                       float eps, void* ws, uint32_t* status, cudaStream_t s);
+
 // argument checks / error text of the C ABI (gf_capi.cu), for gf_host.cu
 int api_check_highres(int dtype, int64_t B, int64_t Cg, int64_t C, int64_t H, int64_t W, int r,
                       double eps);

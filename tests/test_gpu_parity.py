@@ -512,3 +512,32 @@ def test_fused_guidance_net_vs_oracle(gfb, hidden):
         lib.gf_force_generic(old)
     assert abs_max(npy(y2), npy(y)) <= 1e-5
     assert rel_max(npy(dx2), npy(dx)) <= GRAD_TOL32
+
+
+@pytest.mark.parametrize("H,W,r,cg", [(77, 132, 1, 1), (77, 132, 3, 3), (300, 260, 8, 1),
+                                      (40, 36, 16, 3), (5, 8, 2, 1), (90, 70, 20, 1),
+                                      (513, 520, 8, 3)])
+def test_fused_highres_backward_vs_oracle(gfb, H, W, r, cg):
+    """fp32 streaming backward (gf_fused_highres_bwd.cu) against the oracle and
+    against the general float64-intermediate kernels."""
+    from paper_1803_05619_b200 import _lib
+
+    rng = np.random.default_rng(H + 3 * W + r)
+    guide = rng.uniform(0, 1, (2, cg, H, W)).astype(np.float32)
+    src = rng.uniform(0, 1, (2, 3, H, W)).astype(np.float32)
+    d = rng.standard_normal((2, 3, H, W)).astype(np.float32)
+    p = gfb.GuidedFilterParams(r, 1e-2)
+    out, tape = gfb.forward_highres(t32(guide), t32(src), p)
+    g = gfb.backward(tape, t32(d))
+    dg_want, ds_want = O.highres_backward_nchw(guide, src, d, r, 1e-2)
+    assert rel_max(npy(g.d_src), ds_want) <= GRAD_TOL32
+    assert rel_max(npy(g.d_guide_hi), dg_want) <= GRAD_TOL32
+    lib = _lib.load()
+    old = lib.gf_force_generic(1)
+    try:
+        out2, tape2 = gfb.forward_highres(t32(guide), t32(src), p)
+        g2 = gfb.backward(tape2, t32(d))
+    finally:
+        lib.gf_force_generic(old)
+    assert rel_max(npy(g.d_src), npy(g2.d_src)) <= GRAD_TOL32
+    assert rel_max(npy(g.d_guide_hi), npy(g2.d_guide_hi)) <= GRAD_TOL32
