@@ -19,6 +19,7 @@
 
 #include "gf_common.cuh"
 #include "gf_internal.h"
+#include "gf_pair.cuh"
 
 namespace gfb {
 namespace gnf {
@@ -163,35 +164,34 @@ __global__ void __launch_bounds__(NT) k_fwd(const float* __restrict__ x, float* 
   for (int i = threadIdx.x; i < CO; i += NT) sb2[i] = params[P<HID>::b2 + i];
   __syncthreads();
   const int64_t n4 = HW / 4;
+  using namespace pr;
   for (int64_t i = (int64_t)blockIdx.x * NT + threadIdx.x; i < n4; i += (int64_t)gridDim.x * NT) {
-    float xv[CI][4];
+    ulonglong2 X[CI];  // pixel pairs (0,1), (2,3) of each channel
 #pragma unroll
-    for (int c = 0; c < CI; ++c) {
-      const float4 t = __ldg(reinterpret_cast<const float4*>(x + (b * CI + c) * HW) + i);
-      xv[c][0] = t.x; xv[c][1] = t.y; xv[c][2] = t.z; xv[c][3] = t.w;
-    }
-    float out[CO][4];
+    for (int c = 0; c < CI; ++c)
+      X[c] = __ldg(reinterpret_cast<const ulonglong2*>(x + (b * CI + c) * HW) + i);
+    u64 out[CO][2];
 #pragma unroll
-    for (int o = 0; o < CO; ++o)
-#pragma unroll
-      for (int q = 0; q < 4; ++q) out[o][q] = sb2[o];
+    for (int o = 0; o < CO; ++o) out[o][0] = out[o][1] = bc(sb2[o]);
 #pragma unroll
     for (int j = 0; j < HID; ++j) {
-      const float w0 = sw1[j * CI], w1 = sw1[j * CI + 1], w2 = sw1[j * CI + 2], be = sbeta[j];
-      const float v0 = sw2[0 * HID + j], v1 = sw2[1 * HID + j], v2 = sw2[2 * HID + j];
+      const u64 w0 = bc(sw1[j * CI]), w1 = bc(sw1[j * CI + 1]), w2 = bc(sw1[j * CI + 2]);
+      const u64 be = bc(sbeta[j]);
+      const u64 v0 = bc(sw2[0 * HID + j]), v1 = bc(sw2[1 * HID + j]), v2 = bc(sw2[2 * HID + j]);
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        float h = fmaf(w2, xv[2][q], fmaf(w1, xv[1][q], fmaf(w0, xv[0][q], be)));
-        h = fmaxf(h, kLeaky * h);  // leaky ReLU 0.2 (gf/guidance.py:36-39)
-        out[0][q] = fmaf(v0, h, out[0][q]);
-        out[1][q] = fmaf(v1, h, out[1][q]);
-        out[2][q] = fmaf(v2, h, out[2][q]);
+      for (int pp = 0; pp < 2; ++pp) {
+        const u64 x0 = pp ? X[0].y : X[0].x, x1 = pp ? X[1].y : X[1].x,
+                  x2 = pp ? X[2].y : X[2].x;
+        u64 h = fma2(w2, x2, fma2(w1, x1, fma2(w0, x0, be)));
+        h = mul2(h, slope2(h, kLeaky));  // leaky ReLU 0.2 (gf/guidance.py:36-39)
+        out[0][pp] = fma2(v0, h, out[0][pp]);
+        out[1][pp] = fma2(v1, h, out[1][pp]);
+        out[2][pp] = fma2(v2, h, out[2][pp]);
       }
     }
 #pragma unroll
     for (int o = 0; o < CO; ++o)
-      reinterpret_cast<float4*>(y + (b * CO + o) * HW)[i] =
-          make_float4(out[o][0], out[o][1], out[o][2], out[o][3]);
+      reinterpret_cast<ulonglong2*>(y + (b * CO + o) * HW)[i] = make_ulonglong2(out[o][0], out[o][1]);
   }
 }
 
@@ -245,74 +245,77 @@ __global__ void __launch_bounds__(NT, 2) k_bwd_a(const float* __restrict__ x,
   for (int i = threadIdx.x; i < CO * HID; i += NT) sw2[i] = params[P<HID>::w2 + i];
   __syncthreads();
   constexpr int JH = (HID + 1) / 2;  // hidden units per thread
+  using namespace pr;
   const int half = threadIdx.x & 1;
   const int j0 = half * JH;
-  // fp32 per-thread sums (a few hundred pixels each), float64 across threads
-  float sd2[JH], sd2h1[JH], sdw2[CO][JH], sdy[CO];
+  // fp32 per-thread sums on pixel pairs (a few hundred pixels each), float64
+  // across threads
+  u64 sd2[JH], sd2h1[JH], sdw2[CO][JH], sdy[CO];
 #pragma unroll
   for (int jj = 0; jj < JH; ++jj) {
-    sd2[jj] = sd2h1[jj] = 0.f;
+    sd2[jj] = sd2h1[jj] = 0ull;
 #pragma unroll
-    for (int o = 0; o < CO; ++o) sdw2[o][jj] = 0.f;
+    for (int o = 0; o < CO; ++o) sdw2[o][jj] = 0ull;
   }
 #pragma unroll
-  for (int o = 0; o < CO; ++o) sdy[o] = 0.f;
+  for (int o = 0; o < CO; ++o) sdy[o] = 0ull;
   const int64_t n4 = HW / 4;
   const int64_t stride = (int64_t)gridDim.x * (NT / 2);
   for (int64_t i = (int64_t)blockIdx.x * (NT / 2) + (threadIdx.x >> 1); i < n4; i += stride) {
-    float xv[CI][4], gv[CO][4];
+    ulonglong2 X[CI], G[CO];
 #pragma unroll
-    for (int c = 0; c < CI; ++c) {
-      const float4 t = __ldg(reinterpret_cast<const float4*>(x + (b * CI + c) * HW) + i);
-      xv[c][0] = t.x; xv[c][1] = t.y; xv[c][2] = t.z; xv[c][3] = t.w;
-    }
+    for (int c = 0; c < CI; ++c)
+      X[c] = __ldg(reinterpret_cast<const ulonglong2*>(x + (b * CI + c) * HW) + i);
 #pragma unroll
     for (int o = 0; o < CO; ++o) {
-      const float4 t = __ldg(reinterpret_cast<const float4*>(dy + (b * CO + o) * HW) + i);
-      gv[o][0] = t.x; gv[o][1] = t.y; gv[o][2] = t.z; gv[o][3] = t.w;
-#pragma unroll
-      for (int q = 0; q < 4; ++q) sdy[o] += gv[o][q];
+      G[o] = __ldg(reinterpret_cast<const ulonglong2*>(dy + (b * CO + o) * HW) + i);
+      sdy[o] = add2(sdy[o], add2(G[o].x, G[o].y));
     }
 #pragma unroll
     for (int jj = 0; jj < JH; ++jj) {
       const int j = j0 + jj;
       if (j >= HID) break;  // odd HID: the second half has one unit fewer
-      const float a0 = sw1[j * CI], a1 = sw1[j * CI + 1], a2 = sw1[j * CI + 2];
-      const float f0 = sw1f[j * CI], f1 = sw1f[j * CI + 1], f2 = sw1f[j * CI + 2];
-      const float be = sbeta[j];
-      const float v0 = sw2[0 * HID + j], v1 = sw2[1 * HID + j], v2 = sw2[2 * HID + j];
+      const u64 a0 = bc(sw1[j * CI]), a1 = bc(sw1[j * CI + 1]), a2 = bc(sw1[j * CI + 2]);
+      const u64 f0 = bc(sw1f[j * CI]), f1 = bc(sw1f[j * CI + 1]), f2 = bc(sw1f[j * CI + 2]);
+      const u64 be = bc(sbeta[j]);
+      const u64 v0 = bc(sw2[0 * HID + j]), v1 = bc(sw2[1 * HID + j]), v2 = bc(sw2[2 * HID + j]);
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const float h1 = fmaf(a2, xv[2][q], fmaf(a1, xv[1][q], a0 * xv[0][q]));
-        const float h2 = fmaf(f2, xv[2][q], fmaf(f1, xv[1][q], fmaf(f0, xv[0][q], be)));
-        const bool pos = h2 >= 0.f;
-        const float h3 = pos ? h2 : kLeaky * h2;
-        const float d3 = fmaf(v2, gv[2][q], fmaf(v1, gv[1][q], v0 * gv[0][q]));
-        const float d2 = pos ? d3 : kLeaky * d3;
-        sd2[jj] += d2;
-        sd2h1[jj] = fmaf(d2, h1, sd2h1[jj]);
-#pragma unroll
-        for (int o = 0; o < CO; ++o) sdw2[o][jj] = fmaf(gv[o][q], h3, sdw2[o][jj]);
+      for (int pp = 0; pp < 2; ++pp) {
+        const u64 x0 = pp ? X[0].y : X[0].x, x1 = pp ? X[1].y : X[1].x,
+                  x2 = pp ? X[2].y : X[2].x;
+        const u64 g0 = pp ? G[0].y : G[0].x, g1 = pp ? G[1].y : G[1].x,
+                  g2 = pp ? G[2].y : G[2].x;
+        const u64 h1 = fma2(a2, x2, fma2(a1, x1, mul2(a0, x0)));
+        const u64 h2 = fma2(f2, x2, fma2(f1, x1, fma2(f0, x0, be)));
+        const u64 sl = slope2(h2, kLeaky);
+        const u64 h3 = mul2(h2, sl);
+        const u64 d2 = mul2(fma2(v2, g2, fma2(v1, g1, mul2(v0, g0))), sl);
+        sd2[jj] = add2(sd2[jj], d2);
+        sd2h1[jj] = fma2(d2, h1, sd2h1[jj]);
+        sdw2[0][jj] = fma2(g0, h3, sdw2[0][jj]);
+        sdw2[1][jj] = fma2(g1, h3, sdw2[1][jj]);
+        sdw2[2][jj] = fma2(g2, h3, sdw2[2][jj]);
       }
     }
   }
   // value v of the A layout from the thread that owns it (0 elsewhere)
+  auto sum2 = [](u64 p) { return lo(p) + hi(p); };
   auto get = [&](int v) -> float {
     if (v >= A<HID>::dw2) {
       const int u = v - A<HID>::dw2, o = u / HID, j = u - o * HID;
       float r = 0.f;
 #pragma unroll
       for (int jj = 0; jj < JH; ++jj)
-        if (j == j0 + jj) r = sdw2[o][jj];
+        if (j == j0 + jj) r = sum2(sdw2[o][jj]);
       return r;
     }
-    if (v >= A<HID>::dy) return half == 0 ? sdy[v - A<HID>::dy] : 0.f;
+    if (v >= A<HID>::dy) return half == 0 ? sum2(sdy[v - A<HID>::dy]) : 0.f;
     const bool h1f = v >= A<HID>::d2h1;
     const int j = h1f ? v - A<HID>::d2h1 : v;
     float r = 0.f;
 #pragma unroll
     for (int jj = 0; jj < JH; ++jj)
-      if (j == j0 + jj) r = h1f ? sd2h1[jj] : sd2[jj];
+      if (j == j0 + jj) r = sum2(h1f ? sd2h1[jj] : sd2[jj]);
     return r;
   };
   reduce_store_fn<A<HID>::nv>(get, part + (b * gridDim.x + blockIdx.x) * A<HID>::nv);
@@ -391,13 +394,14 @@ __global__ void __launch_bounds__(NT, 2) k_bwd_b(const float* __restrict__ x,
   for (int i = threadIdx.x; i < CO * HID; i += NT) sw2[i] = params[P<HID>::w2 + i];
   __syncthreads();
   constexpr int JH = (HID + 1) / 2;
+  using namespace pr;
   const int half = threadIdx.x & 1;
   const int j0 = half * JH;
-  float fa[JH][CI];
+  u64 fa[JH][CI];  // dW1 partials on pixel pairs
 #pragma unroll
   for (int jj = 0; jj < JH; ++jj)
 #pragma unroll
-    for (int c = 0; c < CI; ++c) fa[jj][c] = 0.f;
+    for (int c = 0; c < CI; ++c) fa[jj][c] = 0ull;
   const int64_t n4 = HW / 4;
   const int64_t stride = (int64_t)gridDim.x * (NT / 2);
   const int64_t first = (int64_t)blockIdx.x * (NT / 2);
@@ -406,52 +410,54 @@ __global__ void __launch_bounds__(NT, 2) k_bwd_b(const float* __restrict__ x,
   for (int64_t it = 0; it < iters; ++it) {
     const int64_t i = first + it * stride + (threadIdx.x >> 1);
     const bool valid = i < n4;  // a lane pair is valid or invalid together
-    float xv[CI][4], gv[CO][4], dxv[CI][4];
+    ulonglong2 X[CI], G[CO];
+    u64 dxv[CI][2];
 #pragma unroll
     for (int c = 0; c < CI; ++c) {
-      const float4 t = valid ? __ldg(reinterpret_cast<const float4*>(x + (b * CI + c) * HW) + i)
-                             : make_float4(0.f, 0.f, 0.f, 0.f);
-      xv[c][0] = t.x; xv[c][1] = t.y; xv[c][2] = t.z; xv[c][3] = t.w;
-#pragma unroll
-      for (int q = 0; q < 4; ++q) dxv[c][q] = 0.f;
+      X[c] = valid ? __ldg(reinterpret_cast<const ulonglong2*>(x + (b * CI + c) * HW) + i)
+                   : make_ulonglong2(0ull, 0ull);
+      dxv[c][0] = dxv[c][1] = 0ull;
     }
 #pragma unroll
-    for (int o = 0; o < CO; ++o) {
-      const float4 t = valid ? __ldg(reinterpret_cast<const float4*>(dy + (b * CO + o) * HW) + i)
-                             : make_float4(0.f, 0.f, 0.f, 0.f);
-      gv[o][0] = t.x; gv[o][1] = t.y; gv[o][2] = t.z; gv[o][3] = t.w;
-    }
+    for (int o = 0; o < CO; ++o)
+      G[o] = valid ? __ldg(reinterpret_cast<const ulonglong2*>(dy + (b * CO + o) * HW) + i)
+                   : make_ulonglong2(0ull, 0ull);
 #pragma unroll
     for (int jj = 0; jj < JH; ++jj) {
       const int j = j0 + jj;
       if (j >= HID) break;
-      const float a0 = sw1[j * CI], a1 = sw1[j * CI + 1], a2 = sw1[j * CI + 2];
-      const float f0 = sw1f[j * CI], f1 = sw1f[j * CI + 1], f2 = sw1f[j * CI + 2];
-      const float be = sbeta[j], al = salpha[j], ka = skap[j], la = slam[j];
-      const float v0 = sw2[0 * HID + j], v1 = sw2[1 * HID + j], v2 = sw2[2 * HID + j];
+      const u64 a0 = bc(sw1[j * CI]), a1 = bc(sw1[j * CI + 1]), a2 = bc(sw1[j * CI + 2]);
+      const u64 f0 = bc(sw1f[j * CI]), f1 = bc(sw1f[j * CI + 1]), f2 = bc(sw1f[j * CI + 2]);
+      const u64 be = bc(sbeta[j]), al = bc(salpha[j]), ka = bc(skap[j]), la = bc(slam[j]);
+      const u64 v0 = bc(sw2[0 * HID + j]), v1 = bc(sw2[1 * HID + j]), v2 = bc(sw2[2 * HID + j]);
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const float h1 = fmaf(a2, xv[2][q], fmaf(a1, xv[1][q], a0 * xv[0][q]));
-        const float h2 = fmaf(f2, xv[2][q], fmaf(f1, xv[1][q], fmaf(f0, xv[0][q], be)));
-        const float d3 = fmaf(v2, gv[2][q], fmaf(v1, gv[1][q], v0 * gv[0][q]));
-        const float d2 = h2 >= 0.f ? d3 : kLeaky * d3;
-        const float dh = fmaf(al, d2, fmaf(la, h1, ka));
-        dxv[0][q] = fmaf(a0, dh, dxv[0][q]);
-        dxv[1][q] = fmaf(a1, dh, dxv[1][q]);
-        dxv[2][q] = fmaf(a2, dh, dxv[2][q]);
-#pragma unroll
-        for (int c = 0; c < CI; ++c) fa[jj][c] = fmaf(dh, xv[c][q], fa[jj][c]);
+      for (int pp = 0; pp < 2; ++pp) {
+        const u64 x0 = pp ? X[0].y : X[0].x, x1 = pp ? X[1].y : X[1].x,
+                  x2 = pp ? X[2].y : X[2].x;
+        const u64 g0 = pp ? G[0].y : G[0].x, g1 = pp ? G[1].y : G[1].x,
+                  g2 = pp ? G[2].y : G[2].x;
+        const u64 h1 = fma2(a2, x2, fma2(a1, x1, mul2(a0, x0)));
+        const u64 h2 = fma2(f2, x2, fma2(f1, x1, fma2(f0, x0, be)));
+        const u64 d2 = mul2(fma2(v2, g2, fma2(v1, g1, mul2(v0, g0))), slope2(h2, kLeaky));
+        const u64 dh = fma2(al, d2, fma2(la, h1, ka));
+        dxv[0][pp] = fma2(a0, dh, dxv[0][pp]);
+        dxv[1][pp] = fma2(a1, dh, dxv[1][pp]);
+        dxv[2][pp] = fma2(a2, dh, dxv[2][pp]);
+        fa[jj][0] = fma2(dh, x0, fa[jj][0]);
+        fa[jj][1] = fma2(dh, x1, fa[jj][1]);
+        fa[jj][2] = fma2(dh, x2, fa[jj][2]);
       }
     }
 #pragma unroll
     for (int c = 0; c < CI; ++c)
 #pragma unroll
-      for (int q = 0; q < 4; ++q) dxv[c][q] += __shfl_xor_sync(0xffffffffu, dxv[c][q], 1);
+      for (int pp = 0; pp < 2; ++pp)
+        dxv[c][pp] = add2(dxv[c][pp], __shfl_xor_sync(0xffffffffu, dxv[c][pp], 1));
     if (valid && half == 0) {
 #pragma unroll
       for (int c = 0; c < CI; ++c)
-        reinterpret_cast<float4*>(dx + (b * CI + c) * HW)[i] =
-            make_float4(dxv[c][0], dxv[c][1], dxv[c][2], dxv[c][3]);
+        reinterpret_cast<ulonglong2*>(dx + (b * CI + c) * HW)[i] =
+            make_ulonglong2(dxv[c][0], dxv[c][1]);
     }
   }
   auto get = [&](int v) -> float {
@@ -461,7 +467,7 @@ __global__ void __launch_bounds__(NT, 2) k_bwd_b(const float* __restrict__ x,
     for (int jj = 0; jj < JH; ++jj)
 #pragma unroll
       for (int cc = 0; cc < CI; ++cc)
-        if (j == j0 + jj && c == cc) r = fa[jj][cc];
+        if (j == j0 + jj && c == cc) r = pr::lo(fa[jj][cc]) + pr::hi(fa[jj][cc]);
     return r;
   };
   reduce_store_fn<HID * CI>(get, part + (b * gridDim.x + blockIdx.x) * (HID * CI));
