@@ -292,6 +292,31 @@ __global__ void __launch_bounds__(NT, (RAD >= 2 && RAD <= 4) ? 4 : 3) k_joint_fw
   }
   bool bad = false;
   const int slo_base = i0 - 1 + 2 * warp;  // global lr row of HA[0]
+  if (Yb >= 2 && Yb + 7 <= 4 * a.h - 3 && Yb + 7 < a.H) {
+    // interior rows (warp-uniform): unclamped taps, static phase weights
+    // f = (2*phase + 5)/8 mod 1 of the half-pixel map (exact in fp32)
+    if (col_ok) {
+      float chk = 0.f;
+#pragma unroll
+      for (int t = 0; t < 8; ++t) {
+        const int q0 = t / 4 + ((t & 3) >= 2 ? 1 : 0);
+        constexpr float fph[4] = {0.625f, 0.875f, 0.125f, 0.375f};
+        const float f = fph[t & 3];
+        const float gv[4] = {g[t].x, g[t].y, g[t].z, g[t].w};
+        float o[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const float Ah = HA[q0][j] + f * (HA[q0 + 1][j] - HA[q0][j]);
+          const float Bh = HB[q0][j] + f * (HB[q0 + 1][j] - HB[q0][j]);
+          o[j] = Bh + Ah * gv[j];
+          chk += o[j] - o[j];  // NaN iff an output is not finite
+        }
+        *reinterpret_cast<float4*>(O + (int64_t)(Yb + t) * a.W + X0) =
+            make_float4(o[0], o[1], o[2], o[3]);
+      }
+      bad = chk != 0.f;
+    }
+  } else {
 #pragma unroll
   for (int t = 0; t < 8; ++t) {
     const int Y = Yb + t;
@@ -317,6 +342,7 @@ __global__ void __launch_bounds__(NT, (RAD >= 2 && RAD <= 4) ? 4 : 3) k_joint_fw
       if (!isfinite(o[j])) bad = true;
     }
     *reinterpret_cast<float4*>(O + (int64_t)Y * a.W + X0) = make_float4(o[0], o[1], o[2], o[3]);
+  }
   }
   if (degen) flag(a.status, GF_STATUS_DEGENERATE);
   if (bad) flag(a.status, GF_STATUS_NONFINITE_OUTPUT);
@@ -388,6 +414,22 @@ __global__ void __launch_bounds__(NT, 4) k_joint_bwd_hr(BwdHrArgs a) {
       }
     }
     const int slo_base = i0 - 1 + 2 * warp;
+    if (Yb >= 2 && Yb + 7 <= 4 * a.h - 3 && Yb + 7 < a.H) {  // interior rows: static taps
+      if (col_ok) {
+#pragma unroll
+        for (int t = 0; t < 8; ++t) {
+          const int q0 = t / 4 + ((t & 3) >= 2 ? 1 : 0);
+          constexpr float fph[4] = {0.625f, 0.875f, 0.125f, 0.375f};
+          const float f = fph[t & 3];
+          const float dd[4] = {dv[t].x, dv[t].y, dv[t].z, dv[t].w};
+          float o[4];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) o[j] = dd[j] * (HA[q0][j] + f * (HA[q0 + 1][j] - HA[q0][j]));
+          *reinterpret_cast<float4*>(DH + (int64_t)(Yb + t) * a.W + X0) =
+              make_float4(o[0], o[1], o[2], o[3]);
+        }
+      }
+    } else {
 #pragma unroll
     for (int t = 0; t < 8; ++t) {
       const int Y = Yb + t;
@@ -404,6 +446,7 @@ __global__ void __launch_bounds__(NT, 4) k_joint_bwd_hr(BwdHrArgs a) {
         o[j] = dd[j] * (alo + ty.f * (ahi - alo));
       }
       *reinterpret_cast<float4*>(DH + (int64_t)Y * a.W + X0) = make_float4(o[0], o[1], o[2], o[3]);
+    }
     }
   }
   // row partials of the adjoint: R[y][k] = sum_X wx(X, k) * (d, d*G) over
