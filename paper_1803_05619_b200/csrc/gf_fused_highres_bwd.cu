@@ -84,21 +84,27 @@ __global__ void __launch_bounds__(NT) k_box_stream(Geom g, In in, Out out) {
   for (int base = 0; y0 + base < yend; base += R) {
     // ---- vertical: rows y0+base .. +R-1 (window [y-r, y+r])
     if (tid < g.tx + 2 * r) {
+      // every entering / leaving row of the batch is loaded before the first
+      // is used: one memory latency per batch, not one per row
+      float e[R][NF], l[R][NF];
 #pragma unroll
       for (int j = 0; j < R; ++j) {
         const int y = y0 + base + j;
         const int ye = y + r, yl = y - r - 1;
+#pragma unroll
+        for (int f = 0; f < NF; ++f) e[j][f] = l[j][f] = 0.f;
         if (col_ok && y < yend) {
-          float e[NF], l[NF];
-#pragma unroll
-          for (int f = 0; f < NF; ++f) e[f] = l[f] = 0.f;
-          if (ye < H) in(plane, ye, gx, sh, e);
-          if (yl >= 0 && yl >= y0 - r) in(plane, yl, gx, sh, l);  // rows added so far
-#pragma unroll
-          for (int f = 0; f < NF; ++f) s[f] += e[f] - l[f];
+          if (ye < H) in(plane, ye, gx, sh, e[j]);
+          if (yl >= 0 && yl >= y0 - r) in(plane, yl, gx, sh, l[j]);  // rows added so far
         }
+      }
 #pragma unroll
-        for (int f = 0; f < NF; ++f) vs[(f * R + j) * PV + tid] = col_ok ? s[f] : 0.f;
+      for (int j = 0; j < R; ++j) {
+#pragma unroll
+        for (int f = 0; f < NF; ++f) {
+          s[f] += e[j][f] - l[j][f];
+          vs[(f * R + j) * PV + tid] = col_ok ? s[f] : 0.f;
+        }
       }
     }
     __syncthreads();
