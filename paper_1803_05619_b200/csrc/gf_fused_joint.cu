@@ -38,6 +38,10 @@ constexpr int TLY = 16, TLX = 32;      // low-res block of the hr kernels
 constexpr int THY = 4 * TLY, THX = 4 * TLX;
 constexpr int NT = 256;
 constexpr int RA = TLY + 2, CA = TLX + 2;  // coefficient cells incl. bilinear halo
+// shared pitches: rows of the horizontal pass are 16 lanes apart and start 16
+// banks apart (pitch = 16 mod 32), so two rows per warp never share a bank
+__host__ __device__ constexpr int pitch16(int n) { return n + ((48 - n % 32) % 32); }
+constexpr int CAP = pitch16(CA);  // As / Bs row pitch
 constexpr int kMaxRadius = 12;  // tail-kernel smem <= 227 KB
 
 __device__ __forceinline__ int wlen(int i, int n, int r) {
@@ -68,24 +72,24 @@ struct SmemCoef {
   // sized for kMaxRadius; carved from dynamic shared memory
   float* xs;    // [RI][CI]
   float* ys;    // [RI][CI]
-  float* vsum;  // [4][RA][CI]
-  float* As;    // [RA][CA]
-  float* Bs;    // [RA][CA]
+  float* vsum;  // [4][RA][VP]
+  float* As;    // [RA][CAP]
+  float* Bs;    // [RA][CAP]
 };
 
 __host__ __device__ inline size_t coef_smem_floats(int r) {
-  const int RI = RA + 2 * r, CI = CA + 2 * r;
-  return (size_t)2 * RI * CI + (size_t)4 * RA * CI + (size_t)2 * RA * CA;
+  const int RI = RA + 2 * r, CI = CA + 2 * r, VP = pitch16(CI);
+  return (size_t)2 * RI * CI + (size_t)4 * RA * VP + (size_t)2 * RA * CAP;
 }
 
 __device__ inline SmemCoef carve(float* base, int r) {
-  const int RI = RA + 2 * r, CI = CA + 2 * r;
+  const int RI = RA + 2 * r, CI = CA + 2 * r, VP = pitch16(CI);
   SmemCoef s;
   s.xs = base;
   s.ys = s.xs + RI * CI;
   s.vsum = s.ys + RI * CI;
-  s.As = s.vsum + 4 * RA * CI;
-  s.Bs = s.As + RA * CA;
+  s.As = s.vsum + 4 * RA * VP;
+  s.Bs = s.As + RA * CAP;
   return s;
 }
 
@@ -128,12 +132,16 @@ __device__ void lr_coeffs(const float* __restrict__ X, const float* __restrict__
   __syncthreads();
   // 2) vertical sliding sums: item = (column, chunk of rows)
   {
-    const int nch = NT / CI > 0 ? (NT / CI < RA ? NT / CI : RA) : 1;
-    const int rc = (RA + nch - 1) / nch;
-    for (int it = tid; it < CI * nch; it += NT) {
-      const int col = it % CI, ch = it / CI;
+    // item = (column, chunk of rows) with warps never straddling two chunks:
+    // the columns of a chunk are padded to a multiple of 32
+    constexpr int CW = (CA + 2 * r + 31) / 32 * 32;
+    constexpr int VP = pitch16(CA + 2 * r);
+    constexpr int nch = NT / CW > 0 ? (NT / CW < RA ? NT / CW : RA) : 1;
+    constexpr int rc = (RA + nch - 1) / nch;
+    for (int it = tid; it < CW * nch; it += NT) {
+      const int col = it % CW, ch = it / CW;
       const int a0 = ch * rc, a1 = min(RA, a0 + rc);
-      if (a0 >= a1) continue;
+      if (a0 >= a1 || col >= CI) continue;
       float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
       for (int d = 0; d < 2 * r; ++d) {
         const float xv = sm.xs[(a0 + d) * CI + col], yv = sm.ys[(a0 + d) * CI + col];
@@ -148,10 +156,10 @@ __device__ void lr_coeffs(const float* __restrict__ X, const float* __restrict__
         s1 += yv;
         s2 += xv * xv;
         s3 += xv * yv;
-        sm.vsum[(0 * RA + a) * CI + col] = s0;
-        sm.vsum[(1 * RA + a) * CI + col] = s1;
-        sm.vsum[(2 * RA + a) * CI + col] = s2;
-        sm.vsum[(3 * RA + a) * CI + col] = s3;
+        sm.vsum[(0 * RA + a) * VP + col] = s0;
+        sm.vsum[(1 * RA + a) * VP + col] = s1;
+        sm.vsum[(2 * RA + a) * VP + col] = s2;
+        sm.vsum[(3 * RA + a) * VP + col] = s3;
         const float xo = sm.xs[a * CI + col], yo = sm.ys[a * CI + col];
         s0 -= xo;
         s1 -= yo;
@@ -163,16 +171,18 @@ __device__ void lr_coeffs(const float* __restrict__ X, const float* __restrict__
   __syncthreads();
   // 3) horizontal sliding sums + coefficients: item = (row, chunk of cols)
   {
-    constexpr int nch = NT / RA < CA ? NT / RA : CA;  // 14
-    constexpr int cc = (CA + nch - 1) / nch;
+    // 16 items per row (2 rows per warp, 16 banks apart), runs of 3 columns
+    constexpr int nch = 16;
+    constexpr int cc = (CA + 11) / 12;
+    constexpr int VP = pitch16(CA + 2 * r);
     for (int it = tid; it < RA * nch; it += NT) {
       const int a = it / nch, ch = it - a * nch;
       const int c0 = ch * cc, c1 = min(CA, c0 + cc);
       if (c0 >= c1) continue;
-      const float* v0 = sm.vsum + (0 * RA + a) * CI;
-      const float* v1 = sm.vsum + (1 * RA + a) * CI;
-      const float* v2 = sm.vsum + (2 * RA + a) * CI;
-      const float* v3 = sm.vsum + (3 * RA + a) * CI;
+      const float* v0 = sm.vsum + (0 * RA + a) * VP;
+      const float* v1 = sm.vsum + (1 * RA + a) * VP;
+      const float* v2 = sm.vsum + (2 * RA + a) * VP;
+      const float* v3 = sm.vsum + (3 * RA + a) * VP;
       float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
       for (int d = 0; d < 2 * r; ++d) {
         s0 += v0[c0 + d];
@@ -199,8 +209,8 @@ __device__ void lr_coeffs(const float* __restrict__ X, const float* __restrict__
           A = cov * fast_rcp(var + eps);
           if (NEED_B) B = (my + sy) - A * (mx + sx);
         }
-        sm.As[a * CA + c] = A;
-        if (NEED_B) sm.Bs[a * CA + c] = B;
+        sm.As[a * CAP + c] = A;
+        if (NEED_B) sm.Bs[a * CAP + c] = B;
         s0 -= v0[c];
         s1 -= v1[c];
         s2 -= v2[c];
@@ -283,8 +293,8 @@ __global__ void __launch_bounds__(NT, (RAD >= 2 && RAD <= 4) ? 4 : 3) k_joint_fw
   for (int q = 0; q < 4; ++q) {
     const int rl = 2 * warp + q;
     if (rl < RA) {
-      hrow(sm.As + rl * CA, ct, HA[q]);
-      hrow(sm.Bs + rl * CA, ct, HB[q]);
+      hrow(sm.As + rl * CAP, ct, HA[q]);
+      hrow(sm.Bs + rl * CAP, ct, HB[q]);
     } else {
 #pragma unroll
       for (int j = 0; j < 4; ++j) HA[q][j] = HB[q][j] = 0.f;
@@ -407,7 +417,7 @@ __global__ void __launch_bounds__(NT, 4) k_joint_bwd_hr(BwdHrArgs a) {
     for (int q = 0; q < 4; ++q) {
       const int rl = 2 * warp + q;
       if (rl < RA) {
-        hrow(sm.As + rl * CA, ct, HA[q]);
+        hrow(sm.As + rl * CAP, ct, HA[q]);
       } else {
 #pragma unroll
         for (int j = 0; j < 4; ++j) HA[q][j] = 0.f;
