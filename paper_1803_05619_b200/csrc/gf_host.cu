@@ -1,9 +1,9 @@
 // Host-buffer entry points (include/gf_b200.h, "host" section): the
 // reference's layer calls take host images (numpy, gf/guided.py:152, :198)
 // and return host images.  These entries keep that contract and hide the PCIe
-// traffic behind the kernels: the batch is streamed chunk by chunk (one plane;
-// one image when a 1-channel guide drives C planes) through two device slots
-// with three streams,
+// traffic behind the kernels: the batch is streamed plane by plane through two
+// device slots (a 1-channel guide is copied once per image into its own pair
+// of slots) with three streams,
 //
 //     copy-in  (chunk b+1)  ||  kernel (chunk b)  ||  copy-out (chunk b-1)
 //
@@ -22,16 +22,16 @@ namespace {
 struct Pipe {
   cudaStream_t in = nullptr, run = nullptr, out = nullptr;
   cudaEvent_t in_done[2] = {nullptr, nullptr}, run_done[2] = {nullptr, nullptr},
-              out_done[2] = {nullptr, nullptr};
+              out_done[2] = {nullptr, nullptr}, grp_in[2] = {nullptr, nullptr},
+              grp_done[2] = {nullptr, nullptr};
   bool ok = true;
   Pipe() {
     ok &= cudaStreamCreateWithFlags(&in, cudaStreamNonBlocking) == cudaSuccess;
     ok &= cudaStreamCreateWithFlags(&run, cudaStreamNonBlocking) == cudaSuccess;
     ok &= cudaStreamCreateWithFlags(&out, cudaStreamNonBlocking) == cudaSuccess;
     for (int s = 0; s < 2; ++s) {
-      ok &= cudaEventCreateWithFlags(&in_done[s], cudaEventDisableTiming) == cudaSuccess;
-      ok &= cudaEventCreateWithFlags(&run_done[s], cudaEventDisableTiming) == cudaSuccess;
-      ok &= cudaEventCreateWithFlags(&out_done[s], cudaEventDisableTiming) == cudaSuccess;
+      for (cudaEvent_t* e : {&in_done[s], &run_done[s], &out_done[s], &grp_in[s], &grp_done[s]})
+        ok &= cudaEventCreateWithFlags(e, cudaEventDisableTiming) == cudaSuccess;
     }
   }
 };
@@ -50,42 +50,78 @@ Pipe* pipe_for_current_device() {
 size_t up256(size_t n) { return (n + 255) / 256 * 256; }
 size_t esize(int dtype) { return dtype == GF_F64 ? 8 : 4; }
 
-// Copies of `nin` inputs per chunk (chunk b: in_bytes[i] at host in[i] +
-// b * in_bytes[i]) and one output; `launch` runs the device entry on the slot
-// buffers.  Returns a GF_* code; *status gets the OR of the device bits.
+// One pipeline input: chunk b reads host block (b / grp) of `bytes`; a group
+// input (grp > 1, e.g. a guide shared by the C planes of an image) is copied
+// once per group into one of two group slots.
+struct Input {
+  const void* host;
+  size_t bytes;
+  int64_t grp;
+};
+
+// Copies of the inputs per chunk, one output per chunk; `launch` runs the
+// device entry on the slot buffers.  Returns a GF_* code; *status gets the OR
+// of the device bits.
 template <class Launch>
-int run_pipeline(int64_t B, int nin, const void* const* in, const size_t* in_bytes, void* out,
-                 size_t out_bytes, char* ws, size_t slot_bytes, uint32_t* status_dev,
-                 uint32_t* status_host, Launch launch) {
+int run_pipeline(int64_t nchunk, int nin, const Input* in, void* out, size_t out_bytes, char* ws,
+                 uint32_t* status_dev, uint32_t* status_host, Launch launch) {
   Pipe* pp = pipe_for_current_device();
   if (!pp || !pp->ok) return gfb::api_fail(GF_ERR_CUDA, "stream/event creation failed");
   Pipe& p = *pp;
   if (cudaMemsetAsync(status_dev, 0, sizeof(uint32_t), p.run) != cudaSuccess)
     return gfb::api_fail(GF_ERR_CUDA, cudaGetErrorString(cudaGetLastError()));
-  for (int64_t b = 0; b < B; ++b) {
-    const int s = (int)(b & 1);
-    char* slot = ws + s * slot_bytes;
-    // slot inputs are free once the kernel of image b-2 ran
-    if (b >= 2) cudaStreamWaitEvent(p.in, p.run_done[s], 0);
-    size_t off = 0;
-    const void* dev_in[4];
-    for (int i = 0; i < nin; ++i) {
-      cudaMemcpyAsync(slot + off, (const char*)in[i] + b * in_bytes[i], in_bytes[i],
-                      cudaMemcpyHostToDevice, p.in);
-      dev_in[i] = slot + off;
-      off += up256(in_bytes[i]);
+  // workspace: per input two slots, then two output slots
+  char* slot[4][2];
+  char* w = ws;
+  for (int i = 0; i < nin; ++i)
+    for (int s = 0; s < 2; ++s) {
+      slot[i][s] = w;
+      w += up256(in[i].bytes);
     }
-    void* dev_out = slot + off;
+  char* oslot[2] = {w, w + up256(out_bytes)};
+  int64_t grp = 1;  // the (single) group size of the group inputs
+  for (int i = 0; i < nin; ++i)
+    if (in[i].grp > 1) grp = in[i].grp;
+  for (int64_t b = 0; b < nchunk; ++b) {
+    const int s = (int)(b & 1);
+    const int64_t g = b / grp;
+    const int gs = (int)(g & 1);
+    const void* dev_in[4];
+    bool grp_copied = false;
+    for (int i = 0; i < nin; ++i) {
+      if (in[i].grp > 1) {
+        if (b % grp == 0) {  // first chunk of the group: its slot is free once
+                             // the last chunk of group g-2 ran
+          if (g >= 2) cudaStreamWaitEvent(p.in, p.grp_done[gs], 0);
+          cudaMemcpyAsync(slot[i][gs], (const char*)in[i].host + g * in[i].bytes, in[i].bytes,
+                          cudaMemcpyHostToDevice, p.in);
+          grp_copied = true;
+        }
+        dev_in[i] = slot[i][gs];
+      }
+    }
+    if (grp_copied) cudaEventRecord(p.grp_in[gs], p.in);
+    // chunk slot inputs are free once the kernel of chunk b-2 ran
+    if (b >= 2) cudaStreamWaitEvent(p.in, p.run_done[s], 0);
+    for (int i = 0; i < nin; ++i) {
+      if (in[i].grp > 1) continue;
+      cudaMemcpyAsync(slot[i][s], (const char*)in[i].host + b * in[i].bytes, in[i].bytes,
+                      cudaMemcpyHostToDevice, p.in);
+      dev_in[i] = slot[i][s];
+    }
     cudaEventRecord(p.in_done[s], p.in);
     cudaStreamWaitEvent(p.run, p.in_done[s], 0);
-    if (b >= 2) cudaStreamWaitEvent(p.run, p.out_done[s], 0);  // slot output copied out
-    if (int e = launch(dev_in, dev_out, p.run)) {
+    if (grp > 1) cudaStreamWaitEvent(p.run, p.grp_in[gs], 0);
+    if (b >= 2) cudaStreamWaitEvent(p.run, p.out_done[s], 0);  // output slot copied out
+    if (int e = launch(dev_in, oslot[s], p.run)) {
       cudaStreamSynchronize(p.run);
       return e;
     }
     cudaEventRecord(p.run_done[s], p.run);
+    if (grp > 1 && (b % grp == grp - 1 || b == nchunk - 1)) cudaEventRecord(p.grp_done[gs], p.run);
     cudaStreamWaitEvent(p.out, p.run_done[s], 0);
-    cudaMemcpyAsync((char*)out + b * out_bytes, dev_out, out_bytes, cudaMemcpyDeviceToHost, p.out);
+    cudaMemcpyAsync((char*)out + b * out_bytes, oslot[s], out_bytes, cudaMemcpyDeviceToHost,
+                    p.out);
     cudaEventRecord(p.out_done[s], p.out);
   }
   cudaStreamWaitEvent(p.out, p.run_done[0], 0);  // status written by every kernel
@@ -101,19 +137,27 @@ int run_pipeline(int64_t B, int nin, const void* const* in, const size_t* in_byt
   return GF_OK;
 }
 
+size_t pipeline_ws(const size_t* in_bytes, int nin, size_t out_bytes) {
+  size_t n = 2 * up256(out_bytes);
+  for (int i = 0; i < nin; ++i) n += 2 * up256(in_bytes[i]);
+  return n;
+}
+
 }  // namespace
 
 extern "C" {
 
 // ---- full-resolution layer -------------------------------------------------
-// chunk = one plane (guide plane c drives src plane c), or one image when a
-// 1-channel guide is broadcast over the C source planes
+// chunk = one plane; a 1-channel guide is copied once per image and shared by
+// the image's C planes
 size_t gf_highres_host_workspace_bytes(int dtype, int64_t Cg, int64_t C, int64_t H, int64_t W,
                                        int radius) {
+  (void)Cg;
+  (void)C;
   const size_t plane = (size_t)H * W * esize(dtype);
-  const int64_t cc = Cg == C ? 1 : C;  // source planes per chunk
-  const size_t slot = up256(plane) + 2 * up256(cc * plane);
-  return 2 * slot + up256(gf_highres_workspace_bytes(dtype, 1, 1, cc, H, W, radius)) + 256;
+  const size_t in_bytes[2] = {plane, plane};
+  return pipeline_ws(in_bytes, 2, plane) +
+         up256(gf_highres_workspace_bytes(dtype, 1, 1, 1, H, W, radius)) + 256;
 }
 
 int gf_highres_fwd_host(int dtype, const void* guide, const void* src, void* out, int64_t B,
@@ -124,18 +168,15 @@ int gf_highres_fwd_host(int dtype, const void* guide, const void* src, void* out
   const size_t need = gf_highres_host_workspace_bytes(dtype, Cg, C, H, W, radius);
   if (workspace_bytes < need) return gfb::api_fail(GF_ERR_WORKSPACE, "host workspace too small");
   const size_t plane = (size_t)H * W * esize(dtype);
-  const int64_t cc = Cg == C ? 1 : C;
-  const int64_t chunks = Cg == C ? B * C : B;
-  const size_t in_bytes[2] = {plane, cc * plane};
-  const size_t slot = up256(plane) + 2 * up256(cc * plane);
+  const Input ins[2] = {{guide, plane, Cg == C ? 1 : C}, {src, plane, 1}};
+  const size_t in_bytes[2] = {plane, plane};
   char* ws = (char*)workspace;
-  char* gws = ws + 2 * slot;
-  const size_t gws_bytes = gf_highres_workspace_bytes(dtype, 1, 1, cc, H, W, radius);
+  char* gws = ws + pipeline_ws(in_bytes, 2, plane);
+  const size_t gws_bytes = gf_highres_workspace_bytes(dtype, 1, 1, 1, H, W, radius);
   uint32_t* st_dev = (uint32_t*)(gws + up256(gws_bytes));
-  const void* ins[2] = {guide, src};
-  return run_pipeline(chunks, 2, ins, in_bytes, out, cc * plane, ws, slot, st_dev, status,
+  return run_pipeline(B * C, 2, ins, out, plane, ws, st_dev, status,
                       [&](const void* const* d, void* o, cudaStream_t s) {
-                        return gf_highres_fwd(dtype, d[0], d[1], o, 1, 1, cc, H, W, radius, eps,
+                        return gf_highres_fwd(dtype, d[0], d[1], o, 1, 1, 1, H, W, radius, eps,
                                               gws, gws_bytes, st_dev, s);
                       });
 }
@@ -146,8 +187,9 @@ size_t gf_joint_host_workspace_bytes(int dtype, int64_t C, int64_t h, int64_t w,
                                      int64_t W, int radius) {
   (void)C;
   const size_t lo = (size_t)h * w * esize(dtype), hi = (size_t)H * W * esize(dtype);
-  const size_t slot = 2 * up256(lo) + 2 * up256(hi);
-  return 2 * slot + up256(gf_joint_workspace_bytes(dtype, 1, 1, h, w, H, W, radius)) + 256;
+  const size_t in_bytes[3] = {lo, lo, hi};
+  return pipeline_ws(in_bytes, 3, hi) +
+         up256(gf_joint_workspace_bytes(dtype, 1, 1, h, w, H, W, radius)) + 256;
 }
 
 int gf_joint_fwd_host(int dtype, const void* lr_x, const void* lr_y, const void* hr_x, void* out,
@@ -159,14 +201,13 @@ int gf_joint_fwd_host(int dtype, const void* lr_x, const void* lr_y, const void*
   const size_t need = gf_joint_host_workspace_bytes(dtype, C, h, w, H, W, radius);
   if (workspace_bytes < need) return gfb::api_fail(GF_ERR_WORKSPACE, "host workspace too small");
   const size_t lo = (size_t)h * w * esize(dtype), hi = (size_t)H * W * esize(dtype);
+  const Input ins[3] = {{lr_x, lo, 1}, {lr_y, lo, 1}, {hr_x, hi, 1}};
   const size_t in_bytes[3] = {lo, lo, hi};
-  const size_t slot = 2 * up256(lo) + 2 * up256(hi);
   char* ws = (char*)workspace;
-  char* gws = ws + 2 * slot;
+  char* gws = ws + pipeline_ws(in_bytes, 3, hi);
   const size_t gws_bytes = gf_joint_workspace_bytes(dtype, 1, 1, h, w, H, W, radius);
   uint32_t* st_dev = (uint32_t*)(gws + up256(gws_bytes));
-  const void* ins[3] = {lr_x, lr_y, hr_x};
-  return run_pipeline(B * C, 3, ins, in_bytes, out, hi, ws, slot, st_dev, status,
+  return run_pipeline(B * C, 3, ins, out, hi, ws, st_dev, status,
                       [&](const void* const* d, void* o, cudaStream_t s) {
                         return gf_joint_fwd(dtype, d[0], d[1], d[2], o, 1, 1, h, w, H, W, radius,
                                             eps, gws, gws_bytes, st_dev, s);
