@@ -19,20 +19,25 @@
 
 namespace {
 
+// chunk slots in flight: three decouple the H2D, kernel and D2H streams (with
+// two, a D2H slowed by PCIe read/write contention stalls the next H2D)
+constexpr int kSlots = 3;
+
 struct Pipe {
   cudaStream_t in = nullptr, run = nullptr, out = nullptr;
-  cudaEvent_t in_done[2] = {nullptr, nullptr}, run_done[2] = {nullptr, nullptr},
-              out_done[2] = {nullptr, nullptr}, grp_in[2] = {nullptr, nullptr},
-              grp_done[2] = {nullptr, nullptr};
+  cudaEvent_t in_done[kSlots] = {}, run_done[kSlots] = {}, out_done[kSlots] = {},
+              grp_in[2] = {}, grp_done[2] = {};
   bool ok = true;
   Pipe() {
     ok &= cudaStreamCreateWithFlags(&in, cudaStreamNonBlocking) == cudaSuccess;
     ok &= cudaStreamCreateWithFlags(&run, cudaStreamNonBlocking) == cudaSuccess;
     ok &= cudaStreamCreateWithFlags(&out, cudaStreamNonBlocking) == cudaSuccess;
-    for (int s = 0; s < 2; ++s) {
-      for (cudaEvent_t* e : {&in_done[s], &run_done[s], &out_done[s], &grp_in[s], &grp_done[s]})
+    for (int s = 0; s < kSlots; ++s)
+      for (cudaEvent_t* e : {&in_done[s], &run_done[s], &out_done[s]})
         ok &= cudaEventCreateWithFlags(e, cudaEventDisableTiming) == cudaSuccess;
-    }
+    for (int s = 0; s < 2; ++s)
+      for (cudaEvent_t* e : {&grp_in[s], &grp_done[s]})
+        ok &= cudaEventCreateWithFlags(e, cudaEventDisableTiming) == cudaSuccess;
   }
 };
 
@@ -71,19 +76,23 @@ int run_pipeline(int64_t nchunk, int nin, const Input* in, void* out, size_t out
   if (cudaMemsetAsync(status_dev, 0, sizeof(uint32_t), p.run) != cudaSuccess)
     return gfb::api_fail(GF_ERR_CUDA, cudaGetErrorString(cudaGetLastError()));
   // workspace: per input two slots, then two output slots
-  char* slot[4][2];
+  char* slot[4][kSlots];
+  char* oslot[kSlots];
   char* w = ws;
   for (int i = 0; i < nin; ++i)
-    for (int s = 0; s < 2; ++s) {
+    for (int s = 0; s < (in[i].grp > 1 ? 2 : kSlots); ++s) {
       slot[i][s] = w;
       w += up256(in[i].bytes);
     }
-  char* oslot[2] = {w, w + up256(out_bytes)};
+  for (int s = 0; s < kSlots; ++s) {
+    oslot[s] = w;
+    w += up256(out_bytes);
+  }
   int64_t grp = 1;  // the (single) group size of the group inputs
   for (int i = 0; i < nin; ++i)
     if (in[i].grp > 1) grp = in[i].grp;
   for (int64_t b = 0; b < nchunk; ++b) {
-    const int s = (int)(b & 1);
+    const int s = (int)(b % kSlots);
     const int64_t g = b / grp;
     const int gs = (int)(g & 1);
     const void* dev_in[4];
@@ -101,8 +110,8 @@ int run_pipeline(int64_t nchunk, int nin, const Input* in, void* out, size_t out
       }
     }
     if (grp_copied) cudaEventRecord(p.grp_in[gs], p.in);
-    // chunk slot inputs are free once the kernel of chunk b-2 ran
-    if (b >= 2) cudaStreamWaitEvent(p.in, p.run_done[s], 0);
+    // chunk slot inputs are free once the kernel of chunk b-kSlots ran
+    if (b >= kSlots) cudaStreamWaitEvent(p.in, p.run_done[s], 0);
     for (int i = 0; i < nin; ++i) {
       if (in[i].grp > 1) continue;
       cudaMemcpyAsync(slot[i][s], (const char*)in[i].host + b * in[i].bytes, in[i].bytes,
@@ -112,7 +121,7 @@ int run_pipeline(int64_t nchunk, int nin, const Input* in, void* out, size_t out
     cudaEventRecord(p.in_done[s], p.in);
     cudaStreamWaitEvent(p.run, p.in_done[s], 0);
     if (grp > 1) cudaStreamWaitEvent(p.run, p.grp_in[gs], 0);
-    if (b >= 2) cudaStreamWaitEvent(p.run, p.out_done[s], 0);  // output slot copied out
+    if (b >= kSlots) cudaStreamWaitEvent(p.run, p.out_done[s], 0);  // output slot copied out
     if (int e = launch(dev_in, oslot[s], p.run)) {
       cudaStreamSynchronize(p.run);
       return e;
@@ -124,8 +133,8 @@ int run_pipeline(int64_t nchunk, int nin, const Input* in, void* out, size_t out
                     p.out);
     cudaEventRecord(p.out_done[s], p.out);
   }
-  cudaStreamWaitEvent(p.out, p.run_done[0], 0);  // status written by every kernel
-  cudaStreamWaitEvent(p.out, p.run_done[1], 0);
+  for (int s = 0; s < kSlots; ++s)  // status written by every kernel
+    if (s < nchunk) cudaStreamWaitEvent(p.out, p.run_done[s], 0);
   uint32_t st = 0;
   cudaMemcpyAsync(&st, status_dev, sizeof(uint32_t), cudaMemcpyDeviceToHost, p.out);
   cudaError_t e1 = cudaStreamSynchronize(p.out), e2 = cudaStreamSynchronize(p.run);
@@ -137,9 +146,9 @@ int run_pipeline(int64_t nchunk, int nin, const Input* in, void* out, size_t out
   return GF_OK;
 }
 
-size_t pipeline_ws(const size_t* in_bytes, int nin, size_t out_bytes) {
-  size_t n = 2 * up256(out_bytes);
-  for (int i = 0; i < nin; ++i) n += 2 * up256(in_bytes[i]);
+size_t pipeline_ws(const Input* in, int nin, size_t out_bytes) {
+  size_t n = kSlots * up256(out_bytes);
+  for (int i = 0; i < nin; ++i) n += (in[i].grp > 1 ? 2 : kSlots) * up256(in[i].bytes);
   return n;
 }
 
@@ -155,8 +164,8 @@ size_t gf_highres_host_workspace_bytes(int dtype, int64_t Cg, int64_t C, int64_t
   (void)Cg;
   (void)C;
   const size_t plane = (size_t)H * W * esize(dtype);
-  const size_t in_bytes[2] = {plane, plane};
-  return pipeline_ws(in_bytes, 2, plane) +
+  const Input ins[2] = {{nullptr, plane, 1}, {nullptr, plane, 1}};  // the larger layout
+  return pipeline_ws(ins, 2, plane) +
          up256(gf_highres_workspace_bytes(dtype, 1, 1, 1, H, W, radius)) + 256;
 }
 
@@ -169,9 +178,8 @@ int gf_highres_fwd_host(int dtype, const void* guide, const void* src, void* out
   if (workspace_bytes < need) return gfb::api_fail(GF_ERR_WORKSPACE, "host workspace too small");
   const size_t plane = (size_t)H * W * esize(dtype);
   const Input ins[2] = {{guide, plane, Cg == C ? 1 : C}, {src, plane, 1}};
-  const size_t in_bytes[2] = {plane, plane};
   char* ws = (char*)workspace;
-  char* gws = ws + pipeline_ws(in_bytes, 2, plane);
+  char* gws = ws + pipeline_ws(ins, 2, plane);
   const size_t gws_bytes = gf_highres_workspace_bytes(dtype, 1, 1, 1, H, W, radius);
   uint32_t* st_dev = (uint32_t*)(gws + up256(gws_bytes));
   return run_pipeline(B * C, 2, ins, out, plane, ws, st_dev, status,
@@ -187,8 +195,8 @@ size_t gf_joint_host_workspace_bytes(int dtype, int64_t C, int64_t h, int64_t w,
                                      int64_t W, int radius) {
   (void)C;
   const size_t lo = (size_t)h * w * esize(dtype), hi = (size_t)H * W * esize(dtype);
-  const size_t in_bytes[3] = {lo, lo, hi};
-  return pipeline_ws(in_bytes, 3, hi) +
+  const Input ins[3] = {{nullptr, lo, 1}, {nullptr, lo, 1}, {nullptr, hi, 1}};
+  return pipeline_ws(ins, 3, hi) +
          up256(gf_joint_workspace_bytes(dtype, 1, 1, h, w, H, W, radius)) + 256;
 }
 
@@ -202,9 +210,8 @@ int gf_joint_fwd_host(int dtype, const void* lr_x, const void* lr_y, const void*
   if (workspace_bytes < need) return gfb::api_fail(GF_ERR_WORKSPACE, "host workspace too small");
   const size_t lo = (size_t)h * w * esize(dtype), hi = (size_t)H * W * esize(dtype);
   const Input ins[3] = {{lr_x, lo, 1}, {lr_y, lo, 1}, {hr_x, hi, 1}};
-  const size_t in_bytes[3] = {lo, lo, hi};
   char* ws = (char*)workspace;
-  char* gws = ws + pipeline_ws(in_bytes, 3, hi);
+  char* gws = ws + pipeline_ws(ins, 3, hi);
   const size_t gws_bytes = gf_joint_workspace_bytes(dtype, 1, 1, h, w, H, W, radius);
   uint32_t* st_dev = (uint32_t*)(gws + up256(gws_bytes));
   return run_pipeline(B * C, 3, ins, out, hi, ws, st_dev, status,
