@@ -65,6 +65,7 @@ SIGNATURES = {
 # test hooks exported by the library but not part of the public header
 EXTRA = {
     "gf_force_generic": (_i, [_i]),
+    "gf_highres_variant": (_i, [_i]),
     "gf_joint_is_fused": (_i, [_i, _i64, _i64, _i64, _i64, _i64, _i64, _i]),
     "gf_highres_fwd_is_fused": (_i, [_i, _i64, _i64, _i64, _i64, _i64, _i]),
 }

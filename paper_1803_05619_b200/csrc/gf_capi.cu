@@ -16,6 +16,9 @@ namespace {
 
 thread_local char g_err[512] = "";
 thread_local int g_force_generic = 0;
+// full-res fp32 forward kernel: 0 = automatic, 1 = batch/TMA kernel, 2 = segment
+// kernel, 3 = segment kernel with 8 columns per lane only
+thread_local int g_highres_variant = 0;
 
 int fail(int code, const char* fmt, ...) {
   va_list ap;
@@ -57,8 +60,15 @@ bool use_fused_joint(int dtype, int64_t B, int64_t C, int64_t h, int64_t w, int6
   return !g_force_generic && dtype == GF_F32 && gfb::fused_joint_ok(B, C, h, w, H, W, r);
 }
 
+bool use_seg_highres(int dtype, int64_t B, int64_t Cg, int64_t C, int64_t H, int64_t W, int r) {
+  if (g_force_generic || dtype != GF_F32 || g_highres_variant == 1) return false;
+  return gfb::seg_highres_fwd_ok(B, Cg, C, H, W, r);
+}
+
 bool use_fused_highres(int dtype, int64_t B, int64_t Cg, int64_t C, int64_t H, int64_t W, int r) {
-  return !g_force_generic && dtype == GF_F32 && gfb::fused_highres_fwd_ok(B, Cg, C, H, W, r);
+  if (use_seg_highres(dtype, B, Cg, C, H, W, r)) return true;
+  return !g_force_generic && dtype == GF_F32 && g_highres_variant < 2 &&
+         gfb::fused_highres_fwd_ok(B, Cg, C, H, W, r);
 }
 
 }  // namespace
@@ -79,6 +89,15 @@ int gf_force_generic(int on) {
 
 // Introspection hooks (not in the public header): 1 when the call would take
 // the fused sm_100a kernels, 0 when it takes the general kernels.
+// Test hook: pick the fp32 full-res forward kernel of THIS thread (0 automatic,
+// 1 batch/TMA kernel, 2 segment kernel, 3 segment kernel with 8 columns per
+// lane).  Returns the old value.
+int gf_highres_variant(int v) {
+  int old = g_highres_variant;
+  g_highres_variant = v;
+  return old;
+}
+
 int gf_joint_is_fused(int dtype, int64_t B, int64_t C, int64_t h, int64_t w, int64_t H,
                       int64_t W, int r) {
   return use_fused_joint(dtype, B, C, h, w, H, W, r) ? 1 : 0;
@@ -287,6 +306,11 @@ int gf_highres_fwd(int dtype, const void* guide, const void* src, void* out, int
   if (int e = check_highres(dtype, B, Cg, C, H, W, radius, eps)) return e;
   if (use_fused_highres(dtype, B, Cg, C, H, W, radius) && aligned16(guide) && aligned16(src) &&
       aligned16(out)) {
+    if (use_seg_highres(dtype, B, Cg, C, H, W, radius)) {
+      gfb::seg_highres_fwd((const float*)guide, (const float*)src, (float*)out, B, Cg, C, H, W,
+                           radius, (float)eps, g_highres_variant != 3, status, S(stream));
+      return check_launch("gf_highres_fwd[seg]");
+    }
     gfb::fused_highres_fwd((const float*)guide, (const float*)src, (float*)out, B, Cg, C, H, W,
                            radius, (float)eps, status, S(stream));
     return check_launch("gf_highres_fwd[fused]");

@@ -56,6 +56,11 @@ void mse_impl(const T* out, const T* tgt, T* d_out, double* loss, int64_t B, int
 
 // ---- fused fast paths (fp32, NCHW); return false when the shape is not
 // covered, in which case the caller takes the generic path ----
+// full-resolution forward, register-segment variant for r <= 8 (gf_highres_seg.cu)
+bool seg_highres_fwd_ok(int64_t B, int64_t Cg, int64_t C, int64_t H, int64_t W, int r);
+void seg_highres_fwd(const float* guide, const float* src, float* out, int64_t B, int64_t Cg,
+                     int64_t C, int64_t H, int64_t W, int r, float eps, bool allow_sw4,
+                     uint32_t* status, cudaStream_t s);
 bool fused_highres_fwd_ok(int64_t B, int64_t Cg, int64_t C, int64_t H, int64_t W, int r);
 void fused_highres_fwd(const float* guide, const float* src, float* out, int64_t B, int64_t Cg,
                        int64_t C, int64_t H, int64_t W, int r, float eps, uint32_t* status,

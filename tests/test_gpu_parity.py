@@ -541,3 +541,52 @@ def test_fused_highres_backward_vs_oracle(gfb, H, W, r, cg):
         lib.gf_force_generic(old)
     assert rel_max(npy(g.d_src), npy(g2.d_src)) <= GRAD_TOL32
     assert rel_max(npy(g.d_guide_hi), npy(g2.d_guide_hi)) <= GRAD_TOL32
+
+
+@pytest.mark.parametrize("H,W,r,cg", [(77, 132, 1, 1), (77, 132, 3, 3), (300, 260, 8, 1),
+                                      (5, 8, 2, 1), (513, 520, 8, 3), (64, 4, 1, 1),
+                                      (9, 12, 7, 3), (1, 8, 2, 1), (40, 1000, 5, 1),
+                                      (1500, 64, 8, 1), (33, 236, 4, 3), (70, 492, 6, 1),
+                                      (50, 300, 4, 1), (20, 700, 8, 3)])
+def test_highres_kernel_variants_vs_oracle(gfb, H, W, r, cg):
+    """Both fp32 full-res forward kernels (batch/TMA and register-segment)
+    against the oracle on ragged shapes: strips not dividing W, W = 4, H = 1,
+    pieces spanning two strips."""
+    from paper_1803_05619_b200 import _lib
+
+    lib = _lib.load()
+    rng = np.random.default_rng(H * 11 + W + r)
+    guide = rng.uniform(0, 1, (2, cg, H, W)).astype(np.float32)
+    src = rng.uniform(0, 1, (2, 3, H, W)).astype(np.float32)
+    p = gfb.GuidedFilterParams(r, 1e-2)
+    want = O.highres_forward_nchw(guide, src, r, 1e-2)
+    outs = []
+    for v in (1, 2, 3):
+        old = lib.gf_highres_variant(v)
+        try:
+            out, _ = gfb.forward_highres(t32(guide), t32(src), p)
+        finally:
+            lib.gf_highres_variant(old)
+        assert abs_max(npy(out), want) <= OUT_TOL32, v
+        outs.append(npy(out))
+
+
+@pytest.mark.parametrize("variant", [1, 2, 3])
+def test_highres_kernel_variants_status(gfb, variant):
+    from paper_1803_05619_b200 import _lib
+
+    lib = _lib.load()
+    old = lib.gf_highres_variant(variant)
+    try:
+        g = torch.rand(1, 1, 64, 64, device="cuda")
+        s = torch.rand(1, 3, 64, 64, device="cuda")
+        s[0, 1, 10, 20] = float("nan")
+        with pytest.raises(ValueError, match="input"):
+            gfb.forward_highres(g, s, gfb.GuidedFilterParams(2, 1e-2))
+        with pytest.raises(gfb.DegenerateWindowError):
+            gfb.forward_highres(torch.full_like(g, 0.5), s.nan_to_num(0.3),
+                                gfb.GuidedFilterParams(2, 0.0))
+        # eps = 0 with non-degenerate windows is fine
+        gfb.forward_highres(g, s.nan_to_num(0.3), gfb.GuidedFilterParams(2, 0.0))
+    finally:
+        lib.gf_highres_variant(old)
