@@ -43,6 +43,7 @@ for r in [int(x) for x in (sys.argv[1:] or ["8"])]:
         o = out.clone()
         if v == 1:
             ref = o
+        print(f"  variant {v}: max|diff vs 1| {float((o - ref).abs().max()):.2e}")
     print(f"r={r}: batch/TMA {res[1]*1e3:.1f} us  segment {res[2]*1e3:.1f} us  "
           f"segment(8/lane) {res[3]*1e3:.1f} us  "
           f"max|diff| {float((o - ref).abs().max()):.2e}")

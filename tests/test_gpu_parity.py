@@ -547,11 +547,13 @@ def test_fused_highres_backward_vs_oracle(gfb, H, W, r, cg):
                                       (5, 8, 2, 1), (513, 520, 8, 3), (64, 4, 1, 1),
                                       (9, 12, 7, 3), (1, 8, 2, 1), (40, 1000, 5, 1),
                                       (1500, 64, 8, 1), (33, 236, 4, 3), (70, 492, 6, 1),
-                                      (50, 300, 4, 1), (20, 700, 8, 3)])
+                                      (50, 300, 4, 1), (20, 700, 8, 3), (33, 1000, 8, 1),
+                                      (70, 2048, 8, 3), (37, 964, 4, 1), (300, 484, 8, 1),
+                                      (2, 12, 8, 1), (45, 512, 8, 3), (19, 496, 4, 3)])
 def test_highres_kernel_variants_vs_oracle(gfb, H, W, r, cg):
-    """Both fp32 full-res forward kernels (batch/TMA and register-segment)
-    against the oracle on ragged shapes: strips not dividing W, W = 4, H = 1,
-    pieces spanning two strips."""
+    """Every fp32 full-res forward kernel (batch/TMA, register-segment with 4
+    and 8 columns per lane) against the oracle on ragged shapes: strips not
+    dividing W, W = 4, H = 1, pieces spanning two strips."""
     from paper_1803_05619_b200 import _lib
 
     lib = _lib.load()
@@ -571,8 +573,8 @@ def test_highres_kernel_variants_vs_oracle(gfb, H, W, r, cg):
         outs.append(npy(out))
 
 
-@pytest.mark.parametrize("variant", [1, 2, 3])
-def test_highres_kernel_variants_status(gfb, variant):
+@pytest.mark.parametrize("variant,r", [(1, 2), (2, 2), (3, 2), (2, 4), (2, 8), (3, 8)])
+def test_highres_kernel_variants_status(gfb, variant, r):
     from paper_1803_05619_b200 import _lib
 
     lib = _lib.load()
@@ -582,11 +584,11 @@ def test_highres_kernel_variants_status(gfb, variant):
         s = torch.rand(1, 3, 64, 64, device="cuda")
         s[0, 1, 10, 20] = float("nan")
         with pytest.raises(ValueError, match="input"):
-            gfb.forward_highres(g, s, gfb.GuidedFilterParams(2, 1e-2))
+            gfb.forward_highres(g, s, gfb.GuidedFilterParams(r, 1e-2))
         with pytest.raises(gfb.DegenerateWindowError):
             gfb.forward_highres(torch.full_like(g, 0.5), s.nan_to_num(0.3),
-                                gfb.GuidedFilterParams(2, 0.0))
+                                gfb.GuidedFilterParams(r, 0.0))
         # eps = 0 with non-degenerate windows is fine
-        gfb.forward_highres(g, s.nan_to_num(0.3), gfb.GuidedFilterParams(2, 0.0))
+        gfb.forward_highres(g, s.nan_to_num(0.3), gfb.GuidedFilterParams(r, 0.0))
     finally:
         lib.gf_highres_variant(old)
