@@ -29,6 +29,23 @@ constexpr int NT = 256;
 constexpr int kBlocks = 128;  // pixel blocks per image (grid.x)
 constexpr float kLeaky = 0.2f;
 constexpr double kVarFloor = 1e-5;
+constexpr int NST = 3;  // cp.async pipeline stages of the streaming passes
+
+// ---- cp.async staging of the streaming passes: the two lanes of a pair
+// share one 4-pixel group; the even lane copies its three x chunks, the odd
+// lane its three dy chunks, and a __syncwarp after the wait_group publishes
+// them to the partner (another before the refill retires the partner's reads)
+__device__ __forceinline__ void cp16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
+                   (uint32_t)__cvta_generic_to_shared(dst)),
+               "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
 
 // packed parameter layout (include/gf_b200.h)
 template <int HID>
@@ -234,14 +251,15 @@ __global__ void __launch_bounds__(NT, 2) k_bwd_a(const float* __restrict__ x,
                                               const float* __restrict__ params,
                                               const float* __restrict__ fold,
                                               double* __restrict__ part, int64_t HW) {
-  __shared__ float sw1[HID * CI], sw1f[HID * CI], sbeta[HID], sw2[CO * HID];
+  __shared__ float sw1[HID * CI], salpha[HID], sbeta[HID], sw2[CO * HID];
+  __shared__ ulonglong2 stage[NST][CI + CO][NT / 2];
   const int64_t b = blockIdx.y;
   const float* f = fold + b * F<HID>::count;
-  for (int i = threadIdx.x; i < HID * CI; i += NT) {
-    sw1[i] = f[F<HID>::w1 + i];
-    sw1f[i] = f[F<HID>::w1f + i];
+  for (int i = threadIdx.x; i < HID * CI; i += NT) sw1[i] = f[F<HID>::w1 + i];
+  for (int i = threadIdx.x; i < HID; i += NT) {
+    sbeta[i] = f[F<HID>::beta + i];
+    salpha[i] = f[F<HID>::alpha + i];
   }
-  for (int i = threadIdx.x; i < HID; i += NT) sbeta[i] = f[F<HID>::beta + i];
   for (int i = threadIdx.x; i < CO * HID; i += NT) sw2[i] = params[P<HID>::w2 + i];
   __syncthreads();
   constexpr int JH = (HID + 1) / 2;  // hidden units per thread
@@ -261,14 +279,37 @@ __global__ void __launch_bounds__(NT, 2) k_bwd_a(const float* __restrict__ x,
   for (int o = 0; o < CO; ++o) sdy[o] = 0ull;
   const int64_t n4 = HW / 4;
   const int64_t stride = (int64_t)gridDim.x * (NT / 2);
-  for (int64_t i = (int64_t)blockIdx.x * (NT / 2) + (threadIdx.x >> 1); i < n4; i += stride) {
+  const int64_t first = (int64_t)blockIdx.x * (NT / 2);
+  const int pr_ = threadIdx.x >> 1;
+  // warp-uniform trip count: the stage hand-off below needs every lane
+  const int64_t iters = n4 > first ? (n4 - first + stride - 1) / stride : 0;
+  // stage iteration `it` of this pair's (x, dy) chunks (NST - 1 ahead)
+  auto issue = [&](int64_t it) {
+    const int64_t i = first + it * stride + pr_;
+    if (it < iters && i < n4) {
+      const int st = (int)(it % NST);
+      const float* base = half ? dy + b * CO * HW : x + b * CI * HW;
+#pragma unroll
+      for (int c = 0; c < 3; ++c)
+        cp16(&stage[st][3 * half + c][pr_], reinterpret_cast<const ulonglong2*>(base + c * HW) + i);
+    }
+    cp_commit();
+  };
+#pragma unroll
+  for (int k = 0; k < NST - 1; ++k) issue(k);
+  for (int64_t it = 0; it < iters; ++it) {
+    const bool valid = first + it * stride + pr_ < n4;  // a lane pair together
+    __syncwarp();  // the partner's reads of the stage refilled below are done
+    issue(it + NST - 1);
+    cp_wait<NST - 1>();
+    __syncwarp();  // the partner's chunks of stage `it` are visible
+    const int st = (int)(it % NST);
     ulonglong2 X[CI], G[CO];
 #pragma unroll
-    for (int c = 0; c < CI; ++c)
-      X[c] = __ldg(reinterpret_cast<const ulonglong2*>(x + (b * CI + c) * HW) + i);
+    for (int c = 0; c < CI; ++c) X[c] = valid ? stage[st][c][pr_] : make_ulonglong2(0ull, 0ull);
 #pragma unroll
     for (int o = 0; o < CO; ++o) {
-      G[o] = __ldg(reinterpret_cast<const ulonglong2*>(dy + (b * CO + o) * HW) + i);
+      G[o] = valid ? stage[st][CI + o][pr_] : make_ulonglong2(0ull, 0ull);
       sdy[o] = add2(sdy[o], add2(G[o].x, G[o].y));
     }
 #pragma unroll
@@ -276,8 +317,7 @@ __global__ void __launch_bounds__(NT, 2) k_bwd_a(const float* __restrict__ x,
       const int j = j0 + jj;
       if (j >= HID) break;  // odd HID: the second half has one unit fewer
       const u64 a0 = bc(sw1[j * CI]), a1 = bc(sw1[j * CI + 1]), a2 = bc(sw1[j * CI + 2]);
-      const u64 f0 = bc(sw1f[j * CI]), f1 = bc(sw1f[j * CI + 1]), f2 = bc(sw1f[j * CI + 2]);
-      const u64 be = bc(sbeta[j]);
+      const u64 al = bc(salpha[j]), be = bc(sbeta[j]);
       const u64 v0 = bc(sw2[0 * HID + j]), v1 = bc(sw2[1 * HID + j]), v2 = bc(sw2[2 * HID + j]);
 #pragma unroll
       for (int pp = 0; pp < 2; ++pp) {
@@ -286,7 +326,7 @@ __global__ void __launch_bounds__(NT, 2) k_bwd_a(const float* __restrict__ x,
         const u64 g0 = pp ? G[0].y : G[0].x, g1 = pp ? G[1].y : G[1].x,
                   g2 = pp ? G[2].y : G[2].x;
         const u64 h1 = fma2(a2, x2, fma2(a1, x1, mul2(a0, x0)));
-        const u64 h2 = fma2(f2, x2, fma2(f1, x1, fma2(f0, x0, be)));
+        const u64 h2 = fma2(al, h1, be);  // (alpha .* W1) x + beta
         const u64 sl = slope2(h2, kLeaky);
         const u64 h3 = mul2(h2, sl);
         const u64 d2 = mul2(fma2(v2, g2, fma2(v1, g1, mul2(v0, g0))), sl);
@@ -298,6 +338,7 @@ __global__ void __launch_bounds__(NT, 2) k_bwd_a(const float* __restrict__ x,
       }
     }
   }
+  cp_wait<0>();
   // value v of the A layout from the thread that owns it (0 elsewhere)
   auto sum2 = [](u64 p) { return lo(p) + hi(p); };
   auto get = [&](int v) -> float {
@@ -377,14 +418,11 @@ __global__ void __launch_bounds__(NT, 2) k_bwd_b(const float* __restrict__ x,
                                               const float* __restrict__ fold,
                                               const float* __restrict__ coef,
                                               double* __restrict__ part, int64_t HW) {
-  __shared__ float sw1[HID * CI], sw1f[HID * CI], sbeta[HID], sw2[CO * HID], salpha[HID],
-      skap[HID], slam[HID];
+  __shared__ float sw1[HID * CI], sbeta[HID], sw2[CO * HID], salpha[HID], skap[HID], slam[HID];
+  __shared__ ulonglong2 stage[NST][CI + CO][NT / 2];
   const int64_t b = blockIdx.y;
   const float* f = fold + b * F<HID>::count;
-  for (int i = threadIdx.x; i < HID * CI; i += NT) {
-    sw1[i] = f[F<HID>::w1 + i];
-    sw1f[i] = f[F<HID>::w1f + i];
-  }
+  for (int i = threadIdx.x; i < HID * CI; i += NT) sw1[i] = f[F<HID>::w1 + i];
   for (int i = threadIdx.x; i < HID; i += NT) {
     sbeta[i] = f[F<HID>::beta + i];
     salpha[i] = f[F<HID>::alpha + i];
@@ -407,27 +445,44 @@ __global__ void __launch_bounds__(NT, 2) k_bwd_b(const float* __restrict__ x,
   const int64_t first = (int64_t)blockIdx.x * (NT / 2);
   // warp-uniform trip count: the dx shuffle below needs every lane
   const int64_t iters = n4 > first ? (n4 - first + stride - 1) / stride : 0;
+  const int pr_ = threadIdx.x >> 1;
+  // stage iteration `it` of this pair's (x, dy) chunks (NST - 1 ahead)
+  auto issue = [&](int64_t it) {
+    const int64_t i = first + it * stride + pr_;
+    if (it < iters && i < n4) {
+      const int st = (int)(it % NST);
+      const float* base = half ? dy + b * CO * HW : x + b * CI * HW;
+#pragma unroll
+      for (int c = 0; c < 3; ++c)
+        cp16(&stage[st][3 * half + c][pr_], reinterpret_cast<const ulonglong2*>(base + c * HW) + i);
+    }
+    cp_commit();
+  };
+#pragma unroll
+  for (int k = 0; k < NST - 1; ++k) issue(k);
   for (int64_t it = 0; it < iters; ++it) {
-    const int64_t i = first + it * stride + (threadIdx.x >> 1);
+    const int64_t i = first + it * stride + pr_;
     const bool valid = i < n4;  // a lane pair is valid or invalid together
+    __syncwarp();  // the partner's reads of the stage refilled below are done
+    issue(it + NST - 1);
+    cp_wait<NST - 1>();
+    __syncwarp();  // the partner's chunks of stage `it` are visible
+    const int st = (int)(it % NST);
     ulonglong2 X[CI], G[CO];
     u64 dxv[CI][2];
 #pragma unroll
     for (int c = 0; c < CI; ++c) {
-      X[c] = valid ? __ldg(reinterpret_cast<const ulonglong2*>(x + (b * CI + c) * HW) + i)
-                   : make_ulonglong2(0ull, 0ull);
+      X[c] = valid ? stage[st][c][pr_] : make_ulonglong2(0ull, 0ull);
       dxv[c][0] = dxv[c][1] = 0ull;
     }
 #pragma unroll
     for (int o = 0; o < CO; ++o)
-      G[o] = valid ? __ldg(reinterpret_cast<const ulonglong2*>(dy + (b * CO + o) * HW) + i)
-                   : make_ulonglong2(0ull, 0ull);
+      G[o] = valid ? stage[st][CI + o][pr_] : make_ulonglong2(0ull, 0ull);
 #pragma unroll
     for (int jj = 0; jj < JH; ++jj) {
       const int j = j0 + jj;
       if (j >= HID) break;
       const u64 a0 = bc(sw1[j * CI]), a1 = bc(sw1[j * CI + 1]), a2 = bc(sw1[j * CI + 2]);
-      const u64 f0 = bc(sw1f[j * CI]), f1 = bc(sw1f[j * CI + 1]), f2 = bc(sw1f[j * CI + 2]);
       const u64 be = bc(sbeta[j]), al = bc(salpha[j]), ka = bc(skap[j]), la = bc(slam[j]);
       const u64 v0 = bc(sw2[0 * HID + j]), v1 = bc(sw2[1 * HID + j]), v2 = bc(sw2[2 * HID + j]);
 #pragma unroll
@@ -437,7 +492,7 @@ __global__ void __launch_bounds__(NT, 2) k_bwd_b(const float* __restrict__ x,
         const u64 g0 = pp ? G[0].y : G[0].x, g1 = pp ? G[1].y : G[1].x,
                   g2 = pp ? G[2].y : G[2].x;
         const u64 h1 = fma2(a2, x2, fma2(a1, x1, mul2(a0, x0)));
-        const u64 h2 = fma2(f2, x2, fma2(f1, x1, fma2(f0, x0, be)));
+        const u64 h2 = fma2(al, h1, be);  // (alpha .* W1) x + beta
         const u64 d2 = mul2(fma2(v2, g2, fma2(v1, g1, mul2(v0, g0))), slope2(h2, kLeaky));
         const u64 dh = fma2(al, d2, fma2(la, h1, ka));
         dxv[0][pp] = fma2(a0, dh, dxv[0][pp]);
@@ -460,6 +515,7 @@ __global__ void __launch_bounds__(NT, 2) k_bwd_b(const float* __restrict__ x,
             make_ulonglong2(dxv[c][0], dxv[c][1]);
     }
   }
+  cp_wait<0>();
   auto get = [&](int v) -> float {
     const int j = v / CI, c = v - j * CI;
     float r = 0.f;
