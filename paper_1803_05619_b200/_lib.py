@@ -66,6 +66,7 @@ SIGNATURES = {
 EXTRA = {
     "gf_force_generic": (_i, [_i]),
     "gf_highres_variant": (_i, [_i]),
+    "gf_joint_bwd_lr_variant": (_i, [_i]),
     "gf_joint_is_fused": (_i, [_i, _i64, _i64, _i64, _i64, _i64, _i64, _i]),
     "gf_highres_fwd_is_fused": (_i, [_i, _i64, _i64, _i64, _i64, _i64, _i]),
 }

@@ -98,6 +98,14 @@ int gf_highres_variant(int v) {
   return old;
 }
 
+// Test hook: pick the fp32 joint-backward low-res tail of THIS thread (0
+// automatic, 1 tile kernel, 2 register-segment kernel where it applies).
+int gf_joint_bwd_lr_variant(int v) {
+  int old = gfb::g_joint_lr_variant;
+  gfb::g_joint_lr_variant = v;
+  return old;
+}
+
 int gf_joint_is_fused(int dtype, int64_t B, int64_t C, int64_t h, int64_t w, int64_t H,
                       int64_t W, int r) {
   return use_fused_joint(dtype, B, C, h, w, H, W, r) ? 1 : 0;

@@ -728,6 +728,8 @@ __global__ void __launch_bounds__(NT) k_joint_bwd_lr(BwdLrArgs a) {
 
 }  // namespace jf
 
+thread_local int g_joint_lr_variant = 0;
+
 bool fused_joint_ok(int64_t B, int64_t C, int64_t h, int64_t w, int64_t H, int64_t W, int r) {
   if (H != 4 * h || W != 4 * w) return false;
   if (r < 0 || r > jf::kMaxRadius) return false;
@@ -809,7 +811,9 @@ void fused_joint_bwd(const float* lr_x, const float* lr_y, const float* hr_x, co
                     eps, status};
     launch(fns.bwd_hr, grid, smem, s, &a);
   }
-  {
+  if (g_joint_lr_variant != 1 && seg_joint_bwd_lr_ok(h, w, r)) {
+    seg_joint_bwd_lr(lr_x, lr_y, db, dA, d_lr_x, d_lr_y, B * C, h, w, r, eps, s);
+  } else {
     const size_t smem = jf::bwd_lr_smem_floats(r) * sizeof(float);
     set_smem(fns.bwd_lr, smem);
     dim3 grid((unsigned)((w + jf::TL - 1) / jf::TL), (unsigned)((h + jf::TL - 1) / jf::TL),

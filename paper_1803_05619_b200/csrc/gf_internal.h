@@ -66,6 +66,13 @@ void fused_highres_fwd(const float* guide, const float* src, float* out, int64_t
                        int64_t C, int64_t H, int64_t W, int r, float eps, uint32_t* status,
                        cudaStream_t s);
 
+// joint backward low-res tail, register-segment walk for r <= 4, w % 4 == 0
+// (gf_joint_bwd_lr_seg.cu); variant hook: 0 automatic, 1 tile kernel, 2 segment
+bool seg_joint_bwd_lr_ok(int64_t h, int64_t w, int r);
+void seg_joint_bwd_lr(const float* lr_x, const float* lr_y, const float* db, const float* dA,
+                      float* d_lr_x, float* d_lr_y, int64_t P, int64_t h, int64_t w, int r,
+                      float eps, cudaStream_t s);
+extern thread_local int g_joint_lr_variant;
 bool fused_joint_ok(int64_t B, int64_t C, int64_t h, int64_t w, int64_t H, int64_t W, int r);
 void fused_joint_fwd(const float* lr_x, const float* lr_y, const float* hr_x, float* out,
                      int64_t B, int64_t C, int64_t h, int64_t w, int64_t H, int64_t W, int r,

@@ -461,6 +461,36 @@ def test_fused_highres_nonfinite_input_is_input_error(gfb):
                             gfb.GuidedFilterParams(2, 0.0))
 
 
+@pytest.mark.parametrize("h,w,r", [(37, 132, 2), (5, 8, 1), (1, 4, 0), (70, 256, 4),
+                                   (33, 120, 3), (200, 244, 2), (9, 500, 1), (64, 128, 4),
+                                   (300, 12, 2), (40, 36, 6)])
+def test_joint_bwd_lr_variants_vs_oracle(gfb, h, w, r):
+    """Both low-res backward tails (tile kernel, register-segment walk) against
+    the oracle: strips not dividing w, w < one strip, h = 1, pieces spanning
+    strips; r = 6 takes the tile kernel under both settings."""
+    from paper_1803_05619_b200 import _lib
+
+    lib = _lib.load()
+    rng = np.random.default_rng(h * 31 + w + r)
+    lr_x = rng.uniform(0, 1, (2, 3, h, w)).astype(np.float32)
+    lr_y = rng.uniform(0, 1, (2, 3, h, w)).astype(np.float32)
+    hr_x = rng.uniform(0, 1, (2, 3, 4 * h, 4 * w)).astype(np.float32)
+    d = rng.standard_normal((2, 3, 4 * h, 4 * w)).astype(np.float32)
+    eps = 1e-3
+    p = gfb.GuidedFilterParams(r, eps)
+    dlx, dly, _ = O.joint_backward_nchw(lr_x, lr_y, hr_x, d, r, eps)
+    scale = max(float(np.abs(dlx).max()), float(np.abs(dly).max()))
+    for v in (1, 2):
+        old = lib.gf_joint_bwd_lr_variant(v)
+        try:
+            _, tape = gfb.forward_joint(t32(lr_x), t32(hr_x), t32(lr_y), p)
+            g = gfb.backward(tape, t32(d))
+        finally:
+            lib.gf_joint_bwd_lr_variant(old)
+        assert abs_max(npy(g.d_guide_lo), dlx) <= GRAD_TOL32 * scale, v
+        assert abs_max(npy(g.d_src), dly) <= GRAD_TOL32 * scale, v
+
+
 def test_fused_joint_nonfinite_input_is_input_error(gfb):
     lr_x = torch.rand(1, 3, 16, 16, device="cuda")
     lr_y = torch.rand(1, 3, 16, 16, device="cuda")
