@@ -221,6 +221,7 @@ __device__ void lr_coeffs(const float* __restrict__ X, const float* __restrict__
   __syncthreads();
 }
 
+
 struct FwdArgs {
   const float* lr_x;
   const float* lr_y;
@@ -405,6 +406,39 @@ __global__ void __launch_bounds__(NT, 4) k_joint_bwd_hr(BwdHrArgs a) {
     const int Y = Yb + t;
     dv[t] = make_float4(0.f, 0.f, 0.f, 0.f);
     if (col_ok && Y < a.H) dv[t] = __ldg(reinterpret_cast<const float4*>(D + (int64_t)Y * a.W + X0));
+  }
+  // the gather below reads hr_x (and the 2-pixel halo of both fields) only
+  // after the coefficient phase: start those DRAM reads now, into L2
+  {
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      const int Y = Yb + t;
+      if (col_ok && Y < a.H)
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(G + (int64_t)Y * a.W + X0));
+    }
+    // halo rows 4 i0 - 2, -1 (warp 0) and 4 i0 + 64, 65 (warp 7)
+    if (warp == 0 || warp == NT / 32 - 1) {
+#pragma unroll
+      for (int t = 0; t < 2; ++t) {
+        const int Y = warp == 0 ? 4 * i0 - 2 + t : 4 * i0 + THY + t;
+        if (col_ok && Y >= 0 && Y < a.H) {
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(G + (int64_t)Y * a.W + X0));
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(D + (int64_t)Y * a.W + X0));
+        }
+      }
+    }
+    // halo columns: the 16-byte chunks left of lane 0 and right of lane 31
+    const int Xh = lane == 0 ? X0 - 4 : (lane == 31 ? X0 + 4 : -1);
+    if (Xh >= 0 && Xh < a.W) {
+#pragma unroll
+      for (int t = 0; t < 8; ++t) {
+        const int Y = Yb + t;
+        if (Y < a.H) {
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(G + (int64_t)Y * a.W + Xh));
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(D + (int64_t)Y * a.W + Xh));
+        }
+      }
+    }
   }
   bool degen = false;
   lr_coeffs<RAD, false>(a.lr_x + p * (int64_t)a.h * a.w, a.lr_y + p * (int64_t)a.h * a.w, a.h, a.w,
@@ -783,11 +817,11 @@ void fused_joint_fwd(const float* lr_x, const float* lr_y, const float* hr_x, fl
                      int64_t C, int64_t h, int64_t w, int64_t H, int64_t W, int r, float eps,
                      uint32_t* status, cudaStream_t s) {
   const JointFns fns = pick_joint(r);
+  jf::FwdArgs a{lr_x, lr_y, hr_x, out, (int)h, (int)w, (int)H, (int)W, r, eps, status};
+  const int tx = (int)((w + jf::TLX - 1) / jf::TLX), ty = (int)((h + jf::TLY - 1) / jf::TLY);
   const size_t smem = jf::coef_smem_floats(r) * sizeof(float);
   set_smem(fns.fwd, smem);
-  dim3 grid((unsigned)((w + jf::TLX - 1) / jf::TLX), (unsigned)((h + jf::TLY - 1) / jf::TLY),
-            (unsigned)(B * C));
-  jf::FwdArgs a{lr_x, lr_y, hr_x, out, (int)h, (int)w, (int)H, (int)W, r, eps, status};
+  dim3 grid((unsigned)tx, (unsigned)ty, (unsigned)(B * C));
   launch(fns.fwd, grid, smem, s, &a);
 }
 
