@@ -152,6 +152,20 @@ int gn_backward(int dtype, const void* x, const void* dy, void* dx, void* dparam
                 int64_t hidden, int64_t H, int64_t W, void* workspace, size_t workspace_bytes,
                 uint32_t* status, void* stream);
 
+/* 1 when gn_forward / gn_backward of this shape take the fused fp32 kernels
+ * (for 16-byte aligned x, y, dy, dx), else 0. */
+int gn_is_fused(int dtype, int64_t Cin, int64_t Cout, int64_t hidden, int64_t H, int64_t W);
+
+/* gn_backward with `workspace` being the one gn_forward filled for this x and
+ * these params (same stream, parameters unchanged since): on the fused path
+ * the per-image input statistics and folded AdaptiveNorm constants are read
+ * from it instead of recomputed (the forward already checked x is finite).
+ * Elsewhere identical to gn_backward. */
+int gn_backward_reuse(int dtype, const void* x, const void* dy, void* dx, void* dparams,
+                      int accumulate, const void* params, int64_t B, int64_t Cin, int64_t Cout,
+                      int64_t hidden, int64_t H, int64_t W, void* workspace,
+                      size_t workspace_bytes, uint32_t* status, void* stream);
+
 /* ---- host-buffer entries: the reference's call shape (host images in, host
  * image out; gf/guided.py:152 guided_filter, :198 guided_filter_full) ----
  * Synchronous: the calls return when `out` (HOST memory) is written.  The

@@ -43,6 +43,9 @@ SIGNATURES = {
     "gn_forward": (_i, [_i, _p, _p, _p, _i64, _i64, _i64, _i64, _i64, _i64, _p, _sz, _p, _p]),
     "gn_backward": (_i, [_i, _p, _p, _p, _p, _i, _p, _i64, _i64, _i64, _i64, _i64, _i64, _p,
                          _sz, _p, _p]),
+    "gn_backward_reuse": (_i, [_i, _p, _p, _p, _p, _i, _p, _i64, _i64, _i64, _i64, _i64, _i64, _p,
+                         _sz, _p, _p]),
+    "gn_is_fused": (_i, [_i, _i64, _i64, _i64, _i64, _i64]),
     "gf_mse_loss": (_i, [_i, _p, _p, _p, _p, _i64, _i64, _i64, _i64, _p, _sz, _p]),
     "gf_mse_workspace_bytes": (_sz, [_i64, _i64, _i64, _i64]),
     "gnk_param_count": (_i64, [_i64, _i64, _i64, _i]),

@@ -19,6 +19,8 @@ thread_local int g_force_generic = 0;
 // full-res fp32 forward kernel: 0 = automatic, 1 = batch/TMA kernel, 2 = segment
 // kernel, 3 = segment kernel with 8 columns per lane only
 thread_local int g_highres_variant = 0;
+// set by gn_backward_reuse for the duration of its gn_backward call
+thread_local bool g_gn_reuse = false;
 
 int fail(int code, const char* fmt, ...) {
   va_list ap;
@@ -416,8 +418,8 @@ int gn_backward(int dtype, const void* x, const void* dy, void* dx, void* dparam
   if (!g_force_generic && dtype == GF_F32 && gfb::gn_fast_ok(Cin, Cout, hidden, H * W) &&
       aligned16(x) && aligned16(dy) && aligned16(dx)) {
     gfb::gn_fast_backward((const float*)x, (const float*)dy, (float*)dx, (float*)dparams,
-                          accumulate, (const float*)params, B, hidden, H * W, workspace, status,
-                          S(stream));
+                          accumulate, (const float*)params, B, hidden, H * W, workspace,
+                          g_gn_reuse, status, S(stream));
     return check_launch("gn_backward[fused]");
   }
   if (dtype == GF_F32)
@@ -429,6 +431,22 @@ int gn_backward(int dtype, const void* x, const void* dy, void* dx, void* dparam
                                   (double*)dparams, accumulate, (const double*)params, B, Cin,
                                   Cout, hidden, H * W, workspace, status, S(stream));
   return check_launch("gn_backward");
+}
+
+int gn_is_fused(int dtype, int64_t Cin, int64_t Cout, int64_t hidden, int64_t H, int64_t W) {
+  return !g_force_generic && dtype == GF_F32 && gfb::gn_fast_ok(Cin, Cout, hidden, H * W) ? 1
+                                                                                        : 0;
+}
+
+int gn_backward_reuse(int dtype, const void* x, const void* dy, void* dx, void* dparams,
+                      int accumulate, const void* params, int64_t B, int64_t Cin, int64_t Cout,
+                      int64_t hidden, int64_t H, int64_t W, void* workspace,
+                      size_t workspace_bytes, uint32_t* status, void* stream) {
+  g_gn_reuse = true;
+  const int rc = gn_backward(dtype, x, dy, dx, dparams, accumulate, params, B, Cin, Cout, hidden,
+                             H, W, workspace, workspace_bytes, status, stream);
+  g_gn_reuse = false;
+  return rc;
 }
 
 // ---------------------------------------------------------------------------

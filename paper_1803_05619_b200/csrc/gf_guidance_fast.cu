@@ -600,8 +600,8 @@ void forward(const float* x, float* y, const float* params, int64_t B, int64_t H
 
 template <int HID>
 void backward(const float* x, const float* dy, float* dx, float* dparams, int accumulate,
-              const float* params, int64_t B, int64_t HW, void* ws, uint32_t* status,
-              cudaStream_t s) {
+              const float* params, int64_t B, int64_t HW, void* ws, bool have_fold,
+              uint32_t* status, cudaStream_t s) {
   Carve c{(char*)ws};
   double* stats = c.take<double>((size_t)B * kBlocks * 9);
   float* fold = c.take<float>((size_t)B * F<HID>::count);
@@ -610,8 +610,10 @@ void backward(const float* x, const float* dy, float* dx, float* dparams, int ac
   double* gsum = c.take<double>((size_t)B * (CO * HID + CO + 2));
   double* pb = c.take<double>((size_t)B * kBlocks * HID * CI);
   dim3 grid(kBlocks, (unsigned)B);
-  k_stats<<<grid, NT, 0, s>>>(x, stats, HW, status);
-  k_prep<HID><<<(unsigned)B, 32, 0, s>>>(stats, params, fold, HW, kBlocks);
+  if (!have_fold) {  // else `ws` holds forward()'s folded constants of this x and params
+    k_stats<<<grid, NT, 0, s>>>(x, stats, HW, status);
+    k_prep<HID><<<(unsigned)B, 32, 0, s>>>(stats, params, fold, HW, kBlocks);
+  }
   k_bwd_a<HID><<<grid, NT, 0, s>>>(x, dy, params, fold, pa, HW);
   k_fin_a<HID><<<(unsigned)B, 128, 0, s>>>(pa, params, fold, coef, gsum, HW, kBlocks);
   k_bwd_b<HID><<<grid, NT, 0, s>>>(x, dy, dx, params, fold, coef, pb, HW);
@@ -650,15 +652,15 @@ void gn_fast_forward(const float* x, float* y, const float* params, int64_t B, i
 
 void gn_fast_backward(const float* x, const float* dy, float* dx, float* dparams, int accumulate,
                       const float* params, int64_t B, int64_t hidden, int64_t HW, void* ws,
-                      uint32_t* status, cudaStream_t s) {
+                      bool have_fold, uint32_t* status, cudaStream_t s) {
   switch (hidden) {
-    case 4: gnf::backward<4>(x, dy, dx, dparams, accumulate, params, B, HW, ws, status, s); break;
-    case 8: gnf::backward<8>(x, dy, dx, dparams, accumulate, params, B, HW, ws, status, s); break;
+    case 4: gnf::backward<4>(x, dy, dx, dparams, accumulate, params, B, HW, ws, have_fold, status, s); break;
+    case 8: gnf::backward<8>(x, dy, dx, dparams, accumulate, params, B, HW, ws, have_fold, status, s); break;
     case 15:
-      gnf::backward<15>(x, dy, dx, dparams, accumulate, params, B, HW, ws, status, s);
+      gnf::backward<15>(x, dy, dx, dparams, accumulate, params, B, HW, ws, have_fold, status, s);
       break;
     case 16:
-      gnf::backward<16>(x, dy, dx, dparams, accumulate, params, B, HW, ws, status, s);
+      gnf::backward<16>(x, dy, dx, dparams, accumulate, params, B, HW, ws, have_fold, status, s);
       break;
   }
 }

@@ -93,7 +93,7 @@ void gn_fast_forward(const float* x, float* y, const float* params, int64_t B, i
                      int64_t HW, void* ws, uint32_t* status, cudaStream_t s);
 void gn_fast_backward(const float* x, const float* dy, float* dx, float* dparams, int accumulate,
                       const float* params, int64_t B, int64_t hidden, int64_t HW, void* ws,
-                      uint32_t* status, cudaStream_t s);
+                      bool have_fold, uint32_t* status, cudaStream_t s);
 // guidance / core net with a k x k dilated first conv (gf_guidance_k.cu)
 size_t gnk_ws_bytes_impl(int64_t B, int64_t Cin, int64_t Cout, int64_t hid, int k, int64_t HW,
                          size_t es);

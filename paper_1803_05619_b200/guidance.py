@@ -39,6 +39,12 @@ def xavier_uniform(rng: np.random.Generator, out_ch: int, in_ch: int, kernel: in
 @dataclass
 class GuidanceTape:
     x: Img
+    # the forward's workspace (per-image statistics and folded AdaptiveNorm
+    # constants) when the fused fp32 kernels ran, and the parameter version
+    # it was computed with; backward reuses it while the parameters are
+    # unchanged
+    ws: torch.Tensor | None = None
+    ws_key: tuple | None = None
 
 
 class GuidanceNet:
@@ -125,12 +131,16 @@ class GuidanceNet:
         params = self._params_as(im.t.dtype)
         y = torch.empty((B, self.out_ch, H, W), dtype=im.t.dtype, device=self.device)
         status = Status(self.device)
+        tape = GuidanceTape(x=im)
         if self.kernel == 1:
             ws = workspace(lib.gn_workspace_bytes(dt, B, self.in_ch, self.out_ch, self.hidden, H,
                                                   W), self.device)
             rc = lib.gn_forward(dt, ptr(im.t), ptr(y), ptr(params), B, self.in_ch, self.out_ch,
                                 self.hidden, H, W, ptr(ws), ws.numel(), status.ptr,
                                 stream_ptr(self.device))
+            if (lib.gn_is_fused(dt, self.in_ch, self.out_ch, self.hidden, H, W)
+                    and ptr(im.t) % 16 == 0 and ptr(y) % 16 == 0):
+                tape.ws, tape.ws_key = ws, self._ws_key(im.t)
         else:
             ws = workspace(lib.gnk_workspace_bytes(dt, B, self.in_ch, self.out_ch, self.hidden,
                                                    self.kernel, H, W), self.device)
@@ -140,7 +150,10 @@ class GuidanceNet:
         _lib.check(rc, "GuidanceNet.forward")
         if check:
             status.raise_if_set("GuidanceNet.forward")
-        return restore(y, im), GuidanceTape(x=im)
+        return restore(y, im), tape
+
+    def _ws_key(self, x: torch.Tensor):
+        return (self.flat._version, x.data_ptr(), x._version, tuple(x.shape), x.dtype)
 
     def backward(self, tape: GuidanceTape, dy, *, dparams: torch.Tensor | None = None,
                  accumulate: bool = False, check: bool = True):
@@ -160,11 +173,16 @@ class GuidanceNet:
             dparams = torch.zeros(self.param_count(), dtype=im.t.dtype, device=self.device)
         status = Status(self.device)
         if self.kernel == 1:
-            ws = workspace(lib.gn_workspace_bytes(dt, B, self.in_ch, self.out_ch, self.hidden, H,
-                                                  W), self.device)
-            rc = lib.gn_backward(dt, ptr(im.t), ptr(d.t), ptr(dx), ptr(dparams), int(accumulate),
-                                 ptr(params), B, self.in_ch, self.out_ch, self.hidden, H, W,
-                                 ptr(ws), ws.numel(), status.ptr, stream_ptr(self.device))
+            # the forward's statistics are reused while x and the parameters
+            # are unchanged (gn_backward_reuse), else recomputed
+            reuse = tape.ws is not None and tape.ws_key == self._ws_key(im.t)
+            ws = tape.ws if reuse else workspace(
+                lib.gn_workspace_bytes(dt, B, self.in_ch, self.out_ch, self.hidden, H, W),
+                self.device)
+            fn = lib.gn_backward_reuse if reuse else lib.gn_backward
+            rc = fn(dt, ptr(im.t), ptr(d.t), ptr(dx), ptr(dparams), int(accumulate),
+                    ptr(params), B, self.in_ch, self.out_ch, self.hidden, H, W,
+                    ptr(ws), ws.numel(), status.ptr, stream_ptr(self.device))
         else:
             ws = workspace(lib.gnk_workspace_bytes(dt, B, self.in_ch, self.out_ch, self.hidden,
                                                    self.kernel, H, W), self.device)

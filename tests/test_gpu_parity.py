@@ -500,6 +500,34 @@ def test_fused_joint_nonfinite_input_is_input_error(gfb):
         gfb.forward_joint(lr_x, hr_x, lr_y, gfb.GuidedFilterParams(1, 1e-4))
 
 
+def test_guidance_backward_reuses_forward_statistics(gfb):
+    """gn_backward_reuse (the tape's forward workspace) is bitwise the full
+    recomputation; a parameter edit after the forward drops the reuse."""
+    from paper_1803_05619_b200 import _lib
+
+    lib = _lib.load()
+    assert lib.gn_is_fused(0, 3, 3, 15, 48, 64) == 1
+    rng = np.random.default_rng(7)
+    net = gfb.GuidanceNet(3, 3, hidden=15, rng=rng)
+    net.parameters()["norm.norm_gain"][:] = 0.4
+    x = t32(rng.uniform(0, 1, (2, 3, 48, 64)).astype(np.float32))
+    dy = t32(rng.standard_normal((2, 3, 48, 64)).astype(np.float32))
+    _, tape = net.forward(x)
+    assert tape.ws is not None
+    dx1, g1 = net.backward(tape, dy)
+    tape_fresh = gfb.guidance.GuidanceTape(x=tape.x)
+    dx2, g2 = net.backward(tape_fresh, dy)
+    assert torch.equal(dx1, dx2)
+    for k in g1:
+        assert torch.equal(g1[k], g2[k]), k
+    # parameters edited after the forward: the stale statistics are not used
+    net.parameters()["norm.norm_gain"][:] = 0.9
+    dx3, _ = net.backward(tape, dy)
+    dx4, _ = net.backward(gfb.guidance.GuidanceTape(x=tape.x), dy)
+    assert torch.equal(dx3, dx4)
+    assert not torch.equal(dx3, dx1)
+
+
 @pytest.mark.parametrize("hidden", [4, 8, 15, 16])
 def test_fused_guidance_net_vs_oracle(gfb, hidden):
     from paper_1803_05619_b200 import _lib
