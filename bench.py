@@ -42,7 +42,7 @@ sys.path.insert(0, ROOT)
 
 METRIC = "guided-filter output Mpix/s (fwd, fwd+bwd) and % of HBM roofline"
 
-from paper_1803_05619_b200.sharding import batch_shard, row_bands  # noqa: E402
+from paper_1803_05619_b200.sharding import allreduce_grads, batch_shard, row_bands  # noqa: E402
 
 
 # ---------------------------------------------------------------------------
@@ -170,7 +170,7 @@ class OursStep:
         import workloads
         from paper_1803_05619_b200 import _lib
 
-        self.c, self.device = c, device
+        self.c, self.device, self.world = c, device, world
         self.lib = _lib.load()
         self.stream = torch.cuda.current_stream(device)
         self.sp = self.stream.cuda_stream
@@ -265,6 +265,8 @@ class OursStep:
 
             lx, ly, hx = self.inputs
             self.res = gfb.train_step(self.net, lx, hx, ly, self.target, self.params)
+            if self.world > 1:  # data-parallel: the 95-float gradient sum (NCCL)
+                allreduce_grads(self.res.dparams)
 
     def e2e(self, steps, warmup):
         """Public API with pinned host buffers, H2D + D2H inside the timed region."""
