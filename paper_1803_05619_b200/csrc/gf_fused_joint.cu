@@ -518,43 +518,69 @@ __global__ void __launch_bounds__(NT, 4) k_joint_bwd_hr(BwdHrArgs a) {
     }
   }
   // row partials of the adjoint: R[y][k] = sum_X wx(X, k) * (d, d*G) over
-  // X in [4k-2, 4k+5] (every hr column whose taps touch lr column k)
+  // X in [4k-2, 4k+5] (every hr column whose taps touch lr column k): the
+  // lane's own 16-byte chunk plus 2 columns of each neighbour lane by shuffle;
+  // lanes 0 and 31 load the chunk outside the tile alongside their own
   {
     const int k = k0 + lane;
     float wx[8];
+    if (k >= 1 && k <= a.w - 2) {  // interior: the static transposed taps
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const int X = 4 * k - 2 + j;
-      wx[j] = 0.f;
-      if (X >= 0 && X < a.W) {
-        const Tap tx = tap4(X, a.w);
-        if (tx.lo == k) wx[j] += 1.f - tx.f;
-        if (tx.hi == k) wx[j] += tx.f;
+      for (int j = 0; j < 8; ++j) wx[j] = (j < 4 ? 2 * j + 1 : 15 - 2 * j) * 0.125f;
+    } else {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int X = 4 * k - 2 + j;
+        wx[j] = 0.f;
+        if (X >= 0 && X < a.W) {
+          const Tap tx = tap4(X, a.w);
+          if (tx.lo == k) wx[j] += 1.f - tx.f;
+          if (tx.hi == k) wx[j] += tx.f;
+        }
       }
     }
-    const bool left = 4 * k - 4 >= 0, right = 4 * k + 4 < a.W;
+    const int Xe = lane == 0 ? 4 * k - 4 : 4 * k + 4;  // edge lanes' outside chunk
+    const bool edge = (lane == 0 || lane == 31) && Xe >= 0 && Xe < a.W;
 #pragma unroll 2
     for (int yl = warp; yl < GR; yl += NT / 32) {
       const int Y = 4 * i0 - 2 + yl;
-      float s1 = 0.f, s2 = 0.f;
-      if (Y >= 0 && Y < a.H && k < a.w) {
-        const float* drow = D + (int64_t)Y * a.W + 4 * k;
-        const float* grow = G + (int64_t)Y * a.W + 4 * k;
-        const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
-        const float4 d0 = left ? __ldg(reinterpret_cast<const float4*>(drow - 4)) : z;
-        const float4 d1 = __ldg(reinterpret_cast<const float4*>(drow));
-        const float4 d2 = right ? __ldg(reinterpret_cast<const float4*>(drow + 4)) : z;
-        const float4 g0 = left ? __ldg(reinterpret_cast<const float4*>(grow - 4)) : z;
-        const float4 g1 = __ldg(reinterpret_cast<const float4*>(grow));
-        const float4 g2 = right ? __ldg(reinterpret_cast<const float4*>(grow + 4)) : z;
-        const float dd[8] = {d0.z, d0.w, d1.x, d1.y, d1.z, d1.w, d2.x, d2.y};
-        const float gg[8] = {g0.z, g0.w, g1.x, g1.y, g1.z, g1.w, g2.x, g2.y};
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          s1 += wx[j] * dd[j];
-          s2 += wx[j] * (dd[j] * gg[j]);
-        }
+      const bool row = Y >= 0 && Y < a.H;
+      const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+      float4 d1 = z, g1 = z, de = z, ge = z;
+      if (row && k < a.w) {
+        d1 = __ldg(reinterpret_cast<const float4*>(D + (int64_t)Y * a.W + 4 * k));
+        g1 = __ldg(reinterpret_cast<const float4*>(G + (int64_t)Y * a.W + 4 * k));
       }
+      if (row && edge) {
+        de = __ldg(reinterpret_cast<const float4*>(D + (int64_t)Y * a.W + Xe));
+        ge = __ldg(reinterpret_cast<const float4*>(G + (int64_t)Y * a.W + Xe));
+      }
+      const float4 q1 = make_float4(d1.x * g1.x, d1.y * g1.y, d1.z * g1.z, d1.w * g1.w);
+      float dl0 = __shfl_up_sync(0xffffffffu, d1.z, 1), dl1 = __shfl_up_sync(0xffffffffu, d1.w, 1);
+      float ql0 = __shfl_up_sync(0xffffffffu, q1.z, 1), ql1 = __shfl_up_sync(0xffffffffu, q1.w, 1);
+      float dr0 = __shfl_down_sync(0xffffffffu, d1.x, 1), dr1 = __shfl_down_sync(0xffffffffu, d1.y, 1);
+      float qr0 = __shfl_down_sync(0xffffffffu, q1.x, 1), qr1 = __shfl_down_sync(0xffffffffu, q1.y, 1);
+      if (lane == 0) {
+        dl0 = de.z;
+        dl1 = de.w;
+        ql0 = de.z * ge.z;
+        ql1 = de.w * ge.w;
+      }
+      if (lane == 31) {
+        dr0 = de.x;
+        dr1 = de.y;
+        qr0 = de.x * ge.x;
+        qr1 = de.y * ge.y;
+      }
+      const float dd[8] = {dl0, dl1, d1.x, d1.y, d1.z, d1.w, dr0, dr1};
+      const float qq[8] = {ql0, ql1, q1.x, q1.y, q1.z, q1.w, qr0, qr1};
+      float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        s1 += wx[j] * dd[j];
+        s2 += wx[j] * qq[j];
+      }
+      if (!(row && k < a.w)) s1 = s2 = 0.f;
       R1[yl * TLX + lane] = s1;
       R2[yl * TLX + lane] = s2;
     }
