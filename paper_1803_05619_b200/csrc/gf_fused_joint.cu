@@ -420,12 +420,13 @@ __global__ void __launch_bounds__(NT, 4) k_joint_bwd_hr(BwdHrArgs a) {
   const int Yb = 4 * i0 + 8 * warp;
   const bool col_ok = X0 < a.W;
 
-  float4 dv[8];
+  // the d_out tile is read after the coefficient phase (registers stay free
+  // for it); its DRAM reads start now, into L2
 #pragma unroll
   for (int t = 0; t < 8; ++t) {
     const int Y = Yb + t;
-    dv[t] = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (col_ok && Y < a.H) dv[t] = __ldg(reinterpret_cast<const float4*>(D + (int64_t)Y * a.W + X0));
+    if (col_ok && Y < a.H)
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(D + (int64_t)Y * a.W + X0));
   }
   // the gather below reads hr_x (and the 2-pixel halo of both fields) only
   // after the coefficient phase: start those DRAM reads now, into L2
@@ -463,6 +464,13 @@ __global__ void __launch_bounds__(NT, 4) k_joint_bwd_hr(BwdHrArgs a) {
   bool degen = false;
   lr_coeffs<RAD, false>(a.lr_x + p * (int64_t)a.h * a.w, a.lr_y + p * (int64_t)a.h * a.w, a.h, a.w,
                    i0, k0, a.eps, sm, degen);
+  float4 dv[8];
+#pragma unroll
+  for (int t = 0; t < 8; ++t) {
+    const int Y = Yb + t;
+    dv[t] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (col_ok && Y < a.H) dv[t] = __ldg(reinterpret_cast<const float4*>(D + (int64_t)Y * a.W + X0));
+  }
   // d_hr = d_out * Up(A)
   {
     const ColTaps ct = col_taps(X0, a.w, k0);
