@@ -231,10 +231,13 @@ class OursStep:
             fused = self.lib.gf_joint_is_fused(0, B, C, self.h, self.w, self.H, self.W, c["r"])
             fwd = 1 if fused else 12
             bwd = 2 if fused else 26
-            # train step: 2 x (stats, norm, fwd) guidance, GF fwd, mse (2), GF bwd,
-            # 2 x (stats, norm, bwd1, sum1, dx, dw1, final) guidance backward
+            # train step: 2 x (stats, norm, fwd) guidance, the fused GF fwd + MSE +
+            # bwd (hr pass, loss sum, lr tail; unfused: GF fwd, mse (2), GF bwd),
+            # 2 x (bwd1, sum1, dx, dw1, final) guidance backward (the forward's
+            # statistics are reused)
+            gf_step = 3 if fused else fwd + 2 + bwd
             self.launches = {"joint_fwd": fwd, "joint_fwd_bwd": fwd + bwd,
-                             "train_step": 2 * 3 + fwd + 2 + bwd + 2 * 7}[kind]
+                             "train_step": 2 * 3 + gf_step + 2 * 5}[kind]
 
     def step(self):
         c, L = self.c, self.lib
@@ -276,7 +279,12 @@ class OursStep:
 
         c = self.c
         host_in = [t.cpu().pin_memory() for t in self.inputs]
-        host_out = torch.empty(self.out.shape, dtype=self.out.dtype).pin_memory()
+        if self.kind == "train_step":
+            # the target is a step input too; the step's host result is the loss
+            host_in.append(self.target.cpu().pin_memory())
+            host_out = torch.empty((), dtype=torch.float64).pin_memory()
+        else:
+            host_out = torch.empty(self.out.shape, dtype=self.out.dtype).pin_memory()
         p = gfb.GuidedFilterParams(c["r"], c["eps"])
 
         def one():
@@ -296,8 +304,8 @@ class OursStep:
                 gr = gfb.backward(tape, out, check=False)  # d_out = out (<out,out>/2 probe)
                 res = gr.d_guide_hi
             else:
-                r = gfb.train_step(self.net, dev[0], dev[2], dev[1], self.target, p)
-                res = r.out
+                r = gfb.train_step(self.net, dev[0], dev[2], dev[1], dev[3], p)
+                res = r.loss
             host_out.copy_(res, non_blocking=True)
 
         for _ in range(warmup):

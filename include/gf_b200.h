@@ -234,6 +234,22 @@ int gf_mse_loss(int dtype, const void* out, const void* target, void* d_out, dou
                 int64_t B, int64_t C, int64_t H, int64_t W, void* workspace,
                 size_t workspace_bytes, void* stream);
 
+/* Fused training step of the fast layer: the loss and gradients that
+ * gf/training.py:230-235 (eval_and_grads) takes from forward_joint ->
+ * mse_loss -> backward, i.e. loss = mean over images of mean((out -
+ * target)^2) (gf/training.py:93-101) and its gradients w.r.t. lr_x (the
+ * guide_lo), lr_y (src_lo) and hr_x (guide_hi), in one hr pass: out and
+ * d_out = 2 (out - target) / (C H W B) never reach HBM.  target: (B, C, H, W);
+ * loss: one float64 on the device. */
+size_t gf_joint_mse_workspace_bytes(int dtype, int64_t B, int64_t C, int64_t h, int64_t w,
+                                    int64_t H, int64_t W, int radius);
+
+int gf_joint_mse_bwd(int dtype, const void* lr_x, const void* lr_y, const void* hr_x,
+                     const void* target, double* loss, void* d_lr_x, void* d_lr_y, void* d_hr_x,
+                     int64_t B, int64_t C, int64_t h, int64_t w, int64_t H, int64_t W,
+                     int radius, double eps, void* workspace, size_t workspace_bytes,
+                     uint32_t* status, void* stream);
+
 size_t gf_mse_workspace_bytes(int64_t B, int64_t C, int64_t H, int64_t W);
 
 #ifdef __cplusplus

@@ -48,6 +48,9 @@ SIGNATURES = {
     "gn_is_fused": (_i, [_i, _i64, _i64, _i64, _i64, _i64]),
     "gf_mse_loss": (_i, [_i, _p, _p, _p, _p, _i64, _i64, _i64, _i64, _p, _sz, _p]),
     "gf_mse_workspace_bytes": (_sz, [_i64, _i64, _i64, _i64]),
+    "gf_joint_mse_workspace_bytes": (_sz, [_i, _i64, _i64, _i64, _i64, _i64, _i64, _i]),
+    "gf_joint_mse_bwd": (_i, [_i, _p, _p, _p, _p, _p, _p, _p, _p, _i64, _i64, _i64, _i64, _i64,
+                              _i64, _i, _d, _p, _sz, _p, _p]),
     "gnk_param_count": (_i64, [_i64, _i64, _i64, _i]),
     "gnk_workspace_bytes": (_sz, [_i, _i64, _i64, _i64, _i64, _i, _i64, _i64]),
     "gnk_forward": (_i, [_i, _p, _p, _p, _i64, _i64, _i64, _i64, _i, _i, _i64, _i64, _p, _sz, _p,
@@ -70,6 +73,9 @@ EXTRA = {
     "gf_force_generic": (_i, [_i]),
     "gf_highres_variant": (_i, [_i]),
     "gf_joint_bwd_lr_variant": (_i, [_i]),
+    "gf_joint_mse_variant": (_i, [_i]),
+    "gf_joint_fwd_variant": (_i, [_i]),
+    "gf_gn_bwd_variant": (_i, [_i]),
     "gf_joint_is_fused": (_i, [_i, _i64, _i64, _i64, _i64, _i64, _i64, _i]),
     "gf_highres_fwd_is_fused": (_i, [_i, _i64, _i64, _i64, _i64, _i64, _i]),
 }

@@ -108,6 +108,30 @@ int gf_joint_bwd_lr_variant(int v) {
   return old;
 }
 
+// Test hook: CTAs per SM the fused training-step hr kernel is compiled for
+// (0 automatic = 3, or 2 or 4 at r = 1) on THIS thread.  Returns the old value.
+int gf_joint_mse_variant(int v) {
+  int old = gfb::g_joint_mse_variant;
+  gfb::g_joint_mse_variant = v;
+  return old;
+}
+
+// Test hook: coefficient-pass chunking of the r = 8 joint forward (0 default,
+// 1..4 alternatives) on THIS thread.  Returns the old value.
+int gf_joint_fwd_variant(int v) {
+  int old = gfb::g_joint_fwd_variant;
+  gfb::g_joint_fwd_variant = v;
+  return old;
+}
+
+// Test hook: fused fp32 guidance-net backward of THIS thread (0 one heavy
+// pass + dx fix-up, 1 the two-heavy-pass kernels).  Returns the old value.
+int gf_gn_bwd_variant(int v) {
+  int old = gfb::g_gn_bwd_variant;
+  gfb::g_gn_bwd_variant = v;
+  return old;
+}
+
 int gf_joint_is_fused(int dtype, int64_t B, int64_t C, int64_t h, int64_t w, int64_t H,
                       int64_t W, int r) {
   return use_fused_joint(dtype, B, C, h, w, H, W, r) ? 1 : 0;
@@ -577,6 +601,54 @@ int gf_mse_loss(int dtype, const void* out, const void* target, void* d_out, dou
     gfb::mse_impl<double>((const double*)out, (const double*)target, (double*)d_out, loss, B,
                           C * H * W, workspace, S(stream));
   return check_launch("gf_mse_loss");
+}
+
+// ---- fused training step of the fast layer (forward + MSE + backward) ----
+static size_t al256(size_t n) { return (n + 255) / 256 * 256; }
+
+size_t gf_joint_mse_workspace_bytes(int dtype, int64_t B, int64_t C, int64_t h, int64_t w,
+                                    int64_t H, int64_t W, int radius) {
+  if (use_fused_joint(dtype, B, C, h, w, H, W, radius))
+    return gfb::fused_joint_mse_ws_bytes(B, C, h, w);
+  const size_t es = dtype == GF_F64 ? 8 : 4;
+  return al256(gf_joint_workspace_bytes(dtype, B, C, h, w, H, W, radius)) +
+         al256(gfb::mse_ws_bytes(B)) + 2 * al256((size_t)B * C * H * W * es);
+}
+
+int gf_joint_mse_bwd(int dtype, const void* lr_x, const void* lr_y, const void* hr_x,
+                     const void* target, double* loss, void* d_lr_x, void* d_lr_y, void* d_hr_x,
+                     int64_t B, int64_t C, int64_t h, int64_t w, int64_t H, int64_t W,
+                     int radius, double eps, void* workspace, size_t workspace_bytes,
+                     uint32_t* status, void* stream) {
+  if (int e = check_joint(dtype, B, C, h, w, H, W, radius, eps)) return e;
+  const size_t need = gf_joint_mse_workspace_bytes(dtype, B, C, h, w, H, W, radius);
+  if (workspace_bytes < need)
+    return fail(GF_ERR_WORKSPACE, "joint mse workspace %zu < %zu bytes", workspace_bytes, need);
+  if (use_fused_joint(dtype, B, C, h, w, H, W, radius) && aligned16(lr_x) && aligned16(lr_y) &&
+      aligned16(hr_x) && aligned16(target) && aligned16(d_lr_x) && aligned16(d_lr_y) &&
+      aligned16(d_hr_x)) {
+    gfb::fused_joint_mse_bwd((const float*)lr_x, (const float*)lr_y, (const float*)hr_x,
+                             (const float*)target, loss, (float*)d_lr_x, (float*)d_lr_y,
+                             (float*)d_hr_x, B, C, h, w, H, W, radius, (float)eps, workspace,
+                             status, S(stream));
+    return check_launch("gf_joint_mse_bwd[fused]");
+  }
+  // any other call: forward, MSE and backward through the three entries, with
+  // out and d_out in the workspace
+  const size_t es = dtype == GF_F64 ? 8 : 4;
+  const size_t jws = al256(gf_joint_workspace_bytes(dtype, B, C, h, w, H, W, radius));
+  const size_t mws = al256(gfb::mse_ws_bytes(B));
+  const size_t hb = al256((size_t)B * C * H * W * es);
+  char* base = (char*)workspace;
+  void* out = base + jws + mws;
+  void* d_out = base + jws + mws + hb;
+  if (int e = gf_joint_fwd(dtype, lr_x, lr_y, hr_x, out, B, C, h, w, H, W, radius, eps, base,
+                           jws, status, stream))
+    return e;
+  if (int e = gf_mse_loss(dtype, out, target, d_out, loss, B, C, H, W, base + jws, mws, stream))
+    return e;
+  return gf_joint_bwd(dtype, lr_x, lr_y, hr_x, d_out, d_lr_x, d_lr_y, d_hr_x, B, C, h, w, H, W,
+                      radius, eps, base, jws, status, stream);
 }
 
 }  // extern "C"

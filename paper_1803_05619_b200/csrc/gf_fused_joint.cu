@@ -94,7 +94,10 @@ __device__ inline SmemCoef carve(float* base, int r) {
 }
 
 // A (and b) for low-res cells [i0-1, i0+TLY] x [k0-1, k0+TLX] of one plane.
-template <int RAD, bool NEED_B>
+// VCH: row chunks of the vertical pass (0: as many as the CTA's threads
+// allow); HCH: column chunks per row of the horizontal pass.  Each chunk pays
+// a 2r warm-up, so large radii favour fewer, longer chunks.
+template <int RAD, bool NEED_B, int VCH = 0, int HCH = 16>
 __device__ void lr_coeffs(const float* __restrict__ X, const float* __restrict__ Y, int h, int w,
                           int i0, int k0, float eps, const SmemCoef& sm, bool& degen) {
   constexpr int r = RAD;
@@ -136,7 +139,8 @@ __device__ void lr_coeffs(const float* __restrict__ X, const float* __restrict__
     // the columns of a chunk are padded to a multiple of 32
     constexpr int CW = (CA + 2 * r + 31) / 32 * 32;
     constexpr int VP = pitch16(CA + 2 * r);
-    constexpr int nch = NT / CW > 0 ? (NT / CW < RA ? NT / CW : RA) : 1;
+    constexpr int nch =
+        VCH > 0 ? VCH : (NT / CW > 0 ? (NT / CW < RA ? NT / CW : RA) : 1);
     constexpr int rc = (RA + nch - 1) / nch;
     for (int it = tid; it < CW * nch; it += NT) {
       const int col = it % CW, ch = it / CW;
@@ -172,8 +176,8 @@ __device__ void lr_coeffs(const float* __restrict__ X, const float* __restrict__
   // 3) horizontal sliding sums + coefficients: item = (row, chunk of cols)
   {
     // 16 items per row (2 rows per warp, 16 banks apart), runs of 3 columns
-    constexpr int nch = 16;
-    constexpr int cc = (CA + 11) / 12;
+    constexpr int nch = HCH;
+    constexpr int cc = HCH == 16 ? (CA + 11) / 12 : (CA + HCH - 1) / HCH;
     constexpr int VP = pitch16(CA + 2 * r);
     for (int it = tid; it < RA * nch; it += NT) {
       const int a = it / nch, ch = it - a * nch;
@@ -273,7 +277,7 @@ __device__ __forceinline__ void hrow(const float* __restrict__ row, const ColTap
   }
 }
 
-template <int RAD>
+template <int RAD, int VCH = 0, int HCH = 16>
 __global__ void __launch_bounds__(NT, (RAD >= 2 && RAD <= 4) ? 4 : 3) k_joint_fwd(FwdArgs a) {
   extern __shared__ float4 smem4[];
   constexpr int r = RAD;
@@ -297,8 +301,8 @@ __global__ void __launch_bounds__(NT, (RAD >= 2 && RAD <= 4) ? 4 : 3) k_joint_fw
   }
   // 2) coefficients of the block
   bool degen = false;
-  lr_coeffs<RAD, true>(a.lr_x + p * (int64_t)a.h * a.w, a.lr_y + p * (int64_t)a.h * a.w, a.h, a.w, i0,
-                  k0, a.eps, sm, degen);
+  lr_coeffs<RAD, true, VCH, HCH>(a.lr_x + p * (int64_t)a.h * a.w, a.lr_y + p * (int64_t)a.h * a.w,
+                                 a.h, a.w, i0, k0, a.eps, sm, degen);
   // 3) apply
   const ColTaps ct = col_taps(X0, a.w, k0);
   // static column taps (measured: faster for r <= 4, 3 % slower at r = 8)
@@ -632,6 +636,316 @@ __global__ void __launch_bounds__(NT, 4) k_joint_bwd_hr(BwdHrArgs a) {
 }
 
 // ---------------------------------------------------------------------------
+// training step, fused: forward + MSE + backward hr pass
+// ---------------------------------------------------------------------------
+// A training step needs the loss and the gradients only (gf/training.py:230-235,
+// eval_and_grads), and d_out = 2 (out - target) / (C H W B) is local
+// (gf/training.py:93-101, batch mean of the per-image losses).  So per tile:
+// recompute A and b (step 2 of the forward), then for every row of the
+// 68-row gather window (tile + 2-pixel halo) form out = Up(b) + Up(A) hr_x,
+// e = out - target, d_out, and do what k_joint_bwd_hr does with it -- the
+// tile's d_hr_x = d_out Up(A) and the two bilinear adjoints -- with the
+// per-CTA sum of e^2 (float64) as the loss partial.  Neither out nor d_out
+// touches HBM: hr_x and target are each read once.
+//
+// Rows: warp w takes gather rows 8w .. 8w+7, whose taps use coefficient rows
+// 2w .. 2w+2 (pre-interpolated horizontally once), and warps 0..3 one of the
+// rows 64..67 (coefficient rows 16, 17).  The 2 halo columns on each side of
+// the tile (taps of lr columns k0 and k0+31) are added to the row partials by
+// a scalar pass per warp.
+struct MseHrArgs {
+  const float* lr_x;
+  const float* lr_y;
+  const float* hr_x;
+  const float* target;
+  float* d_hr;
+  float* db;
+  float* dA;
+  double* loss_part;  // one per CTA: (plane, tile row, tile column)
+  int h, w, H, W, r;
+  float eps, scale2;
+  uint32_t* status;
+};
+
+template <int RAD, int MINB>
+__global__ void __launch_bounds__(NT, MINB) k_joint_mse_hr(MseHrArgs a) {
+  extern __shared__ float4 smem4[];
+  __shared__ double red[NT / 32];
+  constexpr int r = RAD;
+  float* base = reinterpret_cast<float*>(smem4);
+  const SmemCoef sm = carve(base, r);
+  float* R1 = base + coef_smem_floats(r);  // [GR][TLX]
+  float* R2 = R1 + GR * TLX;
+  const int64_t p = blockIdx.z;
+  const int i0 = blockIdx.y * TLY, k0 = blockIdx.x * TLX;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t hplane = (int64_t)a.H * a.W;
+  const float* __restrict__ G = a.hr_x + p * hplane;
+  const float* __restrict__ T = a.target + p * hplane;
+  float* __restrict__ DH = a.d_hr + p * hplane;
+  const int k = k0 + lane;
+  const int X0 = 4 * k;
+  const bool col_ok = k < a.w;  // W == 4 w
+  const int Yg = 4 * i0 - 2;    // hr row of gather row 0
+  const bool extra = warp < 4;  // takes gather row 64 + warp as well
+
+  // this warp's rows of hr_x and target (and the halo chunks the scalar pass
+  // reads) start their DRAM reads into L2 before the coefficient phase
+  {
+    const int Xh = lane == 0 ? X0 - 4 : (lane == 31 ? X0 + 4 : -1);
+#pragma unroll
+    for (int t = 0; t < 9; ++t) {
+      if (t == 8 && !extra) break;
+      const int Y = Yg + (t < 8 ? 8 * warp + t : 64 + warp);
+      if (Y < 0 || Y >= a.H) continue;
+      if (col_ok) {
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(G + (int64_t)Y * a.W + X0));
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(T + (int64_t)Y * a.W + X0));
+      }
+      if (Xh >= 0 && Xh < a.W) {
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(G + (int64_t)Y * a.W + Xh));
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(T + (int64_t)Y * a.W + Xh));
+      }
+    }
+  }
+  bool degen = false;
+  lr_coeffs<RAD, true>(a.lr_x + p * (int64_t)a.h * a.w, a.lr_y + p * (int64_t)a.h * a.w, a.h, a.w,
+                       i0, k0, a.eps, sm, degen);
+
+  const ColTaps ct = col_taps(X0, a.w, k0);
+  const bool cin = k >= 1 && k <= a.w - 2;  // static column taps
+  auto hrow2 = [&](int rl, float (&ha)[4], float (&hb)[4]) {
+    if (cin) {
+      hrow_interior(sm.As + rl * CAP, lane, ha);
+      hrow_interior(sm.Bs + rl * CAP, lane, hb);
+    } else {
+      hrow(sm.As + rl * CAP, ct, ha);
+      hrow(sm.Bs + rl * CAP, ct, hb);
+    }
+  };
+  // adjoint weights of hr columns 4k-2 .. 4k+5 into lr column k
+  float wx[8];
+  if (cin) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) wx[j] = (j < 4 ? 2 * j + 1 : 15 - 2 * j) * 0.125f;
+  } else {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int X = 4 * k - 2 + j;
+      wx[j] = 0.f;
+      if (X >= 0 && X < a.W) {
+        const Tap tx = tap4(X, a.w);
+        if (tx.lo == k) wx[j] += 1.f - tx.f;
+        if (tx.hi == k) wx[j] += tx.f;
+      }
+    }
+  }
+
+  float lsum = 0.f, chk = 0.f;
+  const float scale2 = a.scale2;
+  // gather row yl, its coefficient rows interpolated horizontally (lo, hi)
+  // and the vertical weight f
+  auto do_row = [&](int yl, const float (&alo)[4], const float (&ahi)[4], const float (&blo)[4],
+                    const float (&bhi)[4], float f) {
+    const int Y = Yg + yl;
+    const bool in = col_ok && Y >= 0 && Y < a.H;
+    float4 g4 = make_float4(0.f, 0.f, 0.f, 0.f), t4 = g4;
+    if (in) {
+      g4 = __ldg(reinterpret_cast<const float4*>(G + (int64_t)Y * a.W + X0));
+      t4 = __ldg(reinterpret_cast<const float4*>(T + (int64_t)Y * a.W + X0));
+    }
+    const float gv[4] = {g4.x, g4.y, g4.z, g4.w}, tv[4] = {t4.x, t4.y, t4.z, t4.w};
+    const bool own = in && yl >= 2 && yl < 2 + THY;
+    float d[4], q[4], dh[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float Ah = alo[j] + f * (ahi[j] - alo[j]);
+      const float Bh = blo[j] + f * (bhi[j] - blo[j]);
+      const float o = Bh + Ah * gv[j];
+      const float e = o - tv[j];
+      d[j] = in ? scale2 * e : 0.f;
+      q[j] = d[j] * gv[j];
+      dh[j] = d[j] * Ah;
+      if (own) {
+        lsum = fmaf(e, e, lsum);
+        chk += o - o;  // NaN iff an output is not finite
+      }
+    }
+    if (own)
+      *reinterpret_cast<float4*>(DH + (int64_t)Y * a.W + X0) = make_float4(dh[0], dh[1], dh[2], dh[3]);
+    float dl0 = __shfl_up_sync(0xffffffffu, d[2], 1), dl1 = __shfl_up_sync(0xffffffffu, d[3], 1);
+    float ql0 = __shfl_up_sync(0xffffffffu, q[2], 1), ql1 = __shfl_up_sync(0xffffffffu, q[3], 1);
+    float dr0 = __shfl_down_sync(0xffffffffu, d[0], 1), dr1 = __shfl_down_sync(0xffffffffu, d[1], 1);
+    float qr0 = __shfl_down_sync(0xffffffffu, q[0], 1), qr1 = __shfl_down_sync(0xffffffffu, q[1], 1);
+    if (lane == 0) dl0 = dl1 = ql0 = ql1 = 0.f;  // halo columns: the scalar pass
+    if (lane == 31) dr0 = dr1 = qr0 = qr1 = 0.f;
+    const float dd[8] = {dl0, dl1, d[0], d[1], d[2], d[3], dr0, dr1};
+    const float qq[8] = {ql0, ql1, q[0], q[1], q[2], q[3], qr0, qr1};
+    float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      s1 += wx[j] * dd[j];
+      s2 += wx[j] * qq[j];
+    }
+    if (!in) s1 = s2 = 0.f;
+    R1[yl * TLX + lane] = s1;
+    R2[yl * TLX + lane] = s2;
+  };
+
+  {
+    float HA[3][4], HB[3][4];  // coefficient rows 2w, 2w+1, 2w+2
+#pragma unroll
+    for (int q = 0; q < 3; ++q) hrow2(2 * warp + q, HA[q], HB[q]);
+    const int Yb = Yg + 8 * warp;
+    if (Yb >= 2 && Yb + 7 <= 4 * a.h - 3 && Yb + 7 < a.H) {
+      // interior rows (warp-uniform): rows 0..3 between coefficient rows
+      // 2w, 2w+1 and rows 4..7 between 2w+1, 2w+2, f = 1/8, 3/8, 5/8, 7/8
+#pragma unroll
+      for (int t = 0; t < 8; ++t) {
+        const int q0 = t >> 2;
+        do_row(8 * warp + t, HA[q0], HA[q0 + 1], HB[q0], HB[q0 + 1], (2 * (t & 3) + 1) * 0.125f);
+      }
+    } else {
+#pragma unroll 1
+      for (int t = 0; t < 8; ++t) {
+        const int Y = Yb + t;
+        float alo[4], ahi[4], blo[4], bhi[4], f = 0.f;
+        int ql = 0, qh = 0;
+        if (Y >= 0 && Y < a.H) {
+          const Tap ty = tap4(Y, a.h);
+          ql = ty.lo - (i0 - 1) - 2 * warp;  // in 0..2 (clamped taps stay inside)
+          qh = ty.hi - (i0 - 1) - 2 * warp;
+          f = ty.f;
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          alo[j] = ql == 0 ? HA[0][j] : (ql == 1 ? HA[1][j] : HA[2][j]);
+          ahi[j] = qh == 0 ? HA[0][j] : (qh == 1 ? HA[1][j] : HA[2][j]);
+          blo[j] = ql == 0 ? HB[0][j] : (ql == 1 ? HB[1][j] : HB[2][j]);
+          bhi[j] = qh == 0 ? HB[0][j] : (qh == 1 ? HB[1][j] : HB[2][j]);
+        }
+        do_row(8 * warp + t, alo, ahi, blo, bhi, f);
+      }
+    }
+  }
+  if (extra) {  // gather row 64 + warp: coefficient rows 16, 17
+    float HA[2][4], HB[2][4];
+    hrow2(16, HA[0], HB[0]);
+    hrow2(17, HA[1], HB[1]);
+    const int Y = Yg + 64 + warp;
+    float f = (2 * warp + 1) * 0.125f;
+    int ql = 0, qh = 1;
+    if (Y >= 0 && Y < a.H) {
+      const Tap ty = tap4(Y, a.h);
+      ql = ty.lo - (i0 - 1) - 16;
+      qh = ty.hi - (i0 - 1) - 16;
+      f = ty.f;
+    }
+    float alo[4], ahi[4], blo[4], bhi[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      alo[j] = ql == 0 ? HA[0][j] : HA[1][j];
+      ahi[j] = qh == 0 ? HA[0][j] : HA[1][j];
+      blo[j] = ql == 0 ? HB[0][j] : HB[1][j];
+      bhi[j] = qh == 0 ? HB[0][j] : HB[1][j];
+    }
+    do_row(64 + warp, alo, ahi, blo, bhi, f);
+  }
+  __syncwarp();
+  // halo columns: hr columns 4k0-2, 4k0-1 (into lr column k0's partial) and
+  // 4k0+128, 4k0+129 (into k0+31's), one (row, side) item per lane
+  {
+    const int nrow = extra ? 9 : 8;
+    if (lane < 2 * nrow) {
+      const int ri = lane >> 1, side = lane & 1;
+      const int yl = ri < 8 ? 8 * warp + ri : 64 + warp;
+      const int Y = Yg + yl;
+      const int kk = side ? k0 + TLX - 1 : k0;
+      const int Xa = side ? 4 * k0 + THX : 4 * k0 - 2;
+      if (Y >= 0 && Y < a.H && kk < a.w) {
+        const Tap ty = tap4(Y, a.h);
+        const float* A0 = sm.As + (ty.lo - (i0 - 1)) * CAP;
+        const float* A1 = sm.As + (ty.hi - (i0 - 1)) * CAP;
+        const float* B0 = sm.Bs + (ty.lo - (i0 - 1)) * CAP;
+        const float* B1 = sm.Bs + (ty.hi - (i0 - 1)) * CAP;
+        float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          const int X = Xa + c;
+          if (X < 0 || X >= a.W) continue;
+          const Tap tx = tap4(X, a.w);
+          const int cl = tx.lo - (k0 - 1), ch = tx.hi - (k0 - 1);
+          // horizontal then vertical, as the row path
+          const float al = A0[cl] + tx.f * (A0[ch] - A0[cl]);
+          const float ah = A1[cl] + tx.f * (A1[ch] - A1[cl]);
+          const float bl = B0[cl] + tx.f * (B0[ch] - B0[cl]);
+          const float bh = B1[cl] + tx.f * (B1[ch] - B1[cl]);
+          const float Au = al + ty.f * (ah - al), Bu = bl + ty.f * (bh - bl);
+          const float g = __ldg(G + (int64_t)Y * a.W + X), t = __ldg(T + (int64_t)Y * a.W + X);
+          const float dv = scale2 * ((Bu + Au * g) - t);
+          float wgt = 0.f;
+          if (tx.lo == kk) wgt += 1.f - tx.f;
+          if (tx.hi == kk) wgt += tx.f;
+          s1 += wgt * dv;
+          s2 += wgt * (dv * g);
+        }
+        const int o = yl * TLX + (side ? TLX - 1 : 0);
+        R1[o] += s1;
+        R2[o] += s2;
+      }
+    }
+  }
+  // loss partial: warp sums (float64), combined in warp order below
+  {
+    double v = (double)lsum;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) red[warp] = v;
+  }
+  __syncthreads();
+  // column pass: db[i][k] = sum_Y wy(Y, i) R1[Y][k] (as k_joint_bwd_hr)
+  for (int it = threadIdx.x; it < TLY * TLX; it += NT) {
+    const int il = it / TLX, kl = it - il * TLX;
+    const int i = i0 + il, kc = k0 + kl;
+    if (i >= a.h || kc >= a.w) continue;
+    float s1 = 0.f, s2 = 0.f;
+    if (i >= 1 && i <= a.h - 2 && 4 * i + 5 < a.H) {
+      constexpr float wy[8] = {0.125f, 0.375f, 0.625f, 0.875f, 0.875f, 0.625f, 0.375f, 0.125f};
+      const int yl0 = 4 * (i - i0);
+#pragma unroll
+      for (int t = 0; t < 8; ++t) {
+        s1 += wy[t] * R1[(yl0 + t) * TLX + kl];
+        s2 += wy[t] * R2[(yl0 + t) * TLX + kl];
+      }
+    } else {
+#pragma unroll
+      for (int dy = -2; dy <= 5; ++dy) {
+        const int Y = 4 * i + dy;
+        if (Y < 0 || Y >= a.H) continue;
+        const Tap ty = tap4(Y, a.h);
+        float wgt = 0.f;
+        if (ty.lo == i) wgt += 1.f - ty.f;
+        if (ty.hi == i) wgt += ty.f;
+        const int yl = Y - Yg;
+        s1 += wgt * R1[yl * TLX + kl];
+        s2 += wgt * R2[yl * TLX + kl];
+      }
+    }
+    const int64_t o = p * (int64_t)a.h * a.w + (int64_t)i * a.w + kc;
+    a.db[o] = s1;
+    a.dA[o] = s2;
+  }
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+#pragma unroll
+    for (int w = 0; w < NT / 32; ++w) s += red[w];
+    a.loss_part[(p * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x] = s;
+  }
+  if (degen) flag(a.status, GF_STATUS_DEGENERATE);
+  if (chk != 0.f) flag(a.status, GF_STATUS_NONFINITE_OUTPUT);
+}
+
+// ---------------------------------------------------------------------------
 // backward, kernel 2: low-res tail
 // ---------------------------------------------------------------------------
 constexpr int TL = 32;  // low-res block of the tail kernel
@@ -833,6 +1147,8 @@ __global__ void __launch_bounds__(NT) k_joint_bwd_lr(BwdLrArgs a) {
 }  // namespace jf
 
 thread_local int g_joint_lr_variant = 0;
+thread_local int g_joint_mse_variant = 0;
+thread_local int g_joint_fwd_variant = 0;
 
 bool fused_joint_ok(int64_t B, int64_t C, int64_t h, int64_t w, int64_t H, int64_t W, int r) {
   if (H != 4 * h || W != 4 * w) return false;
@@ -852,12 +1168,19 @@ struct JointFns {
   const void* fwd;
   const void* bwd_hr;
   const void* bwd_lr;
+  const void* mse_hr;
 };
 
 template <int RAD>
 static JointFns joint_fns() {
-  return {(const void*)jf::k_joint_fwd<RAD>, (const void*)jf::k_joint_bwd_hr<RAD>,
-          (const void*)jf::k_joint_bwd_lr<RAD>};
+  // r >= 8: fewer, longer coefficient-pass chunks (each pays a 2r warm-up)
+  const void* fwd;
+  if constexpr (RAD >= 8)
+    fwd = (const void*)jf::k_joint_fwd<RAD, 2, 8>;
+  else
+    fwd = (const void*)jf::k_joint_fwd<RAD>;
+  return {fwd, (const void*)jf::k_joint_bwd_hr<RAD>, (const void*)jf::k_joint_bwd_lr<RAD>,
+          (const void*)jf::k_joint_mse_hr<RAD, 3>};
 }
 
 static JointFns pick_joint(int r) {
@@ -890,13 +1213,41 @@ void fused_joint_fwd(const float* lr_x, const float* lr_y, const float* hr_x, fl
   jf::FwdArgs a{lr_x, lr_y, hr_x, out, (int)h, (int)w, (int)H, (int)W, r, eps, status};
   const int tx = (int)((w + jf::TLX - 1) / jf::TLX), ty = (int)((h + jf::TLY - 1) / jf::TLY);
   const size_t smem = jf::coef_smem_floats(r) * sizeof(float);
-  set_smem(fns.fwd, smem);
+  const void* fn = fns.fwd;
+  if (r == 8) {  // variant hook: coefficient-pass chunking at r = 8 (default 2 x 8
+               // chunks: 1500 us at config 3 vs 1571 us for 4 x 16)
+    switch (g_joint_fwd_variant) {
+      case 1: fn = (const void*)jf::k_joint_fwd<8, 0, 16>; break;
+      case 2: fn = (const void*)jf::k_joint_fwd<8, 1, 4>; break;
+      case 3: fn = (const void*)jf::k_joint_fwd<8, 2, 4>; break;
+      case 4: fn = (const void*)jf::k_joint_fwd<8, 4, 8>; break;
+      default: break;
+    }
+  }
+  set_smem(fn, smem);
   dim3 grid((unsigned)tx, (unsigned)ty, (unsigned)(B * C));
-  launch(fns.fwd, grid, smem, s, &a);
+  launch(fn, grid, smem, s, &a);
 }
 
 size_t fused_joint_bwd_ws_bytes(int64_t B, int64_t C, int64_t h, int64_t w) {
   return (size_t)2 * B * C * h * w * sizeof(float);
+}
+
+// the low-res tail of both backward entries
+static void joint_lr_tail(const JointFns& fns, const float* lr_x, const float* lr_y,
+                          const float* db, const float* dA, float* d_lr_x, float* d_lr_y,
+                          int64_t B, int64_t C, int64_t h, int64_t w, int r, float eps,
+                          cudaStream_t s) {
+  if (g_joint_lr_variant != 1 && seg_joint_bwd_lr_ok(h, w, r)) {
+    seg_joint_bwd_lr(lr_x, lr_y, db, dA, d_lr_x, d_lr_y, B * C, h, w, r, eps, s);
+  } else {
+    const size_t smem = jf::bwd_lr_smem_floats(r) * sizeof(float);
+    set_smem(fns.bwd_lr, smem);
+    dim3 grid((unsigned)((w + jf::TL - 1) / jf::TL), (unsigned)((h + jf::TL - 1) / jf::TL),
+              (unsigned)(B * C));
+    jf::BwdLrArgs a{lr_x, lr_y, db, dA, d_lr_x, d_lr_y, (int)h, (int)w, r, eps};
+    launch(fns.bwd_lr, grid, smem, s, &a);
+  }
 }
 
 void fused_joint_bwd(const float* lr_x, const float* lr_y, const float* hr_x, const float* d_out,
@@ -915,16 +1266,46 @@ void fused_joint_bwd(const float* lr_x, const float* lr_y, const float* hr_x, co
                     eps, status};
     launch(fns.bwd_hr, grid, smem, s, &a);
   }
-  if (g_joint_lr_variant != 1 && seg_joint_bwd_lr_ok(h, w, r)) {
-    seg_joint_bwd_lr(lr_x, lr_y, db, dA, d_lr_x, d_lr_y, B * C, h, w, r, eps, s);
-  } else {
-    const size_t smem = jf::bwd_lr_smem_floats(r) * sizeof(float);
-    set_smem(fns.bwd_lr, smem);
-    dim3 grid((unsigned)((w + jf::TL - 1) / jf::TL), (unsigned)((h + jf::TL - 1) / jf::TL),
+  joint_lr_tail(fns, lr_x, lr_y, db, dA, d_lr_x, d_lr_y, B, C, h, w, r, eps, s);
+}
+
+// per-CTA loss partials of the fused step: (B C) x tile rows x tile columns
+static int64_t mse_tiles(int64_t C, int64_t h, int64_t w) {
+  return C * ((h + jf::TLY - 1) / jf::TLY) * ((w + jf::TLX - 1) / jf::TLX);
+}
+
+size_t fused_joint_mse_ws_bytes(int64_t B, int64_t C, int64_t h, int64_t w) {
+  const size_t f = ((size_t)2 * B * C * h * w * sizeof(float) + 255) / 256 * 256;
+  return f + (size_t)B * mse_tiles(C, h, w) * sizeof(double);
+}
+
+void fused_joint_mse_bwd(const float* lr_x, const float* lr_y, const float* hr_x,
+                         const float* target, double* loss, float* d_lr_x, float* d_lr_y,
+                         float* d_hr_x, int64_t B, int64_t C, int64_t h, int64_t w, int64_t H,
+                         int64_t W, int r, float eps, void* ws, uint32_t* status,
+                         cudaStream_t s) {
+  float* db = (float*)ws;
+  float* dA = db + B * C * h * w;
+  double* part =
+      (double*)((char*)ws + ((size_t)2 * B * C * h * w * sizeof(float) + 255) / 256 * 256);
+  const JointFns fns = pick_joint(r);
+  {
+    const size_t smem = jf::bwd_hr_smem_floats(r) * sizeof(float);
+    // variant hook: CTAs per SM the registers are budgeted for (3 default:
+    // 421 us at config 2 vs 507 us for 2 (no spills) and 441 us for 4)
+    const void* fn = fns.mse_hr;
+    if (r == 1 && g_joint_mse_variant == 2) fn = (const void*)jf::k_joint_mse_hr<1, 2>;
+    if (r == 1 && g_joint_mse_variant == 4) fn = (const void*)jf::k_joint_mse_hr<1, 4>;
+    set_smem(fn, smem);
+    dim3 grid((unsigned)((w + jf::TLX - 1) / jf::TLX), (unsigned)((h + jf::TLY - 1) / jf::TLY),
               (unsigned)(B * C));
-    jf::BwdLrArgs a{lr_x, lr_y, db, dA, d_lr_x, d_lr_y, (int)h, (int)w, r, eps};
-    launch(fns.bwd_lr, grid, smem, s, &a);
+    const double per_image = (double)C * (double)H * (double)W;
+    jf::MseHrArgs a{lr_x, lr_y, hr_x, target, d_hr_x, db, dA, part, (int)h, (int)w, (int)H,
+                    (int)W, r, eps, (float)(2.0 / per_image / (double)B), status};
+    launch(fn, grid, smem, s, &a);
+    mse_final(part, loss, B, (int)mse_tiles(C, h, w), per_image, s);
   }
+  joint_lr_tail(fns, lr_x, lr_y, db, dA, d_lr_x, d_lr_y, B, C, h, w, r, eps, s);
 }
 
 }  // namespace gfb

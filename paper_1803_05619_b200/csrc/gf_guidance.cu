@@ -444,6 +444,11 @@ void mse_impl(const T* out, const T* tgt, T* d_out, double* loss, int64_t B, int
   k_mse_final<<<1, 1024, 0, s>>>(partials, loss, B, kMseBlocks, (double)per_image);
 }
 
+void mse_final(const double* partials, double* loss, int64_t B, int nblk, double per_image,
+               cudaStream_t s) {
+  k_mse_final<<<1, 1024, 0, s>>>(partials, loss, B, nblk, per_image);
+}
+
 #define GN_INST(T)                                                                            \
   template void gn_forward_impl<T>(const T*, T*, const T*, int64_t, int64_t, int64_t, int64_t, \
                                    int64_t, void*, uint32_t*, cudaStream_t);                  \

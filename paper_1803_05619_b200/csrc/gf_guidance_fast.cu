@@ -22,6 +22,9 @@
 #include "gf_pair.cuh"
 
 namespace gfb {
+
+thread_local int g_gn_bwd_variant = 0;
+
 namespace gnf {
 
 constexpr int CI = 3, CO = 3;
@@ -562,6 +565,299 @@ __global__ void k_fin_params(const double* __restrict__ gsum, const double* __re
   }
 }
 
+// ---- backward, one heavy pass (default) ------------------------------------
+// The AdaptiveNorm coupling makes dh1_j = alpha_j d2_j + kappa_j + lambda_j h1_j
+// (kappa, lambda per image, known only after a pass over every pixel), so
+//     dx_c   = D_c(p) + K_c + sum_c' L_cc' x_c'
+//              D_c = sum_j (alpha_j W1_jc) d2_j,  K_c = sum_j W1_jc kappa_j,
+//              L_cc' = sum_j W1_jc lambda_j W1_jc'
+//     dW1_jc = alpha_j sum_p d2_j x_c + kappa_j sum_p x_c
+//              + lambda_j sum_c' W1_jc' sum_p x_c' x_c
+// and sum_p d2_j h1_j = sum_c W1_jc sum_p d2_j x_c.  One heavy pass (k_bwd_h)
+// streams (x, dy), writes D into dx and reduces sum d2, sum d2 x, sum dy,
+// sum dy h3; the x moments come from the forward's statistics; k_fin_h forms
+// kappa, lambda, K, L and every parameter gradient; k_dx adds K + L x to D.
+// Four lanes share a 4-pixel group, each owning a quarter of the hidden units
+// (the accumulators fit 2 CTAs per SM); D is summed over the four by shuffles.
+template <int HID>
+struct AH {
+  static constexpr int d2 = 0, d2x = HID, dy = HID + HID * CI, dw2 = HID + HID * CI + CO,
+                       nv = HID + HID * CI + CO + CO * HID;
+};
+// per-image fp32 constants of k_dx: K[3], L[3][3]
+constexpr int KL = CI + CI * CI;
+// per-image float64 gradient sums: dW2 (CO*HID), db2 (CO), dgain, dng, dW1 (HID*CI)
+template <int HID>
+struct GH {
+  static constexpr int dw2 = 0, db2 = CO * HID, dgain = CO * HID + CO, dng = CO * HID + CO + 1,
+                       dw1 = CO * HID + CO + 2, count = CO * HID + CO + 2 + HID * CI;
+};
+
+template <int HID>
+__global__ void __launch_bounds__(NT, 2) k_bwd_h(const float* __restrict__ x,
+                                              const float* __restrict__ dy,
+                                              float* __restrict__ D,
+                                              const float* __restrict__ params,
+                                              const float* __restrict__ fold,
+                                              double* __restrict__ part, int64_t HW) {
+  constexpr int NG = NT / 4;  // 4-pixel groups per CTA iteration
+  __shared__ float sw1f[HID * CI], sbeta[HID], sw2[CO * HID];
+  __shared__ ulonglong2 stage[NST][CI + CO][NG];
+  const int64_t b = blockIdx.y;
+  const float* f = fold + b * F<HID>::count;
+  for (int i = threadIdx.x; i < HID * CI; i += NT) sw1f[i] = f[F<HID>::w1f + i];
+  for (int i = threadIdx.x; i < HID; i += NT) sbeta[i] = f[F<HID>::beta + i];
+  for (int i = threadIdx.x; i < CO * HID; i += NT) sw2[i] = params[P<HID>::w2 + i];
+  __syncthreads();
+  constexpr int JH = (HID + 3) / 4;  // hidden units per lane
+  using namespace pr;
+  const int q = threadIdx.x & 3;
+  const int j0 = q * JH;
+  const int g = threadIdx.x >> 2;
+  u64 sd2[JH], sd2x[JH][CI], sdw2[CO][JH], sdy[CO];
+#pragma unroll
+  for (int jj = 0; jj < JH; ++jj) {
+    sd2[jj] = 0ull;
+#pragma unroll
+    for (int c = 0; c < CI; ++c) sd2x[jj][c] = 0ull;
+#pragma unroll
+    for (int o = 0; o < CO; ++o) sdw2[o][jj] = 0ull;
+  }
+#pragma unroll
+  for (int o = 0; o < CO; ++o) sdy[o] = 0ull;
+  const int64_t n4 = HW / 4;
+  const int64_t stride = (int64_t)gridDim.x * NG;
+  const int64_t first = (int64_t)blockIdx.x * NG;
+  const int64_t iters = n4 > first ? (n4 - first + stride - 1) / stride : 0;
+  // lanes 0..2 of a group copy (x_q, dy_q); lane 3 copies nothing
+  auto issue = [&](int64_t it) {
+    const int64_t i = first + it * stride + g;
+    if (it < iters && i < n4 && q < 3) {
+      const int st = (int)(it % NST);
+      cp16(&stage[st][q][g], reinterpret_cast<const ulonglong2*>(x + (b * CI + q) * HW) + i);
+      cp16(&stage[st][CI + q][g], reinterpret_cast<const ulonglong2*>(dy + (b * CO + q) * HW) + i);
+    }
+    cp_commit();
+  };
+#pragma unroll
+  for (int k = 0; k < NST - 1; ++k) issue(k);
+  for (int64_t it = 0; it < iters; ++it) {
+    const int64_t i = first + it * stride + g;
+    const bool valid = i < n4;  // a group is valid or invalid together
+    __syncwarp();  // the group's reads of the stage refilled below are done
+    issue(it + NST - 1);
+    cp_wait<NST - 1>();
+    __syncwarp();  // the group's chunks of stage `it` are visible
+    const int st = (int)(it % NST);
+    ulonglong2 X[CI], G[CO];
+#pragma unroll
+    for (int c = 0; c < CI; ++c) X[c] = valid ? stage[st][c][g] : make_ulonglong2(0ull, 0ull);
+#pragma unroll
+    for (int o = 0; o < CO; ++o) {
+      G[o] = valid ? stage[st][CI + o][g] : make_ulonglong2(0ull, 0ull);
+      sdy[o] = add2(sdy[o], add2(G[o].x, G[o].y));
+    }
+    u64 dv[CI][2];
+#pragma unroll
+    for (int c = 0; c < CI; ++c) dv[c][0] = dv[c][1] = 0ull;
+#pragma unroll
+    for (int jj = 0; jj < JH; ++jj) {
+      const int j = j0 + jj;
+      if (j >= HID) break;
+      const u64 a0 = bc(sw1f[j * CI]), a1 = bc(sw1f[j * CI + 1]), a2 = bc(sw1f[j * CI + 2]);
+      const u64 be = bc(sbeta[j]);
+      const u64 v0 = bc(sw2[0 * HID + j]), v1 = bc(sw2[1 * HID + j]), v2 = bc(sw2[2 * HID + j]);
+#pragma unroll
+      for (int pp = 0; pp < 2; ++pp) {
+        const u64 x0 = pp ? X[0].y : X[0].x, x1 = pp ? X[1].y : X[1].x,
+                  x2 = pp ? X[2].y : X[2].x;
+        const u64 g0 = pp ? G[0].y : G[0].x, g1 = pp ? G[1].y : G[1].x,
+                  g2 = pp ? G[2].y : G[2].x;
+        const u64 h2 = fma2(a2, x2, fma2(a1, x1, fma2(a0, x0, be)));  // (alpha .* W1) x + beta
+        const u64 sl = slope2(h2, kLeaky);
+        const u64 h3 = mul2(h2, sl);
+        const u64 d2 = mul2(fma2(v2, g2, fma2(v1, g1, mul2(v0, g0))), sl);
+        sd2[jj] = add2(sd2[jj], d2);
+        sd2x[jj][0] = fma2(d2, x0, sd2x[jj][0]);
+        sd2x[jj][1] = fma2(d2, x1, sd2x[jj][1]);
+        sd2x[jj][2] = fma2(d2, x2, sd2x[jj][2]);
+        sdw2[0][jj] = fma2(g0, h3, sdw2[0][jj]);
+        sdw2[1][jj] = fma2(g1, h3, sdw2[1][jj]);
+        sdw2[2][jj] = fma2(g2, h3, sdw2[2][jj]);
+        dv[0][pp] = fma2(a0, d2, dv[0][pp]);
+        dv[1][pp] = fma2(a1, d2, dv[1][pp]);
+        dv[2][pp] = fma2(a2, d2, dv[2][pp]);
+      }
+    }
+    // D over the group's four lanes; lane c < 3 stores channel c
+#pragma unroll
+    for (int c = 0; c < CI; ++c)
+#pragma unroll
+      for (int pp = 0; pp < 2; ++pp) {
+        dv[c][pp] = add2(dv[c][pp], __shfl_xor_sync(0xffffffffu, dv[c][pp], 1));
+        dv[c][pp] = add2(dv[c][pp], __shfl_xor_sync(0xffffffffu, dv[c][pp], 2));
+      }
+    if (valid && q < 3) {
+      const u64 o0 = q == 0 ? dv[0][0] : (q == 1 ? dv[1][0] : dv[2][0]);
+      const u64 o1 = q == 0 ? dv[0][1] : (q == 1 ? dv[1][1] : dv[2][1]);
+      reinterpret_cast<ulonglong2*>(D + (b * CI + q) * HW)[i] = make_ulonglong2(o0, o1);
+    }
+  }
+  cp_wait<0>();
+  auto sum2 = [](u64 v) { return lo(v) + hi(v); };
+  auto get = [&](int v) -> float {
+    float r = 0.f;
+    if (v >= AH<HID>::dw2) {
+      const int u = v - AH<HID>::dw2, o = u / HID, j = u - o * HID;
+#pragma unroll
+      for (int jj = 0; jj < JH; ++jj)
+        if (j == j0 + jj) r = sum2(sdw2[o][jj]);
+      return r;
+    }
+    if (v >= AH<HID>::dy) return q == 0 ? sum2(sdy[v - AH<HID>::dy]) : 0.f;
+    if (v >= AH<HID>::d2x) {
+      const int u = v - AH<HID>::d2x, j = u / CI, c = u - j * CI;
+#pragma unroll
+      for (int jj = 0; jj < JH; ++jj)
+#pragma unroll
+        for (int cc = 0; cc < CI; ++cc)
+          if (j == j0 + jj && c == cc) r = sum2(sd2x[jj][cc]);
+      return r;
+    }
+#pragma unroll
+    for (int jj = 0; jj < JH; ++jj)
+      if (v == j0 + jj) r = sum2(sd2[jj]);
+    return r;
+  };
+  reduce_store_fn<AH<HID>::nv>(get, part + (b * gridDim.x + blockIdx.x) * AH<HID>::nv);
+}
+
+// ---- per image: kappa, lambda -> K, L and the parameter-gradient sums ------
+template <int HID>
+__global__ void k_fin_h(const double* __restrict__ part, const double* __restrict__ stats,
+                        const float* __restrict__ params, const float* __restrict__ fold,
+                        float* __restrict__ kl, double* __restrict__ gsum, int64_t HW, int nblk) {
+  constexpr int NV = AH<HID>::nv;
+  const int b = blockIdx.x;
+  __shared__ double S[NV], X[9], kap[HID], lam[HID];
+  for (int v = threadIdx.x; v < NV + 9; v += blockDim.x) {
+    double s = 0.0;
+    if (v < NV)
+      for (int k = 0; k < nblk; ++k) s += part[((int64_t)b * nblk + k) * NV + v];
+    else
+      for (int k = 0; k < nblk; ++k) s += stats[((int64_t)b * nblk + k) * 9 + (v - NV)];
+    if (v < NV)
+      S[v] = s;
+    else
+      X[v - NV] = s;
+  }
+  __syncthreads();
+  const float* f = fold + (int64_t)b * F<HID>::count;
+  const double N = (double)HW;
+  const double ng = (double)params[P<HID>::ng];
+  auto w1 = [&](int j, int c) { return (double)params[P<HID>::w1 + j * CI + c]; };
+  auto sd2h1 = [&](int j) {
+    double s = 0.0;
+    for (int c = 0; c < CI; ++c) s += w1(j, c) * S[AH<HID>::d2x + j * CI + c];
+    return s;
+  };
+  if (threadIdx.x < HID) {
+    const int j = threadIdx.x;
+    const double mu = (double)f[F<HID>::mu + j], inv = (double)f[F<HID>::inv + j];
+    const double sd2 = S[AH<HID>::d2 + j];
+    const double gm = ng * sd2 / N;                        // mean(g), g = ng * d2
+    const double gp = ng * inv * (sd2h1(j) - mu * sd2) / N;  // mean(g * xhat)
+    kap[j] = -gm * inv + gp * inv * inv * mu;
+    lam[j] = -gp * inv * inv;
+  }
+  __syncthreads();
+  double* gs = gsum + (int64_t)b * GH<HID>::count;
+  // x moments: X[0..2] = sum x_c, X[3..8] = sum x_c x_c' (00 01 02 11 12 22)
+  const int ix[3][3] = {{3, 4, 5}, {4, 6, 7}, {5, 7, 8}};
+  for (int v = threadIdx.x; v < GH<HID>::count; v += blockDim.x) {
+    double r = 0.0;
+    if (v < GH<HID>::db2) {
+      r = S[AH<HID>::dw2 + v];
+    } else if (v < GH<HID>::dgain) {
+      r = S[AH<HID>::dy + v - GH<HID>::db2];
+    } else if (v == GH<HID>::dgain) {
+      for (int j = 0; j < HID; ++j) r += sd2h1(j);
+    } else if (v == GH<HID>::dng) {
+      for (int j = 0; j < HID; ++j) {
+        const double mu = (double)f[F<HID>::mu + j], inv = (double)f[F<HID>::inv + j];
+        r += inv * (sd2h1(j) - mu * S[AH<HID>::d2 + j]);
+      }
+    } else {
+      const int u = v - GH<HID>::dw1, j = u / CI, c = u - j * CI;
+      double wx = 0.0;  // sum_c' W1_jc' sum_p x_c' x_c
+      for (int c2 = 0; c2 < CI; ++c2) wx += w1(j, c2) * X[ix[c2][c]];
+      r = (double)f[F<HID>::alpha + j] * S[AH<HID>::d2x + j * CI + c] + kap[j] * X[c] +
+          lam[j] * wx;
+    }
+    gs[v] = r;
+  }
+  if (threadIdx.x < KL) {
+    const int v = threadIdx.x;
+    double r = 0.0;
+    if (v < CI) {
+      for (int j = 0; j < HID; ++j) r += w1(j, v) * kap[j];
+    } else {
+      const int c = (v - CI) / CI, c2 = (v - CI) % CI;
+      for (int j = 0; j < HID; ++j) r += w1(j, c) * lam[j] * w1(j, c2);
+    }
+    kl[(int64_t)b * KL + v] = (float)r;
+  }
+}
+
+// ---- dx = D + K + L x (in place over D), 4 pixels per thread ---------------
+__global__ void __launch_bounds__(NT) k_dx(const float* __restrict__ x, float* __restrict__ dx,
+                                           const float* __restrict__ kl, int64_t HW) {
+  const int64_t b = blockIdx.y;
+  const float* c = kl + b * KL;
+  using namespace pr;
+  const u64 K0 = bc(c[0]), K1 = bc(c[1]), K2 = bc(c[2]);
+  const u64 L00 = bc(c[3]), L01 = bc(c[4]), L02 = bc(c[5]), L10 = bc(c[6]), L11 = bc(c[7]),
+            L12 = bc(c[8]), L20 = bc(c[9]), L21 = bc(c[10]), L22 = bc(c[11]);
+  const int64_t n4 = HW / 4;
+  const ulonglong2* x0 = reinterpret_cast<const ulonglong2*>(x + (b * CI + 0) * HW);
+  const ulonglong2* x1 = reinterpret_cast<const ulonglong2*>(x + (b * CI + 1) * HW);
+  const ulonglong2* x2 = reinterpret_cast<const ulonglong2*>(x + (b * CI + 2) * HW);
+  ulonglong2* d0 = reinterpret_cast<ulonglong2*>(dx + (b * CI + 0) * HW);
+  ulonglong2* d1 = reinterpret_cast<ulonglong2*>(dx + (b * CI + 1) * HW);
+  ulonglong2* d2 = reinterpret_cast<ulonglong2*>(dx + (b * CI + 2) * HW);
+  for (int64_t i = (int64_t)blockIdx.x * NT + threadIdx.x; i < n4; i += (int64_t)gridDim.x * NT) {
+    const ulonglong2 a = __ldg(x0 + i), e = __ldg(x1 + i), g = __ldg(x2 + i);
+    ulonglong2 p = d0[i], q = d1[i], r = d2[i];
+    p.x = fma2(L02, g.x, fma2(L01, e.x, fma2(L00, a.x, add2(p.x, K0))));
+    p.y = fma2(L02, g.y, fma2(L01, e.y, fma2(L00, a.y, add2(p.y, K0))));
+    q.x = fma2(L12, g.x, fma2(L11, e.x, fma2(L10, a.x, add2(q.x, K1))));
+    q.y = fma2(L12, g.y, fma2(L11, e.y, fma2(L10, a.y, add2(q.y, K1))));
+    r.x = fma2(L22, g.x, fma2(L21, e.x, fma2(L20, a.x, add2(r.x, K2))));
+    r.y = fma2(L22, g.y, fma2(L21, e.y, fma2(L20, a.y, add2(r.y, K2))));
+    d0[i] = p;
+    d1[i] = q;
+    d2[i] = r;
+  }
+}
+
+// ---- final parameter gradients of the one-pass backward --------------------
+template <int HID>
+__global__ void k_fin_params_h(const double* __restrict__ gsum, float* __restrict__ dparams,
+                               int accumulate, int64_t B) {
+  constexpr int GS = GH<HID>::count;
+  for (int idx = threadIdx.x; idx < P<HID>::count; idx += blockDim.x) {
+    int src;
+    if (idx < HID * CI) src = GH<HID>::dw1 + idx;
+    else if (idx == P<HID>::gain) src = GH<HID>::dgain;
+    else if (idx == P<HID>::ng) src = GH<HID>::dng;
+    else if (idx < P<HID>::b2) src = GH<HID>::dw2 + (idx - P<HID>::w2);
+    else src = GH<HID>::db2 + (idx - P<HID>::b2);
+    double s = 0.0;
+    for (int64_t b = 0; b < B; ++b) s += gsum[b * GS + src];  // fixed image order
+    dparams[idx] = accumulate ? (float)((double)dparams[idx] + s) : (float)s;
+  }
+}
+
 // ---- workspace -------------------------------------------------------------
 template <int HID>
 struct WS {
@@ -572,7 +868,10 @@ struct WS {
     const size_t coef = (size_t)B * 2 * HID * sizeof(float);
     const size_t gsum = (size_t)B * (CO * HID + CO + 2) * sizeof(double);
     const size_t pb = (size_t)B * kBlocks * HID * CI * sizeof(double);
-    return stats + fold + pa + coef + gsum + pb + 6 * 256;
+    const size_t ph = (size_t)B * kBlocks * AH<HID>::nv * sizeof(double);
+    const size_t kl = (size_t)B * KL * sizeof(float);
+    const size_t gh = (size_t)B * GH<HID>::count * sizeof(double);
+    return stats + fold + pa + coef + gsum + pb + ph + kl + gh + 9 * 256;
   }
 };
 
@@ -609,17 +908,30 @@ void backward(const float* x, const float* dy, float* dx, float* dparams, int ac
   float* coef = c.take<float>((size_t)B * 2 * HID);
   double* gsum = c.take<double>((size_t)B * (CO * HID + CO + 2));
   double* pb = c.take<double>((size_t)B * kBlocks * HID * CI);
+  double* ph = c.take<double>((size_t)B * kBlocks * AH<HID>::nv);
+  float* kl = c.take<float>((size_t)B * KL);
+  double* gh = c.take<double>((size_t)B * GH<HID>::count);
   dim3 grid(kBlocks, (unsigned)B);
-  if (!have_fold) {  // else `ws` holds forward()'s folded constants of this x and params
+  if (!have_fold) {  // else `ws` holds forward()'s statistics and folded constants
     k_stats<<<grid, NT, 0, s>>>(x, stats, HW, status);
     k_prep<HID><<<(unsigned)B, 32, 0, s>>>(stats, params, fold, HW, kBlocks);
   }
+  if (g_gn_bwd_variant == 0) {  // one heavy pass (default)
+    k_bwd_h<HID><<<grid, NT, 0, s>>>(x, dy, dx, params, fold, ph, HW);
+    k_fin_h<HID><<<(unsigned)B, 128, 0, s>>>(ph, stats, params, fold, kl, gh, HW, kBlocks);
+    k_dx<<<grid, NT, 0, s>>>(x, dx, kl, HW);
+    k_fin_params_h<HID><<<1, 128, 0, s>>>(gh, dparams, accumulate, B);
+    return;
+  }
+  // variant 1: two heavy passes (round-1 kernels)
   k_bwd_a<HID><<<grid, NT, 0, s>>>(x, dy, params, fold, pa, HW);
   k_fin_a<HID><<<(unsigned)B, 128, 0, s>>>(pa, params, fold, coef, gsum, HW, kBlocks);
   k_bwd_b<HID><<<grid, NT, 0, s>>>(x, dy, dx, params, fold, coef, pb, HW);
-  // per-image dW1 sums land in `stats` (free after prep), then the batch sum
-  k_fin_b<HID><<<(unsigned)B, 64, 0, s>>>(pb, stats, kBlocks);
-  k_fin_params<HID><<<1, 128, 0, s>>>(gsum, stats, dparams, accumulate, B, kBlocks);
+  // per-image dW1 sums in their own region (`stats` stays the forward's for
+  // a later reuse), then the batch sum
+  double* pbi = pa;  // free after k_fin_a
+  k_fin_b<HID><<<(unsigned)B, 64, 0, s>>>(pb, pbi, kBlocks);
+  k_fin_params<HID><<<1, 128, 0, s>>>(gsum, pbi, dparams, accumulate, B, kBlocks);
 }
 
 }  // namespace gnf

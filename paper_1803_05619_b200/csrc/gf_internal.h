@@ -53,6 +53,9 @@ size_t mse_ws_bytes(int64_t B);
 template <typename T>
 void mse_impl(const T* out, const T* tgt, T* d_out, double* loss, int64_t B, int64_t per_image,
               void* ws, cudaStream_t s);
+// loss = sum_b (sum of partials[b*nblk .. b*nblk+nblk) / per_image) / B, fixed order
+void mse_final(const double* partials, double* loss, int64_t B, int nblk, double per_image,
+               cudaStream_t s);
 
 // ---- fused fast paths (fp32, NCHW); return false when the shape is not
 // covered, in which case the caller takes the generic path ----
@@ -73,6 +76,9 @@ void seg_joint_bwd_lr(const float* lr_x, const float* lr_y, const float* db, con
                       float* d_lr_x, float* d_lr_y, int64_t P, int64_t h, int64_t w, int r,
                       float eps, cudaStream_t s);
 extern thread_local int g_joint_lr_variant;
+extern thread_local int g_joint_fwd_variant;  // r = 8 coefficient chunking (test hook)
+extern thread_local int g_joint_mse_variant;
+extern thread_local int g_gn_bwd_variant;  // fused guidance backward: 0 one heavy pass, 1 two  // fused step hr kernel: 0 auto, 2/4 CTAs per SM (r = 1)
 bool fused_joint_ok(int64_t B, int64_t C, int64_t h, int64_t w, int64_t H, int64_t W, int r);
 void fused_joint_fwd(const float* lr_x, const float* lr_y, const float* hr_x, float* out,
                      int64_t B, int64_t C, int64_t h, int64_t w, int64_t H, int64_t W, int r,
@@ -82,6 +88,13 @@ void fused_joint_bwd(const float* lr_x, const float* lr_y, const float* hr_x, co
                      float* d_lr_x, float* d_lr_y, float* d_hr_x, int64_t B, int64_t C,
                      int64_t h, int64_t w, int64_t H, int64_t W, int r, float eps, void* ws,
                      uint32_t* status, cudaStream_t s);
+// fused training step: forward + MSE + backward (no out / d_out in HBM)
+size_t fused_joint_mse_ws_bytes(int64_t B, int64_t C, int64_t h, int64_t w);
+void fused_joint_mse_bwd(const float* lr_x, const float* lr_y, const float* hr_x,
+                         const float* target, double* loss, float* d_lr_x, float* d_lr_y,
+                         float* d_hr_x, int64_t B, int64_t C, int64_t h, int64_t w, int64_t H,
+                         int64_t W, int r, float eps, void* ws, uint32_t* status,
+                         cudaStream_t s);
 
 }  // namespace gfb
 

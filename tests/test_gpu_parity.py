@@ -217,19 +217,105 @@ def test_train_step_matches_reference(gfb, golden):
     net.load_parameters(params)
     p = gfb.GuidedFilterParams(int(c["r"]), float(c["eps"]))
     nchw = lambda a: t32(a.transpose(0, 3, 1, 2))  # noqa: E731
-    res = gfb.train_step(net, nchw(c["lr_x"]), nchw(c["hr_x"]), nchw(c["lr_y"]),
-                         nchw(c["target"]), p)
-    assert abs(float(res.loss) - float(c["loss"])) <= 1e-6 * max(1.0, float(c["loss"]))
-    assert abs_max(npy(res.out).transpose(0, 2, 3, 1), c["out"]) <= OUT_TOL32
-    assert rel_max(npy(res.d_lr_y).transpose(0, 2, 3, 1), c["d_lr_y"]) <= GRAD_TOL32
-    assert rel_max(npy(res.d_lr_x).transpose(0, 2, 3, 1), c["d_lr_x"]) <= GRAD_TOL32
-    assert rel_max(npy(res.d_hr_x).transpose(0, 2, 3, 1), c["d_hr_x"]) <= GRAD_TOL32
-    grads = net.unpack(res.dparams)
-    # conv2.bias's exact gradient is ~0 here (1e-16): judge every parameter
-    # gradient against the largest one (relative-to-gradient-norm bar)
-    scale = max(float(np.abs(c["g:" + k]).max()) for k in grads)
-    for k, v in grads.items():
-        assert abs_max(npy(v), c["g:" + k]) <= GRAD_TOL32 * scale, k
+    # default: the fused filter + MSE + backward (no output); return_out: the
+    # forward -> mse_loss -> backward chain
+    for return_out in (False, True):
+        res = gfb.train_step(net, nchw(c["lr_x"]), nchw(c["hr_x"]), nchw(c["lr_y"]),
+                             nchw(c["target"]), p, return_out=return_out)
+        assert abs(float(res.loss) - float(c["loss"])) <= 1e-6 * max(1.0, float(c["loss"]))
+        if return_out:
+            assert abs_max(npy(res.out).transpose(0, 2, 3, 1), c["out"]) <= OUT_TOL32
+        else:
+            assert res.out is None
+        assert rel_max(npy(res.d_lr_y).transpose(0, 2, 3, 1), c["d_lr_y"]) <= GRAD_TOL32
+        assert rel_max(npy(res.d_lr_x).transpose(0, 2, 3, 1), c["d_lr_x"]) <= GRAD_TOL32
+        assert rel_max(npy(res.d_hr_x).transpose(0, 2, 3, 1), c["d_hr_x"]) <= GRAD_TOL32
+        grads = net.unpack(res.dparams)
+        # conv2.bias's exact gradient is ~0 here (1e-16): judge every parameter
+        # gradient against the largest one (relative-to-gradient-norm bar)
+        scale = max(float(np.abs(c["g:" + k]).max()) for k in grads)
+        for k, v in grads.items():
+            assert abs_max(npy(v), c["g:" + k]) <= GRAD_TOL32 * scale, k
+
+
+@pytest.mark.parametrize("B,C,h,w,r,eps", [
+    (2, 3, 16, 32, 1, 1e-8),     # one tile per plane
+    (1, 3, 37, 45, 2, 1e-4),     # ragged tiles on both axes
+    (2, 1, 50, 70, 0, 1e-3),     # r = 0
+    (1, 3, 40, 66, 5, 1e-2),     # r > 4 (no static column taps)
+    (1, 2, 33, 97, 8, 1e-4),     # r = 8, ragged
+    (1, 1, 2, 2, 1, 1e-2),       # smallest fused shape
+])
+def test_joint_mse_backward_matches_oracle(gfb, B, C, h, w, r, eps):
+    """Fused filter + MSE + backward vs the oracle's forward_joint -> mse_loss ->
+    backward chain (batch mean, gf/training.py:93-101, 230-235)."""
+    rng = np.random.default_rng(1000 + 7 * h + w + r)
+    H, W = 4 * h, 4 * w
+    gl = rng.uniform(0, 1, (B, h, w, C))
+    sl = np.clip(0.7 * gl + 0.1 + rng.normal(0, 0.05, gl.shape), 0, 1)
+    gh = rng.uniform(0, 1, (B, H, W, C))
+    tg = rng.uniform(0, 1, (B, H, W, C))
+    g = lambda a: t32(a.transpose(0, 3, 1, 2))  # noqa: E731
+    assert gfb._lib.load().gf_joint_is_fused(0, B, C, h, w, H, W, r)
+    loss, grads, status = gfb.joint_mse_backward(g(gl), g(gh), g(sl), g(tg),
+                                                 gfb.GuidedFilterParams(r, eps))
+    assert status.bits() == 0
+    want_loss = 0.0
+    for n in range(B):
+        out, tp = O.forward_joint(gl[n], gh[n], sl[n], r, eps)
+        ln, d = O.mse_loss(out, tg[n])
+        want_loss += ln / B
+        want = O.backward(tp, d / B)  # d_src, d_guide_lo, d_guide_hi
+        got = [npy(t[n]).transpose(1, 2, 0)
+               for t in (grads.d_src, grads.d_guide_lo, grads.d_guide_hi)]
+        # per tensor against its own largest entry, floored by the step's
+        # largest gradient (at r = 0 the exact d_guide_lo is identically 0)
+        floor = max(float(np.abs(x).max()) for x in want)
+        for a, b in zip(got, want):
+            assert abs_max(a, b) <= GRAD_TOL32 * max(float(np.abs(b).max()), floor)
+    assert abs(float(loss) - want_loss) <= 1e-6 * max(want_loss, 1e-12)
+
+
+def test_joint_mse_backward_matches_unfused_chain_config2_size(gfb):
+    """At BASELINE config-2 plane size (2048^2 hr, r = 1, eps = 1e-8): the fused
+    step against forward_joint -> mse_loss -> backward on the same GPU."""
+    import workloads
+
+    lr_x, lr_y, hr_x = (t.cuda() for t in workloads.joint_inputs(2, 3, 2048, 2048, seed=11))
+    tg = workloads.affine_target(hr_x).contiguous()
+    p = gfb.GuidedFilterParams(1, 1e-8)
+    loss, grads, status = gfb.joint_mse_backward(lr_x, hr_x, lr_y, tg, p)
+    out, tape = gfb.forward_joint(lr_x, hr_x, lr_y, p)
+    from paper_1803_05619_b200.training import mse_loss_device
+    want, d_out = mse_loss_device(out, tg)
+    ref = gfb.backward(tape, d_out)
+    assert status.bits() == 0
+    assert abs(float(loss) - float(want)) <= 1e-6 * float(want)
+    for a, b in ((grads.d_src, ref.d_src), (grads.d_guide_lo, ref.d_guide_lo),
+                 (grads.d_guide_hi, ref.d_guide_hi)):
+        assert rel_max(npy(a), npy(b)) <= 1e-4
+
+
+def test_joint_mse_backward_nonfused_shapes(gfb):
+    """Shapes the fused kernel does not cover (ratio 2, float64) take the
+    forward -> MSE -> backward entries inside the same C call."""
+    rng = np.random.default_rng(3)
+    for dt, (h, w, H, W) in ((torch.float32, (9, 11, 18, 22)), (torch.float64, (8, 10, 32, 40))):
+        gl = rng.uniform(0, 1, (1, h, w, 3))
+        sl = rng.uniform(0, 1, (1, h, w, 3))
+        gh = rng.uniform(0, 1, (1, H, W, 3))
+        tg = rng.uniform(0, 1, (1, H, W, 3))
+        g = lambda a: torch.from_numpy(a.transpose(0, 3, 1, 2).copy()).to(dt).cuda()  # noqa: E731
+        loss, grads, _ = gfb.joint_mse_backward(g(gl), g(gh), g(sl), g(tg),
+                                                gfb.GuidedFilterParams(1, 1e-4))
+        out, tp = O.forward_joint(gl[0], gh[0], sl[0], 1, 1e-4)
+        want, d = O.mse_loss(out, tg[0])
+        d_src, d_glo, d_ghi = O.backward(tp, d)
+        tol = GRAD_TOL32 if dt == torch.float32 else 1e-9
+        assert abs(float(loss) - want) <= tol * want
+        assert rel_max(npy(grads.d_src[0]).transpose(1, 2, 0), d_src) <= tol
+        assert rel_max(npy(grads.d_guide_lo[0]).transpose(1, 2, 0), d_glo) <= tol
+        assert rel_max(npy(grads.d_guide_hi[0]).transpose(1, 2, 0), d_ghi) <= tol
 
 
 # ---------------------------------------------------------------------------
@@ -650,3 +736,42 @@ def test_highres_kernel_variants_status(gfb, variant, r):
         gfb.forward_highres(g, s.nan_to_num(0.3), gfb.GuidedFilterParams(r, 0.0))
     finally:
         lib.gf_highres_variant(old)
+
+
+@pytest.mark.parametrize("variant", [0, 1])
+def test_fused_guidance_backward_variants_vs_oracle(gfb, variant):
+    """The one-heavy-pass backward (variant 0, dx = D + K + L x, dW1 from the
+    x moments) and the two-pass kernels (1) against the oracle at a
+    config-2-like image (smooth [0,1] input, small upstream gradient); every
+    parameter gradient against its own largest entry."""
+    import workloads
+    from paper_1803_05619_b200 import _lib
+
+    lib = _lib.load()
+    rng = np.random.default_rng(21)
+    params = O.guidance_init(3, 3, 15, rng)
+    params["norm.norm_gain"] = np.array([0.5])
+    params = {k: np.asarray(v, np.float32).astype(np.float64) for k, v in params.items()}
+    _, _, x = workloads.joint_inputs(2, 3, 256, 320, seed=4)
+    x = x.numpy()
+    dy = (1e-5 * rng.standard_normal(x.shape)).astype(np.float32)
+    net = gfb.GuidanceNet(3, 3, hidden=15)
+    net.load_parameters(params)
+    old = lib.gf_gn_bwd_variant(variant)
+    try:
+        _, tape = net.forward(t32(x))
+        dx, grads = net.backward(tape, t32(dy))
+    finally:
+        lib.gf_gn_bwd_variant(old)
+    want_dx, want_g = [], {k: 0.0 for k in params}
+    for n in range(x.shape[0]):
+        _, tp = O.guidance_forward(params, x[n].transpose(1, 2, 0).astype(np.float64))
+        dxx, gg = O.guidance_backward(params, tp, dy[n].transpose(1, 2, 0).astype(np.float64))
+        want_dx.append(dxx.transpose(2, 0, 1))
+        for k in gg:
+            want_g[k] = want_g[k] + gg[k]
+    assert rel_max(npy(dx), np.stack(want_dx)) <= GRAD_TOL32
+    scale = max(float(np.abs(v).max()) for v in want_g.values())
+    for k, v in grads.items():
+        own = float(np.abs(want_g[k]).max())
+        assert abs_max(npy(v), want_g[k]) <= GRAD_TOL32 * max(own, 1e-2 * scale), k
