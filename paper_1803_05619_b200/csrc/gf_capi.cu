@@ -132,6 +132,15 @@ int gf_gn_bwd_variant(int v) {
   return old;
 }
 
+// Test hook: hr pass of the fp32 joint backward on THIS thread (0 single
+// gather pass, 1 the two-read tile kernel, 3 single pass at 3 CTAs/SM for
+// r <= 2).  Returns the old value.
+int gf_joint_bwd_hr_variant(int v) {
+  int old = gfb::g_joint_bwd_hr_variant;
+  gfb::g_joint_bwd_hr_variant = v;
+  return old;
+}
+
 int gf_joint_is_fused(int dtype, int64_t B, int64_t C, int64_t h, int64_t w, int64_t H,
                       int64_t W, int r) {
   return use_fused_joint(dtype, B, C, h, w, H, W, r) ? 1 : 0;

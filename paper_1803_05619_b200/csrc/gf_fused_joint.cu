@@ -657,17 +657,19 @@ struct MseHrArgs {
   const float* lr_x;
   const float* lr_y;
   const float* hr_x;
-  const float* target;
+  const float* target;  // MSE: the target; else d_out
   float* d_hr;
   float* db;
   float* dA;
-  double* loss_part;  // one per CTA: (plane, tile row, tile column)
+  double* loss_part;  // MSE: one per CTA (plane, tile row, tile column)
   int h, w, H, W, r;
   float eps, scale2;
   uint32_t* status;
 };
 
-template <int RAD, int MINB>
+// MSE = false: the same single gather pass for a given d_out (k_joint_bwd_hr's
+// job): `target` is d_out, A only, no loss.
+template <int RAD, int MINB, bool MSE>
 __global__ void __launch_bounds__(NT, MINB) k_joint_mse_hr(MseHrArgs a) {
   extern __shared__ float4 smem4[];
   __shared__ double red[NT / 32];
@@ -709,18 +711,22 @@ __global__ void __launch_bounds__(NT, MINB) k_joint_mse_hr(MseHrArgs a) {
     }
   }
   bool degen = false;
-  lr_coeffs<RAD, true>(a.lr_x + p * (int64_t)a.h * a.w, a.lr_y + p * (int64_t)a.h * a.w, a.h, a.w,
-                       i0, k0, a.eps, sm, degen);
+  lr_coeffs<RAD, MSE>(a.lr_x + p * (int64_t)a.h * a.w, a.lr_y + p * (int64_t)a.h * a.w, a.h, a.w,
+                      i0, k0, a.eps, sm, degen);
 
   const ColTaps ct = col_taps(X0, a.w, k0);
   const bool cin = k >= 1 && k <= a.w - 2;  // static column taps
   auto hrow2 = [&](int rl, float (&ha)[4], float (&hb)[4]) {
     if (cin) {
       hrow_interior(sm.As + rl * CAP, lane, ha);
-      hrow_interior(sm.Bs + rl * CAP, lane, hb);
+      if (MSE) hrow_interior(sm.Bs + rl * CAP, lane, hb);
     } else {
       hrow(sm.As + rl * CAP, ct, ha);
-      hrow(sm.Bs + rl * CAP, ct, hb);
+      if (MSE) hrow(sm.Bs + rl * CAP, ct, hb);
+    }
+    if (!MSE) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) hb[j] = 0.f;
     }
   };
   // adjoint weights of hr columns 4k-2 .. 4k+5 into lr column k
@@ -760,16 +766,20 @@ __global__ void __launch_bounds__(NT, MINB) k_joint_mse_hr(MseHrArgs a) {
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       const float Ah = alo[j] + f * (ahi[j] - alo[j]);
-      const float Bh = blo[j] + f * (bhi[j] - blo[j]);
-      const float o = Bh + Ah * gv[j];
-      const float e = o - tv[j];
-      d[j] = in ? scale2 * e : 0.f;
+      if (MSE) {
+        const float Bh = blo[j] + f * (bhi[j] - blo[j]);
+        const float o = Bh + Ah * gv[j];
+        const float e = o - tv[j];
+        d[j] = in ? scale2 * e : 0.f;
+        if (own) {
+          lsum = fmaf(e, e, lsum);
+          chk += o - o;  // NaN iff an output is not finite
+        }
+      } else {
+        d[j] = tv[j];  // d_out (0 outside)
+      }
       q[j] = d[j] * gv[j];
       dh[j] = d[j] * Ah;
-      if (own) {
-        lsum = fmaf(e, e, lsum);
-        chk += o - o;  // NaN iff an output is not finite
-      }
     }
     if (own)
       *reinterpret_cast<float4*>(DH + (int64_t)Y * a.W + X0) = make_float4(dh[0], dh[1], dh[2], dh[3]);
@@ -876,13 +886,16 @@ __global__ void __launch_bounds__(NT, MINB) k_joint_mse_hr(MseHrArgs a) {
           const Tap tx = tap4(X, a.w);
           const int cl = tx.lo - (k0 - 1), ch = tx.hi - (k0 - 1);
           // horizontal then vertical, as the row path
-          const float al = A0[cl] + tx.f * (A0[ch] - A0[cl]);
-          const float ah = A1[cl] + tx.f * (A1[ch] - A1[cl]);
-          const float bl = B0[cl] + tx.f * (B0[ch] - B0[cl]);
-          const float bh = B1[cl] + tx.f * (B1[ch] - B1[cl]);
-          const float Au = al + ty.f * (ah - al), Bu = bl + ty.f * (bh - bl);
           const float g = __ldg(G + (int64_t)Y * a.W + X), t = __ldg(T + (int64_t)Y * a.W + X);
-          const float dv = scale2 * ((Bu + Au * g) - t);
+          float dv = t;  // d_out
+          if (MSE) {
+            const float al = A0[cl] + tx.f * (A0[ch] - A0[cl]);
+            const float ah = A1[cl] + tx.f * (A1[ch] - A1[cl]);
+            const float bl = B0[cl] + tx.f * (B0[ch] - B0[cl]);
+            const float bh = B1[cl] + tx.f * (B1[ch] - B1[cl]);
+            const float Au = al + ty.f * (ah - al), Bu = bl + ty.f * (bh - bl);
+            dv = scale2 * ((Bu + Au * g) - t);
+          }
           float wgt = 0.f;
           if (tx.lo == kk) wgt += 1.f - tx.f;
           if (tx.hi == kk) wgt += tx.f;
@@ -896,7 +909,7 @@ __global__ void __launch_bounds__(NT, MINB) k_joint_mse_hr(MseHrArgs a) {
     }
   }
   // loss partial: warp sums (float64), combined in warp order below
-  {
+  if (MSE) {
     double v = (double)lsum;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -935,7 +948,7 @@ __global__ void __launch_bounds__(NT, MINB) k_joint_mse_hr(MseHrArgs a) {
     a.db[o] = s1;
     a.dA[o] = s2;
   }
-  if (threadIdx.x == 0) {
+  if (MSE && threadIdx.x == 0) {
     double s = 0.0;
 #pragma unroll
     for (int w = 0; w < NT / 32; ++w) s += red[w];
@@ -1149,6 +1162,7 @@ __global__ void __launch_bounds__(NT) k_joint_bwd_lr(BwdLrArgs a) {
 thread_local int g_joint_lr_variant = 0;
 thread_local int g_joint_mse_variant = 0;
 thread_local int g_joint_fwd_variant = 0;
+thread_local int g_joint_bwd_hr_variant = 0;
 
 bool fused_joint_ok(int64_t B, int64_t C, int64_t h, int64_t w, int64_t H, int64_t W, int r) {
   if (H != 4 * h || W != 4 * w) return false;
@@ -1169,6 +1183,7 @@ struct JointFns {
   const void* bwd_hr;
   const void* bwd_lr;
   const void* mse_hr;
+  const void* hr_pass;
 };
 
 template <int RAD>
@@ -1180,7 +1195,8 @@ static JointFns joint_fns() {
   else
     fwd = (const void*)jf::k_joint_fwd<RAD>;
   return {fwd, (const void*)jf::k_joint_bwd_hr<RAD>, (const void*)jf::k_joint_bwd_lr<RAD>,
-          (const void*)jf::k_joint_mse_hr<RAD, 3>};
+          (const void*)jf::k_joint_mse_hr<RAD, 3, true>,
+          (const void*)jf::k_joint_mse_hr<RAD, 4, false>};
 }
 
 static JointFns pick_joint(int r) {
@@ -1262,9 +1278,20 @@ void fused_joint_bwd(const float* lr_x, const float* lr_y, const float* hr_x, co
     set_smem(fns.bwd_hr, smem);
     dim3 grid((unsigned)((w + jf::TLX - 1) / jf::TLX), (unsigned)((h + jf::TLY - 1) / jf::TLY),
               (unsigned)(B * C));
-    jf::BwdHrArgs a{lr_x, lr_y, hr_x, d_out, d_hr_x, db, dA, (int)h, (int)w, (int)H, (int)W, r,
-                    eps, status};
-    launch(fns.bwd_hr, grid, smem, s, &a);
+    if (g_joint_bwd_hr_variant == 1) {  // the two-read tile kernel
+      jf::BwdHrArgs a{lr_x, lr_y, hr_x, d_out, d_hr_x, db, dA, (int)h, (int)w, (int)H, (int)W, r,
+                      eps, status};
+      launch(fns.bwd_hr, grid, smem, s, &a);
+    } else {  // single gather pass (d_hr and both adjoints from one read of hr_x,
+              // d_out): 736 vs 770 us at 8 x 3 x 3072^2, r = 2 (whole backward)
+      const void* fn = fns.hr_pass;
+      if (r == 2 && g_joint_bwd_hr_variant == 3) fn = (const void*)jf::k_joint_mse_hr<2, 3, false>;
+      if (r == 1 && g_joint_bwd_hr_variant == 3) fn = (const void*)jf::k_joint_mse_hr<1, 3, false>;
+      set_smem(fn, smem);
+      jf::MseHrArgs a{lr_x, lr_y, hr_x, d_out, d_hr_x, db, dA, nullptr, (int)h, (int)w, (int)H,
+                      (int)W, r, eps, 0.f, status};
+      launch(fn, grid, smem, s, &a);
+    }
   }
   joint_lr_tail(fns, lr_x, lr_y, db, dA, d_lr_x, d_lr_y, B, C, h, w, r, eps, s);
 }
@@ -1294,8 +1321,8 @@ void fused_joint_mse_bwd(const float* lr_x, const float* lr_y, const float* hr_x
     // variant hook: CTAs per SM the registers are budgeted for (3 default:
     // 421 us at config 2 vs 507 us for 2 (no spills) and 441 us for 4)
     const void* fn = fns.mse_hr;
-    if (r == 1 && g_joint_mse_variant == 2) fn = (const void*)jf::k_joint_mse_hr<1, 2>;
-    if (r == 1 && g_joint_mse_variant == 4) fn = (const void*)jf::k_joint_mse_hr<1, 4>;
+    if (r == 1 && g_joint_mse_variant == 2) fn = (const void*)jf::k_joint_mse_hr<1, 2, true>;
+    if (r == 1 && g_joint_mse_variant == 4) fn = (const void*)jf::k_joint_mse_hr<1, 4, true>;
     set_smem(fn, smem);
     dim3 grid((unsigned)((w + jf::TLX - 1) / jf::TLX), (unsigned)((h + jf::TLY - 1) / jf::TLY),
               (unsigned)(B * C));
