@@ -175,16 +175,22 @@ template <int HID>
 __global__ void __launch_bounds__(NT) k_fwd(const float* __restrict__ x, float* __restrict__ y,
                                              const float* __restrict__ params,
                                              const float* __restrict__ fold, int64_t HW) {
-  __shared__ float sw1[HID * CI], sbeta[HID], sw2[CO * HID], sb2[CO];
+  // per hidden unit: (W1f row, beta) and (W2 column, 0) as one 16-byte word
+  // each, read by a broadcast LDS.128
+  __shared__ float4 sW[HID], sV[HID];
   const int64_t b = blockIdx.y;
   const float* f = fold + b * F<HID>::count;
-  for (int i = threadIdx.x; i < HID * CI; i += NT) sw1[i] = f[F<HID>::w1f + i];
-  for (int i = threadIdx.x; i < HID; i += NT) sbeta[i] = f[F<HID>::beta + i];
-  for (int i = threadIdx.x; i < CO * HID; i += NT) sw2[i] = params[P<HID>::w2 + i];
-  for (int i = threadIdx.x; i < CO; i += NT) sb2[i] = params[P<HID>::b2 + i];
+  for (int j = threadIdx.x; j < HID; j += NT) {
+    sW[j] = make_float4(f[F<HID>::w1f + j * CI], f[F<HID>::w1f + j * CI + 1],
+                        f[F<HID>::w1f + j * CI + 2], f[F<HID>::beta + j]);
+    sV[j] = make_float4(params[P<HID>::w2 + j], params[P<HID>::w2 + HID + j],
+                        params[P<HID>::w2 + 2 * HID + j], 0.f);
+  }
   __syncthreads();
   const int64_t n4 = HW / 4;
   using namespace pr;
+  const u64 B0 = bc(params[P<HID>::b2]), B1 = bc(params[P<HID>::b2 + 1]),
+            B2 = bc(params[P<HID>::b2 + 2]);
   for (int64_t i = (int64_t)blockIdx.x * NT + threadIdx.x; i < n4; i += (int64_t)gridDim.x * NT) {
     ulonglong2 X[CI];  // pixel pairs (0,1), (2,3) of each channel
 #pragma unroll
@@ -192,12 +198,16 @@ __global__ void __launch_bounds__(NT) k_fwd(const float* __restrict__ x, float* 
       X[c] = __ldg(reinterpret_cast<const ulonglong2*>(x + (b * CI + c) * HW) + i);
     u64 out[CO][2];
 #pragma unroll
-    for (int o = 0; o < CO; ++o) out[o][0] = out[o][1] = bc(sb2[o]);
+    for (int pp = 0; pp < 2; ++pp) {
+      out[0][pp] = B0;
+      out[1][pp] = B1;
+      out[2][pp] = B2;
+    }
 #pragma unroll
     for (int j = 0; j < HID; ++j) {
-      const u64 w0 = bc(sw1[j * CI]), w1 = bc(sw1[j * CI + 1]), w2 = bc(sw1[j * CI + 2]);
-      const u64 be = bc(sbeta[j]);
-      const u64 v0 = bc(sw2[0 * HID + j]), v1 = bc(sw2[1 * HID + j]), v2 = bc(sw2[2 * HID + j]);
+      const float4 wv = sW[j], vv = sV[j];
+      const u64 w0 = bc(wv.x), w1 = bc(wv.y), w2 = bc(wv.z), be = bc(wv.w);
+      const u64 v0 = bc(vv.x), v1 = bc(vv.y), v2 = bc(vv.z);
 #pragma unroll
       for (int pp = 0; pp < 2; ++pp) {
         const u64 x0 = pp ? X[0].y : X[0].x, x1 = pp ? X[1].y : X[1].x,
@@ -601,15 +611,23 @@ __global__ void __launch_bounds__(NT, 2) k_bwd_h(const float* __restrict__ x,
                                               const float* __restrict__ fold,
                                               double* __restrict__ part, int64_t HW) {
   constexpr int NG = NT / 4;  // 4-pixel groups per CTA iteration
-  __shared__ float sw1f[HID * CI], sbeta[HID], sw2[CO * HID];
+  constexpr int JH = (HID + 3) / 4;  // hidden units per lane
+  // unit j = q JH + jj of lane q at [jj][q]: (W1f row, beta), (W2 column, 0),
+  // so the four lanes of a group read four consecutive 16-byte words
+  __shared__ float4 sW[JH * 4], sV[JH * 4];
   __shared__ ulonglong2 stage[NST][CI + CO][NG];
   const int64_t b = blockIdx.y;
   const float* f = fold + b * F<HID>::count;
-  for (int i = threadIdx.x; i < HID * CI; i += NT) sw1f[i] = f[F<HID>::w1f + i];
-  for (int i = threadIdx.x; i < HID; i += NT) sbeta[i] = f[F<HID>::beta + i];
-  for (int i = threadIdx.x; i < CO * HID; i += NT) sw2[i] = params[P<HID>::w2 + i];
+  for (int i = threadIdx.x; i < JH * 4; i += NT) {
+    const int j = (i & 3) * JH + (i >> 2);
+    sW[i] = j < HID ? make_float4(f[F<HID>::w1f + j * CI], f[F<HID>::w1f + j * CI + 1],
+                                  f[F<HID>::w1f + j * CI + 2], f[F<HID>::beta + j])
+                    : make_float4(0.f, 0.f, 0.f, 0.f);
+    sV[i] = j < HID ? make_float4(params[P<HID>::w2 + j], params[P<HID>::w2 + HID + j],
+                                  params[P<HID>::w2 + 2 * HID + j], 0.f)
+                    : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
   __syncthreads();
-  constexpr int JH = (HID + 3) / 4;  // hidden units per lane
   using namespace pr;
   const int q = threadIdx.x & 3;
   const int j0 = q * JH;
@@ -664,9 +682,9 @@ __global__ void __launch_bounds__(NT, 2) k_bwd_h(const float* __restrict__ x,
     for (int jj = 0; jj < JH; ++jj) {
       const int j = j0 + jj;
       if (j >= HID) break;
-      const u64 a0 = bc(sw1f[j * CI]), a1 = bc(sw1f[j * CI + 1]), a2 = bc(sw1f[j * CI + 2]);
-      const u64 be = bc(sbeta[j]);
-      const u64 v0 = bc(sw2[0 * HID + j]), v1 = bc(sw2[1 * HID + j]), v2 = bc(sw2[2 * HID + j]);
+      const float4 wv = sW[jj * 4 + q], vv = sV[jj * 4 + q];
+      const u64 a0 = bc(wv.x), a1 = bc(wv.y), a2 = bc(wv.z), be = bc(wv.w);
+      const u64 v0 = bc(vv.x), v1 = bc(vv.y), v2 = bc(vv.z);
 #pragma unroll
       for (int pp = 0; pp < 2; ++pp) {
         const u64 x0 = pp ? X[0].y : X[0].x, x1 = pp ? X[1].y : X[1].x,

@@ -228,3 +228,49 @@ def test_guidance_and_mse_guarded(lib, hidden):
 
     for a, b in zip(once(True), once(False)):
         assert torch.equal(a, b)
+
+
+def run_joint_mse(lib, lr_x, lr_y, hr_x, tgt, r, eps, guarded):
+    B, C, h, w = lr_x.shape
+    H, W = hr_x.shape[2:]
+    dt = dt_code(lr_x.dtype)
+    wsb = lib.gf_joint_mse_workspace_bytes(dt, B, C, h, w, H, W, r)
+    if guarded:
+        ins = [gin(t) for t in (lr_x, lr_y, hr_x, tgt)]
+        outs = [gout((1,), torch.float64), gout(lr_x.shape, lr_x.dtype),
+                gout(lr_x.shape, lr_x.dtype), gout(hr_x.shape, lr_x.dtype)]
+        ws = gws(wsb)
+        p = lambda g: g.ptr  # noqa: E731
+    else:
+        ins = [lr_x, lr_y, hr_x, tgt]
+        outs = [torch.empty(1, dtype=torch.float64, device="cuda"), torch.empty_like(lr_x),
+                torch.empty_like(lr_x), torch.empty_like(hr_x)]
+        ws = torch.empty(max(wsb, 16), dtype=torch.uint8, device="cuda")
+        p = lambda t: t.data_ptr()  # noqa: E731
+    st = status()
+    rc_ok(lib, lib.gf_joint_mse_bwd(dt, p(ins[0]), p(ins[1]), p(ins[2]), p(ins[3]), p(outs[0]),
+                                    p(outs[1]), p(outs[2]), p(outs[3]), B, C, h, w, H, W, r,
+                                    eps, p(ws), wsb, st.data_ptr(), stream()))
+    torch.cuda.synchronize()
+    assert int(st.item()) == 0
+    if guarded:
+        for g in ins + outs + [ws]:
+            assert g.guards_intact()
+        return [o.view.clone() for o in outs]
+    return outs
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
+@pytest.mark.parametrize("h,w,r", [(37, 45, 0), (33, 17, 5), (2, 3, 1), (130, 66, 2),
+                                   (21, 70, 12)])
+def test_joint_mse_guarded(lib, dtype, h, w, r):
+    """The fused training-step entry (fused kernel for fp32, the three-entry
+    chain for fp64): guard bands intact, bytes equal to an unguarded call."""
+    g = torch.Generator(device="cuda").manual_seed(h * 31 + w + r)
+    mk = lambda *s: torch.rand(*s, generator=g, device="cuda", dtype=dtype)  # noqa: E731
+    lr_x, lr_y = mk(2, 3, h, w), mk(2, 3, h, w)
+    hr_x, tgt = mk(2, 3, 4 * h, 4 * w), mk(2, 3, 4 * h, 4 * w)
+    a = run_joint_mse(lib, lr_x, lr_y, hr_x, tgt, r, 1e-3, guarded=True)
+    b = run_joint_mse(lib, lr_x, lr_y, hr_x, tgt, r, 1e-3, guarded=False)
+    for x, y in zip(a, b):
+        assert torch.equal(x, y)
