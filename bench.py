@@ -496,6 +496,10 @@ def main():
     for k in range(args.steps):
         if flush is not None:
             flush.sum()
+            # keep the device busy while the host enqueues the step, so the
+            # events bracket the step's device time, not the host's launch
+            # latency (matters only for the microsecond-scale configs)
+            torch.cuda._sleep(40000)
         evs[k][0].record()
         st.step()
         evs[k][1].record()

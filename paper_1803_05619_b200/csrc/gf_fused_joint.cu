@@ -1188,10 +1188,14 @@ struct JointFns {
 
 template <int RAD>
 static JointFns joint_fns() {
-  // r >= 8: fewer, longer coefficient-pass chunks (each pays a 2r warm-up)
+  // r >= 2: fewer, longer coefficient-pass chunks (each pays a 2r warm-up):
+  // 8 column chunks per row, and 2 row chunks for r >= 5 (config 3: r = 2
+  // 1352 -> 1296 us, r = 4 1419 -> 1348 us, r = 8 1571 -> 1500 us)
   const void* fwd;
-  if constexpr (RAD >= 8)
+  if constexpr (RAD >= 5)
     fwd = (const void*)jf::k_joint_fwd<RAD, 2, 8>;
+  else if constexpr (RAD >= 2)
+    fwd = (const void*)jf::k_joint_fwd<RAD, 0, 8>;
   else
     fwd = (const void*)jf::k_joint_fwd<RAD>;
   return {fwd, (const void*)jf::k_joint_bwd_hr<RAD>, (const void*)jf::k_joint_bwd_lr<RAD>,
@@ -1230,15 +1234,23 @@ void fused_joint_fwd(const float* lr_x, const float* lr_y, const float* hr_x, fl
   const int tx = (int)((w + jf::TLX - 1) / jf::TLX), ty = (int)((h + jf::TLY - 1) / jf::TLY);
   const size_t smem = jf::coef_smem_floats(r) * sizeof(float);
   const void* fn = fns.fwd;
-  if (r == 8) {  // variant hook: coefficient-pass chunking at r = 8 (default 2 x 8
-               // chunks: 1500 us at config 3 vs 1571 us for 4 x 16)
-    switch (g_joint_fwd_variant) {
-      case 1: fn = (const void*)jf::k_joint_fwd<8, 0, 16>; break;
-      case 2: fn = (const void*)jf::k_joint_fwd<8, 1, 4>; break;
-      case 3: fn = (const void*)jf::k_joint_fwd<8, 2, 4>; break;
-      case 4: fn = (const void*)jf::k_joint_fwd<8, 4, 8>; break;
-      default: break;
-    }
+  // variant hook: coefficient-pass chunking (vertical row chunks x horizontal
+  // column chunks per row; 0 = as many row chunks as the threads allow)
+  switch (g_joint_fwd_variant * 100 + r) {
+    case 108: fn = (const void*)jf::k_joint_fwd<8, 0, 16>; break;
+    case 208: fn = (const void*)jf::k_joint_fwd<8, 1, 4>; break;
+    case 308: fn = (const void*)jf::k_joint_fwd<8, 2, 4>; break;
+    case 408: fn = (const void*)jf::k_joint_fwd<8, 4, 8>; break;
+    case 104: fn = (const void*)jf::k_joint_fwd<4, 0, 16>; break;
+    case 204: fn = (const void*)jf::k_joint_fwd<4, 2, 8>; break;
+    case 304: fn = (const void*)jf::k_joint_fwd<4, 0, 4>; break;
+    case 102: fn = (const void*)jf::k_joint_fwd<2, 0, 16>; break;
+    case 202: fn = (const void*)jf::k_joint_fwd<2, 2, 8>; break;
+    case 302: fn = (const void*)jf::k_joint_fwd<2, 0, 4>; break;
+    case 101: fn = (const void*)jf::k_joint_fwd<1, 0, 8>; break;
+    case 201: fn = (const void*)jf::k_joint_fwd<1, 2, 8>; break;
+    case 301: fn = (const void*)jf::k_joint_fwd<1, 0, 4>; break;
+    default: break;
   }
   set_smem(fn, smem);
   dim3 grid((unsigned)tx, (unsigned)ty, (unsigned)(B * C));
