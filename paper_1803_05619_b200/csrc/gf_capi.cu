@@ -93,7 +93,8 @@ int gf_force_generic(int on) {
 // the fused sm_100a kernels, 0 when it takes the general kernels.
 // Test hook: pick the fp32 full-res forward kernel of THIS thread (0 automatic,
 // 1 batch/TMA kernel, 2 segment kernel, 3 segment kernel with 8 columns per
-// lane).  Returns the old value.
+// lane (the automatic choice), 4 segment kernel with 4 columns per lane).
+// Returns the old value.
 int gf_highres_variant(int v) {
   int old = g_highres_variant;
   g_highres_variant = v;
@@ -351,7 +352,9 @@ int gf_highres_fwd(int dtype, const void* guide, const void* src, void* out, int
       aligned16(out)) {
     if (use_seg_highres(dtype, B, Cg, C, H, W, radius)) {
       gfb::seg_highres_fwd((const float*)guide, (const float*)src, (float*)out, B, Cg, C, H, W,
-                           radius, (float)eps, g_highres_variant != 3, status, S(stream));
+                           radius, (float)eps,
+                           g_highres_variant == 3 ? 1 : g_highres_variant == 4 ? 2 : 0, status,
+                           S(stream));
       return check_launch("gf_highres_fwd[seg]");
     }
     gfb::fused_highres_fwd((const float*)guide, (const float*)src, (float*)out, B, Cg, C, H, W,

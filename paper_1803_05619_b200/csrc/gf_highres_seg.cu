@@ -3,7 +3,8 @@
 // unit, no CTA barriers.
 //
 // A warp owns a strip of 256 image columns (8 consecutive columns per lane:
-// two 16-byte chunks) and streams a piece of rows top to bottom.  Per
+// two 16-byte chunks; 4 per lane as a variant) and streams a piece of rows
+// top to bottom.  Per
 // coefficient row ya:
 //   level 1, vertical   window sums of (g, s, g^2, g*s) over rows ya-r..ya+r
 //                       kept in REGISTERS per column; the entering row is
@@ -48,9 +49,20 @@ struct Geo {
   static constexpr int NC = SW / 4;                        // 16-byte chunks per lane
   static constexpr int WC = 32 * SW;                       // columns per warp
   static constexpr int PAD = up4(2 * RAD);                 // left halo, 16-byte aligned
-  static constexpr int OW = (WC - PAD - 2 * RAD) / 4 * 4;  // output columns per warp
+  // output columns per warp; SW = 8, r = 8: 216 instead of 224 so the ring
+  // spans 29 lanes (31.5 KB: 7 warps per SM instead of 6; W = 2048 still
+  // needs 10 strips)
+  static constexpr int OW = (SW == 8 && RAD == 8) ? 216 : (WC - PAD - 2 * RAD) / 4 * 4;
   static constexpr int ringN = 2 * RAD + 1;                // coefficient rows kept
-  static constexpr size_t smem_bytes = (size_t)ringN * WC * 2 * sizeof(float);
+  // lanes whose columns feed an output ([PAD - r, PAD + OW + r)): only these
+  // keep a ring (the others' level-2 sums are never read)
+  // (8 columns per lane only: at 4 per lane the ring does not bind occupancy
+  // and the lane test measured slower)
+  static constexpr int L0 = SW == 8 ? (PAD - RAD) / SW : 0;
+  static constexpr int L1 =
+      SW == 8 && (PAD + OW + RAD + SW - 1) / SW < 32 ? (PAD + OW + RAD + SW - 1) / SW : 32;
+  static constexpr int RL = L1 - L0;
+  static constexpr size_t smem_bytes = (size_t)ringN * RL * NP * 4 * sizeof(float);
 };
 
 struct Args {
@@ -377,11 +389,13 @@ __device__ __forceinline__ void run_piece(const Piece& P, float4* __restrict__ r
     }
 
     // ---- level-2 vertical: ring slot of row ya holds row ya - ringN
-    float4* rs = ring + slot * (NP * 32) + lane;
-    if (STEADY || ya - ringN >= ya_lo) {
+    constexpr int RL = GG::RL;
+    const bool rlane = lane >= GG::L0 && lane < GG::L1;
+    float4* rs = ring + slot * (NP * RL) + (lane - GG::L0);
+    if (rlane && (STEADY || ya - ringN >= ya_lo)) {
 #pragma unroll
       for (int m = 0; m < NP; ++m) {
-        const float4 q = rs[32 * m];  // (A pair m, b' pair m)
+        const float4 q = rs[RL * m];  // (A pair m, b' pair m)
         VA[m] = sub2(VA[m], lo2(q));
         VB[m] = sub2(VB[m], hi2(q));
       }
@@ -390,7 +404,7 @@ __device__ __forceinline__ void run_piece(const Piece& P, float4* __restrict__ r
     for (int m = 0; m < NP; ++m) {
       VA[m] = add2(VA[m], A2[m]);
       VB[m] = add2(VB[m], B2[m]);
-      rs[32 * m] = make_float4(lo(A2[m]), hi(A2[m]), lo(B2[m]), hi(B2[m]));
+      if (rlane) rs[RL * m] = make_float4(lo(A2[m]), hi(A2[m]), lo(B2[m]), hi(B2[m]));
     }
     if (++slot == ringN) slot = 0;
 
@@ -450,10 +464,11 @@ __device__ __forceinline__ void run_piece(const Piece& P, float4* __restrict__ r
   __syncwarp();
 }
 
-template <int SW, int RAD>
-__global__ void __launch_bounds__(32) k_highres_seg(Args a) {
+// CAP: minimum resident warps per SM asked of ptxas (a register cap; 1 = none)
+template <int SW, int RAD, int CAP>
+__global__ void __launch_bounds__(32, CAP) k_highres_seg(Args a) {
   using GG = Geo<SW, RAD>;
-  extern __shared__ __align__(16) float4 ring[];  // [ringN][SW/2 pairs][32 lanes]
+  extern __shared__ __align__(16) float4 ring[];  // [ringN][SW/2 pairs][RL ring lanes]
   const int lane = threadIdx.x;
   const int H = (int)a.H, W = (int)a.W;
   const int c = (int)(blockIdx.x % a.C);
@@ -500,14 +515,16 @@ struct Launch {
   int ow;
 };
 
-template <int SW, int RAD>
+template <int SW, int RAD, int CAP = 1>
 Launch launch_info() {
-  return {(const void*)k_highres_seg<SW, RAD>, Geo<SW, RAD>::smem_bytes, Geo<SW, RAD>::OW};
+  return {(const void*)k_highres_seg<SW, RAD, CAP>, Geo<SW, RAD>::smem_bytes, Geo<SW, RAD>::OW};
 }
 
-// 4 columns per lane at r = 8 when allowed (twice the warps per SM for the
-// same ring bytes: 333 vs 400 us at config 1), else 8
-Launch pick(int r, bool sw4) {
+// 8 columns per lane; at r = 8 the 29-lane ring fits 7 warps per SM (293 us
+// at config 1, vs 308 us for 4 columns per lane at 12 warps per SM).  Mode 2
+// (test / measurement hook): 4 columns per lane at r = 8, registers capped at
+// 164 (3 warps per scheduler)
+Launch pick(int r, int mode) {
   switch (r) {
     case 1: return launch_info<8, 1>();
     case 2: return launch_info<8, 2>();
@@ -516,7 +533,8 @@ Launch pick(int r, bool sw4) {
     case 5: return launch_info<8, 5>();
     case 6: return launch_info<8, 6>();
     case 7: return launch_info<8, 7>();
-    case 8: return sw4 ? launch_info<4, 8>() : launch_info<8, 8>();
+    case 8:
+      return mode == 2 ? launch_info<4, 8, 12>() : launch_info<8, 8>();
     default: return {nullptr, 0, 0};
   }
 }
@@ -532,12 +550,12 @@ bool seg_highres_fwd_ok(int64_t B, int64_t Cg, int64_t C, int64_t H, int64_t W, 
 }
 
 void seg_highres_fwd(const float* guide, const float* src, float* out, int64_t B, int64_t Cg,
-                     int64_t C, int64_t H, int64_t W, int r, float eps, bool allow_sw4,
+                     int64_t C, int64_t H, int64_t W, int r, float eps, int mode,
                      uint32_t* status, cudaStream_t s) {
-  const hrs::Launch L = hrs::pick(r, allow_sw4);
-  static int per_sm_cache[2][hrs::kMaxRadius + 1] = {{0}};
+  const hrs::Launch L = hrs::pick(r, mode);
+  static int per_sm_cache[3][hrs::kMaxRadius + 1] = {{0}};
   static int sms = 0;
-  int& per_sm_r = per_sm_cache[allow_sw4 ? 1 : 0][r];
+  int& per_sm_r = per_sm_cache[mode][r];
   if (per_sm_r == 0) {
     int dev = 0;
     cudaGetDevice(&dev);

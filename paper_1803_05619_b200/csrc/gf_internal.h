@@ -62,7 +62,7 @@ void mse_final(const double* partials, double* loss, int64_t B, int nblk, double
 // full-resolution forward, register-segment variant for r <= 8 (gf_highres_seg.cu)
 bool seg_highres_fwd_ok(int64_t B, int64_t Cg, int64_t C, int64_t H, int64_t W, int r);
 void seg_highres_fwd(const float* guide, const float* src, float* out, int64_t B, int64_t Cg,
-                     int64_t C, int64_t H, int64_t W, int r, float eps, bool allow_sw4,
+                     int64_t C, int64_t H, int64_t W, int r, float eps, int mode,
                      uint32_t* status, cudaStream_t s);
 bool fused_highres_fwd_ok(int64_t B, int64_t Cg, int64_t C, int64_t H, int64_t W, int r);
 void fused_highres_fwd(const float* guide, const float* src, float* out, int64_t B, int64_t Cg,

@@ -25,7 +25,7 @@ def run(r, eps):
 
 for r in [int(x) for x in (sys.argv[1:] or ["8"])]:
     res = {}
-    for v in (1, 2, 3):
+    for v in (1, 2, 3, 4):
         old = lib.gf_highres_variant(v)
         for _ in range(3):
             run(r, 1e-2)

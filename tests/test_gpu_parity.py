@@ -696,7 +696,7 @@ def test_fused_highres_backward_vs_oracle(gfb, H, W, r, cg):
                                       (2, 12, 8, 1), (45, 512, 8, 3), (19, 496, 4, 3)])
 def test_highres_kernel_variants_vs_oracle(gfb, H, W, r, cg):
     """Every fp32 full-res forward kernel (batch/TMA, register-segment with 4
-    and 8 columns per lane) against the oracle on ragged shapes: strips not
+    and 8 columns per lane, 4 per lane register-capped) against the oracle on ragged shapes: strips not
     dividing W, W = 4, H = 1, pieces spanning two strips."""
     from paper_1803_05619_b200 import _lib
 
@@ -707,7 +707,7 @@ def test_highres_kernel_variants_vs_oracle(gfb, H, W, r, cg):
     p = gfb.GuidedFilterParams(r, 1e-2)
     want = O.highres_forward_nchw(guide, src, r, 1e-2)
     outs = []
-    for v in (1, 2, 3):
+    for v in (1, 2, 3, 4):
         old = lib.gf_highres_variant(v)
         try:
             out, _ = gfb.forward_highres(t32(guide), t32(src), p)
@@ -717,7 +717,7 @@ def test_highres_kernel_variants_vs_oracle(gfb, H, W, r, cg):
         outs.append(npy(out))
 
 
-@pytest.mark.parametrize("variant,r", [(1, 2), (2, 2), (3, 2), (2, 4), (2, 8), (3, 8)])
+@pytest.mark.parametrize("variant,r", [(1, 2), (2, 2), (3, 2), (2, 4), (2, 8), (3, 8), (4, 8)])
 def test_highres_kernel_variants_status(gfb, variant, r):
     from paper_1803_05619_b200 import _lib
 
