@@ -499,7 +499,7 @@ def main():
             # keep the device busy while the host enqueues the step, so the
             # events bracket the step's device time, not the host's launch
             # latency (matters only for the microsecond-scale configs)
-            torch.cuda._sleep(40000)
+            torch.cuda._sleep(200000)  # ~100 us: covers the Python API call
         evs[k][0].record()
         st.step()
         evs[k][1].record()
