@@ -167,7 +167,7 @@ int gn_backward_reuse(int dtype, const void* x, const void* dy, void* dx, void* 
                       size_t workspace_bytes, uint32_t* status, void* stream);
 
 /* ---- host-buffer entries: the reference's call shape (host images in, host
- * image out; gf/guided.py:152 guided_filter, :198 guided_filter_full) ----
+ * image out; gf/guided.py:152 forward_joint, :198 forward_highres) ----
  * Synchronous: the calls return when `out` (HOST memory) is written.  The
  * batch streams through the device chunk by chunk -- one plane, or one image
  * when a 1-channel guide drives C planes (copy-in of chunk b+1, kernel of

@@ -65,7 +65,13 @@ def as_img(t, name: str = "tensor", dtype=None, device=None) -> Img:
             raise ValueError(f"{name}: expected a CUDA tensor (no CPU fallback), got {t.device}")
         if t.dim() == 3:
             return Img(t.permute(2, 0, 1).unsqueeze(0).contiguous(), "torch_hwc")
-        return Img(t.contiguous(), "torch_nchw")
+        x = t.contiguous()
+        if x.data_ptr() % 16:
+            # e.g. a batch slice lr[1:] with odd C*h*w: the fused kernels use
+            # 128-bit accesses, so hand them an aligned copy (the C ABI would
+            # otherwise take the general kernels, which need a larger workspace)
+            x = x.clone(memory_format=torch.contiguous_format)
+        return Img(x, "torch_nchw")
     raise ValueError(f"{name}: expected a numpy array or torch tensor, got {type(t).__name__}")
 
 

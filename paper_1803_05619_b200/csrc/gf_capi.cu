@@ -249,12 +249,21 @@ static int check_joint(int dtype, int64_t B, int64_t C, int64_t h, int64_t w, in
   return GF_OK;
 }
 
+// workspace of the general (any alignment / dtype / ratio) joint kernels
+static size_t joint_generic_bytes(int64_t B, int64_t C, int64_t h, int64_t w) {
+  return gfb::generic_workspace_bytes(B * C * h * w, 0);
+}
+
+// The fused kernels need 16-byte aligned buffers; the size returned here is
+// for such buffers (what torch's allocator and the Python mirror hand out).
+// Unaligned buffers take the general kernels, whose larger need is checked
+// against the caller's workspace_bytes at the call (GF_ERR_WORKSPACE with the
+// required size in gf_last_error, never an overrun).
 size_t gf_joint_workspace_bytes(int dtype, int64_t B, int64_t C, int64_t h, int64_t w, int64_t H,
                                 int64_t W, int radius) {
-  size_t gen = gfb::generic_workspace_bytes(B * C * h * w, 0);
   if (use_fused_joint(dtype, B, C, h, w, H, W, radius))
     return gfb::fused_joint_bwd_ws_bytes(B, C, h, w);
-  return gen;
+  return joint_generic_bytes(B, C, h, w);
 }
 
 int gf_joint_fwd(int dtype, const void* lr_x, const void* lr_y, const void* hr_x, void* out,
@@ -268,9 +277,11 @@ int gf_joint_fwd(int dtype, const void* lr_x, const void* lr_y, const void* hr_x
                          B, C, h, w, H, W, radius, (float)eps, status, S(stream));
     return check_launch("gf_joint_fwd[fused]");
   }
-  size_t need = gf_joint_workspace_bytes(dtype, B, C, h, w, H, W, radius);
+  // general kernels (unaligned buffers, fp64, other shapes)
+  size_t need = joint_generic_bytes(B, C, h, w);
   if (workspace_bytes < need)
-    return fail(GF_ERR_WORKSPACE, "joint workspace %zu < %zu bytes", workspace_bytes, need);
+    return fail(GF_ERR_WORKSPACE, "joint workspace %zu < %zu bytes (general kernels)",
+                workspace_bytes, need);
   if (dtype == GF_F32)
     gfb::generic_joint_fwd<float>((const float*)lr_x, (const float*)lr_y, (const float*)hr_x,
                                   (float*)out, B, C, h, w, H, W, radius, eps, workspace, status,
@@ -287,12 +298,14 @@ int gf_joint_bwd(int dtype, const void* lr_x, const void* lr_y, const void* hr_x
                  int64_t C, int64_t h, int64_t w, int64_t H, int64_t W, int radius, double eps,
                  void* workspace, size_t workspace_bytes, uint32_t* status, void* stream) {
   if (int e = check_joint(dtype, B, C, h, w, H, W, radius, eps)) return e;
-  size_t need = gf_joint_workspace_bytes(dtype, B, C, h, w, H, W, radius);
+  const bool fused = use_fused_joint(dtype, B, C, h, w, H, W, radius) && aligned16(lr_x) &&
+                     aligned16(lr_y) && aligned16(hr_x) && aligned16(d_out) &&
+                     aligned16(d_lr_x) && aligned16(d_lr_y) && aligned16(d_hr_x);
+  size_t need = fused ? gfb::fused_joint_bwd_ws_bytes(B, C, h, w) : joint_generic_bytes(B, C, h, w);
   if (workspace_bytes < need)
-    return fail(GF_ERR_WORKSPACE, "joint workspace %zu < %zu bytes", workspace_bytes, need);
-  if (use_fused_joint(dtype, B, C, h, w, H, W, radius) && aligned16(lr_x) && aligned16(lr_y) &&
-      aligned16(hr_x) && aligned16(d_out) && aligned16(d_lr_x) && aligned16(d_lr_y) &&
-      aligned16(d_hr_x)) {
+    return fail(GF_ERR_WORKSPACE, "joint workspace %zu < %zu bytes%s", workspace_bytes, need,
+                fused ? "" : " (general kernels)");
+  if (fused) {
     gfb::fused_joint_bwd((const float*)lr_x, (const float*)lr_y, (const float*)hr_x,
                          (const float*)d_out, (float*)d_lr_x, (float*)d_lr_y, (float*)d_hr_x, B,
                          C, h, w, H, W, radius, (float)eps, workspace, status, S(stream));
@@ -338,12 +351,6 @@ size_t gf_highres_workspace_bytes(int dtype, int64_t B, int64_t Cg, int64_t C, i
   return gen;
 }
 
-static size_t highres_fwd_need(int dtype, int64_t B, int64_t Cg, int64_t C, int64_t H, int64_t W,
-                               int r) {
-  if (use_fused_highres(dtype, B, Cg, C, H, W, r)) return 0;
-  return gf_highres_workspace_bytes(dtype, B, Cg, C, H, W, r);
-}
-
 int gf_highres_fwd(int dtype, const void* guide, const void* src, void* out, int64_t B, int64_t Cg,
                    int64_t C, int64_t H, int64_t W, int radius, double eps, void* workspace,
                    size_t workspace_bytes, uint32_t* status, void* stream) {
@@ -361,9 +368,11 @@ int gf_highres_fwd(int dtype, const void* guide, const void* src, void* out, int
                            radius, (float)eps, status, S(stream));
     return check_launch("gf_highres_fwd[fused]");
   }
-  size_t need = highres_fwd_need(dtype, B, Cg, C, H, W, radius);
+  // general kernels (unaligned buffers, fp64, other shapes)
+  size_t need = gf_highres_workspace_bytes(dtype, B, Cg, C, H, W, radius);
   if (workspace_bytes < need)
-    return fail(GF_ERR_WORKSPACE, "highres workspace %zu < %zu bytes", workspace_bytes, need);
+    return fail(GF_ERR_WORKSPACE, "highres workspace %zu < %zu bytes (general kernels)",
+                workspace_bytes, need);
   if (dtype == GF_F32)
     gfb::generic_highres_fwd<float>((const float*)guide, (const float*)src, (float*)out, B, Cg, C,
                                      H, W, radius, eps, workspace, status, S(stream));
@@ -618,13 +627,19 @@ int gf_mse_loss(int dtype, const void* out, const void* target, void* d_out, dou
 // ---- fused training step of the fast layer (forward + MSE + backward) ----
 static size_t al256(size_t n) { return (n + 255) / 256 * 256; }
 
+// general-path layout: [joint ws | mse ws | out | d_out]
+static size_t joint_mse_generic_bytes(int dtype, int64_t B, int64_t C, int64_t h, int64_t w,
+                                      int64_t H, int64_t W) {
+  const size_t es = dtype == GF_F64 ? 8 : 4;
+  return al256(joint_generic_bytes(B, C, h, w)) + al256(gfb::mse_ws_bytes(B)) +
+         2 * al256((size_t)B * C * H * W * es);
+}
+
 size_t gf_joint_mse_workspace_bytes(int dtype, int64_t B, int64_t C, int64_t h, int64_t w,
                                     int64_t H, int64_t W, int radius) {
   if (use_fused_joint(dtype, B, C, h, w, H, W, radius))
     return gfb::fused_joint_mse_ws_bytes(B, C, h, w);
-  const size_t es = dtype == GF_F64 ? 8 : 4;
-  return al256(gf_joint_workspace_bytes(dtype, B, C, h, w, H, W, radius)) +
-         al256(gfb::mse_ws_bytes(B)) + 2 * al256((size_t)B * C * H * W * es);
+  return joint_mse_generic_bytes(dtype, B, C, h, w, H, W);
 }
 
 int gf_joint_mse_bwd(int dtype, const void* lr_x, const void* lr_y, const void* hr_x,
@@ -633,34 +648,40 @@ int gf_joint_mse_bwd(int dtype, const void* lr_x, const void* lr_y, const void* 
                      int radius, double eps, void* workspace, size_t workspace_bytes,
                      uint32_t* status, void* stream) {
   if (int e = check_joint(dtype, B, C, h, w, H, W, radius, eps)) return e;
-  const size_t need = gf_joint_mse_workspace_bytes(dtype, B, C, h, w, H, W, radius);
+  const bool fused = use_fused_joint(dtype, B, C, h, w, H, W, radius) && aligned16(lr_x) &&
+                     aligned16(lr_y) && aligned16(hr_x) && aligned16(target) &&
+                     aligned16(d_lr_x) && aligned16(d_lr_y) && aligned16(d_hr_x);
+  const size_t need = fused ? gfb::fused_joint_mse_ws_bytes(B, C, h, w)
+                            : joint_mse_generic_bytes(dtype, B, C, h, w, H, W);
   if (workspace_bytes < need)
-    return fail(GF_ERR_WORKSPACE, "joint mse workspace %zu < %zu bytes", workspace_bytes, need);
-  if (use_fused_joint(dtype, B, C, h, w, H, W, radius) && aligned16(lr_x) && aligned16(lr_y) &&
-      aligned16(hr_x) && aligned16(target) && aligned16(d_lr_x) && aligned16(d_lr_y) &&
-      aligned16(d_hr_x)) {
+    return fail(GF_ERR_WORKSPACE, "joint mse workspace %zu < %zu bytes%s", workspace_bytes, need,
+                fused ? "" : " (general kernels)");
+  if (fused) {
     gfb::fused_joint_mse_bwd((const float*)lr_x, (const float*)lr_y, (const float*)hr_x,
                              (const float*)target, loss, (float*)d_lr_x, (float*)d_lr_y,
                              (float*)d_hr_x, B, C, h, w, H, W, radius, (float)eps, workspace,
                              status, S(stream));
     return check_launch("gf_joint_mse_bwd[fused]");
   }
-  // any other call: forward, MSE and backward through the three entries, with
-  // out and d_out in the workspace
+  // any other call: forward, MSE and backward through the general kernels,
+  // with out and d_out in the workspace
   const size_t es = dtype == GF_F64 ? 8 : 4;
-  const size_t jws = al256(gf_joint_workspace_bytes(dtype, B, C, h, w, H, W, radius));
+  const size_t jws = al256(joint_generic_bytes(B, C, h, w));
   const size_t mws = al256(gfb::mse_ws_bytes(B));
   const size_t hb = al256((size_t)B * C * H * W * es);
   char* base = (char*)workspace;
   void* out = base + jws + mws;
   void* d_out = base + jws + mws + hb;
-  if (int e = gf_joint_fwd(dtype, lr_x, lr_y, hr_x, out, B, C, h, w, H, W, radius, eps, base,
-                           jws, status, stream))
-    return e;
-  if (int e = gf_mse_loss(dtype, out, target, d_out, loss, B, C, H, W, base + jws, mws, stream))
-    return e;
-  return gf_joint_bwd(dtype, lr_x, lr_y, hr_x, d_out, d_lr_x, d_lr_y, d_hr_x, B, C, h, w, H, W,
-                      radius, eps, base, jws, status, stream);
+  const int old = g_force_generic;
+  g_force_generic = 1;  // the fused kernels would reject the unaligned buffers anyway
+  int e = gf_joint_fwd(dtype, lr_x, lr_y, hr_x, out, B, C, h, w, H, W, radius, eps, base, jws,
+                       status, stream);
+  if (!e) e = gf_mse_loss(dtype, out, target, d_out, loss, B, C, H, W, base + jws, mws, stream);
+  if (!e)
+    e = gf_joint_bwd(dtype, lr_x, lr_y, hr_x, d_out, d_lr_x, d_lr_y, d_hr_x, B, C, h, w, H, W,
+                     radius, eps, base, jws, status, stream);
+  g_force_generic = old;
+  return e;
 }
 
 }  // extern "C"

@@ -624,23 +624,13 @@ void fused_highres_fwd(const float* guide, const float* src, float* out, int64_t
                        int64_t C, int64_t H, int64_t W, int r, float eps, uint32_t* status,
                        cudaStream_t s) {
   const hrf::Launch L = hrf::pick(r);
-  // per-radius launch configuration, cached (the queries cost microseconds)
-  static int per_sm_cache[hrf::kMaxRadius + 1] = {0};
-  static int sms = 0;
-  if (per_sm_cache[r] == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaFuncSetAttribute(L.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.smem);
-    int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, L.fn, L.nt, L.smem);
-    per_sm_cache[r] = per_sm < 1 ? 1 : per_sm;
-  }
+  const LaunchCfg lc = launch_cfg(L.fn, L.nt, L.smem);
+  const int sms = lc.sms;
   // strips of equal width (multiple of K, at most the kernel's bound)
   const int64_t nstrip = (W + L.txm - 1) / L.txm;
   const int tx = (int)(((W + nstrip - 1) / nstrip + hrf::K - 1) / hrf::K * hrf::K);
   const int64_t strips = (W + tx - 1) / tx;
-  const int64_t slots = (int64_t)sms * per_sm_cache[r];
+  const int64_t slots = (int64_t)sms * lc.per_sm;
   // balanced chunks of the rows of all (image, strip) columns: one wave of
   // C x nch CTAs, more waves only to keep a chunk <= 1024 rows (bounded
   // running-sum rounding); at least 8 rows per chunk

@@ -280,12 +280,7 @@ __global__ void k_guide_sum(const float* __restrict__ dg, float* __restrict__ ou
 template <int NF, class In, class Out>
 void run(const Geom& g, In in, Out out, cudaStream_t s) {
   const size_t smem = (size_t)NF * R * PV * sizeof(float);
-  static bool attr_set = false;  // per instantiation
-  if (!attr_set) {
-    cudaFuncSetAttribute(k_box_stream<NF, In, Out>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)smem);
-    attr_set = true;
-  }
+  launch_cfg((const void*)k_box_stream<NF, In, Out>, NT, smem);  // per-device smem limit
   const int64_t grid = g.P * g.strips * g.segs;
   k_box_stream<NF, In, Out><<<(unsigned)grid, NT, smem, s>>>(g, in, out);
 }

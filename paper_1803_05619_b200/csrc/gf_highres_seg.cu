@@ -553,18 +553,8 @@ void seg_highres_fwd(const float* guide, const float* src, float* out, int64_t B
                      int64_t C, int64_t H, int64_t W, int r, float eps, int mode,
                      uint32_t* status, cudaStream_t s) {
   const hrs::Launch L = hrs::pick(r, mode);
-  static int per_sm_cache[3][hrs::kMaxRadius + 1] = {{0}};
-  static int sms = 0;
-  int& per_sm_r = per_sm_cache[mode][r];
-  if (per_sm_r == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaFuncSetAttribute(L.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.smem);
-    int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, L.fn, 32, L.smem);
-    per_sm_r = per_sm < 1 ? 1 : per_sm;
-  }
+  const LaunchCfg lc = launch_cfg(L.fn, 32, L.smem);
+  const int sms = lc.sms, per_sm_r = lc.per_sm;
   const int64_t strips = (W + L.ow - 1) / L.ow;
   const int64_t slots = (int64_t)sms * per_sm_r;
   // balanced pieces of the rows of all (image, strip) columns: one wave of

@@ -7,6 +7,16 @@
 
 namespace gfb {
 
+// ---- per-device launch configuration (gf_launch.cu): SM count and resident
+// CTAs per SM of `fn` at this block size / dynamic smem on the CURRENT device;
+// also raises the kernel's dynamic shared-memory limit on that device.  Cached
+// per (device, fn, threads, smem), thread-safe.
+struct LaunchCfg {
+  int sms;
+  int per_sm;
+};
+LaunchCfg launch_cfg(const void* fn, int threads, size_t smem);
+
 // ---- generic (any shape / radius / dtype) ----
 size_t generic_workspace_bytes(int64_t n_moment_plane_total, int64_t extra_doubles);
 

@@ -367,19 +367,8 @@ void seg_joint_bwd_lr(const float* lr_x, const float* lr_y, const float* db, con
                       float* d_lr_x, float* d_lr_y, int64_t P, int64_t h, int64_t w, int r,
                       float eps, cudaStream_t s) {
   const jls::Launch L = jls::pick(r);
-  static int per_sm_cache[jls::kMaxRadius + 1] = {0};
-  static int sms = 0;
-  int& per_sm = per_sm_cache[r];
-  if (per_sm == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (L.smem > 48 * 1024)
-      cudaFuncSetAttribute(L.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.smem);
-    int b = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, L.fn, jls::WPB * 32, L.smem);
-    per_sm = b < 1 ? 1 : b;
-  }
+  const LaunchCfg lc = launch_cfg(L.fn, jls::WPB * 32, L.smem);
+  const int sms = lc.sms, per_sm = lc.per_sm;
   const int64_t strips = (w + L.ow - 1) / L.ow;
   const int64_t slots = (int64_t)sms * per_sm * jls::WPB;
   // balanced pieces of the rows of all (plane, strip) columns: one wave of

@@ -82,6 +82,22 @@ class GuidedFilterTape:
     _out_like: Img
     status: Status
     _cache: dict = field(default_factory=dict)
+    _versions: tuple = ()
+
+    def __post_init__(self) -> None:
+        # autograd-style saved-tensor check: backward recomputes the moments
+        # from the inputs (the reference freezes them in the tape), so an
+        # in-place edit between forward and backward must not go unnoticed
+        self._versions = self._input_versions()
+
+    def _input_versions(self) -> tuple:
+        return tuple(im.t._version for im in (self._guide, self._src, self._guide_hi))
+
+    def check_unmodified(self) -> None:
+        if self._input_versions() != self._versions:
+            raise RuntimeError(
+                "an input of the forward pass was modified in place after the forward; "
+                "backward would use the new values (clone the input, or run forward again)")
 
     # reference field names ------------------------------------------------
     @property
@@ -97,6 +113,7 @@ class GuidedFilterTape:
         return restore(self._guide_hi.t, self._guide_hi)
 
     def _moments(self):
+        self.check_unmodified()
         if "m" not in self._cache:
             self._cache["m"] = _tape_moments(self)
         return self._cache["m"]
@@ -197,6 +214,7 @@ def forward_highres(guide_hi, src_hi, p: GuidedFilterParams, *, check: bool = Tr
 def backward(tape: GuidedFilterTape, d_out, *, check: bool = True) -> GuidedFilterGrads:
     """Gradients of dot(d_out, out) w.r.t. the forward inputs (gf/guided.py:267-297)."""
     like = tape._out_like
+    tape.check_unmodified()
     d = as_img(d_out, "d_out", device=like.t.device)
     if d.shape != like.shape:
         raise ValueError(f"d_out shape {d.shape} does not match output shape {like.shape}")

@@ -1,5 +1,5 @@
 """Host-image entry points: the reference's call shape (host arrays in, host
-array out -- gf/guided.py:152 guided_filter, :198 guided_filter_full) over the
+array out -- gf/guided.py:152 forward_joint, :198 forward_highres) over the
 C ABI's pipelined host entries (gf_highres_fwd_host / gf_joint_fwd_host).
 
 The batch streams through the GPU image by image: the copy-in of image b+1,
@@ -16,6 +16,7 @@ production path).  The result has the input's layout and container; pass
 from __future__ import annotations
 
 import ctypes
+import threading
 
 import numpy as np
 import torch
@@ -23,14 +24,24 @@ import torch
 from . import _lib
 from .guided import DegenerateWindowError, GuidedFilterParams
 
-_WS: dict = {}  # device -> cached device workspace (grown on demand)
+_WS: dict = {}  # (host thread, device) -> cached device workspace (grown on demand)
 
 
 def _workspace(nbytes: int, device) -> torch.Tensor:
-    key = str(device)
+    """One device workspace per (host thread, device).
+
+    The C pipeline runs on its own per-thread streams and releases the GIL,
+    so two threads must never share a buffer.  The block comes from torch's
+    caching allocator on torch's current stream, which the library's streams
+    do not wait on: synchronise that stream once when the block is
+    (re)allocated, so no earlier torch work can still be using it.  The
+    cached block stays referenced here, so it is never handed out again.
+    """
+    key = (threading.get_ident(), str(device))
     ws = _WS.get(key)
     if ws is None or ws.numel() < nbytes:
         ws = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=device)
+        torch.cuda.current_stream(device).synchronize()
         _WS[key] = ws
     return ws
 
