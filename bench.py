@@ -1,29 +1,35 @@
 """Benchmark driver for the B200 guided-filter layer.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg1] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg4a] [--impl ours|reference]
 
-Prints ONE JSON line (rank 0).  Default workload: BASELINE.json configs[1],
-the full-resolution guided filter forward (4 x {1,3} x 2048^2, r=8,
-eps=1e-2, fp32), on seeded synthetic inputs with that config's shapes and
-value distributions (workloads.py).  Other configs: cfg0 (joint fwd 1024^2),
-cfg3 (joint fwd sweep point, --hr/--batch/--radius), cfg4a/cfg4b (joint
-fwd+bwd), cfg2 (training step).
+Prints ONE JSON line (rank 0) on stdout.  Default workload: BASELINE.json
+configs[4](a), the largest single-GPU configuration and the batch-sharded
+multi-GPU one: joint (fast) guided filter forward + backward over a batch of
+64 images of 3 x 3072^2 (low-res 3 x 768^2), r=2, eps=1e-4, fp32, the batch
+split over the N ranks (strong scaling).  Other configs: cfg0 (joint fwd
+1024^2), cfg1 (full-res fwd 4 x 2048^2, r=8), cfg2 (training step), cfg3
+(joint fwd sweep point, --hr/--batch/--radius), cfg4b (one 16384^2 image in
+row bands).  Inputs are seeded synthetic data with the configs' shapes and
+value distributions (workloads.py).
 
+* ``--gpus N`` without a torchrun environment re-launches itself under
+  ``torch.distributed.run`` with N ranks (one process per GPU, NCCL,
+  NCCL_DEBUG=INFO to stderr so the communicator lines show the rank count).
 * ``value``: whole-job output Mpix/s with inputs resident in HBM, timed with
   CUDA events on the launching stream over exactly K steps bracketed by a
   barrier + synchronize, max over ranks.  A "step" is one call of the layer
-  over the whole batch.  Multi-GPU: every rank runs the full per-GPU batch on
-  its own GPU (weak scaling, batch sharding, no data-path collective).
-* ``e2e``: the same metric through the public Python API with pinned HOST
-  buffers: H2D of the step's inputs and D2H of its output inside the timed
-  region.
-* ``roofline``: algorithmic bytes per launch of the dominant kernel (SURVEY
-  8d) / its average CUDA-event duration, against the measured HBM copy peak
-  (MEASURED_PEAKS.json).
-* ``cpu_baseline``: the CPU oracle (numpy port of the reference algorithm)
-  on a bounded sample, rank 0, N=1 only.
-* ``--impl reference``: the oracle port on the host cores (multiprocessing
-  over images), same metric/config, bounded per-step sample.
+  (forward, or forward + backward) over the rank's share of the batch.
+* ``e2e``: the same metric through the public host API with pinned HOST
+  buffers, every input copied in and every output copied out inside the
+  timed region (forward + backward: ``forward_backward_joint_host``, which
+  pipelines copy-in / kernels / copy-out plane by plane).
+* ``roofline``: algorithmic bytes per step / the CUDA-event step
+  time, against the measured HBM copy peak (MEASURED_PEAKS.json).
+* ``cpu_baseline``: the reference's own CPU path (the unmodified
+  ``guidedfilter`` package with its numba kernels, baseline/_ref) on all host
+  cores, one process per image (cpu_reference.py); rank 0, N=1 only.
+* ``--impl reference``: the same CPU reference on the same config, metric and
+  unit, bounded per-step samples; rank 0 only under torchrun.
 """
 
 from __future__ import annotations
@@ -201,6 +207,7 @@ class OursStep:
             if c.get("shard") == "rows":  # config 4b: row bands with the backward halo
                 band = row_bands(H // f, world, c["r"], factor=f, backward=True)[rank]
                 lo, hi = band.crop_lo, band.crop_hi
+                self.row0 = lo  # full-image row of the crop: bitwise band results
                 Hlo, Hhi = band.hr_crop
                 lr_x = lr_x[:, :, lo:hi].contiguous()
                 lr_y = lr_y[:, :, lo:hi].contiguous()
@@ -210,6 +217,7 @@ class OursStep:
                 self.pixels = B * (A1 - A0) * H  # owned output rows only
                 torch.cuda.empty_cache()
             self.inputs = [lr_x, lr_y, hr_x]
+            self.row0 = getattr(self, "row0", 0)
             self.h, self.w = self.H // f, self.W // f
             self.out = torch.empty_like(hr_x)
             nb = self.lib.gf_joint_workspace_bytes(0, B, C, self.h, self.w, self.H, self.W, c["r"])
@@ -257,11 +265,11 @@ class OursStep:
                                 self.sp)
             assert rc == 0, L.gf_last_error()
             if self.kind == "joint_fwd_bwd":
-                rc = L.gf_joint_bwd(0, lx.data_ptr(), ly.data_ptr(), hx.data_ptr(),
-                                    self.d_out.data_ptr(), self.d_lr_x.data_ptr(),
-                                    self.d_lr_y.data_ptr(), self.d_hr_x.data_ptr(), B, C, h, w,
-                                    Hh, Ww, r, eps, self.ws.data_ptr(), self.ws.numel(),
-                                    self.status.data_ptr(), self.sp)
+                rc = L.gf_joint_bwd_band(0, lx.data_ptr(), ly.data_ptr(), hx.data_ptr(),
+                                         self.d_out.data_ptr(), self.d_lr_x.data_ptr(),
+                                         self.d_lr_y.data_ptr(), self.d_hr_x.data_ptr(), B, C, h,
+                                         w, Hh, Ww, r, eps, self.row0, self.ws.data_ptr(),
+                                         self.ws.numel(), self.status.data_ptr(), self.sp)
                 assert rc == 0, L.gf_last_error()
         else:  # train_step
             import paper_1803_05619_b200 as gfb
@@ -272,151 +280,100 @@ class OursStep:
                 allreduce_grads(self.res.dparams)
 
     def e2e(self, steps, warmup):
-        """Public API with pinned host buffers, H2D + D2H inside the timed region."""
+        """Public API with pinned HOST buffers: every input of the step copied
+        in and every output copied out inside the timed region (host wall
+        clock around synchronous calls)."""
         import torch
 
         import paper_1803_05619_b200 as gfb
 
         c = self.c
         host_in = [t.cpu().pin_memory() for t in self.inputs]
-        if self.kind == "train_step":
-            # the target is a step input too; the step's host result is the loss
-            host_in.append(self.target.cpu().pin_memory())
-            host_out = torch.empty((), dtype=torch.float64).pin_memory()
-        else:
-            host_out = torch.empty(self.out.shape, dtype=self.out.dtype).pin_memory()
         p = gfb.GuidedFilterParams(c["r"], c["eps"])
+        if self.kind == "joint_fwd_bwd":
+            host_in.append(self.d_out.cpu().pin_memory())
+            lx, ly, hx, dd = host_in
+            host_out = [torch.empty_like(hx).pin_memory(), torch.empty_like(lx).pin_memory(),
+                        torch.empty_like(ly).pin_memory(), torch.empty_like(hx).pin_memory()]
+        elif self.kind == "train_step":
+            # the target is a step input too; the step's results are the loss
+            # and the packed guidance-net gradient
+            host_in.append(self.target.cpu().pin_memory())
+            host_out = [torch.empty((), dtype=torch.float64).pin_memory(),
+                        torch.empty(self.net.param_count(), dtype=torch.float32).pin_memory()]
+        else:
+            host_out = [torch.empty(self.out.shape, dtype=self.out.dtype).pin_memory()]
 
         def one():
-            # forward-only workloads: the host-image entry points (reference call
-            # shape), which overlap copy-in / kernel / copy-out image by image
             if self.kind == "highres_fwd":
-                gfb.forward_highres_host(host_in[0], host_in[1], p, out=host_out,
+                gfb.forward_highres_host(host_in[0], host_in[1], p, out=host_out[0],
                                          device=self.device, check=False)
-                return
-            if self.kind == "joint_fwd":
-                gfb.forward_joint_host(host_in[0], host_in[2], host_in[1], p, out=host_out,
+            elif self.kind == "joint_fwd":
+                gfb.forward_joint_host(host_in[0], host_in[2], host_in[1], p, out=host_out[0],
                                        device=self.device, check=False)
-                return
-            dev = [t.to(self.device, non_blocking=True) for t in host_in]
-            if self.kind == "joint_fwd_bwd":
-                out, tape = gfb.forward_joint(dev[0], dev[2], dev[1], p, check=False)
-                gr = gfb.backward(tape, out, check=False)  # d_out = out (<out,out>/2 probe)
-                res = gr.d_guide_hi
+            elif self.kind == "joint_fwd_bwd":
+                # forward + backward over host images, pipelined per plane
+                gfb.forward_backward_joint_host(lx, hx, ly, dd, p, outs=host_out,
+                                                device=self.device, check=False)
             else:
+                dev = [t.to(self.device, non_blocking=True) for t in host_in]
                 r = gfb.train_step(self.net, dev[0], dev[2], dev[1], dev[3], p)
-                res = r.loss
-            host_out.copy_(res, non_blocking=True)
+                host_out[0].copy_(r.loss, non_blocking=True)
+                host_out[1].copy_(r.dparams, non_blocking=True)
+                torch.cuda.synchronize(self.device)
 
         for _ in range(warmup):
             one()
         torch.cuda.synchronize(self.device)
-        t0 = torch.cuda.Event(enable_timing=True)
-        t1 = torch.cuda.Event(enable_timing=True)
-        t0.record()
+        t0 = time.perf_counter()
         for _ in range(steps):
             one()
-        t1.record()
         torch.cuda.synchronize(self.device)
-        ms = t0.elapsed_time(t1) / steps
+        ms = (time.perf_counter() - t0) * 1e3 / steps
         h2d = sum(t.numel() * t.element_size() for t in host_in)
-        d2h = host_out.numel() * host_out.element_size()
+        d2h = sum(t.numel() * t.element_size() for t in host_out)
         return ms, h2d, d2h
 
 
 # ---------------------------------------------------------------------------
-# CPU oracle legs
+# CPU reference legs (cpu_reference.py: the reference package, numba on)
 # ---------------------------------------------------------------------------
 
-def _oracle_image(args_tuple):
-    """Worker: one image (or a row band of it) of the config through the oracle."""
-    kind, C, H, rows, factor, r, eps, seed = args_tuple
-    import numpy as np
-
-    from oracle import gf_oracle as O
-
-    rng = np.random.default_rng(seed)
-    if kind == "highres_fwd":
-        g = rng.uniform(0, 1, (rows, H, 1))
-        s = rng.uniform(0, 1, (rows, H, C))
-        t0 = time.perf_counter()
-        O.forward_highres(np.repeat(g, C, axis=2), s, r, eps)
-        return time.perf_counter() - t0, rows * H
-    h_rows = max(1, rows // factor)
-    gl = rng.uniform(0, 1, (h_rows, H // factor, C))
-    sl = rng.uniform(0, 1, (h_rows, H // factor, C))
-    gh = rng.uniform(0, 1, (h_rows * factor, H, C))
-    t0 = time.perf_counter()
-    out, tape = O.forward_joint(gl, gh, sl, r, eps)
-    if kind != "joint_fwd":
-        O.backward(tape, out)
-    return time.perf_counter() - t0, h_rows * factor * H
-
-
-def cpu_sample(c, budget_s=12.0, procs=1, steps=1):
-    """Time the oracle on bounded row-band samples; returns Mpix/s and text."""
-    import multiprocessing as mp
-
-    kind = "joint_fwd_bwd" if c["kind"] in ("joint_fwd_bwd", "train_step") else c["kind"]
-    H, C = c["hr"], c["channels"]
-    rows = min(H, 256)
-    probe = _oracle_image((kind, C, H, rows, c.get("factor", 4), c["r"], c["eps"], 0))
-    per_row = probe[0] / rows
-    want_rows = int(max(16, min(H, budget_s / max(steps, 1) / max(per_row, 1e-9) / 2)))
-    want_rows -= want_rows % 16
-    want_rows = max(16, want_rows)
-    jobs = [(kind, C, H, want_rows, c.get("factor", 4), c["r"], c["eps"], k + 1)
-            for k in range(procs)]
-    results = []
-    for _ in range(steps):
-        t0 = time.perf_counter()
-        if procs == 1:
-            res = [_oracle_image(jobs[0])]
-        else:
-            with mp.get_context("fork").Pool(procs) as pool:
-                res = pool.map(_oracle_image, jobs)
-        wall = time.perf_counter() - t0
-        px = sum(p for _, p in res)
-        results.append((wall, px))
-    wall = sum(w for w, _ in results)
-    px = sum(p for _, p in results)
-    sample = (f"{procs} x {want_rows}x{H} px row-band(s) of the {kind} workload "
-              f"(C={C}, r={c['r']}), float64 numpy oracle, {steps} step(s)")
-    return px / wall / 1e6, sample, wall / steps
-
-
 def run_reference(args, c, rank, world):
-    """--impl reference: the CPU oracle port on the host cores, rank 0 only."""
+    """--impl reference: the reference's CPU path on all host cores, rank 0 only."""
     if rank != 0:
         return
-    cores = len(os.sched_getaffinity(0))
-    procs = max(1, min(cores, c["batch"]))
-    budget = 150.0
-    total_steps = args.steps + args.warmup
-    # bounded per-step sample so the whole run stays within a few minutes
-    value, sample, _ = cpu_sample(c, budget_s=budget / max(total_steps, 1) * args.steps,
-                                  procs=procs, steps=args.steps)
+    import cpu_reference
+
+    total = args.steps + args.warmup
+    step_s = min(8.0, max(1.0, 150.0 / max(total + 1, 1)))
+    res = cpu_reference.run(c, step_seconds=step_s, steps=args.steps, warmup=args.warmup)
     line = {
-        "metric": METRIC, "value": round(value, 4), "unit": "Mpix/s", "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": None,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (seeded uniform [0,1])",
+        "metric": METRIC, "value": round(res["value"], 4), "unit": "Mpix/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(res["ms_per_step"], 3), "higher_is_better": True,
+        "scaling": "strong" if c.get("shard") else "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded uniform [0,1], HWC float64: the reference's layout)",
         "config": config_block(args, c, world), "impl": "reference",
-        "cpu_baseline": {"value": round(value, 4), "unit": "Mpix/s", "cores": procs,
-                         "kind": "port", "sample": sample},
-        "e2e": {"value": round(value, 4), "unit": "Mpix/s", "h2d_bytes_per_step": 0,
+        "cpu_baseline": {"value": round(res["value"], 4), "unit": "Mpix/s", "cores": res["cores"],
+                         "kind": res["kind"], "sample": res["sample"]},
+        "e2e": {"value": round(res["value"], 4), "unit": "Mpix/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
-        "note": "reference is pure Python/numpy (no compiled CPU path to build); timed via the "
-                "pinned float64 oracle port, multiprocessing over images",
     }
     print(json.dumps(line), flush=True)
 
 
 def config_block(args, c, world):
     B, C, H = c["batch"], c["channels"], c["hr"]
+    par = {"rows": f"row-bands x{world} (lr halo max(2r,r+1), no data-path collective)",
+           "batch": f"batch-shard x{world} (no data-path collective)"}.get(
+        c.get("shard"), f"replica x{world} (each rank its own batch)")
+    if c["kind"] == "train_step" and world > 1:
+        par = f"data-parallel x{world} (NCCL allreduce of the 95 guidance-net grads)"
     blk = {"workload": f"{args.config}: {c['kind']}",
-           "batch_per_gpu": (B if not c.get("shard") else f"{B} split over {world}"), "channels": C,
-           "hr": [H, H], "radius": c["r"], "eps": c["eps"], "parallelism": (f"row-bands x{world} (lr halo max(2r,r+1))" if c.get("shard") == "rows" else f"batch-shard x{world}")}
+           "batch_per_gpu": (B if not c.get("shard") else f"{B} split over {world}"),
+           "global_batch": B * (1 if c.get("shard") else world), "channels": C,
+           "hr": [H, H], "radius": c["r"], "eps": c["eps"], "parallelism": par}
     if c["kind"] == "highres_fwd":
         blk["guide_channels"] = 1
     else:
@@ -433,12 +390,44 @@ def config_block(args, c, world):
 # main
 # ---------------------------------------------------------------------------
 
+def relaunch(n):
+    """--gpus N outside torchrun: one process per GPU under torch.distributed.run."""
+    import socket
+
+    sock = socket.socket()
+    sock.bind(("127.0.0.1", 0))
+    port = sock.getsockname()[1]
+    sock.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__),
+           *sys.argv[1:]]
+    return subprocess.call(cmd, env=os.environ.copy())
+
+
+def launch_check(rank, world):
+    """Every rank joins one process group and sums a 1: rank 0 prints the
+    world it saw (tests/test_bench.py runs this on CPU with gloo)."""
+    import torch
+    import torch.distributed as dist
+
+    if world > 1:
+        dist.init_process_group("gloo")
+        t = torch.ones(1)
+        dist.all_reduce(t)
+        n = int(t.item())
+        dist.destroy_process_group()
+    else:
+        n = 1
+    if rank == 0:
+        print(json.dumps({"launch_check": True, "n_gpus": world, "ranks_seen": n}), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", default="cfg1")
+    ap.add_argument("--config", default="cfg4a")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--batch", type=int, default=0)
     ap.add_argument("--hr", type=int, default=0)
@@ -446,14 +435,26 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--launch-check", action="store_true",
+                    help="test hook: check the N-rank launch (gloo, no GPU work) and exit")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
+    # communicator lines (rank count, transport) on stderr; stdout stays one JSON line
+    os.environ.setdefault("NCCL_DEBUG", "INFO")
+    os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl == "ours":
+        sys.exit(relaunch(args.gpus))
+
     rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", "1"))
+    world = int(os.environ.get("WORLD_SIZE", str(args.gpus if args.impl == "reference" else 1)))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     c = workload_spec(args)
 
+    if args.launch_check:
+        launch_check(rank, world)
+        return
     if args.impl == "reference":
         run_reference(args, c, rank, world)
         return
@@ -527,14 +528,18 @@ def main():
 
     e2e = None
     if not args.no_e2e:
-        e_ms, h2d, d2h = st.e2e(steps=max(3, min(args.steps, 10)), warmup=2)
+        e_ms, h2d, d2h = st.e2e(steps=max(3, min(args.steps, 5)), warmup=1)
         if dist:
             t = torch.tensor([e_ms], device=device)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e_ms = float(t.item())
         e2e = {"value": round(px / (e_ms * 1e-3) / 1e6, 3), "unit": "Mpix/s",
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-               "ms_per_step": round(e_ms, 4)}
+               "ms_per_step": round(e_ms, 4),
+               "api": {"joint_fwd_bwd": "forward_backward_joint_host",
+                       "joint_fwd": "forward_joint_host", "highres_fwd": "forward_highres_host",
+                       "train_step": "train_step (H2D inputs + target, D2H loss + grads)"}[
+                           st.kind]}
 
     if rank != 0:
         if dist:
@@ -553,9 +558,11 @@ def main():
 
     cpu = None
     if world == 1 and not args.no_cpu:
-        v, sample, _ = cpu_sample(c, budget_s=12.0, procs=1, steps=1)
-        cpu = {"value": round(v, 4), "unit": "Mpix/s", "cores": 1, "kind": "port",
-               "sample": sample}
+        import cpu_reference
+
+        res = cpu_reference.run(c, step_seconds=4.0, steps=2)
+        cpu = {"value": round(res["value"], 4), "unit": "Mpix/s", "cores": res["cores"],
+               "kind": res["kind"], "sample": res["sample"]}
 
     line = {
         "metric": METRIC, "value": round(value, 3), "unit": "Mpix/s", "n_gpus": world,
@@ -569,9 +576,9 @@ def main():
         "clocks": clocks, "wall_s_timed_region": round(wall, 4),
         "ms_per_step_min": round(min(ms_steps), 5),
     }
-    print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()
+    print(json.dumps(line), flush=True)
 
 
 if __name__ == "__main__":

@@ -108,6 +108,19 @@ int gf_joint_bwd(int dtype, const void* lr_x, const void* lr_y, const void* hr_x
                  int64_t C, int64_t h, int64_t w, int64_t H, int64_t W, int radius, double eps,
                  void* workspace, size_t workspace_bytes, uint32_t* status, void* stream);
 
+/* gf_joint_bwd on a ROW BAND of a larger image (multi-GPU config 4b, SURVEY
+ * 8e): the inputs are the band's aligned crop and `row0` is the FULL image's
+ * low-res row index of the crop's first row.  The kernels cut their row
+ * pieces and shift constants at full-image rows, so with row0 a multiple of
+ * 16 (paper_1803_05619_b200.sharding.row_bands aligns crops so) every owned
+ * row of every output is bitwise equal to the 1-GPU call on the whole image.
+ * row0 = 0 is gf_joint_bwd. */
+int gf_joint_bwd_band(int dtype, const void* lr_x, const void* lr_y, const void* hr_x,
+                      const void* d_out, void* d_lr_x, void* d_lr_y, void* d_hr_x, int64_t B,
+                      int64_t C, int64_t h, int64_t w, int64_t H, int64_t W, int radius,
+                      double eps, int64_t row0, void* workspace, size_t workspace_bytes,
+                      uint32_t* status, void* stream);
+
 /* ---- the full-resolution layer: gf/guided.py:198-233, :284-295 ----
  * guide: (B, Cg, H, W) with Cg == C or Cg == 1 (a 1-channel guide is
  * broadcast over the C source channels, BASELINE config 1); src, out:
@@ -189,6 +202,20 @@ int gf_joint_fwd_host(int dtype, const void* lr_x, const void* lr_y, const void*
                       int64_t B, int64_t C, int64_t h, int64_t w, int64_t H, int64_t W,
                       int radius, double eps, void* workspace, size_t workspace_bytes,
                       uint32_t* status);
+
+/* Forward AND backward of the joint layer on host images, the call a
+ * training framework makes with host tensors (gf/guided.py:152 forward_joint
+ * then :267 backward with d_out): per plane, lr_x, lr_y, hr_x and d_out are
+ * copied in, gf_joint_fwd + gf_joint_bwd run, and out, d_lr_x, d_lr_y,
+ * d_hr_x are copied out, pipelined as above. */
+size_t gf_joint_fwd_bwd_host_workspace_bytes(int dtype, int64_t C, int64_t h, int64_t w,
+                                             int64_t H, int64_t W, int radius);
+
+int gf_joint_fwd_bwd_host(int dtype, const void* lr_x, const void* lr_y, const void* hr_x,
+                          const void* d_out, void* out, void* d_lr_x, void* d_lr_y, void* d_hr_x,
+                          int64_t B, int64_t C, int64_t h, int64_t w, int64_t H, int64_t W,
+                          int radius, double eps, void* workspace, size_t workspace_bytes,
+                          uint32_t* status);
 
 /* ---- guidance / core net with a k x k dilated first convolution ----
  * gf/guidance.py:184-224 with ConvLayer(kernel=k, dilation=d) (:52-124):

@@ -21,7 +21,7 @@ from .guidance import FixedChannelMeanGuidance, GuidanceNet
 from .filters import bilinear_resize, bilinear_resize_adjoint, mean_filter, mean_filter_adjoint
 from .training import affine_target, joint_mse_backward, mse_loss, train_step
 from .nn import FastGuidedFilter, FullResGuidedFilter
-from .host import forward_highres_host, forward_joint_host
+from .host import forward_backward_joint_host, forward_highres_host, forward_joint_host
 from .upsampler import (AdamState, GuidedUpsampler, PipelineTape, TrainConfig, TrainingError,
                         adam_step, build_model, train)
 
@@ -33,6 +33,7 @@ __all__ = [
     "GuidanceNet", "bilinear_resize", "bilinear_resize_adjoint", "mean_filter",
     "mean_filter_adjoint", "affine_target", "mse_loss", "joint_mse_backward", "train_step", "FastGuidedFilter",
     "FullResGuidedFilter", "forward_highres_host", "forward_joint_host",
+    "forward_backward_joint_host",
     "FixedChannelMeanGuidance", "AdamState", "GuidedUpsampler", "PipelineTape", "TrainConfig",
     "TrainingError", "adam_step", "build_model", "train",
 ]

@@ -33,6 +33,8 @@ SIGNATURES = {
                           _sz, _p, _p]),
     "gf_joint_bwd": (_i, [_i, _p, _p, _p, _p, _p, _p, _p, _i64, _i64, _i64, _i64, _i64, _i64,
                           _i, _d, _p, _sz, _p, _p]),
+    "gf_joint_bwd_band": (_i, [_i, _p, _p, _p, _p, _p, _p, _p, _i64, _i64, _i64, _i64, _i64,
+                               _i64, _i, _d, _i64, _p, _sz, _p, _p]),
     "gf_highres_workspace_bytes": (_sz, [_i, _i64, _i64, _i64, _i64, _i64, _i]),
     "gf_highres_fwd": (_i, [_i, _p, _p, _p, _i64, _i64, _i64, _i64, _i64, _i, _d, _p, _sz, _p,
                             _p]),
@@ -66,6 +68,9 @@ SIGNATURES = {
     "gf_joint_host_workspace_bytes": (_sz, [_i, _i64, _i64, _i64, _i64, _i64, _i]),
     "gf_joint_fwd_host": (_i, [_i, _p, _p, _p, _p, _i64, _i64, _i64, _i64, _i64, _i64, _i, _d,
                                _p, _sz, _p]),
+    "gf_joint_fwd_bwd_host_workspace_bytes": (_sz, [_i, _i64, _i64, _i64, _i64, _i64, _i]),
+    "gf_joint_fwd_bwd_host": (_i, [_i, _p, _p, _p, _p, _p, _p, _p, _p, _i64, _i64, _i64, _i64,
+                                   _i64, _i64, _i, _d, _p, _sz, _p]),
 }
 
 # test hooks exported by the library but not part of the public header

@@ -297,7 +297,17 @@ int gf_joint_bwd(int dtype, const void* lr_x, const void* lr_y, const void* hr_x
                  const void* d_out, void* d_lr_x, void* d_lr_y, void* d_hr_x, int64_t B,
                  int64_t C, int64_t h, int64_t w, int64_t H, int64_t W, int radius, double eps,
                  void* workspace, size_t workspace_bytes, uint32_t* status, void* stream) {
+  return gf_joint_bwd_band(dtype, lr_x, lr_y, hr_x, d_out, d_lr_x, d_lr_y, d_hr_x, B, C, h, w, H,
+                           W, radius, eps, 0, workspace, workspace_bytes, status, stream);
+}
+
+int gf_joint_bwd_band(int dtype, const void* lr_x, const void* lr_y, const void* hr_x,
+                      const void* d_out, void* d_lr_x, void* d_lr_y, void* d_hr_x, int64_t B,
+                      int64_t C, int64_t h, int64_t w, int64_t H, int64_t W, int radius,
+                      double eps, int64_t row0, void* workspace, size_t workspace_bytes,
+                      uint32_t* status, void* stream) {
   if (int e = check_joint(dtype, B, C, h, w, H, W, radius, eps)) return e;
+  if (row0 < 0) return fail(GF_ERR_ARG, "row0 must be >= 0, got %lld", (long long)row0);
   const bool fused = use_fused_joint(dtype, B, C, h, w, H, W, radius) && aligned16(lr_x) &&
                      aligned16(lr_y) && aligned16(hr_x) && aligned16(d_out) &&
                      aligned16(d_lr_x) && aligned16(d_lr_y) && aligned16(d_hr_x);
@@ -308,7 +318,7 @@ int gf_joint_bwd(int dtype, const void* lr_x, const void* lr_y, const void* hr_x
   if (fused) {
     gfb::fused_joint_bwd((const float*)lr_x, (const float*)lr_y, (const float*)hr_x,
                          (const float*)d_out, (float*)d_lr_x, (float*)d_lr_y, (float*)d_hr_x, B,
-                         C, h, w, H, W, radius, (float)eps, workspace, status, S(stream));
+                         C, h, w, H, W, radius, (float)eps, workspace, row0, status, S(stream));
     return check_launch("gf_joint_bwd[fused]");
   }
   if (dtype == GF_F32)

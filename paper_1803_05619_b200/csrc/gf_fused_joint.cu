@@ -1265,9 +1265,9 @@ size_t fused_joint_bwd_ws_bytes(int64_t B, int64_t C, int64_t h, int64_t w) {
 static void joint_lr_tail(const JointFns& fns, const float* lr_x, const float* lr_y,
                           const float* db, const float* dA, float* d_lr_x, float* d_lr_y,
                           int64_t B, int64_t C, int64_t h, int64_t w, int r, float eps,
-                          cudaStream_t s) {
+                          int64_t row0, cudaStream_t s) {
   if (g_joint_lr_variant != 1 && seg_joint_bwd_lr_ok(h, w, r)) {
-    seg_joint_bwd_lr(lr_x, lr_y, db, dA, d_lr_x, d_lr_y, B * C, h, w, r, eps, s);
+    seg_joint_bwd_lr(lr_x, lr_y, db, dA, d_lr_x, d_lr_y, B * C, h, w, r, eps, row0, s);
   } else {
     const size_t smem = jf::bwd_lr_smem_floats(r) * sizeof(float);
     set_smem(fns.bwd_lr, smem);
@@ -1280,7 +1280,7 @@ static void joint_lr_tail(const JointFns& fns, const float* lr_x, const float* l
 
 void fused_joint_bwd(const float* lr_x, const float* lr_y, const float* hr_x, const float* d_out,
                      float* d_lr_x, float* d_lr_y, float* d_hr_x, int64_t B, int64_t C, int64_t h,
-                     int64_t w, int64_t H, int64_t W, int r, float eps, void* ws,
+                     int64_t w, int64_t H, int64_t W, int r, float eps, void* ws, int64_t row0,
                      uint32_t* status, cudaStream_t s) {
   float* db = (float*)ws;
   float* dA = db + B * C * h * w;
@@ -1305,7 +1305,7 @@ void fused_joint_bwd(const float* lr_x, const float* lr_y, const float* hr_x, co
       launch(fn, grid, smem, s, &a);
     }
   }
-  joint_lr_tail(fns, lr_x, lr_y, db, dA, d_lr_x, d_lr_y, B, C, h, w, r, eps, s);
+  joint_lr_tail(fns, lr_x, lr_y, db, dA, d_lr_x, d_lr_y, B, C, h, w, r, eps, row0, s);
 }
 
 // per-CTA loss partials of the fused step: (B C) x tile rows x tile columns
@@ -1344,7 +1344,7 @@ void fused_joint_mse_bwd(const float* lr_x, const float* lr_y, const float* hr_x
     launch(fn, grid, smem, s, &a);
     mse_final(part, loss, B, (int)mse_tiles(C, h, w), per_image, s);
   }
-  joint_lr_tail(fns, lr_x, lr_y, db, dA, d_lr_x, d_lr_y, B, C, h, w, r, eps, s);
+  joint_lr_tail(fns, lr_x, lr_y, db, dA, d_lr_x, d_lr_y, B, C, h, w, r, eps, 0, s);
 }
 
 }  // namespace gfb

@@ -64,30 +64,40 @@ struct Input {
   int64_t grp;
 };
 
-// Copies of the inputs per chunk, one output per chunk; `launch` runs the
-// device entry on the slot buffers.  Returns a GF_* code; *status gets the OR
-// of the device bits.
+// One pipeline output: chunk b writes host block b of `bytes`.
+struct Output {
+  void* host;
+  size_t bytes;
+};
+
+constexpr int kMaxIn = 4, kMaxOut = 4;
+
+// Copies of the inputs per chunk, up to four outputs per chunk; `launch` runs
+// the device entry on the slot buffers.  Returns a GF_* code; *status gets the
+// OR of the device bits.
 template <class Launch>
-int run_pipeline(int64_t nchunk, int nin, const Input* in, void* out, size_t out_bytes, char* ws,
+int run_pipeline(int64_t nchunk, int nin, const Input* in, int nout, const Output* outs, char* ws,
                  uint32_t* status_dev, uint32_t* status_host, Launch launch) {
   Pipe* pp = pipe_for_current_device();
   if (!pp || !pp->ok) return gfb::api_fail(GF_ERR_CUDA, "stream/event creation failed");
   Pipe& p = *pp;
   if (cudaMemsetAsync(status_dev, 0, sizeof(uint32_t), p.run) != cudaSuccess)
     return gfb::api_fail(GF_ERR_CUDA, cudaGetErrorString(cudaGetLastError()));
-  // workspace: per input two slots, then two output slots
-  char* slot[4][kSlots];
-  char* oslot[kSlots];
+  // workspace: per input kSlots slots (two for a group input), then kSlots
+  // slots per output
+  char* slot[kMaxIn][kSlots];
+  char* oslot[kMaxOut][kSlots];
   char* w = ws;
   for (int i = 0; i < nin; ++i)
     for (int s = 0; s < (in[i].grp > 1 ? 2 : kSlots); ++s) {
       slot[i][s] = w;
       w += up256(in[i].bytes);
     }
-  for (int s = 0; s < kSlots; ++s) {
-    oslot[s] = w;
-    w += up256(out_bytes);
-  }
+  for (int o = 0; o < nout; ++o)
+    for (int s = 0; s < kSlots; ++s) {
+      oslot[o][s] = w;
+      w += up256(outs[o].bytes);
+    }
   int64_t grp = 1;  // the (single) group size of the group inputs
   for (int i = 0; i < nin; ++i)
     if (in[i].grp > 1) grp = in[i].grp;
@@ -95,7 +105,9 @@ int run_pipeline(int64_t nchunk, int nin, const Input* in, void* out, size_t out
     const int s = (int)(b % kSlots);
     const int64_t g = b / grp;
     const int gs = (int)(g & 1);
-    const void* dev_in[4];
+    const void* dev_in[kMaxIn];
+    void* dev_out[kMaxOut];
+    for (int o = 0; o < nout; ++o) dev_out[o] = oslot[o][s];
     bool grp_copied = false;
     for (int i = 0; i < nin; ++i) {
       if (in[i].grp > 1) {
@@ -122,15 +134,16 @@ int run_pipeline(int64_t nchunk, int nin, const Input* in, void* out, size_t out
     cudaStreamWaitEvent(p.run, p.in_done[s], 0);
     if (grp > 1) cudaStreamWaitEvent(p.run, p.grp_in[gs], 0);
     if (b >= kSlots) cudaStreamWaitEvent(p.run, p.out_done[s], 0);  // output slot copied out
-    if (int e = launch(dev_in, oslot[s], p.run)) {
+    if (int e = launch(dev_in, dev_out, p.run)) {
       cudaStreamSynchronize(p.run);
       return e;
     }
     cudaEventRecord(p.run_done[s], p.run);
     if (grp > 1 && (b % grp == grp - 1 || b == nchunk - 1)) cudaEventRecord(p.grp_done[gs], p.run);
     cudaStreamWaitEvent(p.out, p.run_done[s], 0);
-    cudaMemcpyAsync((char*)out + b * out_bytes, oslot[s], out_bytes, cudaMemcpyDeviceToHost,
-                    p.out);
+    for (int o = 0; o < nout; ++o)
+      cudaMemcpyAsync((char*)outs[o].host + b * outs[o].bytes, oslot[o][s], outs[o].bytes,
+                      cudaMemcpyDeviceToHost, p.out);
     cudaEventRecord(p.out_done[s], p.out);
   }
   for (int s = 0; s < kSlots; ++s)  // status written by every kernel
@@ -146,8 +159,9 @@ int run_pipeline(int64_t nchunk, int nin, const Input* in, void* out, size_t out
   return GF_OK;
 }
 
-size_t pipeline_ws(const Input* in, int nin, size_t out_bytes) {
-  size_t n = kSlots * up256(out_bytes);
+size_t pipeline_ws(const Input* in, int nin, const Output* outs, int nout) {
+  size_t n = 0;
+  for (int o = 0; o < nout; ++o) n += kSlots * up256(outs[o].bytes);
   for (int i = 0; i < nin; ++i) n += (in[i].grp > 1 ? 2 : kSlots) * up256(in[i].bytes);
   return n;
 }
@@ -165,7 +179,8 @@ size_t gf_highres_host_workspace_bytes(int dtype, int64_t Cg, int64_t C, int64_t
   (void)C;
   const size_t plane = (size_t)H * W * esize(dtype);
   const Input ins[2] = {{nullptr, plane, 1}, {nullptr, plane, 1}};  // the larger layout
-  return pipeline_ws(ins, 2, plane) +
+  const Output outs[1] = {{nullptr, plane}};
+  return pipeline_ws(ins, 2, outs, 1) +
          up256(gf_highres_workspace_bytes(dtype, 1, 1, 1, H, W, radius)) + 256;
 }
 
@@ -178,13 +193,14 @@ int gf_highres_fwd_host(int dtype, const void* guide, const void* src, void* out
   if (workspace_bytes < need) return gfb::api_fail(GF_ERR_WORKSPACE, "host workspace too small");
   const size_t plane = (size_t)H * W * esize(dtype);
   const Input ins[2] = {{guide, plane, Cg == C ? 1 : C}, {src, plane, 1}};
+  const Output outs[1] = {{out, plane}};
   char* ws = (char*)workspace;
-  char* gws = ws + pipeline_ws(ins, 2, plane);
+  char* gws = ws + pipeline_ws(ins, 2, outs, 1);
   const size_t gws_bytes = gf_highres_workspace_bytes(dtype, 1, 1, 1, H, W, radius);
   uint32_t* st_dev = (uint32_t*)(gws + up256(gws_bytes));
-  return run_pipeline(B * C, 2, ins, out, plane, ws, st_dev, status,
-                      [&](const void* const* d, void* o, cudaStream_t s) {
-                        return gf_highres_fwd(dtype, d[0], d[1], o, 1, 1, 1, H, W, radius, eps,
+  return run_pipeline(B * C, 2, ins, 1, outs, ws, st_dev, status,
+                      [&](const void* const* d, void* const* o, cudaStream_t s) {
+                        return gf_highres_fwd(dtype, d[0], d[1], o[0], 1, 1, 1, H, W, radius, eps,
                                               gws, gws_bytes, st_dev, s);
                       });
 }
@@ -196,7 +212,8 @@ size_t gf_joint_host_workspace_bytes(int dtype, int64_t C, int64_t h, int64_t w,
   (void)C;
   const size_t lo = (size_t)h * w * esize(dtype), hi = (size_t)H * W * esize(dtype);
   const Input ins[3] = {{nullptr, lo, 1}, {nullptr, lo, 1}, {nullptr, hi, 1}};
-  return pipeline_ws(ins, 3, hi) +
+  const Output outs[1] = {{nullptr, hi}};
+  return pipeline_ws(ins, 3, outs, 1) +
          up256(gf_joint_workspace_bytes(dtype, 1, 1, h, w, H, W, radius)) + 256;
 }
 
@@ -210,14 +227,55 @@ int gf_joint_fwd_host(int dtype, const void* lr_x, const void* lr_y, const void*
   if (workspace_bytes < need) return gfb::api_fail(GF_ERR_WORKSPACE, "host workspace too small");
   const size_t lo = (size_t)h * w * esize(dtype), hi = (size_t)H * W * esize(dtype);
   const Input ins[3] = {{lr_x, lo, 1}, {lr_y, lo, 1}, {hr_x, hi, 1}};
+  const Output outs[1] = {{out, hi}};
   char* ws = (char*)workspace;
-  char* gws = ws + pipeline_ws(ins, 3, hi);
+  char* gws = ws + pipeline_ws(ins, 3, outs, 1);
   const size_t gws_bytes = gf_joint_workspace_bytes(dtype, 1, 1, h, w, H, W, radius);
   uint32_t* st_dev = (uint32_t*)(gws + up256(gws_bytes));
-  return run_pipeline(B * C, 3, ins, out, hi, ws, st_dev, status,
-                      [&](const void* const* d, void* o, cudaStream_t s) {
-                        return gf_joint_fwd(dtype, d[0], d[1], d[2], o, 1, 1, h, w, H, W, radius,
+  return run_pipeline(B * C, 3, ins, 1, outs, ws, st_dev, status,
+                      [&](const void* const* d, void* const* o, cudaStream_t s) {
+                        return gf_joint_fwd(dtype, d[0], d[1], d[2], o[0], 1, 1, h, w, H, W, radius,
                                             eps, gws, gws_bytes, st_dev, s);
+                      });
+}
+
+// forward + backward of the joint layer on host images: per plane, copy in
+// lr_x, lr_y, hr_x, d_out; run gf_joint_fwd and gf_joint_bwd; copy out out,
+// d_lr_x, d_lr_y, d_hr_x (a training framework's layer call with host tensors)
+size_t gf_joint_fwd_bwd_host_workspace_bytes(int dtype, int64_t C, int64_t h, int64_t w,
+                                             int64_t H, int64_t W, int radius) {
+  (void)C;
+  const size_t lo = (size_t)h * w * esize(dtype), hi = (size_t)H * W * esize(dtype);
+  const Input ins[4] = {{nullptr, lo, 1}, {nullptr, lo, 1}, {nullptr, hi, 1}, {nullptr, hi, 1}};
+  const Output outs[4] = {{nullptr, hi}, {nullptr, lo}, {nullptr, lo}, {nullptr, hi}};
+  return pipeline_ws(ins, 4, outs, 4) +
+         up256(gf_joint_workspace_bytes(dtype, 1, 1, h, w, H, W, radius)) + 256;
+}
+
+int gf_joint_fwd_bwd_host(int dtype, const void* lr_x, const void* lr_y, const void* hr_x,
+                          const void* d_out, void* out, void* d_lr_x, void* d_lr_y, void* d_hr_x,
+                          int64_t B, int64_t C, int64_t h, int64_t w, int64_t H, int64_t W,
+                          int radius, double eps, void* workspace, size_t workspace_bytes,
+                          uint32_t* status) {
+  if (int e = gfb::api_check_joint(dtype, B, C, h, w, H, W, radius, eps)) return e;
+  if (!lr_x || !lr_y || !hr_x || !d_out || !out || !d_lr_x || !d_lr_y || !d_hr_x)
+    return gfb::api_fail(GF_ERR_ARG, "null host pointer");
+  const size_t need = gf_joint_fwd_bwd_host_workspace_bytes(dtype, C, h, w, H, W, radius);
+  if (workspace_bytes < need) return gfb::api_fail(GF_ERR_WORKSPACE, "host workspace too small");
+  const size_t lo = (size_t)h * w * esize(dtype), hi = (size_t)H * W * esize(dtype);
+  const Input ins[4] = {{lr_x, lo, 1}, {lr_y, lo, 1}, {hr_x, hi, 1}, {d_out, hi, 1}};
+  const Output outs[4] = {{out, hi}, {d_lr_x, lo}, {d_lr_y, lo}, {d_hr_x, hi}};
+  char* ws = (char*)workspace;
+  char* gws = ws + pipeline_ws(ins, 4, outs, 4);
+  const size_t gws_bytes = gf_joint_workspace_bytes(dtype, 1, 1, h, w, H, W, radius);
+  uint32_t* st_dev = (uint32_t*)(gws + up256(gws_bytes));
+  return run_pipeline(B * C, 4, ins, 4, outs, ws, st_dev, status,
+                      [&](const void* const* d, void* const* o, cudaStream_t s) {
+                        if (int e = gf_joint_fwd(dtype, d[0], d[1], d[2], o[0], 1, 1, h, w, H, W,
+                                                 radius, eps, gws, gws_bytes, st_dev, s))
+                          return e;
+                        return gf_joint_bwd(dtype, d[0], d[1], d[2], d[3], o[1], o[2], o[3], 1, 1,
+                                            h, w, H, W, radius, eps, gws, gws_bytes, st_dev, s);
                       });
 }
 

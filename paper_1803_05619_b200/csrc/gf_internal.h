@@ -84,7 +84,7 @@ void fused_highres_fwd(const float* guide, const float* src, float* out, int64_t
 bool seg_joint_bwd_lr_ok(int64_t h, int64_t w, int r);
 void seg_joint_bwd_lr(const float* lr_x, const float* lr_y, const float* db, const float* dA,
                       float* d_lr_x, float* d_lr_y, int64_t P, int64_t h, int64_t w, int r,
-                      float eps, cudaStream_t s);
+                      float eps, int64_t row0, cudaStream_t s);
 extern thread_local int g_joint_lr_variant;
 extern thread_local int g_joint_fwd_variant;  // r = 8 coefficient chunking (test hook)
 extern thread_local int g_joint_mse_variant;
@@ -98,7 +98,7 @@ size_t fused_joint_bwd_ws_bytes(int64_t B, int64_t C, int64_t h, int64_t w);
 void fused_joint_bwd(const float* lr_x, const float* lr_y, const float* hr_x, const float* d_out,
                      float* d_lr_x, float* d_lr_y, float* d_hr_x, int64_t B, int64_t C,
                      int64_t h, int64_t w, int64_t H, int64_t W, int r, float eps, void* ws,
-                     uint32_t* status, cudaStream_t s);
+                     int64_t row0, uint32_t* status, cudaStream_t s);
 // fused training step: forward + MSE + backward (no out / d_out in HBM)
 size_t fused_joint_mse_ws_bytes(int64_t B, int64_t C, int64_t h, int64_t w);
 void fused_joint_mse_bwd(const float* lr_x, const float* lr_y, const float* hr_x,

@@ -32,6 +32,12 @@ namespace jls {
 
 constexpr int WC = 128;  // columns per warp
 constexpr int kMaxRadius = 4;
+// Pieces (the rows a warp walks with one set of running sums and one shift
+// constant) are cut at multiples of kPiece rows of the FULL image: a row band
+// (multi-GPU config 4b) passes its first row's global index, so its pieces,
+// shifts and summation order over the owned rows are the full image's and the
+// band's d_lr_x, d_lr_y are bitwise equal to the 1-GPU result.
+constexpr int kPiece = 64;
 
 __host__ __device__ constexpr int up4(int n) { return (n + 3) / 4 * 4; }
 
@@ -54,7 +60,8 @@ struct Args {
   float* d_lr_y;
   int64_t h, w;
   int strips;
-  int64_t U, chunk;  // rows of all (plane, strip) columns; rows per warp
+  int npieces, off;     // pieces per (plane, strip) column; row0 % kPiece
+  int64_t U, upw;       // pieces of all columns; pieces per warp
   int64_t nwarps;
   float eps;
 };
@@ -300,15 +307,15 @@ __global__ void __launch_bounds__(WPB * 32) k_joint_bwd_lr_seg(Args a) {
   const int64_t gw = (int64_t)blockIdx.x * WPB + warp;
   if (gw >= a.nwarps) return;
   const int h = (int)a.h, w = (int)a.w;
-  const int64_t u_lo = gw * a.chunk;
-  const int64_t u_hi = min(u_lo + a.chunk, a.U);
+  const int64_t u_lo = gw * a.upw;
+  const int64_t u_hi = min(u_lo + a.upw, a.U);
   const int64_t plane = (int64_t)h * w;
-  for (int64_t u = u_lo; u < u_hi;) {
-    const int64_t col = u / h;
+  for (int64_t u = u_lo; u < u_hi; ++u) {
+    const int64_t col = u / a.npieces;
+    const int k = (int)(u - col * a.npieces);
     Piece P;
-    P.y0 = (int)(u - col * h);
-    P.y1 = (int)min((int64_t)h, P.y0 + (u_hi - u));
-    u += P.y1 - P.y0;
+    P.y0 = max(k * kPiece - a.off, 0);
+    P.y1 = min((k + 1) * kPiece - a.off, h);
     const int64_t pl = col / a.strips;
     const int strip = (int)(col - pl * a.strips);
     const int x0 = strip * GG::OW;
@@ -365,20 +372,21 @@ bool seg_joint_bwd_lr_ok(int64_t h, int64_t w, int r) {
 
 void seg_joint_bwd_lr(const float* lr_x, const float* lr_y, const float* db, const float* dA,
                       float* d_lr_x, float* d_lr_y, int64_t P, int64_t h, int64_t w, int r,
-                      float eps, cudaStream_t s) {
+                      float eps, int64_t row0, cudaStream_t s) {
   const jls::Launch L = jls::pick(r);
   const LaunchCfg lc = launch_cfg(L.fn, jls::WPB * 32, L.smem);
-  const int sms = lc.sms, per_sm = lc.per_sm;
+  const int64_t slots = (int64_t)lc.sms * lc.per_sm * jls::WPB;
   const int64_t strips = (w + L.ow - 1) / L.ow;
-  const int64_t slots = (int64_t)sms * per_sm * jls::WPB;
-  // balanced pieces of the rows of all (plane, strip) columns: one wave of
-  // warps, more waves only to keep a piece <= 512 rows
-  const int64_t U = P * strips * h;
-  const int64_t waves = (U + slots * 512 - 1) / (slots * 512);
-  int64_t chunk = (U + slots * waves - 1) / (slots * waves);
-  if (chunk < 16) chunk = U < 16 ? U : 16;
-  const int64_t nw = (U + chunk - 1) / chunk;
-  jls::Args a{lr_x, lr_y, db, dA, d_lr_x, d_lr_y, h, w, (int)strips, U, chunk, nw, eps};
+  const int off = (int)(row0 % jls::kPiece);
+  const int npieces = (int)((off + h + jls::kPiece - 1) / jls::kPiece);
+  // pieces of all (plane, strip) columns, consecutive pieces of a column on
+  // one warp (its warm-up rows are the previous piece's last rows, in L2);
+  // as few pieces per warp as fill one wave of warps
+  const int64_t U = P * strips * npieces;
+  const int64_t upw = (U + slots - 1) / slots;
+  const int64_t nw = (U + upw - 1) / upw;
+  jls::Args a{lr_x, lr_y, db, dA, d_lr_x, d_lr_y, h, w, (int)strips, npieces, off, U, upw, nw,
+              eps};
   void* args[] = {&a};
   cudaLaunchKernel(L.fn, dim3((unsigned)((nw + jls::WPB - 1) / jls::WPB)), dim3(jls::WPB * 32),
                    args, L.smem, s);

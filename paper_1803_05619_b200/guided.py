@@ -83,6 +83,7 @@ class GuidedFilterTape:
     status: Status
     _cache: dict = field(default_factory=dict)
     _versions: tuple = ()
+    row_origin: int = 0  # full-image low-res row of row 0 (row bands, sharding.py)
 
     def __post_init__(self) -> None:
         # autograd-style saved-tensor check: backward recomputes the moments
@@ -145,8 +146,18 @@ def _same_dtype(*imgs: Img):
     return dt
 
 
-def forward_joint(guide_lo, guide_hi, src_lo, p: GuidedFilterParams, *, check: bool = True):
-    """Joint upsampling: regress src on guide at low res, apply at high res."""
+def forward_joint(guide_lo, guide_hi, src_lo, p: GuidedFilterParams, *, check: bool = True,
+                  row_origin: int = 0):
+    """Joint upsampling: regress src on guide at low res, apply at high res.
+
+    ``row_origin`` (extension, multi-GPU row bands): the full image's low-res
+    row index of the inputs' first row.  It changes no value the reference
+    defines; it makes the backward cut its row pieces at full-image rows so a
+    band's gradients are bitwise those of the whole image (sharding.py).
+    """
+    if isinstance(row_origin, bool) or not isinstance(row_origin, (int, np.integer)) \
+            or row_origin < 0:
+        raise ValueError(f"row_origin must be a non-negative integer, got {row_origin!r}")
     if not isinstance(p, GuidedFilterParams):
         raise ValueError(f"expected GuidedFilterParams, got {type(p).__name__}")
     gl = as_img(guide_lo, "guide_lo")
@@ -176,7 +187,7 @@ def forward_joint(guide_lo, guide_hi, src_lo, p: GuidedFilterParams, *, check: b
     _lib.check(rc, "forward_joint")
     if check:
         status.raise_if_set("forward_joint", (gl.t, gh.t, sl.t))
-    tape = GuidedFilterTape(VARIANT_JOINT, p, gl, sl, gh, gh, status)
+    tape = GuidedFilterTape(VARIANT_JOINT, p, gl, sl, gh, gh, status, row_origin=int(row_origin))
     return restore(out, gh), tape
 
 
@@ -233,9 +244,10 @@ def backward(tape: GuidedFilterTape, d_out, *, check: bool = True) -> GuidedFilt
         d_lr_y = torch.empty_like(sl.t)
         d_hr_x = torch.empty_like(gh.t)
         ws = workspace(lib.gf_joint_workspace_bytes(dt, B, C, h, w, H, W, p.radius), dev)
-        rc = lib.gf_joint_bwd(dt, ptr(gl.t), ptr(sl.t), ptr(gh.t), ptr(d.t), ptr(d_lr_x),
-                              ptr(d_lr_y), ptr(d_hr_x), B, C, h, w, H, W, int(p.radius),
-                              float(p.eps), ptr(ws), ws.numel(), status.ptr, _stream(gl))
+        rc = lib.gf_joint_bwd_band(dt, ptr(gl.t), ptr(sl.t), ptr(gh.t), ptr(d.t), ptr(d_lr_x),
+                                   ptr(d_lr_y), ptr(d_hr_x), B, C, h, w, H, W, int(p.radius),
+                                   float(p.eps), tape.row_origin, ptr(ws), ws.numel(),
+                                   status.ptr, _stream(gl))
         _lib.check(rc, "backward")
         if check:
             status.raise_if_set("backward")

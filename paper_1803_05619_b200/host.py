@@ -154,3 +154,55 @@ def forward_joint_host(guide_lo, guide_hi, src_lo, p: GuidedFilterParams, *, out
     if check:
         _raise(st.value, "forward_joint_host", (lx, hx, ly))
     return restore(o)
+
+
+def forward_backward_joint_host(guide_lo, guide_hi, src_lo, d_out, p: GuidedFilterParams, *,
+                                outs=None, device=None, check: bool = True):
+    """Forward AND backward of the fast layer on host images: the values of
+    ``out, tape = forward_joint(...)`` (gf/guided.py:152-195) and
+    ``backward(tape, d_out)`` (gf/guided.py:267-283) in one pipelined pass
+    (gf_joint_fwd_bwd_host).  Returns ``(out, GuidedFilterGrads)`` with host
+    arrays in the inputs' layout.  ``outs`` = optional preallocated CPU
+    tensors ``(out, d_lr_x, d_lr_y, d_hr_x)`` (NCHW, ideally pinned)."""
+    from .guided import GuidedFilterGrads
+
+    if not isinstance(p, GuidedFilterParams):
+        raise ValueError(f"expected GuidedFilterParams, got {type(p).__name__}")
+    lx, restore_lo = _host_nchw(guide_lo, "guide_lo")
+    hx, restore = _host_nchw(guide_hi, "guide_hi")
+    ly, _ = _host_nchw(src_lo, "src_lo")
+    d, _ = _host_nchw(d_out, "d_out")
+    if not (lx.dtype == hx.dtype == ly.dtype == d.dtype):
+        raise ValueError("guide_lo, guide_hi, src_lo and d_out must share a dtype")
+    if lx.shape != ly.shape:
+        raise ValueError(f"guide_lo/src_lo shape mismatch: {tuple(lx.shape)} vs {tuple(ly.shape)}")
+    B, C, h, w = lx.shape
+    if hx.shape[0] != B or hx.shape[1] != C:
+        raise ValueError(f"guide_hi shape {tuple(hx.shape)} does not match {tuple(lx.shape)}")
+    if d.shape != hx.shape:
+        raise ValueError(f"d_out shape {tuple(d.shape)} does not match {tuple(hx.shape)}")
+    H, W = hx.shape[2:]
+    device = torch.device(device) if device is not None else torch.device("cuda")
+    lib = _lib.load()
+    dt = _lib.GF_F32 if lx.dtype == torch.float32 else _lib.GF_F64
+    if outs is None:
+        outs = (None, None, None, None)
+    o = _out_buffer(outs[0], hx.shape, hx)
+    dlx = _out_buffer(outs[1], lx.shape, lx)
+    dly = _out_buffer(outs[2], ly.shape, ly)
+    dhx = _out_buffer(outs[3], hx.shape, hx)
+    ws = _workspace(lib.gf_joint_fwd_bwd_host_workspace_bytes(dt, C, h, w, H, W, int(p.radius)),
+                    device)
+    st = ctypes.c_uint32(0)
+    with torch.cuda.device(device):
+        rc = lib.gf_joint_fwd_bwd_host(dt, lx.data_ptr(), ly.data_ptr(), hx.data_ptr(),
+                                       d.data_ptr(), o.data_ptr(), dlx.data_ptr(), dly.data_ptr(),
+                                       dhx.data_ptr(), B, C, h, w, H, W, int(p.radius),
+                                       float(p.eps), ws.data_ptr(), ws.numel(),
+                                       ctypes.addressof(st))
+    _lib.check(rc, "forward_backward_joint_host")
+    if check:
+        _raise(st.value, "forward_backward_joint_host", (lx, hx, ly, d))
+    grads = GuidedFilterGrads(d_src=restore_lo(dly), d_guide_lo=restore_lo(dlx),
+                              d_guide_hi=restore(dhx))
+    return restore(o), grads

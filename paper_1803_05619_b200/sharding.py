@@ -15,6 +15,13 @@ no data-path collective:
   owned output row sees the same taps and windows as in the full image.
   Crops are clamped to the image, so window counts stay those of the image.
   Verified exact against the oracle in tests/test_sharding.py.
+  Band edges fall on multiples of ``GRAIN`` (64) low-res rows -- the row
+  pieces of the fp32 backward tail -- and the crop's first row is rounded
+  down to a multiple of ``ALIGN`` (16) -- the row tiling of the fused fp32
+  kernels; the crop's full-image row is handed to the layer (``forward_joint(...,
+  row_origin=crop_lo)``), so every tile, row piece and shift constant of the
+  fp32 kernels sits where it sits for the whole image: a band's owned rows
+  are BITWISE equal to the 1-GPU result (tests/test_gpu_fullsize.py).
 
 The only collective on the path is the data-parallel training step
 (config 2): the packed 95-float guidance-net gradient is summed across ranks
@@ -66,17 +73,31 @@ class Band:
         return (self.a - self.crop_lo) * self.factor, (self.b - self.crop_lo) * self.factor
 
 
+ALIGN = 16  # low-res rows per tile row of the fused fp32 kernels (jf::TLY)
+GRAIN = 64  # low-res rows per row piece of the backward tail (jls::kPiece)
+
+
 def halo(radius: int, backward: bool) -> int:
     return max(2 * radius, radius + 1) if backward else radius + 1
 
 
-def row_bands(h: int, world: int, radius: int, factor: int = 4, backward: bool = True):
-    """Bands of ``world`` ranks over ``h`` low-res rows (balanced)."""
+def row_bands(h: int, world: int, radius: int, factor: int = 4, backward: bool = True,
+              align: int = ALIGN, grain: int = GRAIN):
+    """Bands of ``world`` ranks over ``h`` low-res rows, balanced in units of
+    ``grain`` rows (the backward's row pieces: owned rows then start where a
+    piece of the full image starts) when h >= grain * world, else of single
+    rows; every crop starts on a multiple of ``align`` rows (a tile row)."""
+    if align < 1 or grain < 1:
+        raise ValueError(f"align and grain must be >= 1, got {align}, {grain}")
     out = []
     R = halo(radius, backward)
+    g = grain if h >= grain * world else 1
+    units = -(-h // g)
     for k in range(world):
-        a, b = batch_shard(h, world, k)
-        out.append(Band(a, b, max(0, a - R), min(h, b + R), factor))
+        ua, ub = batch_shard(units, world, k)
+        a, b = min(h, ua * g), min(h, ub * g)
+        lo = max(0, a - R) // align * align
+        out.append(Band(a, b, lo, min(h, b + R), factor))
     return out
 
 
@@ -98,6 +119,31 @@ def joint_band_forward(forward_joint, params, lr_x, lr_y, hr_x, band: Band):
     lo, hi = band.crop_lo, band.crop_hi
     Hlo, Hhi = band.hr_crop
     out, _ = forward_joint(lr_x[:, :, lo:hi].contiguous(), hr_x[:, :, Hlo:Hhi].contiguous(),
-                           lr_y[:, :, lo:hi].contiguous(), params)
+                           lr_y[:, :, lo:hi].contiguous(), params, **_origin(forward_joint, lo))
     y0, y1 = band.hr_local
     return out[:, :, y0:y1]
+
+
+def _origin(fn, lo: int) -> dict:
+    """row_origin for the GPU layer (the oracle in the CPU tests has none)."""
+    import inspect
+
+    try:
+        return {"row_origin": lo} if "row_origin" in inspect.signature(fn).parameters else {}
+    except (TypeError, ValueError):
+        return {}
+
+
+def joint_band_backward(forward_joint, backward, params, lr_x, lr_y, hr_x, d_out, band: Band):
+    """Forward + backward of one band; returns (out, d_lr_x, d_lr_y, d_hr_x)
+    restricted to the band's owned rows.  ``d_out`` has full-image rows."""
+    lo, hi = band.crop_lo, band.crop_hi
+    Hlo, Hhi = band.hr_crop
+    out, tape = forward_joint(lr_x[:, :, lo:hi].contiguous(), hr_x[:, :, Hlo:Hhi].contiguous(),
+                              lr_y[:, :, lo:hi].contiguous(), params,
+                              **_origin(forward_joint, lo))
+    g = backward(tape, d_out[:, :, Hlo:Hhi].contiguous())
+    y0, y1 = band.hr_local
+    l0, l1 = band.lr_local
+    return (out[:, :, y0:y1], g.d_guide_lo[:, :, l0:l1], g.d_src[:, :, l0:l1],
+            g.d_guide_hi[:, :, y0:y1])

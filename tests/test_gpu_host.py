@@ -74,3 +74,38 @@ def test_host_error_semantics(gfb):
         gfb.forward_highres_host(g.cuda(), s, gfb.GuidedFilterParams(2, 1e-2))
     with pytest.raises(ValueError):
         gfb.forward_highres_host(torch.rand(2, 2, 32, 32), s, gfb.GuidedFilterParams(2, 1e-2))
+
+
+@pytest.mark.parametrize("dtype,B,pinned", [(torch.float32, 5, True), (torch.float64, 2, False)])
+def test_joint_fwd_bwd_host_matches_device(gfb, dtype, B, pinned):
+    """gf_joint_fwd_bwd_host: every output equals the device entries' bytes."""
+    g = torch.Generator().manual_seed(B)
+    lx = torch.rand(B, 3, 24, 36, generator=g, dtype=dtype)
+    ly = torch.rand(B, 3, 24, 36, generator=g, dtype=dtype)
+    hx = torch.rand(B, 3, 96, 144, generator=g, dtype=dtype)
+    d = torch.randn(B, 3, 96, 144, generator=g, dtype=dtype)
+    if pinned:
+        lx, ly, hx, d = (t.pin_memory() for t in (lx, ly, hx, d))
+    p = gfb.GuidedFilterParams(2, 1e-4)
+    out, gr = gfb.forward_backward_joint_host(lx, hx, ly, d, p)
+    o_dev, tape = gfb.forward_joint(lx.cuda(), hx.cuda(), ly.cuda(), p)
+    g_dev = gfb.backward(tape, d.cuda())
+    assert torch.equal(out, o_dev.cpu())
+    assert torch.equal(gr.d_guide_lo, g_dev.d_guide_lo.cpu())
+    assert torch.equal(gr.d_src, g_dev.d_src.cpu())
+    assert torch.equal(gr.d_guide_hi, g_dev.d_guide_hi.cpu())
+
+
+def test_joint_fwd_bwd_host_reference_hwc(gfb):
+    """The reference's HWC float64 numpy call shape, against the oracle."""
+    rng = np.random.default_rng(4)
+    lx, ly = rng.uniform(0, 1, (2, 10, 14, 3))
+    hx = rng.uniform(0, 1, (40, 56, 3))
+    d = rng.standard_normal((40, 56, 3))
+    p = gfb.GuidedFilterParams(1, 1e-3)
+    out, gr = gfb.forward_backward_joint_host(lx, hx, ly, d, p)
+    want, tape = O.forward_joint(lx, hx, ly, 1, 1e-3)
+    g = O.backward(tape, d)
+    assert isinstance(out, np.ndarray) and out.shape == hx.shape
+    assert np.abs(out - want).max() <= 1e-10
+    assert np.abs(gr.d_guide_lo - g[1]).max() <= 1e-9 * max(1.0, np.abs(g[1]).max())

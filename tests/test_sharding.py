@@ -152,3 +152,58 @@ def test_gloo_world2_band_forward_and_allreduce(tmp_path):
     mp.spawn(_worker, args=(2, port, str(tmp_path)), nprocs=2, join=True)
     ok, err = open(tmp_path / "result.txt").read().split()
     assert ok == "True", f"band forward mismatch {err}"
+
+
+@pytest.mark.parametrize("h,world,r", [(4096, 8, 2), (4096, 3, 2), (1000, 8, 4), (517, 5, 1),
+                                       (24, 4, 3), (7, 3, 1)])
+def test_row_bands_partition_and_alignment(h, world, r):
+    """Owned bands tile [0, h) in order; crops start on 16-row tiles (when the
+    halo allows) and cover the backward halo."""
+    from paper_1803_05619_b200.sharding import ALIGN, GRAIN
+
+    bands = row_bands(h, world, r, backward=True)
+    assert len(bands) == world and bands[0].a == 0 and bands[-1].b == h
+    R = halo(r, True)
+    for k, bd in enumerate(bands):
+        if k:
+            assert bd.a == bands[k - 1].b
+        assert bd.crop_lo % ALIGN == 0
+        assert bd.crop_lo <= max(0, bd.a - R) and bd.crop_hi == min(h, bd.b + R)
+        if h >= GRAIN * world and bd.b < h:
+            assert bd.b % GRAIN == 0
+
+
+def test_joint_band_backward_helper_exact_on_oracle():
+    """sharding.joint_band_backward with the oracle as the layer (no
+    row_origin keyword) reproduces the full image's gradients."""
+    from paper_1803_05619_b200.sharding import joint_band_backward
+
+    rng = np.random.default_rng(11)
+    h, w, C, r = 40, 12, 1, 2
+    lr_x, lr_y = rng.uniform(0, 1, (2, 1, C, h, w))
+    hr_x = rng.uniform(0, 1, (1, C, 4 * h, 4 * w))
+    d = rng.standard_normal((1, C, 4 * h, 4 * w))
+    full = O.joint_backward_nchw(lr_x, lr_y, hr_x, d, r, 1e-3)
+
+    class _G:
+        def __init__(self, g):
+            self.d_guide_lo, self.d_src, self.d_guide_hi = g
+
+    T = torch.from_numpy
+    n = lambda t: t.numpy()  # noqa: E731
+
+    def fwd(lx, hx, ly, p):
+        return T(O.joint_forward_nchw(n(lx), n(ly), n(hx), r, 1e-3)), (n(lx), n(ly), n(hx))
+
+    def bwd(tape, dd):
+        lx, ly, hx = tape
+        return _G([T(g) for g in O.joint_backward_nchw(lx, ly, hx, n(dd), r, 1e-3)])
+
+    for band in row_bands(h, 2, r, backward=True):
+        _, dlx, dly, dhx = joint_band_backward(fwd, bwd, None, T(lr_x), T(lr_y), T(hr_x), T(d),
+                                               band)
+        dlx, dly, dhx = n(dlx), n(dly), n(dhx)
+        A, B = band.hr_owned
+        assert np.abs(dlx - full[0][:, :, band.a:band.b]).max() <= 1e-10
+        assert np.abs(dly - full[1][:, :, band.a:band.b]).max() <= 1e-10
+        assert np.abs(dhx - full[2][:, :, A:B]).max() <= 1e-10
