@@ -237,6 +237,33 @@ int gnk_backward(int dtype, const void* x, const void* dy, void* dx, void* dpara
                  int64_t hidden, int kernel, int dilation, int64_t H, int64_t W, void* workspace,
                  size_t workspace_bytes, uint32_t* status, void* stream);
 
+/* ---- standalone guidance layers: ConvLayer (gf/guidance.py:52-124) and
+ * AdaptiveNorm (gf/guidance.py:134-173) -- the reference's layer objects
+ * (GuidanceNet.conv1 / .norm / .conv2), computed in float64 internally.
+ * x: (B, Cin, H, W); weight (Cout, Cin, k, k); bias (Cout) or NULL; "same"
+ * zero padding (k-1)*dilation/2.  Parameter gradients are SUMMED over the
+ * batch (each image is one reference call) and overwritten.  gain,
+ * norm_gain and their gradients are single device scalars of dtype;
+ * statistics are per image and channel (population variance, floor 1e-5). */
+int gf_conv2d_fwd(int dtype, const void* x, const void* weight, const void* bias, void* y,
+                  int64_t B, int64_t Cin, int64_t Cout, int64_t H, int64_t W, int kernel,
+                  int dilation, void* stream);
+
+int gf_conv2d_bwd(int dtype, const void* x, const void* weight, const void* dy, void* dx,
+                  void* d_weight, void* d_bias, int64_t B, int64_t Cin, int64_t Cout, int64_t H,
+                  int64_t W, int kernel, int dilation, void* stream);
+
+size_t gf_adaptive_norm_workspace_bytes(int64_t B, int64_t C);
+
+int gf_adaptive_norm_fwd(int dtype, const void* x, void* y, const void* gain,
+                         const void* norm_gain, int64_t B, int64_t C, int64_t H, int64_t W,
+                         void* workspace, size_t workspace_bytes, void* stream);
+
+int gf_adaptive_norm_bwd(int dtype, const void* x, const void* dy, void* dx, void* d_gain,
+                         void* d_norm_gain, const void* gain, const void* norm_gain, int64_t B,
+                         int64_t C, int64_t H, int64_t W, void* workspace,
+                         size_t workspace_bytes, void* stream);
+
 /* ---- FixedChannelMeanGuidance (gf/guidance.py:227-255) ----
  * y (B, Cout, H, W): every channel = mean over the Cin channels of x;
  * adjoint dx (B, Cin, H, W) = (sum over Cout of dy) / Cin. */

@@ -260,6 +260,27 @@ def guidance_init(in_ch, out_ch, hidden, rng):
     }
 
 
+def adaptive_norm_forward(x, gain, norm_gain):
+    """AdaptiveNorm.forward (gf/guidance.py:152-159): per-channel spatial
+    mean / population variance, inv_std = 1/sqrt(var + 1e-5)."""
+    mean = x.mean(axis=(0, 1), keepdims=True)
+    var = x.var(axis=(0, 1), keepdims=True)
+    inv_std = 1.0 / np.sqrt(var + NORM_VAR_FLOOR)
+    xhat = (x - mean) * inv_std
+    return gain * x + norm_gain * xhat, dict(x=x, xhat=xhat, inv_std=inv_std)
+
+
+def adaptive_norm_backward(tape, dy, gain, norm_gain):
+    """AdaptiveNorm.backward (gf/guidance.py:161-173)."""
+    d_gain = float(np.vdot(dy, tape["x"]))
+    d_ng = float(np.vdot(dy, tape["xhat"]))
+    g = norm_gain * dy
+    g_mean = g.mean(axis=(0, 1), keepdims=True)
+    g_proj = (g * tape["xhat"]).mean(axis=(0, 1), keepdims=True)
+    dx = gain * dy + (g - g_mean - tape["xhat"] * g_proj) * tape["inv_std"]
+    return dx, d_gain, d_ng
+
+
 def guidance_forward(params, x):
     """conv1 (1x1, no bias) -> AdaptiveNorm -> leaky ReLU -> conv2 (1x1 + bias).
     gf/guidance.py:87-104 (conv), :152-159 (norm), :36-39 (lrelu), :209-214."""

@@ -17,13 +17,14 @@ from .guided import (
     forward_highres,
     forward_joint,
 )
-from .guidance import FixedChannelMeanGuidance, GuidanceNet
+from .guidance import AdaptiveNorm, ConvLayer, FixedChannelMeanGuidance, GuidanceNet
 from .filters import bilinear_resize, bilinear_resize_adjoint, mean_filter, mean_filter_adjoint
 from .training import affine_target, joint_mse_backward, mse_loss, train_step
 from .nn import FastGuidedFilter, FullResGuidedFilter
 from .host import forward_backward_joint_host, forward_highres_host, forward_joint_host
-from .upsampler import (AdamState, GuidedUpsampler, PipelineTape, TrainConfig, TrainingError,
-                        adam_step, build_model, train)
+from .upsampler import (TASKS, AdamState, GuidedUpsampler, PipelineTape, TrainConfig,
+                        TrainingError, adam_step, build_model, make_dataset, synthetic_images,
+                        train)
 
 __version__ = "0.1.0"
 
@@ -35,5 +36,6 @@ __all__ = [
     "FullResGuidedFilter", "forward_highres_host", "forward_joint_host",
     "forward_backward_joint_host",
     "FixedChannelMeanGuidance", "AdamState", "GuidedUpsampler", "PipelineTape", "TrainConfig",
-    "TrainingError", "adam_step", "build_model", "train",
+    "TrainingError", "adam_step", "build_model", "train", "AdaptiveNorm", "ConvLayer",
+    "make_dataset", "synthetic_images", "TASKS",
 ]

@@ -71,6 +71,13 @@ SIGNATURES = {
     "gf_joint_fwd_bwd_host_workspace_bytes": (_sz, [_i, _i64, _i64, _i64, _i64, _i64, _i]),
     "gf_joint_fwd_bwd_host": (_i, [_i, _p, _p, _p, _p, _p, _p, _p, _p, _i64, _i64, _i64, _i64,
                                    _i64, _i64, _i, _d, _p, _sz, _p]),
+    "gf_conv2d_fwd": (_i, [_i, _p, _p, _p, _p, _i64, _i64, _i64, _i64, _i64, _i, _i, _p]),
+    "gf_conv2d_bwd": (_i, [_i, _p, _p, _p, _p, _p, _p, _i64, _i64, _i64, _i64, _i64, _i, _i,
+                           _p]),
+    "gf_adaptive_norm_workspace_bytes": (_sz, [_i64, _i64]),
+    "gf_adaptive_norm_fwd": (_i, [_i, _p, _p, _p, _p, _i64, _i64, _i64, _i64, _p, _sz, _p]),
+    "gf_adaptive_norm_bwd": (_i, [_i, _p, _p, _p, _p, _p, _p, _p, _i64, _i64, _i64, _i64, _p,
+                                  _sz, _p]),
 }
 
 # test hooks exported by the library but not part of the public header

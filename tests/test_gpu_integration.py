@@ -1,0 +1,42 @@
+"""The REFERENCE's own test modules, run with the B200 backend installed at
+its joint-layer seam (integration/gf_b200_backend.py, reproduced in
+INTEGRATION.md): forward_joint's values and the joint backward come from the
+float64 sm_100a kernels, and the reference's assertions (naive-transcription
+parity at 1e-10, finite-difference gradchecks, linearity, degenerate windows,
+pass-through, training-loop determinism) must hold.
+
+The reference package and its tests are installed into the git-ignored
+baseline/_ref by __graft_entry__.build() in the build container and travel to
+the GPU box with the snapshot; the test skips if they are absent."""
+
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+REF = os.path.join(ROOT, "baseline", "_ref")
+
+
+@pytest.mark.parametrize("module", ["test_guided.py", "test_training.py"])
+def test_reference_suite_through_b200_backend(module, tmp_path):
+    tests = os.path.join(REF, "tests")
+    if not os.path.isfile(os.path.join(tests, module)):
+        pytest.skip("baseline/_ref has no reference tests (run __graft_entry__.build())")
+    calls = tmp_path / "calls.json"
+    env = dict(os.environ, GF_B200_CALLS=str(calls),
+               PYTHONPATH=os.pathsep.join([os.path.join(ROOT, "tests"), tests, REF, ROOT]),
+               NUMBA_CACHE_DIR=str(tmp_path / "numba"), PYTHONDONTWRITEBYTECODE="1")
+    res = subprocess.run([sys.executable, "-m", "pytest", "-q", "-p", "no:cacheprovider",
+                          "-p", "ref_b200_plugin", "-c", os.devnull, "--rootdir", tests,
+                          os.path.join(tests, module)], cwd=tests, env=env,
+                         capture_output=True, text=True, timeout=1200)
+    assert res.returncode == 0, res.stdout[-4000:] + res.stderr[-2000:]
+    n = json.loads(calls.read_text())
+    assert n["forward"] > 0, n  # the B200 kernels really produced the values
+    if module == "test_guided.py":
+        assert n["backward"] > 0, n

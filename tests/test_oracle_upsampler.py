@@ -92,3 +92,38 @@ def test_train(gold):
         # conv2 bias) move by Adam-normalised noise: judge on the unit scale
         for k, v in sub(c, "p1.").items():
             assert close(params[k], v, 1e-8), (name, k)
+
+
+def test_oracle_layers_match_reference_golden():
+    """Oracle ConvLayer / AdaptiveNorm vs the real reference's standalone
+    layers (tests/golden/golden_layers.npz, make_golden_layers.py)."""
+    import os
+
+    from oracle import gf_oracle as O
+    from oracle import upsampler_oracle as U
+
+    z = np.load(os.path.join(os.path.dirname(__file__), "golden", "golden_layers.npz"))
+    cases = sorted({k.split("/")[0] for k in z.files})
+    for c in cases:
+        if c.startswith("data"):
+            continue
+        if c.startswith("conv"):
+            ci, co, k, d, bias = z[f"{c}/meta"]
+            w = z[f"{c}/weight"]
+            y, padded = U.conv_forward(z[f"{c}/x"], w, int(d))
+            if bias:
+                y = y + z[f"{c}/bias"]
+            assert np.abs(y - z[f"{c}/y"]).max() <= 1e-12, c
+            dx, dw = U.conv_backward(padded, w, int(d), z[f"{c}/dy"])
+            assert np.abs(dx - z[f"{c}/dx"]).max() <= 1e-12, c
+            assert np.abs(dw - z[f"{c}/d_weight"]).max() <= 1e-12, c
+            if bias:
+                assert np.abs(z[f"{c}/dy"].sum(axis=(0, 1)) - z[f"{c}/d_bias"]).max() <= 1e-12
+        else:
+            gain, ng = z[f"{c}/gains"]
+            y, tape = O.adaptive_norm_forward(z[f"{c}/x"], gain, ng)
+            assert np.abs(y - z[f"{c}/y"]).max() <= 1e-12, c
+            dx, dg, dn = O.adaptive_norm_backward(tape, z[f"{c}/dy"], gain, ng)
+            assert np.abs(dx - z[f"{c}/dx"]).max() <= 1e-10, c
+            assert abs(dg - z[f"{c}/d_gain"][0]) <= 1e-10 * max(1, abs(dg)), c
+            assert abs(dn - z[f"{c}/d_norm_gain"][0]) <= 1e-10 * max(1, abs(dn)), c
