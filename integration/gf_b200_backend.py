@@ -120,10 +120,13 @@ def install(gf):
                                                 tape.params.radius, tape.params.eps)
         return G.GuidedFilterGrads(d_src=d_src, d_guide_lo=d_gl, d_guide_hi=d_gh)
 
+    # every binding of the two functions in the package's modules, under any
+    # name (training.py imports backward as gf_backward)
     for name, mod in list(sys.modules.items()):
         if name == gf.__name__ or name.startswith(gf.__name__ + "."):
-            if getattr(mod, "forward_joint", None) is ref_fwd:
-                mod.forward_joint = forward_joint
-            if getattr(mod, "backward", None) is ref_bwd:
-                mod.backward = backward
+            for attr, val in list(vars(mod).items()):
+                if val is ref_fwd:
+                    setattr(mod, attr, forward_joint)
+                elif val is ref_bwd:
+                    setattr(mod, attr, backward)
     return forward_joint, backward
