@@ -150,7 +150,7 @@ def _train_step(impl, spec, smp):
         if "params" not in smp:
             smp["params"] = O.guidance_init(3, 3, spec.get("hidden", 15),
                                             np.random.default_rng(0))
-        O.train_step(smp["params"], smp["gl"], smp["gh"], smp["sl"], smp["T"], r, eps)
+        O.train_step(smp["params"], [smp["gl"]], [smp["gh"]], [smp["sl"]], [smp["T"]], r, eps)
 
 
 def _init(spec, rows, use_ref, seed):

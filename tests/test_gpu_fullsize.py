@@ -144,3 +144,64 @@ def test_cfg4b_row_bands_match_one_gpu(gfb, world):
                                ("d_lr_y", dly, full.d_src[:, :, band.a:band.b]),
                                ("d_hr_x", dhx, full.d_guide_hi[:, :, A:B])):
             assert torch.equal(got, ref), (name, band.a, float((got - ref).abs().max()))
+
+
+@pytest.mark.parametrize("r", [1, 2, 4, 8])
+def test_cfg3_full_size_crop_parity(gfb, r):
+    """Config 3 at its largest stated size: batch 16 of 3 x 4096^2 (lr 1024^2),
+    eps = 1e-4, forward, checked against the oracle on aligned crops (halo
+    r + 1) at the corners, the centre and random windows of three images."""
+    import workloads
+
+    eps = 1e-4
+    lr_x, lr_y, hr_x = workloads.joint_inputs(16, 3, 4096, 4096, F, seed=60 + r, device="cuda")
+    out, _ = gfb.forward_joint(lr_x, hr_x, lr_y, gfb.GuidedFilterParams(r, eps))
+    torch.cuda.synchronize()
+    rng = np.random.default_rng(r)
+    R = halo(r, False)
+    h = w = 1024
+    for n in (0, 7, 15):
+        for (a, b, c, d) in _windows(h, w, 12, rng, extra=2):
+            y0, y1, x0, x1 = max(a - R, 0), min(b + R, h), max(c - R, 0), min(d + R, w)
+            lr = lambda t: npy(t[n:n + 1, :, y0:y1, x0:x1])  # noqa: E731
+            hx = npy(hr_x[n:n + 1, :, F * y0:F * y1, F * x0:F * x1])
+            want = O.joint_forward_nchw(lr(lr_x), lr(lr_y), hx, r, eps)
+            got = npy(out[n:n + 1, :, F * a:F * b, F * c:F * d])
+            ref = want[:, :, F * (a - y0):F * (b - y0), F * (c - x0):F * (d - x0)]
+            err = float(np.abs(got - ref).max())
+            assert err <= OUT_TOL32, (n, a, c, err)
+
+
+@pytest.mark.parametrize("norm_gain", [0.0, 0.7])
+def test_cfg2_full_size_step_vs_oracle(gfb, norm_gain):
+    """Config 2's training step at full image size (hr 2048^2, lr 512^2, r=1,
+    eps=1e-8, GuidanceNet 3 -> 15 -> 3) with B = 2 so the batch-mean loss is
+    exercised, against the float64 oracle (gf/training.py:143-183): the loss,
+    d_lr_x, d_lr_y, d_hr_x and all 95 guidance-net gradients.  norm_gain != 0
+    turns on AdaptiveNorm's per-image statistics over 4.2 M pixels
+    (gf/guidance.py:152-173) -- where fp32 accumulation could drift."""
+    import workloads
+
+    r, eps, B = 1, 1e-8, 2
+    lr_x, lr_y, hr_x = (t.cuda() for t in workloads.joint_inputs(B, 3, 2048, 2048, F, seed=21))
+    target = workloads.affine_target(hr_x).contiguous()
+    net = gfb.GuidanceNet(3, 3, hidden=15, kernel=1, rng=np.random.default_rng(5))
+    net.norm.norm_gain[:] = norm_gain
+    res = gfb.train_step(net, lr_x, hr_x, lr_y, target, gfb.GuidedFilterParams(r, eps))
+    torch.cuda.synchronize()
+    params = {k: v.cpu().numpy().copy() for k, v in net.parameters().items()}
+    hwc = lambda t: [x.transpose(1, 2, 0) for x in npy(t)]  # noqa: E731
+    loss, _, dlx, dly, dhx, grads = O.train_step(params, hwc(lr_x), hwc(hr_x), hwc(lr_y),
+                                                 hwc(target), r, eps)
+    assert abs(float(res.loss) - loss) <= 1e-5 * loss, (float(res.loss), loss)
+    for name, got, want in (("d_lr_x", res.d_lr_x, dlx), ("d_lr_y", res.d_lr_y, dly),
+                            ("d_hr_x", res.d_hr_x, dhx)):
+        want = np.stack([x.transpose(2, 0, 1) for x in want])
+        assert rel_max(npy(got), want) <= GRAD_TOL32, name
+    got = net.unpack(res.dparams)
+    scale = max(float(np.abs(v).max()) for v in grads.values())
+    n = 0
+    for k, v in grads.items():
+        n += v.size
+        assert float(np.abs(npy(got[k]) - v).max()) <= GRAD_TOL32 * scale, k
+    assert n == 95
