@@ -28,8 +28,11 @@
 //       box-filter adjoints and d_lr_x, d_lr_y (gf/guided.py:255-263).
 #include <cuda_runtime.h>
 
+#include <algorithm>
+
 #include "gf_common.cuh"
 #include "gf_internal.h"
+#include "gf_tma.cuh"
 
 namespace gfb {
 namespace jf {
@@ -97,16 +100,27 @@ __device__ inline SmemCoef carve(float* base, int r) {
 // VCH: row chunks of the vertical pass (0: as many as the CTA's threads
 // allow); HCH: column chunks per row of the horizontal pass.  Each chunk pays
 // a 2r warm-up, so large radii favour fewer, longer chunks.
-template <int RAD, bool NEED_B, int VCH = 0, int HCH = 16>
+// FROM_SMEM: X, Y are the block's raw low-res values already staged in
+// shared memory by TMA (rows i0-1-r.., columns k0-1-r-cofs.., pitch sp, zeros
+// outside the image); otherwise global planes.
+template <int RAD, bool NEED_B, int VCH = 0, int HCH = 16, bool FROM_SMEM = false>
 __device__ void lr_coeffs(const float* __restrict__ X, const float* __restrict__ Y, int h, int w,
-                          int i0, int k0, float eps, const SmemCoef& sm, bool& degen) {
+                          int i0, int k0, float eps, const SmemCoef& sm, bool& degen,
+                          int sp = 0, int cofs = 0) {
   constexpr int r = RAD;
   const int RI = RA + 2 * r, CI = CA + 2 * r;
   const int tid = threadIdx.x;
   // per-CTA shift (var/cov are shift invariant); any in-image sample works
   const int sy_ = min(max(i0, 0), h - 1), sx_ = min(max(k0, 0), w - 1);
-  const float sx = __ldg(X + (int64_t)sy_ * w + sx_);
-  const float sy = __ldg(Y + (int64_t)sy_ * w + sx_);
+  float sx, sy;
+  if constexpr (FROM_SMEM) {
+    const int o = (sy_ - (i0 - 1 - r)) * sp + (sx_ - (k0 - 1 - r)) + cofs;
+    sx = X[o];
+    sy = Y[o];
+  } else {
+    sx = __ldg(X + (int64_t)sy_ * w + sx_);
+    sy = __ldg(Y + (int64_t)sy_ * w + sx_);
+  }
   // 1) stage inputs (zero outside the image: clamped windows); every load of
   //    the block is issued before the first store, so the CTA waits for one
   //    memory latency, not one per element
@@ -120,8 +134,13 @@ __device__ void lr_coeffs(const float* __restrict__ X, const float* __restrict__
       const int row = idx / CIc, col = idx - row * CIc;
       const int gy = i0 - 1 - r + row, gx = k0 - 1 - r + col;
       const bool ok = idx < RIc * CIc && gy >= 0 && gy < h && gx >= 0 && gx < w;
-      xv[e] = ok ? __ldg(X + (int64_t)gy * w + gx) - sx : 0.f;
-      yv[e] = ok ? __ldg(Y + (int64_t)gy * w + gx) - sy : 0.f;
+      if constexpr (FROM_SMEM) {
+        xv[e] = ok ? X[row * sp + col + cofs] - sx : 0.f;
+        yv[e] = ok ? Y[row * sp + col + cofs] - sy : 0.f;
+      } else {
+        xv[e] = ok ? __ldg(X + (int64_t)gy * w + gx) - sx : 0.f;
+        yv[e] = ok ? __ldg(Y + (int64_t)gy * w + gx) - sy : 0.f;
+      }
     }
 #pragma unroll
     for (int e = 0; e < NE; ++e) {
@@ -378,6 +397,180 @@ __global__ void __launch_bounds__(NT, (RAD >= 2 && RAD <= 4) ? 4 : 3) k_joint_fw
     }
     *reinterpret_cast<float4*>(O + (int64_t)Y * a.W + X0) = make_float4(o[0], o[1], o[2], o[3]);
   }
+  }
+  if (degen) flag(a.status, GF_STATUS_DEGENERATE);
+  if (bad) flag(a.status, GF_STATUS_NONFINITE_OUTPUT);
+}
+
+// ---------------------------------------------------------------------------
+// forward, persistent TMA pipeline (k_joint_fwd_tma)
+// ---------------------------------------------------------------------------
+// The same per-tile arithmetic as k_joint_fwd (bit-identical results), but a
+// CTA walks tiles t = blockIdx.x, +gridDim.x, ... and TMA stages each tile's
+// inputs -- the 64 x 128 high-res guide tile and the low-res x, y halo blocks
+// (zero-filled outside the image by the hardware) -- NS tiles ahead into a
+// ring of shared-memory stages, so the SM's HBM reads for the next tiles are
+// in flight while it computes and stores the current one.  One elected
+// thread issues the copies; an mbarrier per stage carries the byte count.
+// A TMA box must start on a 16-byte column in global memory (an unaligned
+// start raises an illegal-instruction fault on sm_100a), so the low-res box
+// starts PADL >= 1 + r columns left of the block, PADL a multiple of 4.
+template <int RAD>
+struct TmaGeo {
+  static constexpr int RI = RA + 2 * RAD;
+  static constexpr int PADL = (1 + RAD + 3) / 4 * 4;
+  static constexpr int COFS = PADL - 1 - RAD;                // staged column of block col 0
+  static constexpr int LP = (PADL + TLX + 1 + RAD + 3) / 4 * 4;  // box width: 16-byte rows
+  static constexpr int HR = THY * THX;                    // floats
+  static constexpr int LR = (RI * LP + 31) / 32 * 32;     // 128-byte aligned boxes
+  static constexpr int STAGE = HR + 2 * LR;
+  static constexpr uint32_t BYTES = (uint32_t)(HR + 2 * RI * LP) * 4u;
+};
+
+template <int RAD, int NS>
+inline size_t fwd_tma_smem_bytes() {
+  return 128 + (size_t)NS * TmaGeo<RAD>::STAGE * 4 + coef_smem_floats(RAD) * 4;
+}
+
+// out = Up(b) + Up(A) * g for the 8 hr rows (Yb .. Yb+7) x 4 columns (X0 ..)
+// of this thread, coefficients in sm.As / sm.Bs (k_joint_fwd's step 3)
+template <int RAD>
+__device__ __forceinline__ bool apply_rows(const SmemCoef& sm, const float4 (&g)[8], float* O,
+                                           int h, int w, int H, int W, int i0, int k0,
+                                           int lane, int warp) {
+  const int X0 = 4 * (k0 + lane);
+  const int Yb = 4 * i0 + 8 * warp;
+  const bool col_ok = X0 < W;
+  const ColTaps ct = col_taps(X0, w, k0);
+  const bool cin = RAD <= 4 && k0 + lane >= 1 && k0 + lane <= w - 2;
+  float HA[4][4], HB[4][4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int rl = 2 * warp + q;
+    if (rl < RA) {
+      if (cin) {
+        hrow_interior(sm.As + rl * CAP, lane, HA[q]);
+        hrow_interior(sm.Bs + rl * CAP, lane, HB[q]);
+      } else {
+        hrow(sm.As + rl * CAP, ct, HA[q]);
+        hrow(sm.Bs + rl * CAP, ct, HB[q]);
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) HA[q][j] = HB[q][j] = 0.f;
+    }
+  }
+  bool bad = false;
+  const int slo_base = i0 - 1 + 2 * warp;
+  if (Yb >= 2 && Yb + 7 <= 4 * h - 3 && Yb + 7 < H) {
+    if (col_ok) {
+      float chk = 0.f;
+#pragma unroll
+      for (int t = 0; t < 8; ++t) {
+        const int q0 = t / 4 + ((t & 3) >= 2 ? 1 : 0);
+        constexpr float fph[4] = {0.625f, 0.875f, 0.125f, 0.375f};
+        const float f = fph[t & 3];
+        const float gv[4] = {g[t].x, g[t].y, g[t].z, g[t].w};
+        float o[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const float Ah = HA[q0][j] + f * (HA[q0 + 1][j] - HA[q0][j]);
+          const float Bh = HB[q0][j] + f * (HB[q0 + 1][j] - HB[q0][j]);
+          o[j] = Bh + Ah * gv[j];
+          chk += o[j] - o[j];
+        }
+        *reinterpret_cast<float4*>(O + (int64_t)(Yb + t) * W + X0) =
+            make_float4(o[0], o[1], o[2], o[3]);
+      }
+      bad = chk != 0.f;
+    }
+  } else {
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      const int Y = Yb + t;
+      if (!col_ok || Y >= H) continue;
+      const Tap ty = tap4(Y, h);
+      const int q0 = t / 4 + ((t & 3) >= 2 ? 1 : 0);
+      const int slo = slo_base + q0;
+      float o[4];
+      const float gv[4] = {g[t].x, g[t].y, g[t].z, g[t].w};
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float alo = ty.lo == slo ? HA[q0][j] : HA[q0 + 1][j];
+        const float ahi = ty.hi == slo + 1 ? HA[q0 + 1][j] : alo;
+        const float blo = ty.lo == slo ? HB[q0][j] : HB[q0 + 1][j];
+        const float bhi = ty.hi == slo + 1 ? HB[q0 + 1][j] : blo;
+        const float Ah = alo + ty.f * (ahi - alo);
+        const float Bh = blo + ty.f * (bhi - blo);
+        o[j] = Bh + Ah * gv[j];
+        if (!isfinite(o[j])) bad = true;
+      }
+      *reinterpret_cast<float4*>(O + (int64_t)Y * W + X0) = make_float4(o[0], o[1], o[2], o[3]);
+    }
+  }
+  return bad;
+}
+
+template <int RAD, int NS, int MINB, int VCH = 0, int HCH = 16>
+__global__ void __launch_bounds__(NT, MINB)
+    k_joint_fwd_tma(const __grid_constant__ CUtensorMap tmG, const __grid_constant__ CUtensorMap tmX,
+                    const __grid_constant__ CUtensorMap tmY, FwdArgs a, int tiles_x, int tiles_y,
+                    int ntiles) {
+  using TG = TmaGeo<RAD>;
+  extern __shared__ float4 smem4[];
+  __shared__ __align__(8) uint64_t bar[NS];
+  float* base = reinterpret_cast<float*>(
+      (reinterpret_cast<uintptr_t>(smem4) + 127) & ~static_cast<uintptr_t>(127));
+  const SmemCoef sm = carve(base + NS * TG::STAGE, RAD);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) {
+    for (int s = 0; s < NS; ++s) tma::mbar_init(&bar[s], 1);
+  }
+  __syncthreads();
+  auto coords = [&](int t, int& p, int& i0, int& k0) {
+    const int tx = t % tiles_x, rest = t / tiles_x;
+    k0 = tx * TLX;
+    i0 = (rest % tiles_y) * TLY;
+    p = rest / tiles_y;
+  };
+  auto issue = [&](int t, int s) {
+    int p, i0, k0;
+    coords(t, p, i0, k0);
+    float* st = base + s * TG::STAGE;
+    tma::mbar_arrive_expect_tx(&bar[s], TG::BYTES);
+    tma::load_3d(st, &tmG, 4 * k0, 4 * i0, p, &bar[s]);
+    tma::load_3d(st + TG::HR, &tmX, k0 - TG::PADL, i0 - 1 - RAD, p, &bar[s]);
+    tma::load_3d(st + TG::HR + TG::LR, &tmY, k0 - TG::PADL, i0 - 1 - RAD, p, &bar[s]);
+  };
+  if (tid == 0)
+    for (int j = 0; j < NS - 1; ++j) {
+      const int t = blockIdx.x + j * gridDim.x;
+      if (t < ntiles) issue(t, j);
+    }
+  bool degen = false, bad = false;
+  int k = 0;
+  for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++k) {
+    const int s = k % NS;
+    if (tid == 0) {  // refill the stage iteration k-1 released
+      const int tn = t + (NS - 1) * gridDim.x;
+      if (tn < ntiles) issue(tn, (k + NS - 1) % NS);
+    }
+    int p, i0, k0;
+    coords(t, p, i0, k0);
+    tma::mbar_wait(&bar[s], (uint32_t)((k / NS) & 1));
+    const float* st = base + s * TG::STAGE;
+    lr_coeffs<RAD, true, VCH, HCH, true>(st + TG::HR, st + TG::HR + TG::LR, a.h, a.w, i0, k0,
+                                         a.eps, sm, degen, TG::LP, TG::COFS);
+    float4 g[8];
+#pragma unroll
+    for (int r8 = 0; r8 < 8; ++r8)
+      g[r8] = *reinterpret_cast<const float4*>(st + (8 * warp + r8) * THX + 4 * lane);
+    float* O = a.out + (int64_t)p * a.H * a.W;
+    bad |= apply_rows<RAD>(sm, g, O, a.h, a.w, a.H, a.W, i0, k0, lane, warp);
+    // every thread's generic reads of stage s and of the coefficient scratch
+    // are done before thread 0 lets TMA overwrite the stage
+    tma::fence_proxy_async();
+    __syncthreads();
   }
   if (degen) flag(a.status, GF_STATUS_DEGENERATE);
   if (bad) flag(a.status, GF_STATUS_NONFINITE_OUTPUT);
@@ -1226,9 +1419,70 @@ static void launch(const void* fn, dim3 grid, size_t smem, cudaStream_t s, void*
   cudaLaunchKernel(fn, grid, dim3(jf::NT), args, smem, s);
 }
 
+// persistent TMA forward: kernel and dynamic shared memory per radius
+struct FwdTma {
+  const void* fn;
+  size_t smem;
+};
+
+template <int RAD>
+static FwdTma fwd_tma_info() {
+  constexpr int NS = 2;
+  if constexpr (RAD >= 5)
+    return {(const void*)jf::k_joint_fwd_tma<RAD, NS, 1, 2, 8>, jf::fwd_tma_smem_bytes<RAD, NS>()};
+  else if constexpr (RAD >= 2)
+    return {(const void*)jf::k_joint_fwd_tma<RAD, NS, 2, 0, 8>, jf::fwd_tma_smem_bytes<RAD, NS>()};
+  else
+    return {(const void*)jf::k_joint_fwd_tma<RAD, NS, 2>, jf::fwd_tma_smem_bytes<RAD, NS>()};
+}
+
+static FwdTma pick_fwd_tma(int r) {
+  switch (r) {
+    case 0: return fwd_tma_info<0>();
+    case 1: return fwd_tma_info<1>();
+    case 2: return fwd_tma_info<2>();
+    case 3: return fwd_tma_info<3>();
+    case 4: return fwd_tma_info<4>();
+    case 5: return fwd_tma_info<5>();
+    case 6: return fwd_tma_info<6>();
+    case 7: return fwd_tma_info<7>();
+    case 8: return fwd_tma_info<8>();
+    case 9: return fwd_tma_info<9>();
+    case 10: return fwd_tma_info<10>();
+    case 11: return fwd_tma_info<11>();
+    default: return fwd_tma_info<12>();
+  }
+}
+
+// true when launched (the low-res rows must be 16-byte multiples for TMA)
+static bool fused_joint_fwd_tma(const float* lr_x, const float* lr_y, const float* hr_x,
+                                float* out, int64_t P, int64_t h, int64_t w, int64_t H, int64_t W,
+                                int r, float eps, uint32_t* status, cudaStream_t s) {
+  if (w % 4 != 0 || g_joint_fwd_variant == 9) return false;
+  const FwdTma F = pick_fwd_tma(r);
+  const int RI = jf::RA + 2 * r, PADL = (1 + r + 3) / 4 * 4;
+  const int LP = (PADL + jf::TLX + 1 + r + 3) / 4 * 4;  // as jf::TmaGeo
+  CUtensorMap tmG, tmX, tmY;
+  if (!tma::make_plane_map(&tmG, hr_x, W, H, P, jf::THX, jf::THY) ||
+      !tma::make_plane_map(&tmX, lr_x, w, h, P, LP, RI) ||
+      !tma::make_plane_map(&tmY, lr_y, w, h, P, LP, RI))
+    return false;
+  const LaunchCfg lc = launch_cfg(F.fn, jf::NT, F.smem);
+  int tiles_x = (int)((w + jf::TLX - 1) / jf::TLX), tiles_y = (int)((h + jf::TLY - 1) / jf::TLY);
+  const int64_t nt = (int64_t)tiles_x * tiles_y * P;
+  if (nt > 0x7fffffff) return false;
+  int ntiles = (int)nt;
+  const int64_t grid = std::min<int64_t>(nt, (int64_t)lc.sms * lc.per_sm);
+  jf::FwdArgs a{lr_x, lr_y, hr_x, out, (int)h, (int)w, (int)H, (int)W, r, eps, status};
+  void* args[] = {&tmG, &tmX, &tmY, &a, &tiles_x, &tiles_y, &ntiles};
+  cudaLaunchKernel(F.fn, dim3((unsigned)grid), dim3(jf::NT), args, F.smem, s);
+  return true;
+}
+
 void fused_joint_fwd(const float* lr_x, const float* lr_y, const float* hr_x, float* out, int64_t B,
                      int64_t C, int64_t h, int64_t w, int64_t H, int64_t W, int r, float eps,
                      uint32_t* status, cudaStream_t s) {
+  if (fused_joint_fwd_tma(lr_x, lr_y, hr_x, out, B * C, h, w, H, W, r, eps, status, s)) return;
   const JointFns fns = pick_joint(r);
   jf::FwdArgs a{lr_x, lr_y, hr_x, out, (int)h, (int)w, (int)H, (int)W, r, eps, status};
   const int tx = (int)((w + jf::TLX - 1) / jf::TLX), ty = (int)((h + jf::TLY - 1) / jf::TLY);
