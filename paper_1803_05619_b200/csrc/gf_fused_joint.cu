@@ -1454,11 +1454,16 @@ static FwdTma pick_fwd_tma(int r) {
   }
 }
 
-// true when launched (the low-res rows must be 16-byte multiples for TMA)
+// true when launched (the low-res rows must be 16-byte multiples for TMA).
+// Variant hook 10 only: measured slower than the tile kernel at every config
+// (config 3 r = 1: 1515 vs 1276 us; r = 8: 2397 vs 1534 us; config 4a's
+// forward 3579 vs 2984 us; config 0 18.0 vs 21.7 us), because two resident
+// CTAs per SM keep less of the image in flight than four tile CTAs that
+// issue their 32 KB of high-res loads up front.
 static bool fused_joint_fwd_tma(const float* lr_x, const float* lr_y, const float* hr_x,
                                 float* out, int64_t P, int64_t h, int64_t w, int64_t H, int64_t W,
                                 int r, float eps, uint32_t* status, cudaStream_t s) {
-  if (w % 4 != 0 || g_joint_fwd_variant == 9) return false;
+  if (w % 4 != 0 || g_joint_fwd_variant != 10) return false;
   const FwdTma F = pick_fwd_tma(r);
   const int RI = jf::RA + 2 * r, PADL = (1 + r + 3) / 4 * 4;
   const int LP = (PADL + jf::TLX + 1 + r + 3) / 4 * 4;  // as jf::TmaGeo

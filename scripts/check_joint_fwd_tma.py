@@ -12,9 +12,9 @@ for (B, C, h, w) in [(1, 3, 16, 32), (2, 3, 37, 44), (1, 1, 256, 256), (1, 3, 10
         ly = torch.rand(B, C, h, w, device="cuda", generator=g)
         hx = torch.rand(B, C, 4 * h, 4 * w, device="cuda", generator=g)
         p = gfb.GuidedFilterParams(r, 1e-4)
-        a, _ = gfb.forward_joint(lx, hx, ly, p)
-        old = lib.gf_joint_fwd_variant(9)
         b, _ = gfb.forward_joint(lx, hx, ly, p)
+        old = lib.gf_joint_fwd_variant(10)
+        a, _ = gfb.forward_joint(lx, hx, ly, p)
         lib.gf_joint_fwd_variant(old)
         torch.cuda.synchronize()
         eq = torch.equal(a, b)

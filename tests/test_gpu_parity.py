@@ -775,3 +775,26 @@ def test_fused_guidance_backward_variants_vs_oracle(gfb, variant):
     for k, v in grads.items():
         own = float(np.abs(want_g[k]).max())
         assert abs_max(npy(v), want_g[k]) <= GRAD_TOL32 * max(own, 1e-2 * scale), k
+
+
+@pytest.mark.parametrize("r", [0, 1, 2, 4, 8, 12])
+def test_joint_fwd_tma_variant_bitwise(gfb, r):
+    """The persistent TMA joint forward (variant hook 10: cp.async.bulk.tensor
+    ring, tiles two ahead) is bitwise equal to the tile kernel, ragged shapes
+    and image borders included (TMA zero-fills outside the image)."""
+    from paper_1803_05619_b200 import _lib
+
+    lib = _lib.load()
+    for (B, C, h, w) in [(2, 3, 37, 44), (1, 1, 100, 300), (3, 2, 8, 4)]:
+        g = torch.Generator(device="cuda").manual_seed(r + h)
+        lx = torch.rand(B, C, h, w, device="cuda", generator=g)
+        ly = torch.rand(B, C, h, w, device="cuda", generator=g)
+        hx = torch.rand(B, C, 4 * h, 4 * w, device="cuda", generator=g)
+        p = gfb.GuidedFilterParams(r, 1e-4)
+        ref, _ = gfb.forward_joint(lx, hx, ly, p)
+        old = lib.gf_joint_fwd_variant(10)
+        try:
+            got, _ = gfb.forward_joint(lx, hx, ly, p)
+        finally:
+            lib.gf_joint_fwd_variant(old)
+        assert torch.equal(got, ref), (B, C, h, w)
