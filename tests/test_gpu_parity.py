@@ -798,3 +798,35 @@ def test_joint_fwd_tma_variant_bitwise(gfb, r):
         finally:
             lib.gf_joint_fwd_variant(old)
         assert torch.equal(got, ref), (B, C, h, w)
+
+
+def test_mean_filter_cost_is_radius_independent(gfb):
+    """The reference's performance-shape criterion (SPEC.md:541,
+    pkg/tests/test_filters.py:206-220): mean_filter at r = 32 costs at most
+    1.5x r = 1 on a 1024^2 image -- on the GPU general path (float64), and
+    the large-radius result matches the float64 oracle."""
+    import time
+
+    x = torch.rand(1, 3, 1024, 1024, dtype=torch.float64, device="cuda")
+
+    def t(r):
+        for _ in range(2):
+            gfb.mean_filter(x, r)
+        torch.cuda.synchronize()
+        best = 1e9
+        for _ in range(5):
+            t0 = time.perf_counter()
+            gfb.mean_filter(x, r)
+            torch.cuda.synchronize()
+            best = min(best, time.perf_counter() - t0)
+        return best
+
+    t1, t32 = t(1), t(32)
+    assert t32 <= 1.5 * t1 + 2e-4, (t1, t32)
+    small = x[:, :, :160, :200].contiguous()
+    hwc = npy(small)[0].transpose(1, 2, 0)
+    for r in (0, 3, 32, 300):
+        got = npy(gfb.mean_filter(small, r))[0].transpose(1, 2, 0)
+        assert np.abs(got - O.mean_filter(hwc, r)).max() <= 1e-12, r
+        got = npy(gfb.mean_filter_adjoint(small, r))[0].transpose(1, 2, 0)
+        assert np.abs(got - O.mean_filter_adjoint(hwc, r)).max() <= 1e-12, r
