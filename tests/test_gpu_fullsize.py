@@ -194,10 +194,31 @@ def test_cfg2_full_size_step_vs_oracle(gfb, norm_gain):
     loss, _, dlx, dly, dhx, grads = O.train_step(params, hwc(lr_x), hwc(hr_x), hwc(lr_y),
                                                  hwc(target), r, eps)
     assert abs(float(res.loss) - loss) <= 1e-5 * loss, (float(res.loss), loss)
+
+    # The leaky ReLU's derivative jumps at h2 = 0 (gf/guidance.py:36-43): at a
+    # pixel whose pre-activation is within fp32 rounding of 0 (|h2| ~ 1e-7 was
+    # measured for the worst pixel), fp32 and float64 can take different sides
+    # and d2 there differs by 0.8 d3 -- a discontinuity of the gradient, not an
+    # accuracy loss.  Those pixels (|h2| < 1e-4 for some hidden unit: < 0.1 %
+    # of the image) are excluded from the per-pixel input-gradient bars; the
+    # parameter gradients below sum over every pixel.
+    def ambiguous(xs):
+        out = []
+        for x in xs:
+            _, tape = O.guidance_forward(params, x)
+            h2 = params["norm.gain"][0] * tape["h1"] + params["norm.norm_gain"][0] * tape["xhat"]
+            out.append((np.abs(h2) < 1e-4).any(axis=2))
+        return np.stack(out)[:, None]  # (B, 1, h, w)
+
+    amb = {"d_lr_x": ambiguous(hwc(lr_x)), "d_hr_x": ambiguous(hwc(hr_x)),
+           "d_lr_y": np.zeros((B, 1) + tuple(lr_y.shape[2:]), dtype=bool)}
     for name, got, want in (("d_lr_x", res.d_lr_x, dlx), ("d_lr_y", res.d_lr_y, dly),
                             ("d_hr_x", res.d_hr_x, dhx)):
         want = np.stack([x.transpose(2, 0, 1) for x in want])
-        assert rel_max(npy(got), want) <= GRAD_TOL32, name
+        keep = ~np.broadcast_to(amb[name], want.shape)
+        assert amb[name].mean() < 1e-3, (name, amb[name].mean())
+        err = float(np.abs(npy(got) - want)[keep].max()) / float(np.abs(want).max())
+        assert err <= GRAD_TOL32, (name, err)
     got = net.unpack(res.dparams)
     scale = max(float(np.abs(v).max()) for v in grads.values())
     n = 0
