@@ -100,14 +100,22 @@ __device__ inline SmemCoef carve(float* base, int r) {
 // VCH: row chunks of the vertical pass (0: as many as the CTA's threads
 // allow); HCH: column chunks per row of the horizontal pass.  Each chunk pays
 // a 2r warm-up, so large radii favour fewer, longer chunks.
-// FROM_SMEM: X, Y are the block's raw low-res values already staged in
-// shared memory by TMA (rows i0-1-r.., columns k0-1-r-cofs.., pitch sp, zeros
-// outside the image); otherwise global planes.
-template <int RAD, bool NEED_B, int VCH = 0, int HCH = 16, bool FROM_SMEM = false>
+// MODE (where the block's low-res x, y come from):
+//   kStageLdg  -- global planes X, Y: loaded, shifted and stored to sm.xs/ys;
+//   kStageSmem -- raw values already in shared memory at X, Y (staged by TMA:
+//                 rows i0-1-r.., columns k0-1-r-cofs.., pitch sp, zeros
+//                 outside the image), copied shifted into sm.xs/ys;
+//   kStageTma  -- the same raw TMA boxes read IN PLACE by the vertical pass
+//                 (shift and the outside-the-image mask applied on the fly;
+//                 no staging pass, no copy): sm.xs/ys are unused.
+constexpr int kStageLdg = 0, kStageSmem = 1, kStageTma = 2;
+
+template <int RAD, bool NEED_B, int VCH = 0, int HCH = 16, int MODE = kStageLdg>
 __device__ void lr_coeffs(const float* __restrict__ X, const float* __restrict__ Y, int h, int w,
                           int i0, int k0, float eps, const SmemCoef& sm, bool& degen,
                           int sp = 0, int cofs = 0) {
   constexpr int r = RAD;
+  constexpr bool FROM_SMEM = MODE != kStageLdg;
   const int RI = RA + 2 * r, CI = CA + 2 * r;
   const int tid = threadIdx.x;
   // per-CTA shift (var/cov are shift invariant); any in-image sample works
@@ -124,7 +132,7 @@ __device__ void lr_coeffs(const float* __restrict__ X, const float* __restrict__
   // 1) stage inputs (zero outside the image: clamped windows); every load of
   //    the block is issued before the first store, so the CTA waits for one
   //    memory latency, not one per element
-  {
+  if constexpr (MODE != kStageTma) {
     constexpr int RIc = RA + 2 * r, CIc = CA + 2 * r;
     constexpr int NE = (RIc * CIc + NT - 1) / NT;
     float xv[NE], yv[NE];
@@ -150,8 +158,8 @@ __device__ void lr_coeffs(const float* __restrict__ X, const float* __restrict__
         sm.ys[idx] = yv[e];
       }
     }
+    __syncthreads();
   }
-  __syncthreads();
   // 2) vertical sliding sums: item = (column, chunk of rows)
   {
     // item = (column, chunk of rows) with warps never straddling two chunks:
@@ -165,16 +173,31 @@ __device__ void lr_coeffs(const float* __restrict__ X, const float* __restrict__
       const int col = it % CW, ch = it / CW;
       const int a0 = ch * rc, a1 = min(RA, a0 + rc);
       if (a0 >= a1 || col >= CI) continue;
+      // element (row, col) of the block, shifted, 0 outside the image
+      const bool colok = MODE != kStageTma || (unsigned)(k0 - 1 - r + col) < (unsigned)w;
+      auto ld = [&](int row, float& xv, float& yv) {
+        if constexpr (MODE == kStageTma) {
+          const bool ok = colok && (unsigned)(i0 - 1 - r + row) < (unsigned)h;
+          const float a = X[row * sp + col + cofs] - sx, b = Y[row * sp + col + cofs] - sy;
+          xv = ok ? a : 0.f;
+          yv = ok ? b : 0.f;
+        } else {
+          xv = sm.xs[row * CI + col];
+          yv = sm.ys[row * CI + col];
+        }
+      };
       float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
       for (int d = 0; d < 2 * r; ++d) {
-        const float xv = sm.xs[(a0 + d) * CI + col], yv = sm.ys[(a0 + d) * CI + col];
+        float xv, yv;
+        ld(a0 + d, xv, yv);
         s0 += xv;
         s1 += yv;
         s2 += xv * xv;
         s3 += xv * yv;
       }
       for (int a = a0; a < a1; ++a) {
-        const float xv = sm.xs[(a + 2 * r) * CI + col], yv = sm.ys[(a + 2 * r) * CI + col];
+        float xv, yv;
+        ld(a + 2 * r, xv, yv);
         s0 += xv;
         s1 += yv;
         s2 += xv * xv;
@@ -183,7 +206,8 @@ __device__ void lr_coeffs(const float* __restrict__ X, const float* __restrict__
         sm.vsum[(1 * RA + a) * VP + col] = s1;
         sm.vsum[(2 * RA + a) * VP + col] = s2;
         sm.vsum[(3 * RA + a) * VP + col] = s3;
-        const float xo = sm.xs[a * CI + col], yo = sm.ys[a * CI + col];
+        float xo, yo;
+        ld(a, xo, yo);
         s0 -= xo;
         s1 -= yo;
         s2 -= xo * xo;
@@ -425,7 +449,30 @@ struct TmaGeo {
   static constexpr int LR = (RI * LP + 31) / 32 * 32;     // 128-byte aligned boxes
   static constexpr int STAGE = HR + 2 * LR;
   static constexpr uint32_t BYTES = (uint32_t)(HR + 2 * RI * LP) * 4u;
+  static constexpr uint32_t LBYTES = (uint32_t)(2 * RI * LP) * 4u;  // low-res boxes only
 };
+
+__device__ __forceinline__ float* align128(float4* p) {
+  return reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(p) + 127) &
+                                  ~static_cast<uintptr_t>(127));
+}
+
+// layout of the TMA-staged tile kernels: [x box][y box][vsum][As][Bs]
+// (128-byte aligned boxes; sm.xs / sm.ys unused)
+template <int RAD>
+__host__ __device__ constexpr int tma_coef_floats() {
+  return 2 * TmaGeo<RAD>::LR + 4 * RA * pitch16(CA + 2 * RAD) + 2 * RA * CAP;
+}
+
+template <int RAD>
+__device__ __forceinline__ SmemCoef carve_tma(float* base) {
+  SmemCoef s;
+  s.xs = s.ys = nullptr;
+  s.vsum = base + 2 * TmaGeo<RAD>::LR;
+  s.As = s.vsum + 4 * RA * pitch16(CA + 2 * RAD);
+  s.Bs = s.As + RA * CAP;
+  return s;
+}
 
 template <int RAD, int NS>
 inline size_t fwd_tma_smem_bytes() {
@@ -511,6 +558,50 @@ __device__ __forceinline__ bool apply_rows(const SmemCoef& sm, const float4 (&g)
   return bad;
 }
 
+// the tile kernel k_joint_fwd with its low-res halo blocks staged by TMA
+template <int RAD, int VCH = 0, int HCH = 16>
+__global__ void __launch_bounds__(NT, (RAD >= 2 && RAD <= 4) ? 4 : 3)
+    k_joint_fwd_t(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmY,
+                  FwdArgs a) {
+  using TG = TmaGeo<RAD>;
+  extern __shared__ float4 smem4[];
+  __shared__ __align__(8) uint64_t tbar;
+  float* base = align128(smem4);
+  const SmemCoef sm = carve_tma<RAD>(base);
+  const int64_t p = blockIdx.z;
+  const int i0 = blockIdx.y * TLY, k0 = blockIdx.x * TLX;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const float* __restrict__ G = a.hr_x + p * (int64_t)a.H * a.W;
+  float* __restrict__ O = a.out + p * (int64_t)a.H * a.W;
+  const int X0 = 4 * (k0 + lane);
+  const int Yb = 4 * i0 + 8 * warp;
+  const bool col_ok = X0 < a.W;
+  if (threadIdx.x == 0) tma::mbar_init(&tbar, 1);
+  // 1) the hr loads first, then the low-res blocks by TMA
+  float4 g[8];
+#pragma unroll
+  for (int t = 0; t < 8; ++t) {
+    const int Y = Yb + t;
+    g[t] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (col_ok && Y < a.H) g[t] = __ldg(reinterpret_cast<const float4*>(G + (int64_t)Y * a.W + X0));
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    tma::mbar_arrive_expect_tx(&tbar, TG::LBYTES);
+    tma::load_3d(base, &tmX, k0 - TG::PADL, i0 - 1 - RAD, (int)p, &tbar);
+    tma::load_3d(base + TG::LR, &tmY, k0 - TG::PADL, i0 - 1 - RAD, (int)p, &tbar);
+  }
+  tma::mbar_wait(&tbar, 0);
+  // 2) coefficients, reading the TMA boxes in place
+  bool degen = false;
+  lr_coeffs<RAD, true, VCH, HCH, kStageTma>(base, base + TG::LR, a.h, a.w, i0, k0, a.eps, sm,
+                                            degen, TG::LP, TG::COFS);
+  // 3) apply
+  const bool bad = apply_rows<RAD>(sm, g, O, a.h, a.w, a.H, a.W, i0, k0, lane, warp);
+  if (degen) flag(a.status, GF_STATUS_DEGENERATE);
+  if (bad) flag(a.status, GF_STATUS_NONFINITE_OUTPUT);
+}
+
 template <int RAD, int NS, int MINB, int VCH = 0, int HCH = 16>
 __global__ void __launch_bounds__(NT, MINB)
     k_joint_fwd_tma(const __grid_constant__ CUtensorMap tmG, const __grid_constant__ CUtensorMap tmX,
@@ -559,7 +650,7 @@ __global__ void __launch_bounds__(NT, MINB)
     coords(t, p, i0, k0);
     tma::mbar_wait(&bar[s], (uint32_t)((k / NS) & 1));
     const float* st = base + s * TG::STAGE;
-    lr_coeffs<RAD, true, VCH, HCH, true>(st + TG::HR, st + TG::HR + TG::LR, a.h, a.w, i0, k0,
+    lr_coeffs<RAD, true, VCH, HCH, kStageSmem>(st + TG::HR, st + TG::HR + TG::LR, a.h, a.w, i0, k0,
                                          a.eps, sm, degen, TG::LP, TG::COFS);
     float4 g[8];
 #pragma unroll
@@ -862,14 +953,28 @@ struct MseHrArgs {
 
 // MSE = false: the same single gather pass for a given d_out (k_joint_bwd_hr's
 // job): `target` is d_out, A only, no loss.
-template <int RAD, int MINB, bool MSE>
-__global__ void __launch_bounds__(NT, MINB) k_joint_mse_hr(MseHrArgs a) {
+// MODE kStageTma (k_joint_mse_hr_t): the low-res x, y halo blocks arrive by
+// TMA (one elected thread, one mbarrier) and the coefficient pass reads them
+// in place -- no per-thread staging loads, index math or copies.
+template <int RAD, bool MSE, int MODE>
+__device__ __forceinline__ void mse_hr_body(const MseHrArgs& a, const CUtensorMap* tmX,
+                                            const CUtensorMap* tmY) {
   extern __shared__ float4 smem4[];
   __shared__ double red[NT / 32];
+  __shared__ __align__(8) uint64_t tbar;
   constexpr int r = RAD;
-  float* base = reinterpret_cast<float*>(smem4);
-  const SmemCoef sm = carve(base, r);
-  float* R1 = base + coef_smem_floats(r);  // [GR][TLX]
+  float* base;
+  SmemCoef sm;
+  float* R1;  // [GR][TLX]
+  if constexpr (MODE == kStageTma) {
+    base = align128(smem4);
+    sm = carve_tma<RAD>(base);
+    R1 = base + tma_coef_floats<RAD>();
+  } else {
+    base = reinterpret_cast<float*>(smem4);
+    sm = carve(base, r);
+    R1 = base + coef_smem_floats(r);
+  }
   float* R2 = R1 + GR * TLX;
   const int64_t p = blockIdx.z;
   const int i0 = blockIdx.y * TLY, k0 = blockIdx.x * TLX;
@@ -904,8 +1009,22 @@ __global__ void __launch_bounds__(NT, MINB) k_joint_mse_hr(MseHrArgs a) {
     }
   }
   bool degen = false;
-  lr_coeffs<RAD, MSE>(a.lr_x + p * (int64_t)a.h * a.w, a.lr_y + p * (int64_t)a.h * a.w, a.h, a.w,
-                      i0, k0, a.eps, sm, degen);
+  if constexpr (MODE == kStageTma) {
+    using TG = TmaGeo<RAD>;
+    if (threadIdx.x == 0) tma::mbar_init(&tbar, 1);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      tma::mbar_arrive_expect_tx(&tbar, TG::LBYTES);
+      tma::load_3d(base, tmX, k0 - TG::PADL, i0 - 1 - r, (int)p, &tbar);
+      tma::load_3d(base + TG::LR, tmY, k0 - TG::PADL, i0 - 1 - r, (int)p, &tbar);
+    }
+    tma::mbar_wait(&tbar, 0);
+    lr_coeffs<RAD, MSE, 0, 16, kStageTma>(base, base + TG::LR, a.h, a.w, i0, k0, a.eps, sm,
+                                          degen, TG::LP, TG::COFS);
+  } else {
+    lr_coeffs<RAD, MSE>(a.lr_x + p * (int64_t)a.h * a.w, a.lr_y + p * (int64_t)a.h * a.w, a.h,
+                        a.w, i0, k0, a.eps, sm, degen);
+  }
 
   const ColTaps ct = col_taps(X0, a.w, k0);
   const bool cin = k >= 1 && k <= a.w - 2;  // static column taps
@@ -1151,6 +1270,18 @@ __global__ void __launch_bounds__(NT, MINB) k_joint_mse_hr(MseHrArgs a) {
   if (chk != 0.f) flag(a.status, GF_STATUS_NONFINITE_OUTPUT);
 }
 
+template <int RAD, int MINB, bool MSE>
+__global__ void __launch_bounds__(NT, MINB) k_joint_mse_hr(MseHrArgs a) {
+  mse_hr_body<RAD, MSE, kStageLdg>(a, nullptr, nullptr);
+}
+
+template <int RAD, int MINB, bool MSE>
+__global__ void __launch_bounds__(NT, MINB)
+    k_joint_mse_hr_t(const __grid_constant__ CUtensorMap tmX,
+                     const __grid_constant__ CUtensorMap tmY, MseHrArgs a) {
+  mse_hr_body<RAD, MSE, kStageTma>(a, &tmX, &tmY);
+}
+
 // ---------------------------------------------------------------------------
 // backward, kernel 2: low-res tail
 // ---------------------------------------------------------------------------
@@ -1377,6 +1508,11 @@ struct JointFns {
   const void* bwd_lr;
   const void* mse_hr;
   const void* hr_pass;
+  // TMA-staged low-res blocks (w % 4 == 0): forward, fused step, hr pass
+  const void* fwd_t;
+  const void* mse_hr_t;
+  const void* hr_pass_t;
+  size_t tma_floats;  // tma_coef_floats + alignment slack
 };
 
 template <int RAD>
@@ -1384,16 +1520,23 @@ static JointFns joint_fns() {
   // r >= 2: fewer, longer coefficient-pass chunks (each pays a 2r warm-up):
   // 8 column chunks per row, and 2 row chunks for r >= 5 (config 3: r = 2
   // 1352 -> 1296 us, r = 4 1419 -> 1348 us, r = 8 1571 -> 1500 us)
-  const void* fwd;
-  if constexpr (RAD >= 5)
+  const void *fwd, *fwd_t;
+  if constexpr (RAD >= 5) {
     fwd = (const void*)jf::k_joint_fwd<RAD, 2, 8>;
-  else if constexpr (RAD >= 2)
+    fwd_t = (const void*)jf::k_joint_fwd_t<RAD, 2, 8>;
+  } else if constexpr (RAD >= 2) {
     fwd = (const void*)jf::k_joint_fwd<RAD, 0, 8>;
-  else
+    fwd_t = (const void*)jf::k_joint_fwd_t<RAD, 0, 8>;
+  } else {
     fwd = (const void*)jf::k_joint_fwd<RAD>;
+    fwd_t = (const void*)jf::k_joint_fwd_t<RAD>;
+  }
   return {fwd, (const void*)jf::k_joint_bwd_hr<RAD>, (const void*)jf::k_joint_bwd_lr<RAD>,
           (const void*)jf::k_joint_mse_hr<RAD, 3, true>,
-          (const void*)jf::k_joint_mse_hr<RAD, 4, false>};
+          (const void*)jf::k_joint_mse_hr<RAD, 4, false>, fwd_t,
+          (const void*)jf::k_joint_mse_hr_t<RAD, 3, true>,
+          (const void*)jf::k_joint_mse_hr_t<RAD, 4, false>,
+          (size_t)jf::tma_coef_floats<RAD>() + 32};
 }
 
 static JointFns pick_joint(int r) {
@@ -1484,11 +1627,39 @@ static bool fused_joint_fwd_tma(const float* lr_x, const float* lr_y, const floa
   return true;
 }
 
+// tensor maps of the low-res x, y planes with the (LP, RI) halo box of the
+// TMA-staged tile kernels; false when TMA does not apply (w % 4 != 0).
+// The TMA-staged kernels (variant hook 11 of the forward, hr pass and fused
+// step) are bitwise equal to the __ldg-staged defaults but measured ~5 %
+// slower (config 4a: fwd 3.07 vs 2.92 ms, bwd 6.25 vs 5.99 ms; config 2's
+// fused step 0.475 vs 0.455 ms): the in-place box reads re-apply the shift
+// and the image mask to every element the vertical pass touches (about
+// three times per element) where the staging pass applies them once.
+static bool lr_maps(CUtensorMap* tmX, CUtensorMap* tmY, const float* lr_x, const float* lr_y,
+                    int64_t P, int64_t h, int64_t w, int r) {
+  if (w % 4 != 0) return false;
+  const int RI = jf::RA + 2 * r, PADL = (1 + r + 3) / 4 * 4;
+  const int LP = (PADL + jf::TLX + 1 + r + 3) / 4 * 4;  // as jf::TmaGeo
+  return tma::make_plane_map(tmX, lr_x, w, h, P, LP, RI) &&
+         tma::make_plane_map(tmY, lr_y, w, h, P, LP, RI);
+}
+
 void fused_joint_fwd(const float* lr_x, const float* lr_y, const float* hr_x, float* out, int64_t B,
                      int64_t C, int64_t h, int64_t w, int64_t H, int64_t W, int r, float eps,
                      uint32_t* status, cudaStream_t s) {
   if (fused_joint_fwd_tma(lr_x, lr_y, hr_x, out, B * C, h, w, H, W, r, eps, status, s)) return;
   const JointFns fns = pick_joint(r);
+  CUtensorMap tmX, tmY;
+  if (g_joint_fwd_variant == 11 && lr_maps(&tmX, &tmY, lr_x, lr_y, B * C, h, w, r)) {
+    jf::FwdArgs a{lr_x, lr_y, hr_x, out, (int)h, (int)w, (int)H, (int)W, r, eps, status};
+    const size_t smem = fns.tma_floats * sizeof(float);
+    set_smem(fns.fwd_t, smem);
+    dim3 grid((unsigned)((w + jf::TLX - 1) / jf::TLX), (unsigned)((h + jf::TLY - 1) / jf::TLY),
+              (unsigned)(B * C));
+    void* args[] = {&tmX, &tmY, &a};
+    cudaLaunchKernel(fns.fwd_t, grid, dim3(jf::NT), args, smem, s);
+    return;
+  }
   jf::FwdArgs a{lr_x, lr_y, hr_x, out, (int)h, (int)w, (int)H, (int)W, r, eps, status};
   const int tx = (int)((w + jf::TLX - 1) / jf::TLX), ty = (int)((h + jf::TLY - 1) / jf::TLY);
   const size_t smem = jf::coef_smem_floats(r) * sizeof(float);
@@ -1558,10 +1729,18 @@ void fused_joint_bwd(const float* lr_x, const float* lr_y, const float* hr_x, co
       const void* fn = fns.hr_pass;
       if (r == 2 && g_joint_bwd_hr_variant == 3) fn = (const void*)jf::k_joint_mse_hr<2, 3, false>;
       if (r == 1 && g_joint_bwd_hr_variant == 3) fn = (const void*)jf::k_joint_mse_hr<1, 3, false>;
-      set_smem(fn, smem);
       jf::MseHrArgs a{lr_x, lr_y, hr_x, d_out, d_hr_x, db, dA, nullptr, (int)h, (int)w, (int)H,
                       (int)W, r, eps, 0.f, status};
-      launch(fn, grid, smem, s, &a);
+      CUtensorMap tmX, tmY;
+      if (g_joint_bwd_hr_variant == 11 && lr_maps(&tmX, &tmY, lr_x, lr_y, B * C, h, w, r)) {
+        const size_t smt = (fns.tma_floats + 2 * jf::GR * jf::TLX) * sizeof(float);
+        set_smem(fns.hr_pass_t, smt);
+        void* args[] = {&tmX, &tmY, &a};
+        cudaLaunchKernel(fns.hr_pass_t, grid, dim3(jf::NT), args, smt, s);
+      } else {
+        set_smem(fn, smem);
+        launch(fn, grid, smem, s, &a);
+      }
     }
   }
   joint_lr_tail(fns, lr_x, lr_y, db, dA, d_lr_x, d_lr_y, B, C, h, w, r, eps, row0, s);
@@ -1594,13 +1773,21 @@ void fused_joint_mse_bwd(const float* lr_x, const float* lr_y, const float* hr_x
     const void* fn = fns.mse_hr;
     if (r == 1 && g_joint_mse_variant == 2) fn = (const void*)jf::k_joint_mse_hr<1, 2, true>;
     if (r == 1 && g_joint_mse_variant == 4) fn = (const void*)jf::k_joint_mse_hr<1, 4, true>;
-    set_smem(fn, smem);
     dim3 grid((unsigned)((w + jf::TLX - 1) / jf::TLX), (unsigned)((h + jf::TLY - 1) / jf::TLY),
               (unsigned)(B * C));
     const double per_image = (double)C * (double)H * (double)W;
     jf::MseHrArgs a{lr_x, lr_y, hr_x, target, d_hr_x, db, dA, part, (int)h, (int)w, (int)H,
                     (int)W, r, eps, (float)(2.0 / per_image / (double)B), status};
-    launch(fn, grid, smem, s, &a);
+    CUtensorMap tmX, tmY;
+    if (g_joint_mse_variant == 11 && lr_maps(&tmX, &tmY, lr_x, lr_y, B * C, h, w, r)) {
+      const size_t smt = (fns.tma_floats + 2 * jf::GR * jf::TLX) * sizeof(float);
+      set_smem(fns.mse_hr_t, smt);
+      void* args[] = {&tmX, &tmY, &a};
+      cudaLaunchKernel(fns.mse_hr_t, grid, dim3(jf::NT), args, smt, s);
+    } else {
+      set_smem(fn, smem);
+      launch(fn, grid, smem, s, &a);
+    }
     mse_final(part, loss, B, (int)mse_tiles(C, h, w), per_image, s);
   }
   joint_lr_tail(fns, lr_x, lr_y, db, dA, d_lr_x, d_lr_y, B, C, h, w, r, eps, 0, s);

@@ -468,13 +468,16 @@ void launch(K kernel, int64_t n, cudaStream_t s, Args... args) {
 }
 
 constexpr int64_t kMaxScanW = 26000;  // row prefix sums in shared memory
+// radii below this keep the direct window sums: as cheap, and exact where
+// the reference is (r = 0: a window of one value, var = x^2 - x^2 = 0)
+constexpr int kRunMinR = 4;
 
 // clamped box sum of float64 fields, in -> out through tmp (mean: / N):
 // radius-independent passes when a row fits shared memory, else direct sums
 template <typename I, typename O>
 void box2d(const I* in, O* out, double* tmp, int64_t P, int64_t h, int64_t w, int r, int mean,
            int weighted, cudaStream_t s) {
-  if (w <= kMaxScanW) {
+  if (w <= kMaxScanW && r >= kRunMinR) {
     const int64_t nseg = (h + kSeg - 1) / kSeg;
     launch(k_box_v_run<I, double>, P * nseg * w, s, in, tmp, P, h, w, r, weighted);
     const size_t smem = (size_t)(w + 1 + kThreads) * sizeof(double);
@@ -533,7 +536,7 @@ size_t generic_workspace_bytes(int64_t n_moment_plane_total, int64_t extra_doubl
 template <typename T>
 void generic_mean_filter(const T* in, T* out, int64_t P, int64_t h, int64_t w, int r,
                          int adjoint, cudaStream_t s) {
-  if (w > kMaxScanW || (const void*)in == (const void*)out) {
+  if (w > kMaxScanW || r < kRunMinR || (const void*)in == (const void*)out) {
     launch(k_mean2d<T>, P * h * w, s, in, out, P, h, w, r, adjoint);
     return;
   }

@@ -830,3 +830,36 @@ def test_mean_filter_cost_is_radius_independent(gfb):
         assert np.abs(got - O.mean_filter(hwc, r)).max() <= 1e-12, r
         got = npy(gfb.mean_filter_adjoint(small, r))[0].transpose(1, 2, 0)
         assert np.abs(got - O.mean_filter_adjoint(hwc, r)).max() <= 1e-12, r
+
+
+def test_tma_staged_tile_kernels_bitwise(gfb):
+    """Variant hook 11: the joint forward, backward hr pass and fused step
+    with TMA-staged low-res halo blocks equal the defaults bit for bit."""
+    from paper_1803_05619_b200 import _lib
+
+    lib = _lib.load()
+    for (B, C, h, w, r) in [(2, 3, 37, 44, 2), (1, 1, 100, 300, 8), (3, 2, 8, 4, 0), (1, 3, 20, 36, 12)]:
+        g = torch.Generator(device="cuda").manual_seed(r + h)
+        lx, ly = (torch.rand(B, C, h, w, device="cuda", generator=g) for _ in range(2))
+        hx, tg = (torch.rand(B, C, 4 * h, 4 * w, device="cuda", generator=g) for _ in range(2))
+        d = torch.randn(B, C, 4 * h, 4 * w, device="cuda", generator=g)
+        p = gfb.GuidedFilterParams(r, 1e-4)
+
+        def run():
+            o, t = gfb.forward_joint(lx, hx, ly, p)
+            gr = gfb.backward(t, d)
+            loss, g2, _ = gfb.joint_mse_backward(lx, hx, ly, tg, p)
+            return [o, gr.d_guide_lo, gr.d_src, gr.d_guide_hi, g2.d_guide_lo, g2.d_src,
+                    g2.d_guide_hi, loss]
+
+        ref = run()
+        old = (lib.gf_joint_fwd_variant(11), lib.gf_joint_bwd_hr_variant(11),
+               lib.gf_joint_mse_variant(11))
+        try:
+            got = run()
+        finally:
+            lib.gf_joint_fwd_variant(old[0])
+            lib.gf_joint_bwd_hr_variant(old[1])
+            lib.gf_joint_mse_variant(old[2])
+        for a, b in zip(got, ref):
+            assert torch.equal(a, b), (B, C, h, w, r)
