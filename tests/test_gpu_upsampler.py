@@ -181,3 +181,25 @@ def test_guidance_k_argument_errors(gfb):
         gfb.TrainConfig(batch_size=2)
     with pytest.raises(ValueError):
         gfb.train(gfb.build_model(core_hidden=4, guide_hidden=4), [], gfb.TrainConfig(steps=1))
+
+
+@pytest.mark.parametrize("dtype", [torch.float64, torch.float32])
+def test_training_is_bitwise_deterministic(gfb, dtype):
+    """Run-to-run bitwise determinism of train() (the reference's
+    pkg/tests/test_training.py:227-234): identical loss histories and trained
+    parameters -- every reduction on the path (guidance-net gradients, the
+    MSE loss, Adam) is a fixed-order one, no floating-point atomics."""
+
+    def run():
+        model = gfb.build_model(seed=12, core_hidden=4, guide_hidden=4, low_res_side=8)
+        dataset = gfb.make_dataset("affine", count=3, height=24, width=24, seed=12)
+        model, history = gfb.train(model, dataset, gfb.TrainConfig(steps=25, seed=12),
+                                   dtype=dtype)
+        return history, {k: v.clone() for k, v in model.parameters().items()}
+
+    h1, p1 = run()
+    h2, p2 = run()
+    assert h1 == h2
+    for k in p1:
+        assert torch.equal(p1[k], p2[k]), k
+    assert h1[-1] < h1[0]

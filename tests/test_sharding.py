@@ -207,3 +207,63 @@ def test_joint_band_backward_helper_exact_on_oracle():
         assert np.abs(dlx - full[0][:, :, band.a:band.b]).max() <= 1e-10
         assert np.abs(dly - full[1][:, :, band.a:band.b]).max() <= 1e-10
         assert np.abs(dhx - full[2][:, :, A:B]).max() <= 1e-10
+
+
+# ---------------------------------------------------------------------------
+# data-parallel training loop (upsampler.train_loop), gloo world 2
+# ---------------------------------------------------------------------------
+
+def _fake_eval(i):
+    """Deterministic per-image loss and packed gradients (stand-ins for the
+    GPU model; the loop's scheduling and reduction are what is tested)."""
+    g1 = torch.arange(5, dtype=torch.float64) * (i + 1)
+    g2 = torch.full((3,), float(i * i), dtype=torch.float64)
+    return torch.tensor(float(i) + 0.5, dtype=torch.float64), [g1, g2]
+
+
+def _dp_worker(rank, world, port, tmpdir):
+    import torch.distributed as dist
+
+    from paper_1803_05619_b200.upsampler import train_loop
+
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
+                            world_size=world)
+    seen = []
+
+    def update(step, grads):
+        seen.append(torch.cat([g.clone() for g in grads]))
+
+    hist = train_loop(3, 5, _fake_eval, update)
+    torch.save({"hist": hist, "seen": seen}, os.path.join(tmpdir, f"r{rank}.pt"))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_train_loop_world1_is_reference_order():
+    from paper_1803_05619_b200.upsampler import train_loop
+
+    seen = []
+    hist = train_loop(4, 3, _fake_eval, lambda s, g: seen.append(torch.cat(g)))
+    # images in order, cycling (gf/training.py:240-262): 0 1 2 0, final 1
+    assert hist == [0.5, 1.5, 2.5, 0.5, 1.5]
+    assert torch.equal(seen[2], torch.cat(_fake_eval(2)[1]))
+
+
+def test_gloo_world2_data_parallel_train_loop(tmp_path):
+    """Global batch of 2 images per step (rank k: image 2*step + k), gradients
+    and loss averaged by one all-reduce; both ranks see identical updates."""
+    import torch.multiprocessing as mp
+
+    port = _free_port()
+    mp.spawn(_dp_worker, args=(2, port, str(tmp_path)), nprocs=2, join=True)
+    r0, r1 = (torch.load(tmp_path / f"r{k}.pt") for k in (0, 1))
+    assert r0["hist"] == r1["hist"]
+    for a, b in zip(r0["seen"], r1["seen"]):
+        assert torch.equal(a, b)
+    n = 5
+    for step in range(3):
+        i, j = (2 * step) % n, (2 * step + 1) % n
+        want = (torch.cat(_fake_eval(i)[1]) + torch.cat(_fake_eval(j)[1])) / 2
+        assert torch.allclose(r0["seen"][step], want)
+        assert r0["hist"][step] == pytest.approx((i + j + 1.0) / 2)
+    assert len(r0["hist"]) == 4
