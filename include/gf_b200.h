@@ -264,6 +264,16 @@ int gf_adaptive_norm_bwd(int dtype, const void* x, const void* dy, void* dx, voi
                          int64_t C, int64_t H, int64_t W, void* workspace,
                          size_t workspace_bytes, void* stream);
 
+/* ---- 8-bit images for the upsample CLI (gf/fileio.py:104-141) ----
+ * unpack: interleaved (H, W, C) uint8 -> (1, C, H, W) value / 255;
+ * pack: (1, C, H, W) -> (H, W, C) uint8 rint(clip(v, 0, 1) * 255) (round
+ * half to even).  Device pointers; asynchronous on `stream`. */
+int gf_image_unpack_u8(int dtype, const uint8_t* hwc, void* nchw, int64_t H, int64_t W,
+                       int64_t C, void* stream);
+
+int gf_image_pack_u8(int dtype, const void* nchw, uint8_t* hwc, int64_t H, int64_t W, int64_t C,
+                     void* stream);
+
 /* ---- FixedChannelMeanGuidance (gf/guidance.py:227-255) ----
  * y (B, Cout, H, W): every channel = mean over the Cin channels of x;
  * adjoint dx (B, Cin, H, W) = (sum over Cout of dy) / Cin. */

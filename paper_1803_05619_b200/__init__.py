@@ -23,8 +23,9 @@ from .training import affine_target, joint_mse_backward, mse_loss, train_step
 from .nn import FastGuidedFilter, FullResGuidedFilter
 from .host import forward_backward_joint_host, forward_highres_host, forward_joint_host
 from .upsampler import (TASKS, AdamState, GuidedUpsampler, PipelineTape, TrainConfig,
-                        TrainingError, adam_step, build_model, make_dataset, synthetic_images,
-                        train)
+                        TrainingError, adam_step, build_model, load_checkpoint, make_dataset,
+                        save_checkpoint, synthetic_images, train, train_loop)
+from . import fileio
 
 __version__ = "0.1.0"
 
@@ -37,5 +38,6 @@ __all__ = [
     "forward_backward_joint_host",
     "FixedChannelMeanGuidance", "AdamState", "GuidedUpsampler", "PipelineTape", "TrainConfig",
     "TrainingError", "adam_step", "build_model", "train", "AdaptiveNorm", "ConvLayer",
-    "make_dataset", "synthetic_images", "TASKS",
+    "make_dataset", "synthetic_images", "TASKS", "save_checkpoint", "load_checkpoint",
+    "train_loop", "fileio",
 ]

@@ -78,6 +78,8 @@ SIGNATURES = {
     "gf_adaptive_norm_fwd": (_i, [_i, _p, _p, _p, _p, _i64, _i64, _i64, _i64, _p, _sz, _p]),
     "gf_adaptive_norm_bwd": (_i, [_i, _p, _p, _p, _p, _p, _p, _p, _i64, _i64, _i64, _i64, _p,
                                   _sz, _p]),
+    "gf_image_unpack_u8": (_i, [_i, _p, _p, _i64, _i64, _i64, _p]),
+    "gf_image_pack_u8": (_i, [_i, _p, _p, _i64, _i64, _i64, _p]),
 }
 
 # test hooks exported by the library but not part of the public header
