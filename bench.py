@@ -500,7 +500,7 @@ def main():
             # keep the device busy while the host enqueues the step, so the
             # events bracket the step's device time, not the host's launch
             # latency (matters only for the microsecond-scale configs)
-            torch.cuda._sleep(200000)  # ~100 us: covers the Python API call
+            torch.cuda._sleep(800000)  # ~400 us: covers the Python API call
         evs[k][0].record()
         st.step()
         evs[k][1].record()
@@ -552,6 +552,7 @@ def main():
     achieved = alg / (ms * 1e-3) / 1e9
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "traffic": ncu_traffic(args.config),
+                "traffic_scope": "DRAM bytes of one step, all kernels (profiles/traffic.json)",
                 "peak_kind": peak_kind,
                 "algorithmic_bytes_per_launch": alg,
                 "frac_of_8TBps_nominal": round(achieved / 8000.0, 4)}

@@ -19,7 +19,7 @@ for cfg in ("cfg4a", "cfg0", "cfg1", "cfg2", "cfg3", "cfg4b"):
     res = subprocess.run([sys.executable, os.path.join(ROOT, "scripts", "summarize_launches.py"),
                           csv], capture_output=True, text=True, check=True)
     rows = [json.loads(ln) for ln in res.stdout.splitlines() if ln.startswith("{")]
-    steps = rows[0]["launches"]  # the dominant kernel runs once per step
+    steps = min(r["launches"] for r in rows)  # the rarest kernel runs once per step
     total = sum(r["launches"] * r["mean_dram_bytes"] for r in rows)
     out[cfg] = int(round(total / steps))
     out[cfg + "_kernel"] = rows[0]["kernel"]
