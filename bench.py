@@ -224,6 +224,7 @@ class OursStep:
             self.ws = torch.empty(max(nb, 16), dtype=torch.uint8, device=device)
             if kind in ("joint_fwd_bwd", "train_step"):
                 self.d_out = torch.randn(hr_x.shape, generator=g).to(device)
+                self.slope = torch.empty_like(lr_x)  # the tape's low-res slopes
                 self.d_lr_x = torch.empty_like(lr_x)
                 self.d_lr_y = torch.empty_like(lr_y)
                 self.d_hr_x = torch.empty_like(hr_x)
@@ -259,17 +260,23 @@ class OursStep:
         elif self.kind in ("joint_fwd", "joint_fwd_bwd"):
             lx, ly, hx = self.inputs
             B, h, w, Hh, Ww = self.B, self.h, self.w, self.H, self.W
-            rc = L.gf_joint_fwd(0, lx.data_ptr(), ly.data_ptr(), hx.data_ptr(),
-                                self.out.data_ptr(), B, C, h, w, Hh, Ww, r, eps,
-                                self.ws.data_ptr(), self.ws.numel(), self.status.data_ptr(),
-                                self.sp)
-            assert rc == 0, L.gf_last_error()
-            if self.kind == "joint_fwd_bwd":
-                rc = L.gf_joint_bwd_band(0, lx.data_ptr(), ly.data_ptr(), hx.data_ptr(),
-                                         self.d_out.data_ptr(), self.d_lr_x.data_ptr(),
-                                         self.d_lr_y.data_ptr(), self.d_hr_x.data_ptr(), B, C, h,
-                                         w, Hh, Ww, r, eps, self.row0, self.ws.data_ptr(),
-                                         self.ws.numel(), self.status.data_ptr(), self.sp)
+            if self.kind == "joint_fwd":
+                rc = L.gf_joint_fwd(0, lx.data_ptr(), ly.data_ptr(), hx.data_ptr(),
+                                    self.out.data_ptr(), B, C, h, w, Hh, Ww, r, eps,
+                                    self.ws.data_ptr(), self.ws.numel(), self.status.data_ptr(),
+                                    self.sp)
+                assert rc == 0, L.gf_last_error()
+            else:  # forward keeping the tape's slopes, backward on them (forward_joint/backward)
+                rc = L.gf_joint_fwd_tape(0, lx.data_ptr(), ly.data_ptr(), hx.data_ptr(),
+                                         self.out.data_ptr(), self.slope.data_ptr(), B, C, h, w,
+                                         Hh, Ww, r, eps, self.status.data_ptr(), self.sp)
+                assert rc == 0, L.gf_last_error()
+                rc = L.gf_joint_bwd_tape(0, lx.data_ptr(), ly.data_ptr(), hx.data_ptr(),
+                                         self.slope.data_ptr(), self.d_out.data_ptr(),
+                                         self.d_lr_x.data_ptr(), self.d_lr_y.data_ptr(),
+                                         self.d_hr_x.data_ptr(), B, C, h, w, Hh, Ww, r, eps,
+                                         self.row0, self.ws.data_ptr(), self.ws.numel(),
+                                         self.status.data_ptr(), self.sp)
                 assert rc == 0, L.gf_last_error()
         else:  # train_step
             import paper_1803_05619_b200 as gfb

@@ -121,6 +121,25 @@ int gf_joint_bwd_band(int dtype, const void* lr_x, const void* lr_y, const void*
                       double eps, int64_t row0, void* workspace, size_t workspace_bytes,
                       uint32_t* status, void* stream);
 
+/* Tape variants of the fast path (calls gf_joint_is_fused accepts, 16-byte
+ * aligned buffers; anything else returns GF_ERR_UNSUPPORTED and computes
+ * nothing -- use gf_joint_fwd / gf_joint_bwd).  gf_joint_fwd_tape also writes
+ * the low-res slope A = cov / (var + eps) of every cell to `slope_lo`
+ * (B, C, h, w): the reference's tape keeps it (gf/guided.py:147, :181-194).
+ * gf_joint_bwd_tape reads it back, so its high-res pass streams hr_x and
+ * d_out without recomputing window moments (the low-res tail still does);
+ * row0 as gf_joint_bwd_band.  Results equal gf_joint_bwd's to fp32
+ * rounding (a tile's halo slopes come from the neighbouring tile). */
+int gf_joint_fwd_tape(int dtype, const void* lr_x, const void* lr_y, const void* hr_x, void* out,
+                      void* slope_lo, int64_t B, int64_t C, int64_t h, int64_t w, int64_t H,
+                      int64_t W, int radius, double eps, uint32_t* status, void* stream);
+
+int gf_joint_bwd_tape(int dtype, const void* lr_x, const void* lr_y, const void* hr_x,
+                      const void* slope_lo, const void* d_out, void* d_lr_x, void* d_lr_y,
+                      void* d_hr_x, int64_t B, int64_t C, int64_t h, int64_t w, int64_t H,
+                      int64_t W, int radius, double eps, int64_t row0, void* workspace,
+                      size_t workspace_bytes, uint32_t* status, void* stream);
+
 /* ---- the full-resolution layer: gf/guided.py:198-233, :284-295 ----
  * guide: (B, Cg, H, W) with Cg == C or Cg == 1 (a 1-channel guide is
  * broadcast over the C source channels, BASELINE config 1); src, out:

@@ -293,6 +293,39 @@ int gf_joint_fwd(int dtype, const void* lr_x, const void* lr_y, const void* hr_x
   return check_launch("gf_joint_fwd");
 }
 
+int gf_joint_fwd_tape(int dtype, const void* lr_x, const void* lr_y, const void* hr_x, void* out,
+                      void* slope_lo, int64_t B, int64_t C, int64_t h, int64_t w, int64_t H,
+                      int64_t W, int radius, double eps, uint32_t* status, void* stream) {
+  if (int e = check_joint(dtype, B, C, h, w, H, W, radius, eps)) return e;
+  if (!(use_fused_joint(dtype, B, C, h, w, H, W, radius) && aligned16(lr_x) && aligned16(lr_y) &&
+        aligned16(hr_x) && aligned16(out) && slope_lo))
+    return fail(GF_ERR_UNSUPPORTED, "gf_joint_fwd_tape: not a fused-path call (use gf_joint_fwd)");
+  gfb::fused_joint_fwd((const float*)lr_x, (const float*)lr_y, (const float*)hr_x, (float*)out, B,
+                       C, h, w, H, W, radius, (float)eps, status, S(stream), (float*)slope_lo);
+  return check_launch("gf_joint_fwd_tape");
+}
+
+int gf_joint_bwd_tape(int dtype, const void* lr_x, const void* lr_y, const void* hr_x,
+                      const void* slope_lo, const void* d_out, void* d_lr_x, void* d_lr_y,
+                      void* d_hr_x, int64_t B, int64_t C, int64_t h, int64_t w, int64_t H,
+                      int64_t W, int radius, double eps, int64_t row0, void* workspace,
+                      size_t workspace_bytes, uint32_t* status, void* stream) {
+  if (int e = check_joint(dtype, B, C, h, w, H, W, radius, eps)) return e;
+  if (row0 < 0) return fail(GF_ERR_ARG, "row0 must be >= 0, got %lld", (long long)row0);
+  if (!(use_fused_joint(dtype, B, C, h, w, H, W, radius) && aligned16(lr_x) && aligned16(lr_y) &&
+        aligned16(hr_x) && aligned16(d_out) && aligned16(d_lr_x) && aligned16(d_lr_y) &&
+        aligned16(d_hr_x) && slope_lo))
+    return fail(GF_ERR_UNSUPPORTED, "gf_joint_bwd_tape: not a fused-path call (use gf_joint_bwd)");
+  const size_t need = gfb::fused_joint_bwd_ws_bytes(B, C, h, w);
+  if (workspace_bytes < need)
+    return fail(GF_ERR_WORKSPACE, "joint workspace %zu < %zu bytes", workspace_bytes, need);
+  gfb::fused_joint_bwd((const float*)lr_x, (const float*)lr_y, (const float*)hr_x,
+                       (const float*)d_out, (float*)d_lr_x, (float*)d_lr_y, (float*)d_hr_x, B, C,
+                       h, w, H, W, radius, (float)eps, workspace, row0, status, S(stream),
+                       (const float*)slope_lo);
+  return check_launch("gf_joint_bwd_tape");
+}
+
 int gf_joint_bwd(int dtype, const void* lr_x, const void* lr_y, const void* hr_x,
                  const void* d_out, void* d_lr_x, void* d_lr_y, void* d_hr_x, int64_t B,
                  int64_t C, int64_t h, int64_t w, int64_t H, int64_t W, int radius, double eps,

@@ -109,6 +109,15 @@ __device__ inline SmemCoef carve(float* base, int r) {
 //                 (shift and the outside-the-image mask applied on the fly;
 //                 no staging pass, no copy): sm.xs/ys are unused.
 constexpr int kStageLdg = 0, kStageSmem = 1, kStageTma = 2;
+// (mse_hr_body only) kStageTape: the slopes A of the block's 18 x 34 cells
+// are read from the forward's tape instead of recomputed
+constexpr int kStageTape = 3;
+// kStageTapeTile: the tape's slopes, and the high-res gather window of hr_x
+// and d_out (68 x 136 incl. the halo) staged by TMA into shared memory at CTA
+// start (the whole tile's reads in flight at once, no registers held)
+constexpr int kStageTapeTile = 4;
+constexpr int HTW = THX + 8, HTH = THY + 4;       // staged window: 136 x 68 (= GR rows)
+constexpr int HTF = HTW * HTH;                    // floats per field (128-byte multiple)
 
 template <int RAD, bool NEED_B, int VCH = 0, int HCH = 16, int MODE = kStageLdg>
 __device__ void lr_coeffs(const float* __restrict__ X, const float* __restrict__ Y, int h, int w,
@@ -277,6 +286,7 @@ struct FwdArgs {
   int h, w, H, W, r;
   float eps;
   uint32_t* status;
+  float* A_tape = nullptr;  // optional: the low-res slope A of every cell (the tape)
 };
 
 // Horizontal pre-interpolation of one coefficient row for the 4 hr phases of
@@ -346,9 +356,20 @@ __global__ void __launch_bounds__(NT, (RAD >= 2 && RAD <= 4) ? 4 : 3) k_joint_fw
   bool degen = false;
   lr_coeffs<RAD, true, VCH, HCH>(a.lr_x + p * (int64_t)a.h * a.w, a.lr_y + p * (int64_t)a.h * a.w,
                                  a.h, a.w, i0, k0, a.eps, sm, degen);
+  // the tile's own 16 x 32 slopes to the tape (the backward's hr pass reads
+  // them instead of recomputing the window moments; gf/guided.py:181-194
+  // keeps the slope in the tape the same way)
+  if (a.A_tape) {
+    for (int it = threadIdx.x; it < TLY * TLX; it += NT) {
+      const int il = it / TLX, kl = it - il * TLX;
+      const int i = i0 + il, kk = k0 + kl;
+      if (i < a.h && kk < a.w)
+        a.A_tape[p * (int64_t)a.h * a.w + (int64_t)i * a.w + kk] = sm.As[(il + 1) * CAP + kl + 1];
+    }
+  }
   // 3) apply
-  const ColTaps ct = col_taps(X0, a.w, k0);
   // static column taps (measured: faster for r <= 4, 3 % slower at r = 8)
+  const ColTaps ct = col_taps(X0, a.w, k0);
   const bool cin = RAD <= 4 && k0 + lane >= 1 && k0 + lane <= a.w - 2;
   // local coefficient rows 2*warp .. 2*warp+3 cover every tap of rows Yb..Yb+7
   float HA[4][4], HB[4][4];
@@ -387,7 +408,7 @@ __global__ void __launch_bounds__(NT, (RAD >= 2 && RAD <= 4) ? 4 : 3) k_joint_fw
           const float Ah = HA[q0][j] + f * (HA[q0 + 1][j] - HA[q0][j]);
           const float Bh = HB[q0][j] + f * (HB[q0 + 1][j] - HB[q0][j]);
           o[j] = Bh + Ah * gv[j];
-          chk += o[j] - o[j];  // NaN iff an output is not finite
+          chk = fmaf(o[j], 0.f, chk);  // NaN iff an output is not finite
         }
         *reinterpret_cast<float4*>(O + (int64_t)(Yb + t) * a.W + X0) =
             make_float4(o[0], o[1], o[2], o[3]);
@@ -488,8 +509,9 @@ __device__ __forceinline__ bool apply_rows(const SmemCoef& sm, const float4 (&g)
   const int X0 = 4 * (k0 + lane);
   const int Yb = 4 * i0 + 8 * warp;
   const bool col_ok = X0 < W;
-  const ColTaps ct = col_taps(X0, w, k0);
   const bool cin = RAD <= 4 && k0 + lane >= 1 && k0 + lane <= w - 2;
+  ColTaps ct;
+  if (!cin) ct = col_taps(X0, w, k0);
   float HA[4][4], HB[4][4];
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
@@ -524,7 +546,7 @@ __device__ __forceinline__ bool apply_rows(const SmemCoef& sm, const float4 (&g)
           const float Ah = HA[q0][j] + f * (HA[q0 + 1][j] - HA[q0][j]);
           const float Bh = HB[q0][j] + f * (HB[q0 + 1][j] - HB[q0][j]);
           o[j] = Bh + Ah * gv[j];
-          chk += o[j] - o[j];
+          chk = fmaf(o[j], 0.f, chk);
         }
         *reinterpret_cast<float4*>(O + (int64_t)(Yb + t) * W + X0) =
             make_float4(o[0], o[1], o[2], o[3]);
@@ -949,6 +971,7 @@ struct MseHrArgs {
   int h, w, H, W, r;
   float eps, scale2;
   uint32_t* status;
+  const float* A_tape = nullptr;  // kStageTape: the forward's low-res slopes
 };
 
 // MSE = false: the same single gather pass for a given d_out (k_joint_bwd_hr's
@@ -970,6 +993,18 @@ __device__ __forceinline__ void mse_hr_body(const MseHrArgs& a, const CUtensorMa
     base = align128(smem4);
     sm = carve_tma<RAD>(base);
     R1 = base + tma_coef_floats<RAD>();
+  } else if constexpr (MODE == kStageTape) {
+    base = reinterpret_cast<float*>(smem4);
+    sm.xs = sm.ys = sm.vsum = nullptr;
+    sm.As = base;
+    sm.Bs = base + RA * CAP;
+    R1 = base + 2 * RA * CAP;
+  } else if constexpr (MODE == kStageTapeTile) {
+    base = align128(smem4);
+    sm.xs = sm.ys = sm.vsum = nullptr;
+    sm.As = base + 2 * HTF;
+    sm.Bs = sm.As + RA * CAP;
+    R1 = sm.Bs + RA * CAP;
   } else {
     base = reinterpret_cast<float*>(smem4);
     sm = carve(base, r);
@@ -989,23 +1024,20 @@ __device__ __forceinline__ void mse_hr_body(const MseHrArgs& a, const CUtensorMa
   const int Yg = 4 * i0 - 2;    // hr row of gather row 0
   const bool extra = warp < 4;  // takes gather row 64 + warp as well
 
-  // this warp's rows of hr_x and target (and the halo chunks the scalar pass
-  // reads) start their DRAM reads into L2 before the coefficient phase
-  {
-    const int Xh = lane == 0 ? X0 - 4 : (lane == 31 ? X0 + 4 : -1);
-#pragma unroll
-    for (int t = 0; t < 9; ++t) {
-      if (t == 8 && !extra) break;
-      const int Y = Yg + (t < 8 ? 8 * warp + t : 64 + warp);
-      if (Y < 0 || Y >= a.H) continue;
-      if (col_ok) {
-        asm volatile("prefetch.global.L2 [%0];" ::"l"(G + (int64_t)Y * a.W + X0));
-        asm volatile("prefetch.global.L2 [%0];" ::"l"(T + (int64_t)Y * a.W + X0));
-      }
-      if (Xh >= 0 && Xh < a.W) {
-        asm volatile("prefetch.global.L2 [%0];" ::"l"(G + (int64_t)Y * a.W + Xh));
-        asm volatile("prefetch.global.L2 [%0];" ::"l"(T + (int64_t)Y * a.W + Xh));
-      }
+  // the tile's gather rows of hr_x and target (with the 4-column halo chunk
+  // on each side the scalar pass reads) start their DRAM reads into L2
+  // before the coefficient phase: ONE bulk L2 prefetch per (row, field), by
+  // 2 x 68 threads (one instruction each)
+  const float* tG = base;        // kStageTapeTile: staged gather window
+  const float* tT = base + HTF;
+  if (MODE != kStageTapeTile && threadIdx.x < 2 * GR) {
+    const int yl = threadIdx.x >> 1, Y = Yg + yl;
+    const int xa = max(4 * k0 - 4, 0), xb = min(4 * k0 + THX + 4, a.W);
+    if (Y >= 0 && Y < a.H && xb > xa) {
+      const float* src = ((threadIdx.x & 1) ? T : G) + (int64_t)Y * a.W + xa;
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src),
+                   "r"((unsigned)(xb - xa) * 4u)
+                   : "memory");
     }
   }
   bool degen = false;
@@ -1021,13 +1053,34 @@ __device__ __forceinline__ void mse_hr_body(const MseHrArgs& a, const CUtensorMa
     tma::mbar_wait(&tbar, 0);
     lr_coeffs<RAD, MSE, 0, 16, kStageTma>(base, base + TG::LR, a.h, a.w, i0, k0, a.eps, sm,
                                           degen, TG::LP, TG::COFS);
+  } else if constexpr (MODE == kStageTape || MODE == kStageTapeTile) {
+    static_assert(!MSE, "the tape has A only");
+    if constexpr (MODE == kStageTapeTile) {
+      if (threadIdx.x == 0) tma::mbar_init(&tbar, 1);
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        tma::mbar_arrive_expect_tx(&tbar, 2u * HTF * 4u);
+        tma::load_3d(base, tmX, 4 * k0 - 4, Yg, (int)p, &tbar);
+        tma::load_3d(base + HTF, tmY, 4 * k0 - 4, Yg, (int)p, &tbar);
+      }
+    }
+    const float* At = a.A_tape + p * (int64_t)a.h * a.w;
+    for (int it = threadIdx.x; it < RA * CA; it += NT) {
+      const int ar = it / CA, c = it - ar * CA;
+      const int gy = i0 - 1 + ar, gx = k0 - 1 + c;
+      sm.As[ar * CAP + c] =
+          (gy >= 0 && gy < a.h && gx >= 0 && gx < a.w) ? __ldg(At + (int64_t)gy * a.w + gx) : 0.f;
+    }
+    __syncthreads();
+    if constexpr (MODE == kStageTapeTile) tma::mbar_wait(&tbar, 0);
   } else {
     lr_coeffs<RAD, MSE>(a.lr_x + p * (int64_t)a.h * a.w, a.lr_y + p * (int64_t)a.h * a.w, a.h,
                         a.w, i0, k0, a.eps, sm, degen);
   }
 
-  const ColTaps ct = col_taps(X0, a.w, k0);
   const bool cin = k >= 1 && k <= a.w - 2;  // static column taps
+  ColTaps ct;
+  if (!cin) ct = col_taps(X0, a.w, k0);
   auto hrow2 = [&](int rl, float (&ha)[4], float (&hb)[4]) {
     if (cin) {
       hrow_interior(sm.As + rl * CAP, lane, ha);
@@ -1067,10 +1120,14 @@ __device__ __forceinline__ void mse_hr_body(const MseHrArgs& a, const CUtensorMa
                     const float (&bhi)[4], float f) {
     const int Y = Yg + yl;
     const bool in = col_ok && Y >= 0 && Y < a.H;
+    const int64_t off = (int64_t)Y * a.W + X0;  // one address for the 3 accesses
     float4 g4 = make_float4(0.f, 0.f, 0.f, 0.f), t4 = g4;
-    if (in) {
-      g4 = __ldg(reinterpret_cast<const float4*>(G + (int64_t)Y * a.W + X0));
-      t4 = __ldg(reinterpret_cast<const float4*>(T + (int64_t)Y * a.W + X0));
+    if constexpr (MODE == kStageTapeTile) {  // zeros outside the image (TMA)
+      g4 = *reinterpret_cast<const float4*>(tG + yl * HTW + 4 + 4 * lane);
+      t4 = *reinterpret_cast<const float4*>(tT + yl * HTW + 4 + 4 * lane);
+    } else if (in) {
+      g4 = __ldg(reinterpret_cast<const float4*>(G + off));
+      t4 = __ldg(reinterpret_cast<const float4*>(T + off));
     }
     const float gv[4] = {g4.x, g4.y, g4.z, g4.w}, tv[4] = {t4.x, t4.y, t4.z, t4.w};
     const bool own = in && yl >= 2 && yl < 2 + THY;
@@ -1085,7 +1142,7 @@ __device__ __forceinline__ void mse_hr_body(const MseHrArgs& a, const CUtensorMa
         d[j] = in ? scale2 * e : 0.f;
         if (own) {
           lsum = fmaf(e, e, lsum);
-          chk += o - o;  // NaN iff an output is not finite
+          chk = fmaf(o, 0.f, chk);  // NaN iff an output is not finite
         }
       } else {
         d[j] = tv[j];  // d_out (0 outside)
@@ -1093,8 +1150,7 @@ __device__ __forceinline__ void mse_hr_body(const MseHrArgs& a, const CUtensorMa
       q[j] = d[j] * gv[j];
       dh[j] = d[j] * Ah;
     }
-    if (own)
-      *reinterpret_cast<float4*>(DH + (int64_t)Y * a.W + X0) = make_float4(dh[0], dh[1], dh[2], dh[3]);
+    if (own) *reinterpret_cast<float4*>(DH + off) = make_float4(dh[0], dh[1], dh[2], dh[3]);
     float dl0 = __shfl_up_sync(0xffffffffu, d[2], 1), dl1 = __shfl_up_sync(0xffffffffu, d[3], 1);
     float ql0 = __shfl_up_sync(0xffffffffu, q[2], 1), ql1 = __shfl_up_sync(0xffffffffu, q[3], 1);
     float dr0 = __shfl_down_sync(0xffffffffu, d[0], 1), dr1 = __shfl_down_sync(0xffffffffu, d[1], 1);
@@ -1198,7 +1254,14 @@ __device__ __forceinline__ void mse_hr_body(const MseHrArgs& a, const CUtensorMa
           const Tap tx = tap4(X, a.w);
           const int cl = tx.lo - (k0 - 1), ch = tx.hi - (k0 - 1);
           // horizontal then vertical, as the row path
-          const float g = __ldg(G + (int64_t)Y * a.W + X), t = __ldg(T + (int64_t)Y * a.W + X);
+          float g, t;
+          if constexpr (MODE == kStageTapeTile) {
+            g = tG[yl * HTW + X - (4 * k0 - 4)];
+            t = tT[yl * HTW + X - (4 * k0 - 4)];
+          } else {
+            g = __ldg(G + (int64_t)Y * a.W + X);
+            t = __ldg(T + (int64_t)Y * a.W + X);
+          }
           float dv = t;  // d_out
           if (MSE) {
             const float al = A0[cl] + tx.f * (A0[ch] - A0[cl]);
@@ -1273,6 +1336,21 @@ __device__ __forceinline__ void mse_hr_body(const MseHrArgs& a, const CUtensorMa
 template <int RAD, int MINB, bool MSE>
 __global__ void __launch_bounds__(NT, MINB) k_joint_mse_hr(MseHrArgs a) {
   mse_hr_body<RAD, MSE, kStageLdg>(a, nullptr, nullptr);
+}
+
+// the backward hr pass on the forward's tape of slopes (no window moments)
+template <int RAD, int MINB>
+__global__ void __launch_bounds__(NT, MINB) k_joint_mse_hr_a(MseHrArgs a) {
+  mse_hr_body<RAD, false, kStageTape>(a, nullptr, nullptr);
+}
+
+// ... with the gather window of hr_x and d_out staged by TMA (tmG, tmD:
+// (136, 68) boxes of the high-res planes)
+template <int RAD, int MINB>
+__global__ void __launch_bounds__(NT, MINB)
+    k_joint_mse_hr_at(const __grid_constant__ CUtensorMap tmG,
+                      const __grid_constant__ CUtensorMap tmD, MseHrArgs a) {
+  mse_hr_body<RAD, false, kStageTapeTile>(a, &tmG, &tmD);
 }
 
 template <int RAD, int MINB, bool MSE>
@@ -1513,6 +1591,8 @@ struct JointFns {
   const void* mse_hr_t;
   const void* hr_pass_t;
   size_t tma_floats;  // tma_coef_floats + alignment slack
+  const void* hr_pass_a;   // hr pass on the forward's tape of slopes
+  const void* hr_pass_at;  // ... with the gather window staged by TMA
 };
 
 template <int RAD>
@@ -1536,7 +1616,8 @@ static JointFns joint_fns() {
           (const void*)jf::k_joint_mse_hr<RAD, 4, false>, fwd_t,
           (const void*)jf::k_joint_mse_hr_t<RAD, 3, true>,
           (const void*)jf::k_joint_mse_hr_t<RAD, 4, false>,
-          (size_t)jf::tma_coef_floats<RAD>() + 32};
+          (size_t)jf::tma_coef_floats<RAD>() + 32, (const void*)jf::k_joint_mse_hr_a<RAD, 4>,
+          (const void*)jf::k_joint_mse_hr_at<RAD, 2>};
 }
 
 static JointFns pick_joint(int r) {
@@ -1646,11 +1727,12 @@ static bool lr_maps(CUtensorMap* tmX, CUtensorMap* tmY, const float* lr_x, const
 
 void fused_joint_fwd(const float* lr_x, const float* lr_y, const float* hr_x, float* out, int64_t B,
                      int64_t C, int64_t h, int64_t w, int64_t H, int64_t W, int r, float eps,
-                     uint32_t* status, cudaStream_t s) {
-  if (fused_joint_fwd_tma(lr_x, lr_y, hr_x, out, B * C, h, w, H, W, r, eps, status, s)) return;
+                     uint32_t* status, cudaStream_t s, float* A_tape) {
+  if (!A_tape && fused_joint_fwd_tma(lr_x, lr_y, hr_x, out, B * C, h, w, H, W, r, eps, status, s))
+    return;
   const JointFns fns = pick_joint(r);
   CUtensorMap tmX, tmY;
-  if (g_joint_fwd_variant == 11 && lr_maps(&tmX, &tmY, lr_x, lr_y, B * C, h, w, r)) {
+  if (!A_tape && g_joint_fwd_variant == 11 && lr_maps(&tmX, &tmY, lr_x, lr_y, B * C, h, w, r)) {
     jf::FwdArgs a{lr_x, lr_y, hr_x, out, (int)h, (int)w, (int)H, (int)W, r, eps, status};
     const size_t smem = fns.tma_floats * sizeof(float);
     set_smem(fns.fwd_t, smem);
@@ -1660,7 +1742,7 @@ void fused_joint_fwd(const float* lr_x, const float* lr_y, const float* hr_x, fl
     cudaLaunchKernel(fns.fwd_t, grid, dim3(jf::NT), args, smem, s);
     return;
   }
-  jf::FwdArgs a{lr_x, lr_y, hr_x, out, (int)h, (int)w, (int)H, (int)W, r, eps, status};
+  jf::FwdArgs a{lr_x, lr_y, hr_x, out, (int)h, (int)w, (int)H, (int)W, r, eps, status, A_tape};
   const int tx = (int)((w + jf::TLX - 1) / jf::TLX), ty = (int)((h + jf::TLY - 1) / jf::TLY);
   const size_t smem = jf::coef_smem_floats(r) * sizeof(float);
   const void* fn = fns.fwd;
@@ -1711,7 +1793,7 @@ static void joint_lr_tail(const JointFns& fns, const float* lr_x, const float* l
 void fused_joint_bwd(const float* lr_x, const float* lr_y, const float* hr_x, const float* d_out,
                      float* d_lr_x, float* d_lr_y, float* d_hr_x, int64_t B, int64_t C, int64_t h,
                      int64_t w, int64_t H, int64_t W, int r, float eps, void* ws, int64_t row0,
-                     uint32_t* status, cudaStream_t s) {
+                     uint32_t* status, cudaStream_t s, const float* A_tape) {
   float* db = (float*)ws;
   float* dA = db + B * C * h * w;
   const JointFns fns = pick_joint(r);
@@ -1732,7 +1814,23 @@ void fused_joint_bwd(const float* lr_x, const float* lr_y, const float* hr_x, co
       jf::MseHrArgs a{lr_x, lr_y, hr_x, d_out, d_hr_x, db, dA, nullptr, (int)h, (int)w, (int)H,
                       (int)W, r, eps, 0.f, status};
       CUtensorMap tmX, tmY;
-      if (g_joint_bwd_hr_variant == 11 && lr_maps(&tmX, &tmY, lr_x, lr_y, B * C, h, w, r)) {
+      CUtensorMap tmG, tmD;
+      if (A_tape && g_joint_bwd_hr_variant == 0 &&
+          tma::make_plane_map(&tmG, hr_x, W, H, B * C, jf::HTW, jf::HTH) &&
+          tma::make_plane_map(&tmD, d_out, W, H, B * C, jf::HTW, jf::HTH)) {
+        // the forward's slopes, and the gather window by TMA
+        a.A_tape = A_tape;
+        const size_t sma =
+            128 + (2 * jf::HTF + 2 * jf::RA * jf::CAP + 2 * jf::GR * jf::TLX) * sizeof(float);
+        set_smem(fns.hr_pass_at, sma);
+        void* args[] = {&tmG, &tmD, &a};
+        cudaLaunchKernel(fns.hr_pass_at, grid, dim3(jf::NT), args, sma, s);
+      } else if (A_tape && g_joint_bwd_hr_variant == 12) {  // slopes, global loads
+        a.A_tape = A_tape;
+        const size_t sma = (2 * jf::RA * jf::CAP + 2 * jf::GR * jf::TLX) * sizeof(float);
+        set_smem(fns.hr_pass_a, sma);
+        launch(fns.hr_pass_a, grid, sma, s, &a);
+      } else if (g_joint_bwd_hr_variant == 11 && lr_maps(&tmX, &tmY, lr_x, lr_y, B * C, h, w, r)) {
         const size_t smt = (fns.tma_floats + 2 * jf::GR * jf::TLX) * sizeof(float);
         set_smem(fns.hr_pass_t, smt);
         void* args[] = {&tmX, &tmY, &a};

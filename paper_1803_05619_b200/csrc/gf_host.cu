@@ -17,6 +17,9 @@
 #include "../../include/gf_b200.h"
 #include "gf_internal.h"
 
+extern "C" int gf_joint_is_fused(int dtype, int64_t B, int64_t C, int64_t h, int64_t w,
+                                 int64_t H, int64_t W, int r);
+
 namespace {
 
 // chunk slots in flight: three decouple the H2D, kernel and D2H streams (with
@@ -249,7 +252,7 @@ size_t gf_joint_fwd_bwd_host_workspace_bytes(int dtype, int64_t C, int64_t h, in
   const Input ins[4] = {{nullptr, lo, 1}, {nullptr, lo, 1}, {nullptr, hi, 1}, {nullptr, hi, 1}};
   const Output outs[4] = {{nullptr, hi}, {nullptr, lo}, {nullptr, lo}, {nullptr, hi}};
   return pipeline_ws(ins, 4, outs, 4) +
-         up256(gf_joint_workspace_bytes(dtype, 1, 1, h, w, H, W, radius)) + 256;
+         up256(gf_joint_workspace_bytes(dtype, 1, 1, h, w, H, W, radius)) + up256(lo) + 256;
 }
 
 int gf_joint_fwd_bwd_host(int dtype, const void* lr_x, const void* lr_y, const void* hr_x,
@@ -268,9 +271,21 @@ int gf_joint_fwd_bwd_host(int dtype, const void* lr_x, const void* lr_y, const v
   char* ws = (char*)workspace;
   char* gws = ws + pipeline_ws(ins, 4, outs, 4);
   const size_t gws_bytes = gf_joint_workspace_bytes(dtype, 1, 1, h, w, H, W, radius);
-  uint32_t* st_dev = (uint32_t*)(gws + up256(gws_bytes));
+  void* slope = gws + up256(gws_bytes);  // one plane's slope tape (fast path)
+  uint32_t* st_dev = (uint32_t*)((char*)slope + up256(lo));
+  // the device API's path: forward keeping the slope tape, backward on it
+  // (forward_joint / backward do the same), else the moments-recomputing pair
+  const bool tape = gf_joint_is_fused(dtype, 1, 1, h, w, H, W, radius) != 0;
   return run_pipeline(B * C, 4, ins, 4, outs, ws, st_dev, status,
                       [&](const void* const* d, void* const* o, cudaStream_t s) {
+                        if (tape) {
+                          if (int e = gf_joint_fwd_tape(dtype, d[0], d[1], d[2], o[0], slope, 1,
+                                                        1, h, w, H, W, radius, eps, st_dev, s))
+                            return e;
+                          return gf_joint_bwd_tape(dtype, d[0], d[1], d[2], slope, d[3], o[1],
+                                                   o[2], o[3], 1, 1, h, w, H, W, radius, eps, 0,
+                                                   gws, gws_bytes, st_dev, s);
+                        }
                         if (int e = gf_joint_fwd(dtype, d[0], d[1], d[2], o[0], 1, 1, h, w, H, W,
                                                  radius, eps, gws, gws_bytes, st_dev, s))
                           return e;

@@ -93,12 +93,13 @@ extern thread_local int g_gn_bwd_variant;  // fused guidance backward: 0 one hea
 bool fused_joint_ok(int64_t B, int64_t C, int64_t h, int64_t w, int64_t H, int64_t W, int r);
 void fused_joint_fwd(const float* lr_x, const float* lr_y, const float* hr_x, float* out,
                      int64_t B, int64_t C, int64_t h, int64_t w, int64_t H, int64_t W, int r,
-                     float eps, uint32_t* status, cudaStream_t s);
+                     float eps, uint32_t* status, cudaStream_t s, float* A_tape = nullptr);
 size_t fused_joint_bwd_ws_bytes(int64_t B, int64_t C, int64_t h, int64_t w);
 void fused_joint_bwd(const float* lr_x, const float* lr_y, const float* hr_x, const float* d_out,
                      float* d_lr_x, float* d_lr_y, float* d_hr_x, int64_t B, int64_t C,
                      int64_t h, int64_t w, int64_t H, int64_t W, int r, float eps, void* ws,
-                     int64_t row0, uint32_t* status, cudaStream_t s);
+                     int64_t row0, uint32_t* status, cudaStream_t s,
+                     const float* A_tape = nullptr);
 // fused training step: forward + MSE + backward (no out / d_out in HBM)
 size_t fused_joint_mse_ws_bytes(int64_t B, int64_t C, int64_t h, int64_t w);
 void fused_joint_mse_bwd(const float* lr_x, const float* lr_y, const float* hr_x,

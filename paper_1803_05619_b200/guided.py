@@ -84,6 +84,10 @@ class GuidedFilterTape:
     _cache: dict = field(default_factory=dict)
     _versions: tuple = ()
     row_origin: int = 0  # full-image low-res row of row 0 (row bands, sharding.py)
+    # fast fp32 path: the low-res slope A of every cell, written by the forward
+    # (gf_joint_fwd_tape) so the backward's high-res pass needs no window
+    # moments -- the reference's tape keeps the slope too (gf/guided.py:181-194)
+    _slope_lo: object = None
 
     def __post_init__(self) -> None:
         # autograd-style saved-tensor check: backward recomputes the moments
@@ -179,15 +183,24 @@ def forward_joint(guide_lo, guide_hi, src_lo, p: GuidedFilterParams, *, check: b
     dt = dtype_code(gl.t)
     out = torch.empty_like(gh.t)
     status = Status(dev)
-    nbytes = lib.gf_joint_workspace_bytes(dt, B, C, h, w, H, W, p.radius)
-    ws = workspace(nbytes, dev)
-    rc = lib.gf_joint_fwd(dt, ptr(gl.t), ptr(sl.t), ptr(gh.t), ptr(out), B, C, h, w, H, W,
-                          int(p.radius), float(p.eps), ptr(ws), ws.numel(), status.ptr,
-                          _stream(gl))
+    slope = None
+    if lib.gf_joint_is_fused(dt, B, C, h, w, H, W, p.radius) and not any(
+            t.data_ptr() % 16 for t in (gl.t, sl.t, gh.t, out)):
+        slope = torch.empty_like(gl.t)
+        rc = lib.gf_joint_fwd_tape(dt, ptr(gl.t), ptr(sl.t), ptr(gh.t), ptr(out), ptr(slope), B,
+                                   C, h, w, H, W, int(p.radius), float(p.eps), status.ptr,
+                                   _stream(gl))
+    else:
+        nbytes = lib.gf_joint_workspace_bytes(dt, B, C, h, w, H, W, p.radius)
+        ws = workspace(nbytes, dev)
+        rc = lib.gf_joint_fwd(dt, ptr(gl.t), ptr(sl.t), ptr(gh.t), ptr(out), B, C, h, w, H, W,
+                              int(p.radius), float(p.eps), ptr(ws), ws.numel(), status.ptr,
+                              _stream(gl))
     _lib.check(rc, "forward_joint")
     if check:
         status.raise_if_set("forward_joint", (gl.t, gh.t, sl.t))
-    tape = GuidedFilterTape(VARIANT_JOINT, p, gl, sl, gh, gh, status, row_origin=int(row_origin))
+    tape = GuidedFilterTape(VARIANT_JOINT, p, gl, sl, gh, gh, status, row_origin=int(row_origin),
+                            _slope_lo=slope)
     return restore(out, gh), tape
 
 
@@ -244,10 +257,17 @@ def backward(tape: GuidedFilterTape, d_out, *, check: bool = True) -> GuidedFilt
         d_lr_y = torch.empty_like(sl.t)
         d_hr_x = torch.empty_like(gh.t)
         ws = workspace(lib.gf_joint_workspace_bytes(dt, B, C, h, w, H, W, p.radius), dev)
-        rc = lib.gf_joint_bwd_band(dt, ptr(gl.t), ptr(sl.t), ptr(gh.t), ptr(d.t), ptr(d_lr_x),
-                                   ptr(d_lr_y), ptr(d_hr_x), B, C, h, w, H, W, int(p.radius),
-                                   float(p.eps), tape.row_origin, ptr(ws), ws.numel(),
-                                   status.ptr, _stream(gl))
+        if tape._slope_lo is not None and not any(
+                t.data_ptr() % 16 for t in (d.t, d_lr_x, d_lr_y, d_hr_x)):
+            rc = lib.gf_joint_bwd_tape(dt, ptr(gl.t), ptr(sl.t), ptr(gh.t), ptr(tape._slope_lo),
+                                       ptr(d.t), ptr(d_lr_x), ptr(d_lr_y), ptr(d_hr_x), B, C, h,
+                                       w, H, W, int(p.radius), float(p.eps), tape.row_origin,
+                                       ptr(ws), ws.numel(), status.ptr, _stream(gl))
+        else:
+            rc = lib.gf_joint_bwd_band(dt, ptr(gl.t), ptr(sl.t), ptr(gh.t), ptr(d.t),
+                                       ptr(d_lr_x), ptr(d_lr_y), ptr(d_hr_x), B, C, h, w, H, W,
+                                       int(p.radius), float(p.eps), tape.row_origin, ptr(ws),
+                                       ws.numel(), status.ptr, _stream(gl))
         _lib.check(rc, "backward")
         if check:
             status.raise_if_set("backward")

@@ -274,3 +274,55 @@ def test_joint_mse_guarded(lib, dtype, h, w, r):
     b = run_joint_mse(lib, lr_x, lr_y, hr_x, tgt, r, 1e-3, guarded=False)
     for x, y in zip(a, b):
         assert torch.equal(x, y)
+
+
+def run_joint_tape(lib, lr_x, lr_y, hr_x, d, r, eps, guarded):
+    """gf_joint_fwd_tape + gf_joint_bwd_tape (the slope tape and the TMA-staged
+    gather window of the backward's hr pass) with every buffer guarded."""
+    B, C, h, w = lr_x.shape
+    H, W = hr_x.shape[2:]
+    wsb = lib.gf_joint_workspace_bytes(0, B, C, h, w, H, W, r)
+    if guarded:
+        ins = [gin(t) for t in (lr_x, lr_y, hr_x, d)]
+        outs = [gout(hr_x.shape, lr_x.dtype), gout(lr_x.shape, lr_x.dtype),
+                gout(lr_x.shape, lr_x.dtype), gout(hr_x.shape, lr_x.dtype),
+                gout(lr_x.shape, lr_x.dtype)]  # the last: the slope tape
+        ws = gws(wsb)
+        p = lambda g: g.ptr  # noqa: E731
+    else:
+        ins = [lr_x, lr_y, hr_x, d]
+        outs = [torch.empty_like(hr_x), torch.empty_like(lr_x), torch.empty_like(lr_x),
+                torch.empty_like(hr_x), torch.empty_like(lr_x)]
+        ws = torch.empty(max(wsb, 16), dtype=torch.uint8, device="cuda")
+        p = lambda t: t.data_ptr()  # noqa: E731
+    st = status()
+    rc_ok(lib, lib.gf_joint_fwd_tape(0, p(ins[0]), p(ins[1]), p(ins[2]), p(outs[0]), p(outs[4]),
+                                     B, C, h, w, H, W, r, eps, st.data_ptr(), stream()))
+    rc_ok(lib, lib.gf_joint_bwd_tape(0, p(ins[0]), p(ins[1]), p(ins[2]), p(outs[4]), p(ins[3]),
+                                     p(outs[1]), p(outs[2]), p(outs[3]), B, C, h, w, H, W, r, eps,
+                                     0, p(ws), wsb, st.data_ptr(), stream()))
+    torch.cuda.synchronize()
+    assert int(st.item()) == 0
+    if guarded:
+        for g in ins + outs + [ws]:
+            assert g.guards_intact()
+        return [o.view.clone() for o in outs]
+    return outs
+
+
+@pytest.mark.parametrize("h,w,r", [(37, 44, 0), (33, 16, 5), (21, 72, 12), (2, 4, 1),
+                                   (130, 68, 3), (16, 32, 2)])
+def test_joint_tape_guarded(lib, h, w, r):
+    g = torch.Generator(device="cuda").manual_seed(h * 100 + w + r)
+    mk = lambda *s: torch.rand(*s, generator=g, device="cuda")  # noqa: E731
+    lr_x, lr_y = mk(2, 3, h, w), mk(2, 3, h, w)
+    hr_x, d = mk(2, 3, 4 * h, 4 * w), mk(2, 3, 4 * h, 4 * w) - 0.5
+    a = run_joint_tape(lib, lr_x, lr_y, hr_x, d, r, 1e-3, guarded=True)
+    b = run_joint_tape(lib, lr_x, lr_y, hr_x, d, r, 1e-3, guarded=False)
+    for x, y in zip(a, b):
+        assert torch.equal(x, y)
+    # against the moments-recomputing backward: out and d_lr bitwise (the low-res
+    # tail recomputes), d_hr to fp32 rounding (halo slopes of neighbouring tiles)
+    c = run_joint(lib, lr_x, lr_y, hr_x, d, r, 1e-3, guarded=False)
+    assert torch.equal(a[0], c[0]) and torch.equal(a[1], c[1]) and torch.equal(a[2], c[2])
+    assert float((a[3] - c[3]).abs().max()) <= 1e-5 * float(c[3].abs().max())
