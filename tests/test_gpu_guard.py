@@ -322,7 +322,10 @@ def test_joint_tape_guarded(lib, h, w, r):
     for x, y in zip(a, b):
         assert torch.equal(x, y)
     # against the moments-recomputing backward: out and d_lr bitwise (the low-res
-    # tail recomputes), d_hr to fp32 rounding (halo slopes of neighbouring tiles)
+    # tail recomputes), d_hr to fp32 rounding of the slopes (a tile's halo
+    # slopes come from the neighbouring tile, computed with its own shift; at
+    # r = 0 the exact slope is 0 and both are rounding noise ~ 1e-7 / eps)
     c = run_joint(lib, lr_x, lr_y, hr_x, d, r, 1e-3, guarded=False)
     assert torch.equal(a[0], c[0]) and torch.equal(a[1], c[1]) and torch.equal(a[2], c[2])
-    assert float((a[3] - c[3]).abs().max()) <= 1e-5 * float(c[3].abs().max())
+    tol = 1e-5 * float(c[3].abs().max()) + 1e-4 * float(d.abs().max())
+    assert float((a[3] - c[3]).abs().max()) <= tol

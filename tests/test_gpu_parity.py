@@ -861,5 +861,11 @@ def test_tma_staged_tile_kernels_bitwise(gfb):
             lib.gf_joint_fwd_variant(old[0])
             lib.gf_joint_bwd_hr_variant(old[1])
             lib.gf_joint_mse_variant(old[2])
-        for a, b in zip(got, ref):
-            assert torch.equal(a, b), (B, C, h, w, r)
+        # the default backward runs on the forward's slope tape; variant 11
+        # recomputes the moments: d_hr (index 3) agrees to fp32 rounding
+        for i, (a, b) in enumerate(zip(got, ref)):
+            if i == 3:
+                tol = 1e-5 * float(b.abs().max()) + 1e-4 * float(d.abs().max())
+                assert float((a - b).abs().max()) <= tol, (B, C, h, w, r)
+            else:
+                assert torch.equal(a, b), (i, B, C, h, w, r)
