@@ -849,8 +849,14 @@ def test_tma_staged_tile_kernels_bitwise(gfb):
             o, t = gfb.forward_joint(lx, hx, ly, p)
             gr = gfb.backward(t, d)
             loss, g2, _ = gfb.joint_mse_backward(lx, hx, ly, tg, p)
+            # the plain forward entry (forward_joint takes the slope-tape one)
+            o2 = torch.empty_like(hx)
+            st = torch.zeros(1, dtype=torch.int32, device="cuda")
+            assert lib.gf_joint_fwd(0, lx.data_ptr(), ly.data_ptr(), hx.data_ptr(), o2.data_ptr(),
+                                    B, C, h, w, 4 * h, 4 * w, r, 1e-4, 0, 0, st.data_ptr(),
+                                    torch.cuda.current_stream().cuda_stream) == 0
             return [o, gr.d_guide_lo, gr.d_src, gr.d_guide_hi, g2.d_guide_lo, g2.d_src,
-                    g2.d_guide_hi, loss]
+                    g2.d_guide_hi, loss, o2]
 
         ref = run()
         old = (lib.gf_joint_fwd_variant(11), lib.gf_joint_bwd_hr_variant(11),
