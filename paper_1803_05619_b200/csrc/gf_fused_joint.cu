@@ -972,6 +972,7 @@ struct MseHrArgs {
   float eps, scale2;
   uint32_t* status;
   const float* A_tape = nullptr;  // kStageTape: the forward's low-res slopes
+  const float* B_tape = nullptr;  // ... and intercepts (MSE: k_joint_coeffs)
 };
 
 // MSE = false: the same single gather pass for a given d_out (k_joint_bwd_hr's
@@ -1054,7 +1055,7 @@ __device__ __forceinline__ void mse_hr_body(const MseHrArgs& a, const CUtensorMa
     lr_coeffs<RAD, MSE, 0, 16, kStageTma>(base, base + TG::LR, a.h, a.w, i0, k0, a.eps, sm,
                                           degen, TG::LP, TG::COFS);
   } else if constexpr (MODE == kStageTape || MODE == kStageTapeTile) {
-    static_assert(!MSE, "the tape has A only");
+    static_assert(!MSE || MODE == kStageTapeTile, "the forward's tape has A only");
     if constexpr (MODE == kStageTapeTile) {
       if (threadIdx.x == 0) tma::mbar_init(&tbar, 1);
       __syncthreads();
@@ -1068,8 +1069,10 @@ __device__ __forceinline__ void mse_hr_body(const MseHrArgs& a, const CUtensorMa
     for (int it = threadIdx.x; it < RA * CA; it += NT) {
       const int ar = it / CA, c = it - ar * CA;
       const int gy = i0 - 1 + ar, gx = k0 - 1 + c;
-      sm.As[ar * CAP + c] =
-          (gy >= 0 && gy < a.h && gx >= 0 && gx < a.w) ? __ldg(At + (int64_t)gy * a.w + gx) : 0.f;
+      const bool inimg = gy >= 0 && gy < a.h && gx >= 0 && gx < a.w;
+      const int64_t o = (int64_t)gy * a.w + gx;
+      sm.As[ar * CAP + c] = inimg ? __ldg(At + o) : 0.f;
+      if constexpr (MSE) sm.Bs[ar * CAP + c] = inimg ? __ldg(a.B_tape + p * (int64_t)a.h * a.w + o) : 0.f;
     }
     __syncthreads();
     if constexpr (MODE == kStageTapeTile) tma::mbar_wait(&tbar, 0);
@@ -1345,12 +1348,36 @@ __global__ void __launch_bounds__(NT, MINB) k_joint_mse_hr_a(MseHrArgs a) {
 }
 
 // ... with the gather window of hr_x and d_out staged by TMA (tmG, tmD:
-// (136, 68) boxes of the high-res planes)
-template <int RAD, int MINB>
+// (136, 68) boxes of the high-res planes).  MSE: the fused training step on
+// the coefficients of k_joint_coeffs (A and b), tmD over the target.
+template <int RAD, int MINB, bool MSE = false>
 __global__ void __launch_bounds__(NT, MINB)
     k_joint_mse_hr_at(const __grid_constant__ CUtensorMap tmG,
                       const __grid_constant__ CUtensorMap tmD, MseHrArgs a) {
-  mse_hr_body<RAD, false, kStageTapeTile>(a, &tmG, &tmD);
+  mse_hr_body<RAD, MSE, kStageTapeTile>(a, &tmG, &tmD);
+}
+
+// A and b of every low-res cell (the fused training step's coefficient tape):
+// the forward's coefficient phase on 16 x 32 blocks, own cells written
+template <int RAD, int VCH = 0, int HCH = 16>
+__global__ void __launch_bounds__(NT, 4) k_joint_coeffs(FwdArgs a, float* A_out, float* B_out) {
+  extern __shared__ float4 smem4[];
+  const SmemCoef sm = carve(reinterpret_cast<float*>(smem4), RAD);
+  const int64_t p = blockIdx.z;
+  const int i0 = blockIdx.y * TLY, k0 = blockIdx.x * TLX;
+  bool degen = false;
+  lr_coeffs<RAD, true, VCH, HCH>(a.lr_x + p * (int64_t)a.h * a.w, a.lr_y + p * (int64_t)a.h * a.w,
+                                 a.h, a.w, i0, k0, a.eps, sm, degen);
+  for (int it = threadIdx.x; it < TLY * TLX; it += NT) {
+    const int il = it / TLX, kl = it - il * TLX;
+    const int i = i0 + il, kk = k0 + kl;
+    if (i < a.h && kk < a.w) {
+      const int64_t o = p * (int64_t)a.h * a.w + (int64_t)i * a.w + kk;
+      A_out[o] = sm.As[(il + 1) * CAP + kl + 1];
+      B_out[o] = sm.Bs[(il + 1) * CAP + kl + 1];
+    }
+  }
+  if (degen) flag(a.status, GF_STATUS_DEGENERATE);
 }
 
 template <int RAD, int MINB, bool MSE>
@@ -1593,6 +1620,8 @@ struct JointFns {
   size_t tma_floats;  // tma_coef_floats + alignment slack
   const void* hr_pass_a;   // hr pass on the forward's tape of slopes
   const void* hr_pass_at;  // ... with the gather window staged by TMA
+  const void* coeffs;      // A, b of every low-res cell (fused step)
+  const void* mse_hr_at;   // fused step on them, gather window by TMA
 };
 
 template <int RAD>
@@ -1600,7 +1629,13 @@ static JointFns joint_fns() {
   // r >= 2: fewer, longer coefficient-pass chunks (each pays a 2r warm-up):
   // 8 column chunks per row, and 2 row chunks for r >= 5 (config 3: r = 2
   // 1352 -> 1296 us, r = 4 1419 -> 1348 us, r = 8 1571 -> 1500 us)
-  const void *fwd, *fwd_t;
+  const void *fwd, *fwd_t, *coeffs;
+  if constexpr (RAD >= 5)
+    coeffs = (const void*)jf::k_joint_coeffs<RAD, 2, 8>;
+  else if constexpr (RAD >= 2)
+    coeffs = (const void*)jf::k_joint_coeffs<RAD, 0, 8>;
+  else
+    coeffs = (const void*)jf::k_joint_coeffs<RAD>;
   if constexpr (RAD >= 5) {
     fwd = (const void*)jf::k_joint_fwd<RAD, 2, 8>;
     fwd_t = (const void*)jf::k_joint_fwd_t<RAD, 2, 8>;
@@ -1617,7 +1652,8 @@ static JointFns joint_fns() {
           (const void*)jf::k_joint_mse_hr_t<RAD, 3, true>,
           (const void*)jf::k_joint_mse_hr_t<RAD, 4, false>,
           (size_t)jf::tma_coef_floats<RAD>() + 32, (const void*)jf::k_joint_mse_hr_a<RAD, 4>,
-          (const void*)jf::k_joint_mse_hr_at<RAD, 2>};
+          (const void*)jf::k_joint_mse_hr_at<RAD, 2>, coeffs,
+          (const void*)jf::k_joint_mse_hr_at<RAD, 2, true>};
 }
 
 static JointFns pick_joint(int r) {
@@ -1849,9 +1885,11 @@ static int64_t mse_tiles(int64_t C, int64_t h, int64_t w) {
   return C * ((h + jf::TLY - 1) / jf::TLY) * ((w + jf::TLX - 1) / jf::TLX);
 }
 
+// workspace of the fused step: db, dA (lr), loss partials, then A, b (lr)
 size_t fused_joint_mse_ws_bytes(int64_t B, int64_t C, int64_t h, int64_t w) {
   const size_t f = ((size_t)2 * B * C * h * w * sizeof(float) + 255) / 256 * 256;
-  return f + (size_t)B * mse_tiles(C, h, w) * sizeof(double);
+  const size_t pt = ((size_t)B * mse_tiles(C, h, w) * sizeof(double) + 255) / 256 * 256;
+  return f + pt + (size_t)2 * B * C * h * w * sizeof(float);
 }
 
 void fused_joint_mse_bwd(const float* lr_x, const float* lr_y, const float* hr_x,
@@ -1876,8 +1914,28 @@ void fused_joint_mse_bwd(const float* lr_x, const float* lr_y, const float* hr_x
     const double per_image = (double)C * (double)H * (double)W;
     jf::MseHrArgs a{lr_x, lr_y, hr_x, target, d_hr_x, db, dA, part, (int)h, (int)w, (int)H,
                     (int)W, r, eps, (float)(2.0 / per_image / (double)B), status};
-    CUtensorMap tmX, tmY;
-    if (g_joint_mse_variant == 11 && lr_maps(&tmX, &tmY, lr_x, lr_y, B * C, h, w, r)) {
+    CUtensorMap tmX, tmY, tmG, tmT;
+    if (g_joint_mse_variant == 0 &&
+        tma::make_plane_map(&tmG, hr_x, W, H, B * C, jf::HTW, jf::HTH) &&
+        tma::make_plane_map(&tmT, target, W, H, B * C, jf::HTW, jf::HTH)) {
+      // coefficient tape (A, b of every cell), then the hr pass on it with the
+      // gather window of hr_x and the target staged by TMA
+      float* Acoef = (float*)((char*)part + ((size_t)B * mse_tiles(C, h, w) * sizeof(double) + 255) /
+                                                 256 * 256);
+      float* Bcoef = Acoef + B * C * h * w;
+      jf::FwdArgs fa{lr_x, lr_y, hr_x, nullptr, (int)h, (int)w, (int)H, (int)W, r, eps, status};
+      const size_t smc = jf::coef_smem_floats(r) * sizeof(float);
+      set_smem(fns.coeffs, smc);
+      void* cargs[] = {&fa, &Acoef, &Bcoef};
+      cudaLaunchKernel(fns.coeffs, grid, dim3(jf::NT), cargs, smc, s);
+      a.A_tape = Acoef;
+      a.B_tape = Bcoef;
+      const size_t sma =
+          128 + (2 * jf::HTF + 2 * jf::RA * jf::CAP + 2 * jf::GR * jf::TLX) * sizeof(float);
+      set_smem(fns.mse_hr_at, sma);
+      void* args[] = {&tmG, &tmT, &a};
+      cudaLaunchKernel(fns.mse_hr_at, grid, dim3(jf::NT), args, sma, s);
+    } else if (g_joint_mse_variant == 11 && lr_maps(&tmX, &tmY, lr_x, lr_y, B * C, h, w, r)) {
       const size_t smt = (fns.tma_floats + 2 * jf::GR * jf::TLX) * sizeof(float);
       set_smem(fns.mse_hr_t, smt);
       void* args[] = {&tmX, &tmY, &a};
