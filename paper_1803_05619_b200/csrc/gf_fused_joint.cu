@@ -1915,7 +1915,10 @@ void fused_joint_mse_bwd(const float* lr_x, const float* lr_y, const float* hr_x
     jf::MseHrArgs a{lr_x, lr_y, hr_x, target, d_hr_x, db, dA, part, (int)h, (int)w, (int)H,
                     (int)W, r, eps, (float)(2.0 / per_image / (double)B), status};
     CUtensorMap tmX, tmY, tmG, tmT;
-    if (g_joint_mse_variant == 0 &&
+    // variant 15: coefficient tape + TMA gather window -- measured slower than
+    // the moments-recomputing kernel at config 2 (461 vs 436 us: the extra
+    // coefficient kernel, 2 instead of 3 CTAs per SM); kept as a variant
+    if (g_joint_mse_variant == 15 &&
         tma::make_plane_map(&tmG, hr_x, W, H, B * C, jf::HTW, jf::HTH) &&
         tma::make_plane_map(&tmT, target, W, H, B * C, jf::HTW, jf::HTH)) {
       // coefficient tape (A, b of every cell), then the hr pass on it with the

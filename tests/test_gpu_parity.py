@@ -880,10 +880,11 @@ def test_tma_staged_tile_kernels_bitwise(gfb):
 @pytest.mark.parametrize("B,C,h,w,r", [(2, 3, 37, 44, 1), (1, 3, 64, 128, 2), (1, 2, 20, 36, 8),
                                        (2, 1, 5, 8, 0)])
 def test_fused_step_coefficient_tape_matches_recompute(gfb, B, C, h, w, r):
-    """The fused training step's default path (k_joint_coeffs writes A and b of
-    every low-res cell, the hr pass reads them and gets its gather window of
-    hr_x and the target by TMA) against the moments-recomputing kernel
-    (variant 3): the loss and the gradients agree to fp32 rounding."""
+    """The fused training step on a coefficient tape (variant 15:
+    k_joint_coeffs writes A and b of every low-res cell, the hr pass reads them
+    and gets its gather window of hr_x and the target by TMA) against the
+    default moments-recomputing kernel: the loss and the gradients agree to
+    fp32 rounding."""
     from paper_1803_05619_b200 import _lib
 
     lib = _lib.load()
@@ -891,10 +892,10 @@ def test_fused_step_coefficient_tape_matches_recompute(gfb, B, C, h, w, r):
     lx, ly = (torch.rand(B, C, h, w, device="cuda", generator=g) for _ in range(2))
     hx, tg = (torch.rand(B, C, 4 * h, 4 * w, device="cuda", generator=g) for _ in range(2))
     p = gfb.GuidedFilterParams(r, 1e-3)
-    l0, g0, _ = gfb.joint_mse_backward(lx, hx, ly, tg, p)
-    old = lib.gf_joint_mse_variant(3)
+    l1, g1, _ = gfb.joint_mse_backward(lx, hx, ly, tg, p)
+    old = lib.gf_joint_mse_variant(15)
     try:
-        l1, g1, _ = gfb.joint_mse_backward(lx, hx, ly, tg, p)
+        l0, g0, _ = gfb.joint_mse_backward(lx, hx, ly, tg, p)
     finally:
         lib.gf_joint_mse_variant(old)
     assert abs(float(l0) - float(l1)) <= 1e-6 * float(l1)
