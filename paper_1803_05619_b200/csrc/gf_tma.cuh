@@ -14,16 +14,17 @@ namespace tma {
 // included) are zero-filled by the hardware.
 inline bool make_plane_map(CUtensorMap* map, const float* base, int64_t W, int64_t H,
                            int64_t planes, int box_w, int box_h) {
-  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
-  if (!encode) {
+  // resolved once per process (a thread-safe function-local static)
+  static const PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
     void* fn = nullptr;
     cudaDriverEntryPointQueryResult q;
     if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) !=
             cudaSuccess ||
-        q != cudaDriverEntryPointSuccess || !fn)
-      return false;
-    encode = (PFN_cuTensorMapEncodeTiled_v12000)fn;
-  }
+        q != cudaDriverEntryPointSuccess)
+      fn = nullptr;
+    return (PFN_cuTensorMapEncodeTiled_v12000)fn;
+  }();
+  if (!encode) return false;
   const cuuint64_t dims[3] = {(cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)planes};
   const cuuint64_t strides[2] = {(cuuint64_t)W * 4, (cuuint64_t)(H * W) * 4};
   const cuuint32_t box[3] = {(cuuint32_t)box_w, (cuuint32_t)box_h, 1};
