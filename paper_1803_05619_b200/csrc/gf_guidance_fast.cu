@@ -17,6 +17,8 @@
 // reducing dW1 = sum dh1 x^T.  Every reduction is deterministic.
 #include <cuda_runtime.h>
 
+#include <algorithm>
+
 #include "gf_common.cuh"
 #include "gf_internal.h"
 #include "gf_pair.cuh"
@@ -30,6 +32,9 @@ namespace gnf {
 constexpr int CI = 3, CO = 3;
 constexpr int NT = 256;
 constexpr int kBlocks = 128;  // pixel blocks per image (grid.x)
+// the one-pass backward's blocks per image: one wave of the SM's CTA slots
+// spread over the batch (<= kBlocksH)
+constexpr int kBlocksH = 512;
 constexpr float kLeaky = 0.2f;
 constexpr double kVarFloor = 1e-5;
 constexpr int NST = 3;  // cp.async pipeline stages of the streaming passes
@@ -750,18 +755,192 @@ __global__ void __launch_bounds__(NT, 2) k_bwd_h(const float* __restrict__ x,
   reduce_store_fn<AH<HID>::nv>(get, part + (b * gridDim.x + blockIdx.x) * AH<HID>::nv);
 }
 
+// ---- the same pass with two lanes per 4-pixel group (default) --------------
+// Lane q of a group owns hidden units [q UL, q UL + UL) (a padding unit has
+// zero weights and contributes exact zeros), so every per-pixel cost -- the
+// (x, dy) loads, the D exchange and store, the loop -- is shared by UL units
+// instead of HID/4, and D needs one exchange (a reduce-scatter of its six
+// pixel pairs over the two lanes) instead of two: 488 instead of 4 x 397
+// SASS instructions per 4 pixels at hidden 15.  Both lanes load the group's
+// 96 bytes straight from global memory one iteration ahead (one request per
+// warp; the duplicate lanes coalesce).  The per-thread fp32 sums go through
+// shared memory at the end: thread v < nv adds accumulator v over the 64
+// owning threads in float64, in a fixed order.  The grid is one wave of the
+// SMs' CTA slots spread over the batch.  Measured at config 2's high-res
+// site (8 x 3 x 2048^2): whole backward 708 us vs 808 for k_bwd_h; at 232
+// registers it runs 8 warps per SM (capping it at 3 CTAs per SM spills:
+// 1021 us; staging (x, dy) by cp.async instead of registers: 836 us).
+constexpr int NT2 = 128;
+template <int HID, int MINB>
+__global__ void __launch_bounds__(NT2, MINB) k_bwd_h2(const float* __restrict__ x,
+                                                 const float* __restrict__ dy,
+                                                 float* __restrict__ D,
+                                                 const float* __restrict__ params,
+                                                 const float* __restrict__ fold,
+                                                 double* __restrict__ part, int64_t HW) {
+  constexpr int UL = (HID + 1) / 2;  // hidden units per lane
+  constexpr int NGR = NT2 / 2;       // groups per CTA
+  constexpr int NA = 7 * UL + CO;    // fp32 sums per thread
+  constexpr int NAP = NA + 1;        // shared pitch
+  // unit j = q UL + jj at [jj][q]: (W1f row, beta), (W2 column, 0)
+  __shared__ float4 sW[UL * 2], sV[UL * 2];
+  __shared__ float red[NT2 * NAP];
+  const int64_t b = blockIdx.y;
+  const float* f = fold + b * F<HID>::count;
+  for (int i = threadIdx.x; i < UL * 2; i += NT2) {
+    const int j = (i & 1) * UL + (i >> 1);
+    sW[i] = j < HID ? make_float4(f[F<HID>::w1f + j * CI], f[F<HID>::w1f + j * CI + 1],
+                                  f[F<HID>::w1f + j * CI + 2], f[F<HID>::beta + j])
+                    : make_float4(0.f, 0.f, 0.f, 0.f);
+    sV[i] = j < HID ? make_float4(params[P<HID>::w2 + j], params[P<HID>::w2 + HID + j],
+                                  params[P<HID>::w2 + 2 * HID + j], 0.f)
+                    : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  __syncthreads();
+  using namespace pr;
+  const int q = threadIdx.x & 1;
+  const int g = threadIdx.x >> 1;
+  u64 sd2[UL], sd2x[UL][CI], sdw2[CO][UL], sdy[CO];
+#pragma unroll
+  for (int jj = 0; jj < UL; ++jj) {
+    sd2[jj] = 0ull;
+#pragma unroll
+    for (int c = 0; c < CI; ++c) sd2x[jj][c] = 0ull;
+#pragma unroll
+    for (int o = 0; o < CO; ++o) sdw2[o][jj] = 0ull;
+  }
+#pragma unroll
+  for (int o = 0; o < CO; ++o) sdy[o] = 0ull;
+  const int64_t n4 = HW / 4;
+  const ulonglong2* xp[CI];
+  const ulonglong2* gp[CO];
+#pragma unroll
+  for (int c = 0; c < CI; ++c) xp[c] = reinterpret_cast<const ulonglong2*>(x + (b * CI + c) * HW);
+  u64* const dbase = reinterpret_cast<u64*>(D + b * CI * HW);
+  const int64_t HW2 = HW / 2;
+#pragma unroll
+  for (int o = 0; o < CO; ++o) gp[o] = reinterpret_cast<const ulonglong2*>(dy + (b * CO + o) * HW);
+  const int64_t stride = (int64_t)gridDim.x * NGR;
+  // a warp-uniform trip count (groups past the end read zeros and store
+  // nothing), so the pair exchange below runs converged
+  const int64_t wfirst = (int64_t)blockIdx.x * NGR + (g & ~15);
+  const int64_t iters = n4 > wfirst ? (n4 - wfirst + stride - 1) / stride : 0;
+  // the group's next (x, dy), requested one iteration ahead
+  ulonglong2 Xn[CI], Gn[CO];
+  auto fetch = [&](int64_t i) {
+    const bool ok = i < n4;
+#pragma unroll
+    for (int c = 0; c < CI; ++c) Xn[c] = ok ? __ldg(xp[c] + i) : make_ulonglong2(0ull, 0ull);
+#pragma unroll
+    for (int o = 0; o < CO; ++o) Gn[o] = ok ? __ldg(gp[o] + i) : make_ulonglong2(0ull, 0ull);
+  };
+  const int64_t first = (int64_t)blockIdx.x * NGR + g;
+  fetch(first);
+  for (int64_t it = 0; it < iters; ++it) {
+    const int64_t i = first + it * stride;
+    ulonglong2 X[CI], G[CO];
+#pragma unroll
+    for (int c = 0; c < CI; ++c) X[c] = Xn[c];
+#pragma unroll
+    for (int o = 0; o < CO; ++o) G[o] = Gn[o];
+    fetch(i + stride);
+#pragma unroll
+    for (int o = 0; o < CO; ++o) sdy[o] = add2(sdy[o], add2(G[o].x, G[o].y));
+    u64 dv[CI][2];
+#pragma unroll
+    for (int c = 0; c < CI; ++c) dv[c][0] = dv[c][1] = 0ull;
+#pragma unroll
+    for (int jj = 0; jj < UL; ++jj) {
+      const float4 wv = sW[jj * 2 + q], vv = sV[jj * 2 + q];
+      const u64 a0 = bc(wv.x), a1 = bc(wv.y), a2 = bc(wv.z), be = bc(wv.w);
+      const u64 v0 = bc(vv.x), v1 = bc(vv.y), v2 = bc(vv.z);
+#pragma unroll
+      for (int pp = 0; pp < 2; ++pp) {
+        const u64 x0 = pp ? X[0].y : X[0].x, x1 = pp ? X[1].y : X[1].x,
+                  x2 = pp ? X[2].y : X[2].x;
+        const u64 g0 = pp ? G[0].y : G[0].x, g1 = pp ? G[1].y : G[1].x,
+                  g2 = pp ? G[2].y : G[2].x;
+        const u64 h2 = fma2(a2, x2, fma2(a1, x1, fma2(a0, x0, be)));  // (alpha .* W1) x + beta
+        const u64 sl = slope2(h2, kLeaky);
+        const u64 h3 = mul2(h2, sl);
+        const u64 d2 = mul2(fma2(v2, g2, fma2(v1, g1, mul2(v0, g0))), sl);
+        sd2[jj] = add2(sd2[jj], d2);
+        sd2x[jj][0] = fma2(d2, x0, sd2x[jj][0]);
+        sd2x[jj][1] = fma2(d2, x1, sd2x[jj][1]);
+        sd2x[jj][2] = fma2(d2, x2, sd2x[jj][2]);
+        sdw2[0][jj] = fma2(g0, h3, sdw2[0][jj]);
+        sdw2[1][jj] = fma2(g1, h3, sdw2[1][jj]);
+        sdw2[2][jj] = fma2(g2, h3, sdw2[2][jj]);
+        dv[0][pp] = fma2(a0, d2, dv[0][pp]);
+        dv[1][pp] = fma2(a1, d2, dv[1][pp]);
+        dv[2][pp] = fma2(a2, d2, dv[2][pp]);
+      }
+    }
+    // D: pixel pair k = 2c + pp; lane 0 finishes k = 0..2, lane 1 k = 3..5
+#pragma unroll
+    for (int m = 0; m < 3; ++m) {
+      const int k0 = m, k1 = m + 3;
+      const u64 mine = q ? dv[k1 >> 1][k1 & 1] : dv[k0 >> 1][k0 & 1];
+      const u64 send = q ? dv[k0 >> 1][k0 & 1] : dv[k1 >> 1][k1 & 1];
+      const u64 o = add2(mine, __shfl_xor_sync(0xffffffffu, send, 1));
+      const int k = q ? k1 : k0;
+      if (i < n4) dbase[(k >> 1) * HW2 + 2 * i + (k & 1)] = o;
+    }
+  }
+  // per-thread sums -> shared -> float64 over the 64 threads of each lane parity
+  {
+    float* row = red + threadIdx.x * NAP;
+    auto sum2 = [](u64 v) { return lo(v) + hi(v); };
+#pragma unroll
+    for (int jj = 0; jj < UL; ++jj) {
+      row[jj] = sum2(sd2[jj]);
+#pragma unroll
+      for (int c = 0; c < CI; ++c) row[UL + jj * CI + c] = sum2(sd2x[jj][c]);
+#pragma unroll
+      for (int o = 0; o < CO; ++o) row[4 * UL + o * UL + jj] = sum2(sdw2[o][jj]);
+    }
+#pragma unroll
+    for (int o = 0; o < CO; ++o) row[7 * UL + o] = q == 0 ? sum2(sdy[o]) : 0.f;
+  }
+  __syncthreads();
+  constexpr int NV = AH<HID>::nv;
+  double* out = part + (b * gridDim.x + blockIdx.x) * NV;
+  for (int v = threadIdx.x; v < NV; v += NT2) {
+    int slot, qq;
+    if (v >= AH<HID>::dw2) {
+      const int u = v - AH<HID>::dw2, o = u / HID, j = u - o * HID;
+      qq = j / UL;
+      slot = 4 * UL + o * UL + (j - qq * UL);
+    } else if (v >= AH<HID>::dy) {
+      qq = 0;
+      slot = 7 * UL + (v - AH<HID>::dy);
+    } else if (v >= AH<HID>::d2x) {
+      const int u = v - AH<HID>::d2x, j = u / CI, c = u - j * CI;
+      qq = j / UL;
+      slot = UL + (j - qq * UL) * CI + c;
+    } else {
+      qq = v / UL;
+      slot = v - qq * UL;
+    }
+    double s = 0.0;
+    for (int t = qq; t < NT2; t += 2) s += (double)red[t * NAP + slot];
+    out[v] = s;
+  }
+}
+
 // ---- per image: kappa, lambda -> K, L and the parameter-gradient sums ------
 template <int HID>
 __global__ void k_fin_h(const double* __restrict__ part, const double* __restrict__ stats,
                         const float* __restrict__ params, const float* __restrict__ fold,
-                        float* __restrict__ kl, double* __restrict__ gsum, int64_t HW, int nblk) {
+                        float* __restrict__ kl, double* __restrict__ gsum, int64_t HW, int nblk,
+                        int nblk_h) {
   constexpr int NV = AH<HID>::nv;
   const int b = blockIdx.x;
   __shared__ double S[NV], X[9], kap[HID], lam[HID];
   for (int v = threadIdx.x; v < NV + 9; v += blockDim.x) {
     double s = 0.0;
     if (v < NV)
-      for (int k = 0; k < nblk; ++k) s += part[((int64_t)b * nblk + k) * NV + v];
+      for (int k = 0; k < nblk_h; ++k) s += part[((int64_t)b * nblk_h + k) * NV + v];
     else
       for (int k = 0; k < nblk; ++k) s += stats[((int64_t)b * nblk + k) * 9 + (v - NV)];
     if (v < NV)
@@ -886,7 +1065,7 @@ struct WS {
     const size_t coef = (size_t)B * 2 * HID * sizeof(float);
     const size_t gsum = (size_t)B * (CO * HID + CO + 2) * sizeof(double);
     const size_t pb = (size_t)B * kBlocks * HID * CI * sizeof(double);
-    const size_t ph = (size_t)B * kBlocks * AH<HID>::nv * sizeof(double);
+    const size_t ph = (size_t)B * kBlocksH * AH<HID>::nv * sizeof(double);
     const size_t kl = (size_t)B * KL * sizeof(float);
     const size_t gh = (size_t)B * GH<HID>::count * sizeof(double);
     return stats + fold + pa + coef + gsum + pb + ph + kl + gh + 9 * 256;
@@ -926,7 +1105,7 @@ void backward(const float* x, const float* dy, float* dx, float* dparams, int ac
   float* coef = c.take<float>((size_t)B * 2 * HID);
   double* gsum = c.take<double>((size_t)B * (CO * HID + CO + 2));
   double* pb = c.take<double>((size_t)B * kBlocks * HID * CI);
-  double* ph = c.take<double>((size_t)B * kBlocks * AH<HID>::nv);
+  double* ph = c.take<double>((size_t)B * kBlocksH * AH<HID>::nv);
   float* kl = c.take<float>((size_t)B * KL);
   double* gh = c.take<double>((size_t)B * GH<HID>::count);
   dim3 grid(kBlocks, (unsigned)B);
@@ -934,9 +1113,26 @@ void backward(const float* x, const float* dy, float* dx, float* dparams, int ac
     k_stats<<<grid, NT, 0, s>>>(x, stats, HW, status);
     k_prep<HID><<<(unsigned)B, 32, 0, s>>>(stats, params, fold, HW, kBlocks);
   }
-  if (g_gn_bwd_variant == 0) {  // one heavy pass (default)
-    k_bwd_h<HID><<<grid, NT, 0, s>>>(x, dy, dx, params, fold, ph, HW);
-    k_fin_h<HID><<<(unsigned)B, 128, 0, s>>>(ph, stats, params, fold, kl, gh, HW, kBlocks);
+  if (g_gn_bwd_variant != 1) {  // one heavy pass (default)
+    // 0: two lanes per pixel group (k_bwd_h2); 2: four lanes (k_bwd_h, the
+    // round-1 kernel); 3: k_bwd_h2 capped at 3 CTAs per SM (spills)
+    const bool two = g_gn_bwd_variant != 2;
+    const void* fn = g_gn_bwd_variant == 3   ? (const void*)k_bwd_h2<HID, 3>
+                     : g_gn_bwd_variant == 2 ? (const void*)k_bwd_h<HID>
+                                             : (const void*)k_bwd_h2<HID, 2>;
+    const int nt = two ? NT2 : NT;
+    const LaunchCfg lc = launch_cfg(fn, nt, 0);
+    const int64_t slots = (int64_t)lc.sms * lc.per_sm;
+    const int nbh = (int)std::min<int64_t>(kBlocksH, std::max<int64_t>(1, slots / B));
+    const dim3 gh_grid((unsigned)nbh, (unsigned)B);
+    if (two) {
+      void* args[] = {(void*)&x, (void*)&dy, (void*)&dx, (void*)&params, (void*)&fold,
+                      (void*)&ph, (void*)&HW};
+      cudaLaunchKernel(fn, gh_grid, dim3(NT2), args, 0, s);
+    }
+    else
+      k_bwd_h<HID><<<gh_grid, NT, 0, s>>>(x, dy, dx, params, fold, ph, HW);
+    k_fin_h<HID><<<(unsigned)B, 128, 0, s>>>(ph, stats, params, fold, kl, gh, HW, kBlocks, nbh);
     k_dx<<<grid, NT, 0, s>>>(x, dx, kl, HW);
     k_fin_params_h<HID><<<1, 128, 0, s>>>(gh, dparams, accumulate, B);
     return;

@@ -89,7 +89,9 @@ extern thread_local int g_joint_lr_variant;
 extern thread_local int g_joint_fwd_variant;  // r = 8 coefficient chunking (test hook)
 extern thread_local int g_joint_mse_variant;
 extern thread_local int g_joint_bwd_hr_variant;  // 0 single gather pass, 1 tile kernel, 3: 3 CTAs/SM
-extern thread_local int g_gn_bwd_variant;  // fused guidance backward: 0 one heavy pass, 1 two  // fused step hr kernel: 0 auto, 2/4 CTAs per SM (r = 1)
+extern thread_local int g_gn_bwd_variant;  // fused guidance backward: 0 one heavy pass (2 lanes per
+                                           // pixel group), 1 two passes, 2 one pass with 4 lanes,
+                                           // 3 = 0 capped at 3 CTAs per SM
 bool fused_joint_ok(int64_t B, int64_t C, int64_t h, int64_t w, int64_t H, int64_t W, int r);
 void fused_joint_fwd(const float* lr_x, const float* lr_y, const float* hr_x, float* out,
                      int64_t B, int64_t C, int64_t h, int64_t w, int64_t H, int64_t W, int r,

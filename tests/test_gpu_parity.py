@@ -738,10 +738,12 @@ def test_highres_kernel_variants_status(gfb, variant, r):
         lib.gf_highres_variant(old)
 
 
-@pytest.mark.parametrize("variant", [0, 1])
+@pytest.mark.parametrize("variant", [0, 1, 2, 3])
 def test_fused_guidance_backward_variants_vs_oracle(gfb, variant):
     """The one-heavy-pass backward (variant 0, dx = D + K + L x, dW1 from the
-    x moments) and the two-pass kernels (1) against the oracle at a
+    x moments, two lanes per pixel group; 2: four lanes per group, the
+    round-1 kernel; 3: variant 0 capped at 3 CTAs per SM) and the two-pass
+    kernels (1) against the oracle at a
     config-2-like image (smooth [0,1] input, small upstream gradient); every
     parameter gradient against its own largest entry."""
     import workloads
