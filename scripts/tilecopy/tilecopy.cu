@@ -1,9 +1,9 @@
 // Microbenchmark: DRAM efficiency of tile-shaped streaming (read a TH x TW
+// fp32 tile, write it back elsewhere) vs a linear copy, on 3072-wide planes.
 // Measured (B200, gpurun_out/tc): every tile shape 64x128 .. 8x1024 copies at
 // 6.78-6.84 TB/s, a grid-stride linear copy at 6.12 TB/s -- the joint
 // kernels' 64 x 128 hr tiles cost no DRAM efficiency.
 // Build: nvcc -O3 -gencode arch=compute_100a,code=sm_100a -o tilecopy tilecopy.cu
-// fp32 tile, write it back elsewhere) vs a linear copy, on 3072-wide planes.
 #include <cstdio>
 #include <cuda_runtime.h>
 
