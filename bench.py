@@ -269,7 +269,8 @@ class OursStep:
             else:  # forward keeping the tape's slopes, backward on them (forward_joint/backward)
                 rc = L.gf_joint_fwd_tape(0, lx.data_ptr(), ly.data_ptr(), hx.data_ptr(),
                                          self.out.data_ptr(), self.slope.data_ptr(), B, C, h, w,
-                                         Hh, Ww, r, eps, self.status.data_ptr(), self.sp)
+                                         Hh, Ww, r, eps, self.ws.data_ptr(), self.ws.numel(),
+                                         self.status.data_ptr(), self.sp)
                 assert rc == 0, L.gf_last_error()
                 rc = L.gf_joint_bwd_tape(0, lx.data_ptr(), ly.data_ptr(), hx.data_ptr(),
                                          self.slope.data_ptr(), self.d_out.data_ptr(),

@@ -121,6 +121,29 @@ int gf_joint_bwd_band(int dtype, const void* lr_x, const void* lr_y, const void*
                       double eps, int64_t row0, void* workspace, size_t workspace_bytes,
                       uint32_t* status, void* stream);
 
+/* The two kernels of the fast forward, callable on their own (fp32 calls
+ * gf_joint_is_fused accepts, 16-byte aligned buffers; else
+ * GF_ERR_UNSUPPORTED).  gf_joint_coeffs: the window moments and the slope
+ * A = cov / (var + eps) and intercept b = mean_y - A mean_x of EVERY low-res
+ * cell (gf/guided.py:136-149, :170-173) -> slope_lo, intercept_lo (B, C, h, w).
+ * gf_joint_apply: out = Up(intercept_lo) + Up(slope_lo) * hr_x, the bilinear
+ * resize of both and the affine combine in one pass over hr_x
+ * (gf/guided.py:174-178, gf/_kernels.py:104-124).  gf_joint_fwd on large
+ * images is exactly this pair with the coefficients in its workspace. */
+/* B*C*H*W from which gf_joint_fwd / gf_joint_fwd_tape (given a workspace)
+ * run as this pair.  gf_joint_fwd_mode sets the choice for the CALLING THREAD
+ * and returns the old one: 0 by size, 1 the one-kernel tile forward, 2 the
+ * two-kernel forward (a row band passes the choice of its full image, so
+ * band results stay bitwise the image's). */
+int64_t gf_joint_split_threshold(void);
+int gf_joint_fwd_mode(int mode);
+int gf_joint_coeffs(int dtype, const void* lr_x, const void* lr_y, void* slope_lo,
+                    void* intercept_lo, int64_t B, int64_t C, int64_t h, int64_t w, int radius,
+                    double eps, uint32_t* status, void* stream);
+int gf_joint_apply(int dtype, const void* slope_lo, const void* intercept_lo, const void* hr_x,
+                   void* out, int64_t B, int64_t C, int64_t h, int64_t w, int64_t H, int64_t W,
+                   uint32_t* status, void* stream);
+
 /* Tape variants of the fast path (calls gf_joint_is_fused accepts, 16-byte
  * aligned buffers; anything else returns GF_ERR_UNSUPPORTED and computes
  * nothing -- use gf_joint_fwd / gf_joint_bwd).  gf_joint_fwd_tape also writes
@@ -129,10 +152,13 @@ int gf_joint_bwd_band(int dtype, const void* lr_x, const void* lr_y, const void*
  * gf_joint_bwd_tape reads it back, so its high-res pass streams hr_x and
  * d_out without recomputing window moments (the low-res tail still does);
  * row0 as gf_joint_bwd_band.  Results equal gf_joint_bwd's to fp32
- * rounding (a tile's halo slopes come from the neighbouring tile). */
+ * rounding (a tile's halo slopes come from the neighbouring tile).
+ * gf_joint_fwd_tape's workspace (gf_joint_workspace_bytes; may be NULL) lets
+ * large images take the two-kernel forward, the intercepts in the workspace. */
 int gf_joint_fwd_tape(int dtype, const void* lr_x, const void* lr_y, const void* hr_x, void* out,
                       void* slope_lo, int64_t B, int64_t C, int64_t h, int64_t w, int64_t H,
-                      int64_t W, int radius, double eps, uint32_t* status, void* stream);
+                      int64_t W, int radius, double eps, void* workspace, size_t workspace_bytes,
+                      uint32_t* status, void* stream);
 
 int gf_joint_bwd_tape(int dtype, const void* lr_x, const void* lr_y, const void* hr_x,
                       const void* slope_lo, const void* d_out, void* d_lr_x, void* d_lr_y,

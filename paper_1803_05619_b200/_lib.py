@@ -35,8 +35,12 @@ SIGNATURES = {
                           _i, _d, _p, _sz, _p, _p]),
     "gf_joint_bwd_band": (_i, [_i, _p, _p, _p, _p, _p, _p, _p, _i64, _i64, _i64, _i64, _i64,
                                _i64, _i, _d, _i64, _p, _sz, _p, _p]),
+    "gf_joint_split_threshold": (_i64, []),
+    "gf_joint_fwd_mode": (_i, [_i]),
+    "gf_joint_coeffs": (_i, [_i, _p, _p, _p, _p, _i64, _i64, _i64, _i64, _i, _d, _p, _p]),
+    "gf_joint_apply": (_i, [_i, _p, _p, _p, _p, _i64, _i64, _i64, _i64, _i64, _i64, _p, _p]),
     "gf_joint_fwd_tape": (_i, [_i, _p, _p, _p, _p, _p, _i64, _i64, _i64, _i64, _i64, _i64, _i,
-                               _d, _p, _p]),
+                               _d, _p, _sz, _p, _p]),
     "gf_joint_bwd_tape": (_i, [_i, _p, _p, _p, _p, _p, _p, _p, _p, _i64, _i64, _i64, _i64,
                                _i64, _i64, _i, _d, _i64, _p, _sz, _p, _p]),
     "gf_highres_workspace_bytes": (_sz, [_i, _i64, _i64, _i64, _i64, _i64, _i]),

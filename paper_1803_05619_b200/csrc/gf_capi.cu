@@ -273,8 +273,14 @@ int gf_joint_fwd(int dtype, const void* lr_x, const void* lr_y, const void* hr_x
   if (int e = check_joint(dtype, B, C, h, w, H, W, radius, eps)) return e;
   if (use_fused_joint(dtype, B, C, h, w, H, W, radius) && aligned16(lr_x) && aligned16(lr_y) &&
       aligned16(hr_x) && aligned16(out)) {
+    // the two-kernel forward keeps A, b of every cell in the workspace when the
+    // caller passed one of gf_joint_workspace_bytes
+    float* coef_ws = workspace && aligned16(workspace) &&
+                             workspace_bytes >= gfb::fused_joint_bwd_ws_bytes(B, C, h, w)
+                         ? (float*)workspace
+                         : nullptr;
     gfb::fused_joint_fwd((const float*)lr_x, (const float*)lr_y, (const float*)hr_x, (float*)out,
-                         B, C, h, w, H, W, radius, (float)eps, status, S(stream));
+                         B, C, h, w, H, W, radius, (float)eps, status, S(stream), nullptr, coef_ws);
     return check_launch("gf_joint_fwd[fused]");
   }
   // general kernels (unaligned buffers, fp64, other shapes)
@@ -293,15 +299,55 @@ int gf_joint_fwd(int dtype, const void* lr_x, const void* lr_y, const void* hr_x
   return check_launch("gf_joint_fwd");
 }
 
+int64_t gf_joint_split_threshold(void) { return gfb::kJointSplitElems; }
+
+int gf_joint_fwd_mode(int mode) {
+  const int v = gfb::g_joint_fwd_variant;
+  const int old = v == 19 ? 1 : (v == 20 ? 2 : 0);
+  gfb::g_joint_fwd_variant = mode == 1 ? 19 : (mode == 2 ? 20 : 0);
+  return old;
+}
+
+int gf_joint_coeffs(int dtype, const void* lr_x, const void* lr_y, void* slope_lo,
+                    void* intercept_lo, int64_t B, int64_t C, int64_t h, int64_t w, int radius,
+                    double eps, uint32_t* status, void* stream) {
+  if (int e = check_joint(dtype, B, C, h, w, 4 * h, 4 * w, radius, eps)) return e;
+  if (!(use_fused_joint(dtype, B, C, h, w, 4 * h, 4 * w, radius) && aligned16(lr_x) &&
+        aligned16(lr_y) && aligned16(slope_lo) && aligned16(intercept_lo)))
+    return fail(GF_ERR_UNSUPPORTED, "gf_joint_coeffs: not a fused-path call (use gf_joint_fwd)");
+  gfb::fused_joint_coeffs((const float*)lr_x, (const float*)lr_y, (float*)slope_lo,
+                          (float*)intercept_lo, B * C, h, w, radius, (float)eps, status, S(stream));
+  return check_launch("gf_joint_coeffs");
+}
+
+int gf_joint_apply(int dtype, const void* slope_lo, const void* intercept_lo, const void* hr_x,
+                   void* out, int64_t B, int64_t C, int64_t h, int64_t w, int64_t H, int64_t W,
+                   uint32_t* status, void* stream) {
+  if (int e = check_joint(dtype, B, C, h, w, H, W, 0, 1.0)) return e;
+  if (!(use_fused_joint(dtype, B, C, h, w, H, W, 0) && aligned16(slope_lo) &&
+        aligned16(intercept_lo) && aligned16(hr_x) && aligned16(out)))
+    return fail(GF_ERR_UNSUPPORTED, "gf_joint_apply: not a fused-path call (use gf_joint_fwd)");
+  gfb::joint_apply((const float*)slope_lo, (const float*)intercept_lo, (const float*)hr_x,
+                   (float*)out, B * C, h, w, H, W, status, S(stream));
+  return check_launch("gf_joint_apply");
+}
+
 int gf_joint_fwd_tape(int dtype, const void* lr_x, const void* lr_y, const void* hr_x, void* out,
                       void* slope_lo, int64_t B, int64_t C, int64_t h, int64_t w, int64_t H,
-                      int64_t W, int radius, double eps, uint32_t* status, void* stream) {
+                      int64_t W, int radius, double eps, void* workspace, size_t workspace_bytes,
+                      uint32_t* status, void* stream) {
   if (int e = check_joint(dtype, B, C, h, w, H, W, radius, eps)) return e;
   if (!(use_fused_joint(dtype, B, C, h, w, H, W, radius) && aligned16(lr_x) && aligned16(lr_y) &&
         aligned16(hr_x) && aligned16(out) && slope_lo))
     return fail(GF_ERR_UNSUPPORTED, "gf_joint_fwd_tape: not a fused-path call (use gf_joint_fwd)");
+  // intercepts of the two-kernel forward (the slopes go to the tape)
+  float* coef_ws = workspace && aligned16(workspace) &&
+                           workspace_bytes >= (size_t)B * C * h * w * sizeof(float)
+                       ? (float*)workspace
+                       : nullptr;
   gfb::fused_joint_fwd((const float*)lr_x, (const float*)lr_y, (const float*)hr_x, (float*)out, B,
-                       C, h, w, H, W, radius, (float)eps, status, S(stream), (float*)slope_lo);
+                       C, h, w, H, W, radius, (float)eps, status, S(stream), (float*)slope_lo,
+                       coef_ws);
   return check_launch("gf_joint_fwd_tape");
 }
 

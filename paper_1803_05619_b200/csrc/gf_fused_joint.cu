@@ -33,14 +33,11 @@
 #include "gf_common.cuh"
 #include "gf_internal.h"
 #include "gf_tma.cuh"
+#include "gf_joint_taps.cuh"
 
 namespace gfb {
 namespace jf {
 
-constexpr int TLY = 16, TLX = 32;      // low-res block of the hr kernels
-constexpr int THY = 4 * TLY, THX = 4 * TLX;
-constexpr int NT = 256;
-constexpr int RA = TLY + 2, CA = TLX + 2;  // coefficient cells incl. bilinear halo
 // shared pitches: rows of the horizontal pass are 16 lanes apart and start 16
 // banks apart (pitch = 16 mod 32), so two rows per warp never share a bank
 __host__ __device__ constexpr int pitch16(int n) { return n + ((48 - n % 32) % 32); }
@@ -51,24 +48,6 @@ __device__ __forceinline__ int wlen(int i, int n, int r) {
   int a = i - r < 0 ? 0 : i - r;
   int b = i + r > n - 1 ? n - 1 : i + r;
   return b - a + 1;
-}
-
-// factor-4 half-pixel tap of hr coordinate d into an axis of n low-res cells:
-// s = (d + 0.5)/4 - 0.5 = (2d - 3)/8 exactly, clamped (gf/filters.py:126-131)
-struct Tap {
-  int lo, hi;
-  float f;
-};
-__device__ __forceinline__ Tap tap4(int d, int n) {
-  float s = (float)(2 * d - 3) * 0.125f;
-  const float top = (float)(n - 1);
-  s = s < 0.f ? 0.f : (s > top ? top : s);
-  Tap t;
-  t.lo = (int)floorf(s);
-  if (t.lo > n - 1) t.lo = n - 1;
-  t.f = s - (float)t.lo;
-  t.hi = t.lo + 1 > n - 1 ? n - 1 : t.lo + 1;
-  return t;
 }
 
 struct SmemCoef {
@@ -289,47 +268,6 @@ struct FwdArgs {
   float* A_tape = nullptr;  // optional: the low-res slope A of every cell (the tape)
 };
 
-// Horizontal pre-interpolation of one coefficient row for the 4 hr phases of
-// lr cell column (k0 + lane): taps into local columns.
-struct ColTaps {
-  int lo[4], hi[4];
-  float f[4];
-};
-
-__device__ __forceinline__ ColTaps col_taps(int X0, int w, int k0) {
-  ColTaps t;
-#pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    Tap tp = tap4(X0 + j, w);
-    t.lo[j] = tp.lo - (k0 - 1);
-    t.hi[j] = tp.hi - (k0 - 1);
-    t.f[j] = tp.f;
-  }
-  return t;
-}
-
-// Interior lr columns (1 <= k <= w-2): the factor-4 half-pixel taps are
-// static -- phases 0, 1 between cells k-1 and k (f = 5/8, 7/8), phases 2, 3
-// between k and k+1 (f = 1/8, 3/8); local column of cell k-1 is the lane.
-// Same arithmetic as hrow with the exact taps (bit-identical).
-__device__ __forceinline__ void hrow_interior(const float* __restrict__ row, int lane,
-                                              float (&o)[4]) {
-  const float a0 = row[lane], a1 = row[lane + 1], a2 = row[lane + 2];
-  o[0] = a0 + 0.625f * (a1 - a0);
-  o[1] = a0 + 0.875f * (a1 - a0);
-  o[2] = a1 + 0.125f * (a2 - a1);
-  o[3] = a1 + 0.375f * (a2 - a1);
-}
-
-__device__ __forceinline__ void hrow(const float* __restrict__ row, const ColTaps& ct,
-                                     float (&o)[4]) {
-#pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    const float a = row[ct.lo[j]];
-    o[j] = a + ct.f[j] * (row[ct.hi[j]] - a);
-  }
-}
-
 template <int RAD, int VCH = 0, int HCH = 16>
 __global__ void __launch_bounds__(NT, (RAD >= 2 && RAD <= 4) ? 4 : 3) k_joint_fwd(FwdArgs a) {
   extern __shared__ float4 smem4[];
@@ -502,7 +440,7 @@ inline size_t fwd_tma_smem_bytes() {
 
 // out = Up(b) + Up(A) * g for the 8 hr rows (Yb .. Yb+7) x 4 columns (X0 ..)
 // of this thread, coefficients in sm.As / sm.Bs (k_joint_fwd's step 3)
-template <int RAD>
+template <int RAD, int CAP = jf::CAP>  // CAP: row pitch of sm.As / sm.Bs
 __device__ __forceinline__ bool apply_rows(const SmemCoef& sm, const float4 (&g)[8], float* O,
                                            int h, int w, int H, int W, int i0, int k0,
                                            int lane, int warp) {
@@ -1761,12 +1699,59 @@ static bool lr_maps(CUtensorMap* tmX, CUtensorMap* tmY, const float* lr_x, const
          tma::make_plane_map(tmY, lr_y, w, h, P, LP, RI);
 }
 
+// A, b of every low-res cell: the register-segment walk (r <= 8, w % 4 == 0),
+// else the tile kernel's coefficient phase on 16 x 32 blocks
+void fused_joint_coeffs(const float* lr_x, const float* lr_y, float* A, float* B, int64_t P,
+                        int64_t h, int64_t w, int r, float eps, uint32_t* status, cudaStream_t s) {
+  const int v = g_joint_fwd_variant;
+  if (v != 21 && seg_joint_coeffs_ok(h, w, r)) {
+    g_joint_coeffs_sw = v == 22 ? 8 : 0;
+    seg_joint_coeffs(lr_x, lr_y, A, B, P, h, w, r, eps, status, s);
+    return;
+  }
+  const JointFns fns = pick_joint(r);
+  dim3 grid((unsigned)((w + jf::TLX - 1) / jf::TLX), (unsigned)((h + jf::TLY - 1) / jf::TLY),
+            (unsigned)P);
+  jf::FwdArgs fa{lr_x, lr_y, nullptr, nullptr, (int)h, (int)w, (int)(4 * h), (int)(4 * w), r, eps,
+                 status};
+  const size_t smc = jf::coef_smem_floats(r) * sizeof(float);
+  set_smem(fns.coeffs, smc);
+  void* cargs[] = {&fa, &A, &B};
+  cudaLaunchKernel(fns.coeffs, grid, dim3(jf::NT), cargs, smc, s);
+}
+
+// Two-kernel forward: coefficients of every cell (A into the tape when one is
+// kept, else into the workspace), then the high-res apply pass on them.
+static void fused_joint_fwd_split(const float* lr_x, const float* lr_y, const float* hr_x,
+                                  float* out, int64_t P, int64_t h, int64_t w, int64_t H,
+                                  int64_t W, int r, float eps, uint32_t* status, cudaStream_t s,
+                                  float* A_tape, float* coef_ws) {
+  float* Bc = coef_ws;
+  float* Ac = A_tape ? A_tape : coef_ws + P * h * w;
+  fused_joint_coeffs(lr_x, lr_y, Ac, Bc, P, h, w, r, eps, status, s);
+  const int v = g_joint_fwd_variant;
+  g_joint_apply_variant = v == 23 || v == 25 || v == 26 ? v - 20 : 0;
+  joint_apply(Ac, Bc, hr_x, out, P, h, w, H, W, status, s);
+}
+
 void fused_joint_fwd(const float* lr_x, const float* lr_y, const float* hr_x, float* out, int64_t B,
                      int64_t C, int64_t h, int64_t w, int64_t H, int64_t W, int r, float eps,
-                     uint32_t* status, cudaStream_t s, float* A_tape) {
+                     uint32_t* status, cudaStream_t s, float* A_tape, float* coef_ws) {
   if (!A_tape && fused_joint_fwd_tma(lr_x, lr_y, hr_x, out, B * C, h, w, H, W, r, eps, status, s))
     return;
   const JointFns fns = pick_joint(r);
+  // Large calls (>= 48 M high-res elements; measured break-even ~ one 3 x 3072^2
+  // image) take the two-kernel forward when the caller gave a workspace for
+  // the coefficients.  Variant hook: 19 forces the one-kernel tile forward,
+  // 20..29 force the split (21 tile-kernel coefficients, 22 8 columns per lane,
+  // 23/25/26 CTAs per SM of the apply pass).
+  const int fv = g_joint_fwd_variant;
+  const bool big = B * C * H * W >= kJointSplitElems;
+  if (coef_ws && ((fv == 0 && big) || (fv >= 20 && fv < 30))) {
+    fused_joint_fwd_split(lr_x, lr_y, hr_x, out, B * C, h, w, H, W, r, eps, status, s, A_tape,
+                          coef_ws);
+    return;
+  }
   CUtensorMap tmX, tmY;
   if (!A_tape && g_joint_fwd_variant == 11 && lr_maps(&tmX, &tmY, lr_x, lr_y, B * C, h, w, r)) {
     jf::FwdArgs a{lr_x, lr_y, hr_x, out, (int)h, (int)w, (int)H, (int)W, r, eps, status};

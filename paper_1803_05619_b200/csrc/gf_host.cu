@@ -280,7 +280,8 @@ int gf_joint_fwd_bwd_host(int dtype, const void* lr_x, const void* lr_y, const v
                       [&](const void* const* d, void* const* o, cudaStream_t s) {
                         if (tape) {
                           if (int e = gf_joint_fwd_tape(dtype, d[0], d[1], d[2], o[0], slope, 1,
-                                                        1, h, w, H, W, radius, eps, st_dev, s))
+                                                        1, h, w, H, W, radius, eps, gws,
+                                                        gws_bytes, st_dev, s))
                             return e;
                           return gf_joint_bwd_tape(dtype, d[0], d[1], d[2], slope, d[3], o[1],
                                                    o[2], o[3], 1, 1, h, w, H, W, radius, eps, 0,

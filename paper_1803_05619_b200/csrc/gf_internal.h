@@ -95,7 +95,24 @@ extern thread_local int g_gn_bwd_variant;  // fused guidance backward: 0 one hea
 bool fused_joint_ok(int64_t B, int64_t C, int64_t h, int64_t w, int64_t H, int64_t W, int r);
 void fused_joint_fwd(const float* lr_x, const float* lr_y, const float* hr_x, float* out,
                      int64_t B, int64_t C, int64_t h, int64_t w, int64_t H, int64_t W, int r,
-                     float eps, uint32_t* status, cudaStream_t s, float* A_tape = nullptr);
+                     float eps, uint32_t* status, cudaStream_t s, float* A_tape = nullptr,
+                     float* coef_ws = nullptr);  // coef_ws: 2 B C h w floats (A, b of every cell)
+// second kernel of the two-kernel forward (gf_joint_apply.cu): out = Up(B) + Up(A) hr_x
+void joint_apply(const float* A, const float* B, const float* hr_x, float* out, int64_t P,
+                 int64_t h, int64_t w, int64_t H, int64_t W, uint32_t* status, cudaStream_t s);
+extern thread_local int g_joint_apply_variant;
+// high-res elements (B C H W) from which gf_joint_fwd takes the two-kernel forward
+constexpr int64_t kJointSplitElems = (int64_t)48 << 20;
+// first kernel of the two-kernel forward, register-segment walk for r <= 8,
+// w % 4 == 0 (gf_joint_coeffs_seg.cu): A, b of every low-res cell
+bool seg_joint_coeffs_ok(int64_t h, int64_t w, int r);
+void seg_joint_coeffs(const float* lr_x, const float* lr_y, float* A, float* B, int64_t P,
+                      int64_t h, int64_t w, int r, float eps, uint32_t* status, cudaStream_t s);
+extern thread_local int g_joint_coeffs_sw;
+// A, b of every low-res cell: the segment walk where it applies, else the
+// tile kernel (gf_fused_joint.cu)
+void fused_joint_coeffs(const float* lr_x, const float* lr_y, float* A, float* B, int64_t P,
+                        int64_t h, int64_t w, int r, float eps, uint32_t* status, cudaStream_t s);
 size_t fused_joint_bwd_ws_bytes(int64_t B, int64_t C, int64_t h, int64_t w);
 void fused_joint_bwd(const float* lr_x, const float* lr_y, const float* hr_x, const float* d_out,
                      float* d_lr_x, float* d_lr_y, float* d_hr_x, int64_t B, int64_t C,

@@ -151,13 +151,15 @@ def _same_dtype(*imgs: Img):
 
 
 def forward_joint(guide_lo, guide_hi, src_lo, p: GuidedFilterParams, *, check: bool = True,
-                  row_origin: int = 0):
+                  row_origin: int = 0, full_rows: int | None = None):
     """Joint upsampling: regress src on guide at low res, apply at high res.
 
     ``row_origin`` (extension, multi-GPU row bands): the full image's low-res
     row index of the inputs' first row.  It changes no value the reference
     defines; it makes the backward cut its row pieces at full-image rows so a
     band's gradients are bitwise those of the whole image (sharding.py).
+    ``full_rows`` (with it): the full image's low-res height, so the band takes
+    the kernel path (one- or two-kernel forward) the whole image would.
     """
     if isinstance(row_origin, bool) or not isinstance(row_origin, (int, np.integer)) \
             or row_origin < 0:
@@ -184,18 +186,29 @@ def forward_joint(guide_lo, guide_hi, src_lo, p: GuidedFilterParams, *, check: b
     out = torch.empty_like(gh.t)
     status = Status(dev)
     slope = None
+    mode = 0
+    if full_rows is not None:
+        if isinstance(full_rows, bool) or not isinstance(full_rows, (int, np.integer)) \
+                or full_rows < h:
+            raise ValueError(f"full_rows must be an integer >= the band's rows, got {full_rows!r}")
+        full_elems = B * C * (int(full_rows) * H // h) * W
+        mode = 2 if full_elems >= lib.gf_joint_split_threshold() else 1
+        mode_old = lib.gf_joint_fwd_mode(mode)
     if lib.gf_joint_is_fused(dt, B, C, h, w, H, W, p.radius) and not any(
             t.data_ptr() % 16 for t in (gl.t, sl.t, gh.t, out)):
         slope = torch.empty_like(gl.t)
+        ws = workspace(lib.gf_joint_workspace_bytes(dt, B, C, h, w, H, W, p.radius), dev)
         rc = lib.gf_joint_fwd_tape(dt, ptr(gl.t), ptr(sl.t), ptr(gh.t), ptr(out), ptr(slope), B,
-                                   C, h, w, H, W, int(p.radius), float(p.eps), status.ptr,
-                                   _stream(gl))
+                                   C, h, w, H, W, int(p.radius), float(p.eps), ptr(ws),
+                                   ws.numel(), status.ptr, _stream(gl))
     else:
         nbytes = lib.gf_joint_workspace_bytes(dt, B, C, h, w, H, W, p.radius)
         ws = workspace(nbytes, dev)
         rc = lib.gf_joint_fwd(dt, ptr(gl.t), ptr(sl.t), ptr(gh.t), ptr(out), B, C, h, w, H, W,
                               int(p.radius), float(p.eps), ptr(ws), ws.numel(), status.ptr,
                               _stream(gl))
+    if mode:
+        lib.gf_joint_fwd_mode(mode_old)
     _lib.check(rc, "forward_joint")
     if check:
         status.raise_if_set("forward_joint", (gl.t, gh.t, sl.t))

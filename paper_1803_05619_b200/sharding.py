@@ -75,6 +75,7 @@ class Band:
 
 ALIGN = 16  # low-res rows per tile row of the fused fp32 kernels (jf::TLY)
 GRAIN = 64  # low-res rows per row piece of the backward tail (jls::kPiece)
+PIECE = 16  # low-res rows per piece of the forward's coefficient walk (jcs::kPiece)
 
 
 def halo(radius: int, backward: bool) -> int:
@@ -96,7 +97,11 @@ def row_bands(h: int, world: int, radius: int, factor: int = 4, backward: bool =
     for k in range(world):
         ua, ub = batch_shard(units, world, k)
         a, b = min(h, ua * g), min(h, ub * g)
-        lo = max(0, a - R) // align * align
+        # the two-kernel forward's coefficient walk restarts its running sums
+        # at rows 16 j - 1: the piece holding row a - 1 (the first coefficient
+        # row the band's bilinear taps read) needs its r warm-up rows in the crop
+        piece = (a // PIECE) * PIECE - 1
+        lo = max(0, min(a - R, piece - radius)) // align * align
         out.append(Band(a, b, lo, min(h, b + R), factor))
     return out
 
@@ -119,19 +124,27 @@ def joint_band_forward(forward_joint, params, lr_x, lr_y, hr_x, band: Band):
     lo, hi = band.crop_lo, band.crop_hi
     Hlo, Hhi = band.hr_crop
     out, _ = forward_joint(lr_x[:, :, lo:hi].contiguous(), hr_x[:, :, Hlo:Hhi].contiguous(),
-                           lr_y[:, :, lo:hi].contiguous(), params, **_origin(forward_joint, lo))
+                           lr_y[:, :, lo:hi].contiguous(), params,
+                           **_origin(forward_joint, lo, lr_x.shape[2]))
     y0, y1 = band.hr_local
     return out[:, :, y0:y1]
 
 
-def _origin(fn, lo: int) -> dict:
-    """row_origin for the GPU layer (the oracle in the CPU tests has none)."""
+def _origin(fn, lo: int, h_full: int) -> dict:
+    """row_origin / full_rows for the GPU layer (the oracle in the CPU tests
+    has neither)."""
     import inspect
 
     try:
-        return {"row_origin": lo} if "row_origin" in inspect.signature(fn).parameters else {}
+        params = inspect.signature(fn).parameters
     except (TypeError, ValueError):
         return {}
+    kw = {}
+    if "row_origin" in params:
+        kw["row_origin"] = lo
+    if "full_rows" in params:
+        kw["full_rows"] = h_full
+    return kw
 
 
 def joint_band_backward(forward_joint, backward, params, lr_x, lr_y, hr_x, d_out, band: Band):
@@ -141,7 +154,7 @@ def joint_band_backward(forward_joint, backward, params, lr_x, lr_y, hr_x, d_out
     Hlo, Hhi = band.hr_crop
     out, tape = forward_joint(lr_x[:, :, lo:hi].contiguous(), hr_x[:, :, Hlo:Hhi].contiguous(),
                               lr_y[:, :, lo:hi].contiguous(), params,
-                              **_origin(forward_joint, lo))
+                              **_origin(forward_joint, lo, lr_x.shape[2]))
     g = backward(tape, d_out[:, :, Hlo:Hhi].contiguous())
     y0, y1 = band.hr_local
     l0, l1 = band.lr_local

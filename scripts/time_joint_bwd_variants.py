@@ -16,7 +16,7 @@ st = torch.zeros(1, dtype=torch.int32, device="cuda")
 ws = torch.empty(L.gf_joint_workspace_bytes(0, B, C, h, h, H, H, r), dtype=torch.uint8, device="cuda")
 out = torch.empty_like(hx); A = torch.empty_like(lx)
 P = lambda t: t.data_ptr()
-assert L.gf_joint_fwd_tape(0, P(lx), P(ly), P(hx), P(out), P(A), B, C, h, h, H, H, r, eps, P(st), sp) == 0
+assert L.gf_joint_fwd_tape(0, P(lx), P(ly), P(hx), P(out), P(A), B, C, h, h, H, H, r, eps, P(ws), ws.numel(), P(st), sp) == 0
 res = {}
 for v in (0, 12, 0):
     g = [torch.empty_like(lx), torch.empty_like(ly), torch.empty_like(hx)]

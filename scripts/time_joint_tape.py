@@ -22,7 +22,7 @@ def plain():
     assert L.gf_joint_fwd(0, P(lx), P(ly), P(hx), P(out), B, C, h, h, H, H, r, eps, P(ws), ws.numel(), P(st), sp) == 0
     assert L.gf_joint_bwd(0, P(lx), P(ly), P(hx), P(d), P(g1[0]), P(g1[1]), P(g1[2]), B, C, h, h, H, H, r, eps, P(ws), ws.numel(), P(st), sp) == 0
 def tape():
-    assert L.gf_joint_fwd_tape(0, P(lx), P(ly), P(hx), P(out2), P(A), B, C, h, h, H, H, r, eps, P(st), sp) == 0, L.gf_last_error()
+    assert L.gf_joint_fwd_tape(0, P(lx), P(ly), P(hx), P(out2), P(A), B, C, h, h, H, H, r, eps, P(ws), ws.numel(), P(st), sp) == 0, L.gf_last_error()
     assert L.gf_joint_bwd_tape(0, P(lx), P(ly), P(hx), P(A), P(d), P(g2[0]), P(g2[1]), P(g2[2]), B, C, h, h, H, H, r, eps, 0, P(ws), ws.numel(), P(st), sp) == 0, L.gf_last_error()
 plain(); tape(); torch.cuda.synchronize()
 print("out bitwise:", torch.equal(out, out2))

@@ -297,7 +297,8 @@ def run_joint_tape(lib, lr_x, lr_y, hr_x, d, r, eps, guarded):
         p = lambda t: t.data_ptr()  # noqa: E731
     st = status()
     rc_ok(lib, lib.gf_joint_fwd_tape(0, p(ins[0]), p(ins[1]), p(ins[2]), p(outs[0]), p(outs[4]),
-                                     B, C, h, w, H, W, r, eps, st.data_ptr(), stream()))
+                                     B, C, h, w, H, W, r, eps, p(ws), wsb, st.data_ptr(),
+                                     stream()))
     rc_ok(lib, lib.gf_joint_bwd_tape(0, p(ins[0]), p(ins[1]), p(ins[2]), p(outs[4]), p(ins[3]),
                                      p(outs[1]), p(outs[2]), p(outs[3]), B, C, h, w, H, W, r, eps,
                                      0, p(ws), wsb, st.data_ptr(), stream()))
