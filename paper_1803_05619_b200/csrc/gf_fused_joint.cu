@@ -97,6 +97,8 @@ constexpr int kStageTape = 3;
 constexpr int kStageTapeTile = 4;
 constexpr int HTW = THX + 8, HTH = THY + 4;       // staged window: 136 x 68 (= GR rows)
 constexpr int HTF = HTW * HTH;                    // floats per field (128-byte multiple)
+constexpr int kTileBox = 4;                       // rows per TMA box of the window
+constexpr int kTileGroups = 9;                    // mbarriers: 8 groups of 8 rows + rows 64..67
 
 template <int RAD, bool NEED_B, int VCH = 0, int HCH = 16, int MODE = kStageLdg>
 __device__ void lr_coeffs(const float* __restrict__ X, const float* __restrict__ Y, int h, int w,
@@ -924,6 +926,7 @@ __device__ __forceinline__ void mse_hr_body(const MseHrArgs& a, const CUtensorMa
   extern __shared__ float4 smem4[];
   __shared__ double red[NT / 32];
   __shared__ __align__(8) uint64_t tbar;
+  __shared__ __align__(8) uint64_t gbar[kTileGroups];  // kStageTapeTile: per row group
   constexpr int r = RAD;
   float* base;
   SmemCoef sm;
@@ -994,26 +997,61 @@ __device__ __forceinline__ void mse_hr_body(const MseHrArgs& a, const CUtensorMa
                                           degen, TG::LP, TG::COFS);
   } else if constexpr (MODE == kStageTape || MODE == kStageTapeTile) {
     static_assert(!MSE || MODE == kStageTapeTile, "the forward's tape has A only");
-    if constexpr (MODE == kStageTapeTile) {
-      if (threadIdx.x == 0) tma::mbar_init(&tbar, 1);
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        tma::mbar_arrive_expect_tx(&tbar, 2u * HTF * 4u);
-        tma::load_3d(base, tmX, 4 * k0 - 4, Yg, (int)p, &tbar);
-        tma::load_3d(base + HTF, tmY, 4 * k0 - 4, Yg, (int)p, &tbar);
+    // the tile's coefficient cells are requested FIRST (they gate every warp's
+    // start; behind the window's 74 KB they would return last), held in
+    // registers until the window's copies have been issued
+    constexpr int NEA = (RA * CA + NT - 1) / NT;
+    float av[NEA], bv[NEA];
+    {
+      const float* At = a.A_tape + p * (int64_t)a.h * a.w;
+#pragma unroll
+      for (int e = 0; e < NEA; ++e) {
+        const int it = threadIdx.x + e * NT;
+        const int ar = it / CA, c = it - ar * CA;
+        const int gy = i0 - 1 + ar, gx = k0 - 1 + c;
+        const bool inimg = it < RA * CA && gy >= 0 && gy < a.h && gx >= 0 && gx < a.w;
+        const int64_t o = (int64_t)gy * a.w + gx;
+        av[e] = inimg ? __ldg(At + o) : 0.f;
+        bv[e] = 0.f;
+        if constexpr (MSE) bv[e] = inimg ? __ldg(a.B_tape + p * (int64_t)a.h * a.w + o) : 0.f;
       }
     }
-    const float* At = a.A_tape + p * (int64_t)a.h * a.w;
-    for (int it = threadIdx.x; it < RA * CA; it += NT) {
-      const int ar = it / CA, c = it - ar * CA;
-      const int gy = i0 - 1 + ar, gx = k0 - 1 + c;
-      const bool inimg = gy >= 0 && gy < a.h && gx >= 0 && gx < a.w;
-      const int64_t o = (int64_t)gy * a.w + gx;
-      sm.As[ar * CAP + c] = inimg ? __ldg(At + o) : 0.f;
-      if constexpr (MSE) sm.Bs[ar * CAP + c] = inimg ? __ldg(a.B_tape + p * (int64_t)a.h * a.w + o) : 0.f;
+    if constexpr (MODE == kStageTapeTile) {
+      // the window arrives as kTileBox-row boxes in row order, one mbarrier
+      // per 8-row group (= per warp) and one for rows 64..67: a warp starts
+      // on its rows as soon as THEY have landed, while the rest of the
+      // window is still in flight
+      if (threadIdx.x == 0) {
+#pragma unroll
+        for (int c = 0; c < kTileGroups; ++c) tma::mbar_init(&gbar[c], 1);
+        tma::fence_proxy_async();
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+#pragma unroll
+        for (int c = 0; c < kTileGroups; ++c) {
+          const int rows = c < 8 ? 8 : HTH - 64;
+          tma::mbar_arrive_expect_tx(&gbar[c], 2u * rows * HTW * 4u);
+#pragma unroll
+          for (int b = 0; b < rows; b += kTileBox) {
+            const int yl = 8 * c + b;
+            tma::load_3d(base + yl * HTW, tmX, 4 * k0 - 4, Yg + yl, (int)p, &gbar[c]);
+            tma::load_3d(base + HTF + yl * HTW, tmY, 4 * k0 - 4, Yg + yl, (int)p, &gbar[c]);
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int e = 0; e < NEA; ++e) {
+      const int it = threadIdx.x + e * NT;
+      if (it < RA * CA) {
+        const int ar = it / CA, c = it - ar * CA;
+        sm.As[ar * CAP + c] = av[e];
+        if constexpr (MSE) sm.Bs[ar * CAP + c] = bv[e];
+      }
     }
     __syncthreads();
-    if constexpr (MODE == kStageTapeTile) tma::mbar_wait(&tbar, 0);
+    if constexpr (MODE == kStageTapeTile) tma::mbar_wait(&gbar[warp], 0);
   } else {
     lr_coeffs<RAD, MSE>(a.lr_x + p * (int64_t)a.h * a.w, a.lr_y + p * (int64_t)a.h * a.w, a.h,
                         a.w, i0, k0, a.eps, sm, degen);
@@ -1148,6 +1186,7 @@ __device__ __forceinline__ void mse_hr_body(const MseHrArgs& a, const CUtensorMa
     }
   }
   if (extra) {  // gather row 64 + warp: coefficient rows 16, 17
+    if constexpr (MODE == kStageTapeTile) tma::mbar_wait(&gbar[8], 0);
     float HA[2][4], HB[2][4];
     hrow2(16, HA[0], HB[0]);
     hrow2(17, HA[1], HB[1]);
@@ -1837,8 +1876,8 @@ void fused_joint_bwd(const float* lr_x, const float* lr_y, const float* hr_x, co
       CUtensorMap tmX, tmY;
       CUtensorMap tmG, tmD;
       if (A_tape && g_joint_bwd_hr_variant == 0 &&
-          tma::make_plane_map(&tmG, hr_x, W, H, B * C, jf::HTW, jf::HTH) &&
-          tma::make_plane_map(&tmD, d_out, W, H, B * C, jf::HTW, jf::HTH)) {
+          tma::make_plane_map(&tmG, hr_x, W, H, B * C, jf::HTW, jf::kTileBox) &&
+          tma::make_plane_map(&tmD, d_out, W, H, B * C, jf::HTW, jf::kTileBox)) {
         // the forward's slopes, and the gather window by TMA
         a.A_tape = A_tape;
         const size_t sma =
@@ -1900,22 +1939,20 @@ void fused_joint_mse_bwd(const float* lr_x, const float* lr_y, const float* hr_x
     jf::MseHrArgs a{lr_x, lr_y, hr_x, target, d_hr_x, db, dA, part, (int)h, (int)w, (int)H,
                     (int)W, r, eps, (float)(2.0 / per_image / (double)B), status};
     CUtensorMap tmX, tmY, tmG, tmT;
-    // variant 15: coefficient tape + TMA gather window -- measured slower than
-    // the moments-recomputing kernel at config 2 (461 vs 436 us: the extra
-    // coefficient kernel, 2 instead of 3 CTAs per SM); kept as a variant
-    if (g_joint_mse_variant == 15 &&
-        tma::make_plane_map(&tmG, hr_x, W, H, B * C, jf::HTW, jf::HTH) &&
-        tma::make_plane_map(&tmT, target, W, H, B * C, jf::HTW, jf::HTH)) {
+    // coefficient tape + TMA gather window: the default for large calls (config
+    // 2's filter step 388 vs 436 us for the moments-recomputing kernel, since
+    // the coefficients come from the register-segment walk); variant hook 15
+    // forces it, 16 forces the moments-recomputing kernel
+    const bool big = B * C * H * W >= kJointSplitElems;
+    if (((g_joint_mse_variant == 0 && big) || g_joint_mse_variant == 15) &&
+        tma::make_plane_map(&tmG, hr_x, W, H, B * C, jf::HTW, jf::kTileBox) &&
+        tma::make_plane_map(&tmT, target, W, H, B * C, jf::HTW, jf::kTileBox)) {
       // coefficient tape (A, b of every cell), then the hr pass on it with the
       // gather window of hr_x and the target staged by TMA
       float* Acoef = (float*)((char*)part + ((size_t)B * mse_tiles(C, h, w) * sizeof(double) + 255) /
                                                  256 * 256);
       float* Bcoef = Acoef + B * C * h * w;
-      jf::FwdArgs fa{lr_x, lr_y, hr_x, nullptr, (int)h, (int)w, (int)H, (int)W, r, eps, status};
-      const size_t smc = jf::coef_smem_floats(r) * sizeof(float);
-      set_smem(fns.coeffs, smc);
-      void* cargs[] = {&fa, &Acoef, &Bcoef};
-      cudaLaunchKernel(fns.coeffs, grid, dim3(jf::NT), cargs, smc, s);
+      fused_joint_coeffs(lr_x, lr_y, Acoef, Bcoef, B * C, h, w, r, eps, status, s);
       a.A_tape = Acoef;
       a.B_tape = Bcoef;
       const size_t sma =
