@@ -238,13 +238,15 @@ class OursStep:
                 self.target = workloads.affine_target(hr_x).contiguous()
                 self.params = gfb.GuidedFilterParams(c["r"], c["eps"])
             fused = self.lib.gf_joint_is_fused(0, B, C, self.h, self.w, self.H, self.W, c["r"])
-            fwd = 1 if fused else 12
+            # large calls: the two-kernel forward (coefficients, apply pass)
+            split = fused and B * C * self.H * self.W >= self.lib.gf_joint_split_threshold()
+            fwd = (2 if split else 1) if fused else 12
             bwd = 2 if fused else 26
             # train step: 2 x (stats, norm, fwd) guidance, the fused GF fwd + MSE +
             # bwd (hr pass, loss sum, lr tail; unfused: GF fwd, mse (2), GF bwd),
             # 2 x (bwd1, sum1, dx, dw1, final) guidance backward (the forward's
             # statistics are reused)
-            gf_step = 3 if fused else fwd + 2 + bwd
+            gf_step = (4 if split else 3) if fused else fwd + 2 + bwd
             self.launches = {"joint_fwd": fwd, "joint_fwd_bwd": fwd + bwd,
                              "train_step": 2 * 3 + gf_step + 2 * 5}[kind]
 

@@ -1091,6 +1091,34 @@ __device__ __forceinline__ void mse_hr_body(const MseHrArgs& a, const CUtensorMa
     }
   }
 
+  // kStageTapeTile without the MSE: the 2 halo columns on each side of the
+  // tile are in the staged window, so lanes 0 and 31 add their row partials
+  // in the row pass itself (every lane runs the same 2-element load and two
+  // FMAs, with zero weights except on the edge lanes) instead of a scalar pass
+  // per warp; the shuffled-in neighbours of the edge lanes get zero weights
+  // instead of being zeroed.  Same products, same summation order: bitwise the
+  // scalar pass's result.
+  constexpr bool INLINE_HALO = MODE == kStageTapeTile && !MSE;
+  float wxe[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) wxe[j] = wx[j];
+  float hw0 = 0.f, hw1 = 0.f;
+  int hoff = 4 + 4 * lane;
+  if (INLINE_HALO) {
+    if (lane == 0) {
+      hw0 = wx[0];
+      hw1 = wx[1];
+      wxe[0] = wxe[1] = 0.f;
+      hoff = 2;
+    }
+    if (lane == 31) {
+      hw0 = wx[6];
+      hw1 = wx[7];
+      wxe[6] = wxe[7] = 0.f;
+      hoff = 4 + THX;
+    }
+  }
+
   float lsum = 0.f, chk = 0.f;
   const float scale2 = a.scale2;
   // gather row yl, its coefficient rows interpolated horizontally (lo, hi)
@@ -1134,15 +1162,23 @@ __device__ __forceinline__ void mse_hr_body(const MseHrArgs& a, const CUtensorMa
     float ql0 = __shfl_up_sync(0xffffffffu, q[2], 1), ql1 = __shfl_up_sync(0xffffffffu, q[3], 1);
     float dr0 = __shfl_down_sync(0xffffffffu, d[0], 1), dr1 = __shfl_down_sync(0xffffffffu, d[1], 1);
     float qr0 = __shfl_down_sync(0xffffffffu, q[0], 1), qr1 = __shfl_down_sync(0xffffffffu, q[1], 1);
-    if (lane == 0) dl0 = dl1 = ql0 = ql1 = 0.f;  // halo columns: the scalar pass
-    if (lane == 31) dr0 = dr1 = qr0 = qr1 = 0.f;
+    if (!INLINE_HALO) {
+      if (lane == 0) dl0 = dl1 = ql0 = ql1 = 0.f;  // halo columns: the scalar pass
+      if (lane == 31) dr0 = dr1 = qr0 = qr1 = 0.f;
+    }
     const float dd[8] = {dl0, dl1, d[0], d[1], d[2], d[3], dr0, dr1};
     const float qq[8] = {ql0, ql1, q[0], q[1], q[2], q[3], qr0, qr1};
     float s1 = 0.f, s2 = 0.f;
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
-      s1 += wx[j] * dd[j];
-      s2 += wx[j] * qq[j];
+      s1 = fmaf(wxe[j], dd[j], s1);
+      s2 = fmaf(wxe[j], qq[j], s2);
+    }
+    if constexpr (INLINE_HALO) {
+      const float2 ht = *reinterpret_cast<const float2*>(tT + yl * HTW + hoff);
+      const float2 hg = *reinterpret_cast<const float2*>(tG + yl * HTW + hoff);
+      s1 += fmaf(hw1, ht.y, hw0 * ht.x);
+      s2 += fmaf(hw1, ht.y * hg.y, hw0 * (ht.x * hg.x));
     }
     if (!in) s1 = s2 = 0.f;
     R1[yl * TLX + lane] = s1;
@@ -1212,7 +1248,7 @@ __device__ __forceinline__ void mse_hr_body(const MseHrArgs& a, const CUtensorMa
   __syncwarp();
   // halo columns: hr columns 4k0-2, 4k0-1 (into lr column k0's partial) and
   // 4k0+128, 4k0+129 (into k0+31's), one (row, side) item per lane
-  {
+  if constexpr (!INLINE_HALO) {
     const int nrow = extra ? 9 : 8;
     if (lane < 2 * nrow) {
       const int ri = lane >> 1, side = lane & 1;

@@ -126,6 +126,7 @@ __device__ __forceinline__ float el(const float4& v, int j) {
 
 struct Bufs {
   float4 ex, ey, lx, ly;  // entering / leaving rows
+  float4 db, da;          // adjoint fields of the step's moment row (HBM: a step ahead)
 };
 
 struct Piece {
@@ -188,15 +189,17 @@ __device__ __forceinline__ void run_piece(const Piece& P, float4* __restrict__ r
     B.ey = ld4(Y + (e * w + xc));
     B.lx = ld4(X + (l * w + xc));
     B.ly = ld4(Y + (l * w + xc));
+    const int ym = STEADY ? ya : min(ya, h - 1);
+    B.db = ld4(P.DB + (ym * w + xc));
+    B.da = ld4(P.DA + (ym * w + xc));
   };
 
   int slot = 0;
   auto step = [&](auto steady, int ya, Bufs& cur) {
     constexpr bool STEADY = decltype(steady)::value;
-    // adjoint fields of moment row ya and inputs of output row ya - r (L2)
-    const int ym = STEADY ? ya : min(ya, h - 1);
-    const float4 dbv = ld4(P.DB + (ym * w + xc));
-    const float4 dav = ld4(P.DA + (ym * w + xc));
+    // adjoint fields of moment row ya (fetched a step ahead with the entering
+    // rows) and inputs of output row ya - r (L2)
+    const float4 dbv = cur.db, dav = cur.da;
     const int yo = STEADY ? ya - r : min(max(ya - r, 0), h - 1);
     const float4 ox = ld4(X + (yo * w + xc));
     const float4 oy = ld4(Y + (yo * w + xc));
