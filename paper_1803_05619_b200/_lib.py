@@ -99,6 +99,7 @@ EXTRA = {
     "gf_joint_fwd_variant": (_i, [_i]),
     "gf_gn_bwd_variant": (_i, [_i]),
     "gf_joint_bwd_hr_variant": (_i, [_i]),
+    "gf_joint_bwd_hr_tile": (_i, [_i]),
     "gf_joint_is_fused": (_i, [_i, _i64, _i64, _i64, _i64, _i64, _i64, _i]),
     "gf_highres_fwd_is_fused": (_i, [_i, _i64, _i64, _i64, _i64, _i64, _i]),
 }

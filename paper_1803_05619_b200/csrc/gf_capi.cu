@@ -136,6 +136,13 @@ int gf_gn_bwd_variant(int v) {
 // Test hook: hr pass of the fp32 joint backward on THIS thread (0 single
 // gather pass, 1 the two-read tile kernel, 3 single pass at 3 CTAs/SM for
 // r <= 2).  Returns the old value.
+// Test hook: low-res rows per tile of the tape hr pass of THIS thread (16 or 8)
+int gf_joint_bwd_hr_tile(int v) {
+  int old = gfb::g_joint_bwd_hr_tile;
+  gfb::g_joint_bwd_hr_tile = v == 8 ? 8 : 16;
+  return old;
+}
+
 int gf_joint_bwd_hr_variant(int v) {
   int old = gfb::g_joint_bwd_hr_variant;
   gfb::g_joint_bwd_hr_variant = v;

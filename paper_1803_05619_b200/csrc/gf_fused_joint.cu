@@ -920,9 +920,18 @@ struct MseHrArgs {
 // MODE kStageTma (k_joint_mse_hr_t): the low-res x, y halo blocks arrive by
 // TMA (one elected thread, one mbarrier) and the coefficient pass reads them
 // in place -- no per-thread staging loads, index math or copies.
-template <int RAD, bool MSE, int MODE>
+// TY: low-res rows per tile (the namespace's TLY = 16, or 8: a 32-row high-res
+// tile of 4 warps, each with 8 rows and one of the 4 extra rows; kStageTapeTile
+// without the MSE only).  The per-pixel products, the row partials and the
+// column sums do not depend on the tile height: results are bitwise the same.
+template <int RAD, bool MSE, int MODE, int TY = jf::TLY>
 __device__ __forceinline__ void mse_hr_body(const MseHrArgs& a, const CUtensorMap* tmX,
                                             const CUtensorMap* tmY) {
+  // this tile's geometry (shadows the namespace's 16-row constants)
+  constexpr int TLY = TY, THY = 4 * TY, NT = 32 * (TY / 2);
+  constexpr int RA = TY + 2, GR = THY + 4, HTH = THY + 4, HTF = HTW * HTH;
+  constexpr int kTileGroups = TY / 2 + 1;  // 8-row groups + the 4 extra rows
+  static_assert(TY == jf::TLY || (MODE == kStageTapeTile && !MSE), "8-row tiles: tape + TMA only");
   extern __shared__ float4 smem4[];
   __shared__ double red[NT / 32];
   __shared__ __align__(8) uint64_t tbar;
@@ -964,7 +973,7 @@ __device__ __forceinline__ void mse_hr_body(const MseHrArgs& a, const CUtensorMa
   const int X0 = 4 * k;
   const bool col_ok = k < a.w;  // W == 4 w
   const int Yg = 4 * i0 - 2;    // hr row of gather row 0
-  const bool extra = warp < 4;  // takes gather row 64 + warp as well
+  const bool extra = warp < 4;  // takes gather row THY + warp as well
 
   // the tile's gather rows of hr_x and target (with the 4-column halo chunk
   // on each side the scalar pass reads) start their DRAM reads into L2
@@ -1030,7 +1039,7 @@ __device__ __forceinline__ void mse_hr_body(const MseHrArgs& a, const CUtensorMa
       if (threadIdx.x == 0) {
 #pragma unroll
         for (int c = 0; c < kTileGroups; ++c) {
-          const int rows = c < 8 ? 8 : HTH - 64;
+          const int rows = c < kTileGroups - 1 ? 8 : HTH - THY;
           tma::mbar_arrive_expect_tx(&gbar[c], 2u * rows * HTW * 4u);
 #pragma unroll
           for (int b = 0; b < rows; b += kTileBox) {
@@ -1221,18 +1230,18 @@ __device__ __forceinline__ void mse_hr_body(const MseHrArgs& a, const CUtensorMa
       }
     }
   }
-  if (extra) {  // gather row 64 + warp: coefficient rows 16, 17
-    if constexpr (MODE == kStageTapeTile) tma::mbar_wait(&gbar[8], 0);
+  if (extra) {  // gather row THY + warp: coefficient rows TLY, TLY + 1
+    if constexpr (MODE == kStageTapeTile) tma::mbar_wait(&gbar[kTileGroups - 1], 0);
     float HA[2][4], HB[2][4];
-    hrow2(16, HA[0], HB[0]);
-    hrow2(17, HA[1], HB[1]);
-    const int Y = Yg + 64 + warp;
+    hrow2(TLY, HA[0], HB[0]);
+    hrow2(TLY + 1, HA[1], HB[1]);
+    const int Y = Yg + THY + warp;
     float f = (2 * warp + 1) * 0.125f;
     int ql = 0, qh = 1;
     if (Y >= 0 && Y < a.H) {
       const Tap ty = tap4(Y, a.h);
-      ql = ty.lo - (i0 - 1) - 16;
-      qh = ty.hi - (i0 - 1) - 16;
+      ql = ty.lo - (i0 - 1) - TLY;
+      qh = ty.hi - (i0 - 1) - TLY;
       f = ty.f;
     }
     float alo[4], ahi[4], blo[4], bhi[4];
@@ -1243,7 +1252,7 @@ __device__ __forceinline__ void mse_hr_body(const MseHrArgs& a, const CUtensorMa
       blo[j] = ql == 0 ? HB[0][j] : HB[1][j];
       bhi[j] = qh == 0 ? HB[0][j] : HB[1][j];
     }
-    do_row(64 + warp, alo, ahi, blo, bhi, f);
+    do_row(THY + warp, alo, ahi, blo, bhi, f);
   }
   __syncwarp();
   // halo columns: hr columns 4k0-2, 4k0-1 (into lr column k0's partial) and
@@ -1252,7 +1261,7 @@ __device__ __forceinline__ void mse_hr_body(const MseHrArgs& a, const CUtensorMa
     const int nrow = extra ? 9 : 8;
     if (lane < 2 * nrow) {
       const int ri = lane >> 1, side = lane & 1;
-      const int yl = ri < 8 ? 8 * warp + ri : 64 + warp;
+      const int yl = ri < 8 ? 8 * warp + ri : THY + warp;
       const int Y = Yg + yl;
       const int kk = side ? k0 + TLX - 1 : k0;
       const int Xa = side ? 4 * k0 + THX : 4 * k0 - 2;
@@ -1363,11 +1372,13 @@ __global__ void __launch_bounds__(NT, MINB) k_joint_mse_hr_a(MseHrArgs a) {
 // ... with the gather window of hr_x and d_out staged by TMA (tmG, tmD:
 // (136, 68) boxes of the high-res planes).  MSE: the fused training step on
 // the coefficients of k_joint_coeffs (A and b), tmD over the target.
-template <int RAD, int MINB, bool MSE = false>
-__global__ void __launch_bounds__(NT, MINB)
+// TY = 8: 32-row tiles of 128 threads (52 KB of shared memory: 4 independent
+// CTAs per SM instead of 2)
+template <int RAD, int MINB, bool MSE = false, int TY = TLY>
+__global__ void __launch_bounds__(32 * (TY / 2), MINB)
     k_joint_mse_hr_at(const __grid_constant__ CUtensorMap tmG,
                       const __grid_constant__ CUtensorMap tmD, MseHrArgs a) {
-  mse_hr_body<RAD, MSE, kStageTapeTile>(a, &tmG, &tmD);
+  mse_hr_body<RAD, MSE, kStageTapeTile, TY>(a, &tmG, &tmD);
 }
 
 // A and b of every low-res cell (the fused training step's coefficient tape):
@@ -1603,6 +1614,7 @@ __global__ void __launch_bounds__(NT) k_joint_bwd_lr(BwdLrArgs a) {
 
 thread_local int g_joint_lr_variant = 0;
 thread_local int g_joint_mse_variant = 0;
+thread_local int g_joint_bwd_hr_tile = 16;  // low-res rows per tile of the tape hr pass (16 or 8)
 thread_local int g_joint_fwd_variant = 0;
 thread_local int g_joint_bwd_hr_variant = 0;
 
@@ -1633,6 +1645,7 @@ struct JointFns {
   size_t tma_floats;  // tma_coef_floats + alignment slack
   const void* hr_pass_a;   // hr pass on the forward's tape of slopes
   const void* hr_pass_at;  // ... with the gather window staged by TMA
+  const void* hr_pass_at8;  // ... on 32-row tiles (4 CTAs per SM)
   const void* coeffs;      // A, b of every low-res cell (fused step)
   const void* mse_hr_at;   // fused step on them, gather window by TMA
 };
@@ -1665,7 +1678,8 @@ static JointFns joint_fns() {
           (const void*)jf::k_joint_mse_hr_t<RAD, 3, true>,
           (const void*)jf::k_joint_mse_hr_t<RAD, 4, false>,
           (size_t)jf::tma_coef_floats<RAD>() + 32, (const void*)jf::k_joint_mse_hr_a<RAD, 4>,
-          (const void*)jf::k_joint_mse_hr_at<RAD, 2>, coeffs,
+          (const void*)jf::k_joint_mse_hr_at<RAD, 2>,
+          (const void*)jf::k_joint_mse_hr_at<RAD, 4, false, 8>, coeffs,
           (const void*)jf::k_joint_mse_hr_at<RAD, 2, true>};
 }
 
@@ -1780,7 +1794,7 @@ void fused_joint_coeffs(const float* lr_x, const float* lr_y, float* A, float* B
                         int64_t h, int64_t w, int r, float eps, uint32_t* status, cudaStream_t s) {
   const int v = g_joint_fwd_variant;
   if (v != 21 && seg_joint_coeffs_ok(h, w, r)) {
-    g_joint_coeffs_sw = v == 22 ? 8 : 0;
+    g_joint_coeffs_sw = v == 22 ? 8 : (v == 24 ? 4 : 0);  // 24: the register walk at 4 per lane
     seg_joint_coeffs(lr_x, lr_y, A, B, P, h, w, r, eps, status, s);
     return;
   }
@@ -1916,11 +1930,20 @@ void fused_joint_bwd(const float* lr_x, const float* lr_y, const float* hr_x, co
           tma::make_plane_map(&tmD, d_out, W, H, B * C, jf::HTW, jf::kTileBox)) {
         // the forward's slopes, and the gather window by TMA
         a.A_tape = A_tape;
-        const size_t sma =
-            128 + (2 * jf::HTF + 2 * jf::RA * jf::CAP + 2 * jf::GR * jf::TLX) * sizeof(float);
-        set_smem(fns.hr_pass_at, sma);
         void* args[] = {&tmG, &tmD, &a};
-        cudaLaunchKernel(fns.hr_pass_at, grid, dim3(jf::NT), args, sma, s);
+        if (g_joint_bwd_hr_tile == 8 && (h + 7) / 8 <= 65535) {  // 32-row tiles, 128 threads
+          constexpr int TY = 8, GR8 = 4 * TY + 4;
+          const size_t sma = 128 + (2 * jf::HTW * GR8 + 2 * (TY + 2) * jf::CAP +
+                                    2 * GR8 * jf::TLX) * sizeof(float);
+          set_smem(fns.hr_pass_at8, sma);
+          dim3 grid8(grid.x, (unsigned)((h + TY - 1) / TY), grid.z);
+          cudaLaunchKernel(fns.hr_pass_at8, grid8, dim3(32 * (TY / 2)), args, sma, s);
+        } else {
+          const size_t sma =
+              128 + (2 * jf::HTF + 2 * jf::RA * jf::CAP + 2 * jf::GR * jf::TLX) * sizeof(float);
+          set_smem(fns.hr_pass_at, sma);
+          cudaLaunchKernel(fns.hr_pass_at, grid, dim3(jf::NT), args, sma, s);
+        }
       } else if (A_tape && g_joint_bwd_hr_variant == 12) {  // slopes, global loads
         a.A_tape = A_tape;
         const size_t sma = (2 * jf::RA * jf::CAP + 2 * jf::GR * jf::TLX) * sizeof(float);

@@ -88,6 +88,7 @@ void seg_joint_bwd_lr(const float* lr_x, const float* lr_y, const float* db, con
 extern thread_local int g_joint_lr_variant;
 extern thread_local int g_joint_fwd_variant;  // r = 8 coefficient chunking (test hook)
 extern thread_local int g_joint_mse_variant;
+extern thread_local int g_joint_bwd_hr_tile;
 extern thread_local int g_joint_bwd_hr_variant;  // 0 single gather pass, 1 tile kernel, 3: 3 CTAs/SM
 extern thread_local int g_gn_bwd_variant;  // fused guidance backward: 0 one heavy pass (2 lanes per
                                            // pixel group), 1 two passes, 2 one pass with 4 lanes,

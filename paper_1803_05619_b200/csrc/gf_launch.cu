@@ -36,6 +36,12 @@ LaunchCfg launch_cfg(const void* fn, int threads, size_t smem) {
   cudaDeviceGetAttribute(&c.sms, cudaDevAttrMultiProcessorCount, dev);
   if (smem > 48 * 1024)
     cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  // kernels sized by their shared memory (rings, staged windows) want the
+  // largest carve-out: the default heuristic can leave a 48 KB kernel with
+  // fewer CTAs per SM than its shared memory allows
+  if (smem >= 16 * 1024)
+    cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout,
+                         cudaSharedmemCarveoutMaxShared);
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, smem);
   c.per_sm = per_sm < 1 ? 1 : per_sm;

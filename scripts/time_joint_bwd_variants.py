@@ -18,9 +18,10 @@ out = torch.empty_like(hx); A = torch.empty_like(lx)
 P = lambda t: t.data_ptr()
 assert L.gf_joint_fwd_tape(0, P(lx), P(ly), P(hx), P(out), P(A), B, C, h, h, H, H, r, eps, P(ws), ws.numel(), P(st), sp) == 0
 res = {}
-for v in (0, 12, 0):
+for v in (0, 12, 0, 8, 8):  # 8: the default hr pass on 32-row tiles
     g = [torch.empty_like(lx), torch.empty_like(ly), torch.empty_like(hx)]
-    old = L.gf_joint_bwd_hr_variant(v)
+    old = L.gf_joint_bwd_hr_variant(0 if v == 8 else v)
+    oldt = L.gf_joint_bwd_hr_tile(8 if v == 8 else 16)
     f = lambda: L.gf_joint_bwd_tape(0, P(lx), P(ly), P(hx), P(A), P(d), P(g[0]), P(g[1]), P(g[2]), B, C, h, h, H, H, r, eps, 0, P(ws), ws.numel(), P(st), sp)
     for _ in range(3): assert f() == 0
     torch.cuda.synchronize()
@@ -29,6 +30,7 @@ for v in (0, 12, 0):
     for _ in range(10): f()
     e1.record(); torch.cuda.synchronize()
     L.gf_joint_bwd_hr_variant(old)
+    L.gf_joint_bwd_hr_tile(oldt)
     res.setdefault(v, g)
     print("variant", v, round(e0.elapsed_time(e1) / 10, 3), "ms  bitwise vs default:",
           all(torch.equal(a, b) for a, b in zip(g, res[0])), flush=True)

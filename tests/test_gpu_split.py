@@ -261,3 +261,38 @@ def test_full_rows_selects_the_full_images_path(lib, gfb):
     assert lib.gf_joint_fwd_mode(0) == 0  # the call restored the thread's mode
     with pytest.raises(ValueError):
         gfb.forward_joint(lr_x, hr_x, lr_y, p, full_rows=h - 1)
+
+
+@pytest.mark.parametrize("h,w,r", [(64, 256, 1), (130, 132, 2), (37, 44, 3), (300, 768, 4)])
+def test_ring_walk_is_bitwise_the_register_walk(lib, h, w, r):
+    """r <= 4: the coefficient walk's cp.async ring (the default) and its
+    register walk (variant hook 24) run the same arithmetic in the same order."""
+    lr_x, lr_y, _ = workloads.joint_inputs(2, 3, 4 * h, 4 * w, seed=5 * h + w + r, device="cuda")
+    A0, B0, _ = coeffs(lib, lr_x, lr_y, r, 1e-4)
+    old = lib.gf_joint_fwd_variant(24)
+    try:
+        A1, B1, _ = coeffs(lib, lr_x, lr_y, r, 1e-4)
+    finally:
+        lib.gf_joint_fwd_variant(old)
+    assert torch.equal(A0, A1) and torch.equal(B0, B1)
+
+
+@pytest.mark.parametrize("h,w,r", [(37, 44, 2), (130, 132, 1), (64, 256, 4), (21, 72, 8)])
+def test_hr_pass_tile_height_is_bitwise(lib, gfb, h, w, r):
+    """The tape backward's hr pass on 32-row tiles (hook gf_joint_bwd_hr_tile(8),
+    4 CTAs of 128 threads per SM; measured slower, kept as a variant) gives
+    bitwise the 64-row tiles' gradients: products, row partials and column sums
+    do not depend on the tile height."""
+    lr_x, lr_y, hr_x = workloads.joint_inputs(2, 3, 4 * h, 4 * w, seed=h + w + r, device="cuda")
+    p = gfb.GuidedFilterParams(r, 1e-4)
+    out, tape = gfb.forward_joint(lr_x, hr_x, lr_y, p)
+    d = torch.randn(out.shape, device="cuda", generator=torch.Generator("cuda").manual_seed(3))
+    g0 = gfb.backward(tape, d)
+    old = lib.gf_joint_bwd_hr_tile(8)
+    try:
+        g1 = gfb.backward(tape, d)
+    finally:
+        assert lib.gf_joint_bwd_hr_tile(old) == 8
+    for a, b in ((g0.d_src, g1.d_src), (g0.d_guide_lo, g1.d_guide_lo),
+                 (g0.d_guide_hi, g1.d_guide_hi)):
+        assert torch.equal(a, b)
