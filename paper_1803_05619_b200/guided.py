@@ -193,22 +193,24 @@ def forward_joint(guide_lo, guide_hi, src_lo, p: GuidedFilterParams, *, check: b
             raise ValueError(f"full_rows must be an integer >= the band's rows, got {full_rows!r}")
         full_elems = B * C * (int(full_rows) * H // h) * W
         mode = 2 if full_elems >= lib.gf_joint_split_threshold() else 1
-        mode_old = lib.gf_joint_fwd_mode(mode)
-    if lib.gf_joint_is_fused(dt, B, C, h, w, H, W, p.radius) and not any(
-            t.data_ptr() % 16 for t in (gl.t, sl.t, gh.t, out)):
-        slope = torch.empty_like(gl.t)
-        ws = workspace(lib.gf_joint_workspace_bytes(dt, B, C, h, w, H, W, p.radius), dev)
-        rc = lib.gf_joint_fwd_tape(dt, ptr(gl.t), ptr(sl.t), ptr(gh.t), ptr(out), ptr(slope), B,
-                                   C, h, w, H, W, int(p.radius), float(p.eps), ptr(ws),
-                                   ws.numel(), status.ptr, _stream(gl))
-    else:
-        nbytes = lib.gf_joint_workspace_bytes(dt, B, C, h, w, H, W, p.radius)
-        ws = workspace(nbytes, dev)
-        rc = lib.gf_joint_fwd(dt, ptr(gl.t), ptr(sl.t), ptr(gh.t), ptr(out), B, C, h, w, H, W,
-                              int(p.radius), float(p.eps), ptr(ws), ws.numel(), status.ptr,
-                              _stream(gl))
-    if mode:
-        lib.gf_joint_fwd_mode(mode_old)
+    mode_old = lib.gf_joint_fwd_mode(mode) if mode else 0
+    try:
+        if lib.gf_joint_is_fused(dt, B, C, h, w, H, W, p.radius) and not any(
+                t.data_ptr() % 16 for t in (gl.t, sl.t, gh.t, out)):
+            slope = torch.empty_like(gl.t)
+            ws = workspace(lib.gf_joint_workspace_bytes(dt, B, C, h, w, H, W, p.radius), dev)
+            rc = lib.gf_joint_fwd_tape(dt, ptr(gl.t), ptr(sl.t), ptr(gh.t), ptr(out), ptr(slope), B,
+                                       C, h, w, H, W, int(p.radius), float(p.eps), ptr(ws),
+                                       ws.numel(), status.ptr, _stream(gl))
+        else:
+            nbytes = lib.gf_joint_workspace_bytes(dt, B, C, h, w, H, W, p.radius)
+            ws = workspace(nbytes, dev)
+            rc = lib.gf_joint_fwd(dt, ptr(gl.t), ptr(sl.t), ptr(gh.t), ptr(out), B, C, h, w, H, W,
+                                  int(p.radius), float(p.eps), ptr(ws), ws.numel(), status.ptr,
+                                  _stream(gl))
+    finally:
+        if mode:
+            lib.gf_joint_fwd_mode(mode_old)
     _lib.check(rc, "forward_joint")
     if check:
         status.raise_if_set("forward_joint", (gl.t, gh.t, sl.t))
