@@ -85,7 +85,9 @@ def apply(lib, A, Bc, hr_x):
 
 # widths: multiples of 4 (segment walk; 4 or 8 columns per lane), one strip and
 # several, a ragged last strip; 125 / 30 (w % 4 != 0: the tile kernel)
-SHAPES = [(37, 44), (64, 256), (130, 132), (16, 512), (50, 125), (9, 30), (2, 4), (300, 768)]
+SHAPES = [(37, 44), (64, 256), (130, 132), (16, 512), (50, 125), (9, 30), (2, 4), (300, 768),
+          # heights around the 16-row pieces and below the window, widths around the strips
+          (2, 8), (3, 4), (17, 12), (15, 124), (16, 128), (33, 252), (5, 248)]
 
 
 @pytest.mark.parametrize("r", [0, 1, 2, 3, 4, 5, 8])
