@@ -177,7 +177,7 @@ __global__ void k_prep(const double* __restrict__ part, const float* __restrict_
 
 // ---- forward: y = W2 lrelu(W1f x + beta) + b2 ------------------------------
 template <int HID>
-__global__ void __launch_bounds__(NT) k_fwd(const float* __restrict__ x, float* __restrict__ y,
+__global__ void __launch_bounds__(NT, 3) k_fwd(const float* __restrict__ x, float* __restrict__ y,
                                              const float* __restrict__ params,
                                              const float* __restrict__ fold, int64_t HW) {
   // per hidden unit: (W1f row, beta) and (W2 column, 0) as one 16-byte word
@@ -196,14 +196,23 @@ __global__ void __launch_bounds__(NT) k_fwd(const float* __restrict__ x, float* 
   using namespace pr;
   const u64 B0 = bc(params[P<HID>::b2]), B1 = bc(params[P<HID>::b2 + 1]),
             B2 = bc(params[P<HID>::b2 + 2]);
-  for (int64_t i = (int64_t)blockIdx.x * NT + threadIdx.x; i < n4; i += (int64_t)gridDim.x * NT) {
-    ulonglong2 X[CI];  // pixel pairs (0,1), (2,3) of each channel
+  // two 4-pixel groups per iteration (i and i + stride): the seven weight
+  // broadcasts of a hidden unit serve four pixel pairs.  leaky ReLU as
+  // max(h, 0.2 h) (slope < 1: the same values as h * slope(h)).
+  const int64_t stride = (int64_t)gridDim.x * NT;
+  const u64 LK = bc(kLeaky);
+  for (int64_t i = (int64_t)blockIdx.x * NT + threadIdx.x; i < n4; i += 2 * stride) {
+    const bool two = i + stride < n4;
+    const int64_t i1 = two ? i + stride : i;
+    ulonglong2 X[2][CI];  // pixel pairs (0,1), (2,3) of each channel, both groups
 #pragma unroll
-    for (int c = 0; c < CI; ++c)
-      X[c] = __ldg(reinterpret_cast<const ulonglong2*>(x + (b * CI + c) * HW) + i);
-    u64 out[CO][2];
+    for (int c = 0; c < CI; ++c) {
+      X[0][c] = __ldg(reinterpret_cast<const ulonglong2*>(x + (b * CI + c) * HW) + i);
+      X[1][c] = __ldg(reinterpret_cast<const ulonglong2*>(x + (b * CI + c) * HW) + i1);
+    }
+    u64 out[CO][4];
 #pragma unroll
-    for (int pp = 0; pp < 2; ++pp) {
+    for (int pp = 0; pp < 4; ++pp) {
       out[0][pp] = B0;
       out[1][pp] = B1;
       out[2][pp] = B2;
@@ -214,19 +223,25 @@ __global__ void __launch_bounds__(NT) k_fwd(const float* __restrict__ x, float* 
       const u64 w0 = bc(wv.x), w1 = bc(wv.y), w2 = bc(wv.z), be = bc(wv.w);
       const u64 v0 = bc(vv.x), v1 = bc(vv.y), v2 = bc(vv.z);
 #pragma unroll
-      for (int pp = 0; pp < 2; ++pp) {
-        const u64 x0 = pp ? X[0].y : X[0].x, x1 = pp ? X[1].y : X[1].x,
-                  x2 = pp ? X[2].y : X[2].x;
+      for (int pp = 0; pp < 4; ++pp) {
+        const int g = pp >> 1;
+        const u64 x0 = (pp & 1) ? X[g][0].y : X[g][0].x, x1 = (pp & 1) ? X[g][1].y : X[g][1].x,
+                  x2 = (pp & 1) ? X[g][2].y : X[g][2].x;
         u64 h = fma2(w2, x2, fma2(w1, x1, fma2(w0, x0, be)));
-        h = mul2(h, slope2(h, kLeaky));  // leaky ReLU 0.2 (gf/guidance.py:36-39)
+        const u64 hl = mul2(h, LK);
+        h = pk(fmaxf(lo(h), lo(hl)), fmaxf(hi(h), hi(hl)));  // leaky ReLU 0.2 (gf/guidance.py:36-39)
         out[0][pp] = fma2(v0, h, out[0][pp]);
         out[1][pp] = fma2(v1, h, out[1][pp]);
         out[2][pp] = fma2(v2, h, out[2][pp]);
       }
     }
 #pragma unroll
-    for (int o = 0; o < CO; ++o)
+    for (int o = 0; o < CO; ++o) {
       reinterpret_cast<ulonglong2*>(y + (b * CO + o) * HW)[i] = make_ulonglong2(out[o][0], out[o][1]);
+      if (two)
+        reinterpret_cast<ulonglong2*>(y + (b * CO + o) * HW)[i1] =
+            make_ulonglong2(out[o][2], out[o][3]);
+    }
   }
 }
 
