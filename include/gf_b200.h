@@ -91,7 +91,13 @@ int gf_bilinear_resize_adjoint(int dtype, const void* g, void* out, int64_t plan
 /* ---- the fast (joint-upsampling) layer: gf/guided.py:152-195, :267-283 ----
  * lr_x = guide_lo, lr_y = src_lo: (B, C, h, w); hr_x = guide_hi: (B, C, H, W)
  * with H >= h, W >= w (any ratio).  out: (B, C, H, W).  NO smoothing of A, b
- * on this path (gf/guided.py:170-178). */
+ * on this path (gf/guided.py:170-178).
+ * gf_joint_fwd on the fp32 fast path (factor 4, 16-byte aligned buffers): calls
+ * of gf_joint_split_threshold() or more high-res elements run as the two
+ * kernels gf_joint_coeffs + gf_joint_apply with the coefficients of every
+ * low-res cell in `workspace` (gf_joint_workspace_bytes; a NULL or smaller
+ * workspace keeps the one-kernel tile forward, which needs none); smaller
+ * calls as one kernel.  Both agree to fp32 rounding of the coefficients. */
 size_t gf_joint_workspace_bytes(int dtype, int64_t B, int64_t C, int64_t h, int64_t w,
                                 int64_t H, int64_t W, int radius);
 
