@@ -298,3 +298,37 @@ def test_hr_pass_tile_height_is_bitwise(lib, gfb, h, w, r):
     for a, b in ((g0.d_src, g1.d_src), (g0.d_guide_lo, g1.d_guide_lo),
                  (g0.d_guide_hi, g1.d_guide_hi)):
         assert torch.equal(a, b)
+
+
+def test_default_path_selection_by_size_and_workspace(lib):
+    """gf_joint_fwd at the threshold (3 x 4096^2 = 48 Mi high-res elements): with
+    a workspace it is the two-kernel forward (bitwise mode 2), without one the
+    one-kernel forward (bitwise mode 1); just below the threshold always the
+    one-kernel forward."""
+    def fwd(lr_x, lr_y, hr_x, r, ws, mode):
+        B, C, h, w = lr_x.shape
+        out = torch.empty_like(hr_x)
+        st = torch.zeros(1, dtype=torch.int32, device="cuda")
+        old = lib.gf_joint_fwd_mode(mode)
+        try:
+            ok(lib, lib.gf_joint_fwd(0, lr_x.data_ptr(), lr_y.data_ptr(), hr_x.data_ptr(),
+                                     out.data_ptr(), B, C, h, w, 4 * h, 4 * w, r, 1e-4,
+                                     ws.data_ptr() if ws is not None else 0,
+                                     ws.numel() if ws is not None else 0, st.data_ptr(), stream()))
+        finally:
+            lib.gf_joint_fwd_mode(old)
+        torch.cuda.synchronize()
+        assert int(st.item()) == 0
+        return out
+
+    assert lib.gf_joint_split_threshold() == 48 << 20
+    for H, split in ((4096, True), (4092, False)):
+        lr_x, lr_y, hr_x = workloads.joint_inputs(1, 3, H, H, seed=H, device="cuda")
+        h = H // 4
+        ws = torch.empty(lib.gf_joint_workspace_bytes(0, 1, 3, h, h, H, H, 2), dtype=torch.uint8,
+                         device="cuda")
+        auto = fwd(lr_x, lr_y, hr_x, 2, ws, 0)
+        assert torch.equal(auto, fwd(lr_x, lr_y, hr_x, 2, ws, 2 if split else 1))
+        one = fwd(lr_x, lr_y, hr_x, 2, None, 0)
+        assert torch.equal(one, fwd(lr_x, lr_y, hr_x, 2, ws, 1))
+        assert float((auto - one).abs().max()) <= 2e-5
