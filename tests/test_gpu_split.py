@@ -332,3 +332,50 @@ def test_default_path_selection_by_size_and_workspace(lib):
         one = fwd(lr_x, lr_y, hr_x, 2, None, 0)
         assert torch.equal(one, fwd(lr_x, lr_y, hr_x, 2, ws, 1))
         assert float((auto - one).abs().max()) <= 2e-5
+
+
+def test_cuda_graph_capture_of_forward_and_backward(lib):
+    """The two-kernel forward (TMA tensor maps passed by value, cp.async ring)
+    and the tape backward capture into a CUDA graph; replays are bitwise the
+    eager results (launch-bound loops can run as graphs)."""
+    B, C, H, r, eps = 2, 3, 512, 2, 1e-4
+    h = H // 4
+    lx, ly, hx = workloads.joint_inputs(B, C, H, H, seed=3, device="cuda")
+    d = torch.randn_like(hx)
+    out, A = torch.empty_like(hx), torch.empty_like(lx)
+    g = [torch.empty_like(lx), torch.empty_like(lx), torch.empty_like(hx)]
+    ws = torch.empty(lib.gf_joint_workspace_bytes(0, B, C, h, h, H, H, r), dtype=torch.uint8,
+                     device="cuda")
+    st = torch.zeros(1, dtype=torch.int32, device="cuda")
+    p = lambda t: t.data_ptr()  # noqa: E731
+
+    def run(sp):
+        ok(lib, lib.gf_joint_fwd_tape(0, p(lx), p(ly), p(hx), p(out), p(A), B, C, h, h, H, H, r,
+                                      eps, p(ws), ws.numel(), p(st), sp))
+        ok(lib, lib.gf_joint_bwd_tape(0, p(lx), p(ly), p(hx), p(A), p(d), p(g[0]), p(g[1]),
+                                      p(g[2]), B, C, h, h, H, H, r, eps, 0, p(ws), ws.numel(),
+                                      p(st), sp))
+
+    old = lib.gf_joint_fwd_mode(2)
+    try:
+        run(torch.cuda.current_stream().cuda_stream)
+        torch.cuda.synchronize()
+        ref = [out.clone()] + [t.clone() for t in g]
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            run(s.cuda_stream)  # the per-device launch setup happens outside the capture
+        torch.cuda.synchronize()
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=s):
+            run(torch.cuda.current_stream().cuda_stream)
+        for t in [out] + g:
+            t.zero_()
+        graph.replay()
+        graph.replay()
+        torch.cuda.synchronize()
+    finally:
+        lib.gf_joint_fwd_mode(old)
+    assert int(st.item()) == 0
+    for a, b in zip(ref, [out] + g):
+        assert torch.equal(a, b)
