@@ -95,9 +95,12 @@ constexpr int kStageTape = 3;
 // and d_out (68 x 136 incl. the halo) staged by TMA into shared memory at CTA
 // start (the whole tile's reads in flight at once, no registers held)
 constexpr int kStageTapeTile = 4;
-constexpr int HTW = THX + 8, HTH = THY + 4;       // staged window: 136 x 68 (= GR rows)
+// staged window: 136 columns x 68 rows (= GR) used; 72 rows loaded and held, so
+// every TMA box is 8 rows (18 copies per tile instead of 34 with 4-row boxes;
+// rows 68..71 arrive and are ignored)
+constexpr int kTileBox = 8;                       // rows per TMA box of the window
+constexpr int HTW = THX + 8, HTH = THY + kTileBox;
 constexpr int HTF = HTW * HTH;                    // floats per field (128-byte multiple)
-constexpr int kTileBox = 4;                       // rows per TMA box of the window
 constexpr int kTileGroups = 9;                    // mbarriers: 8 groups of 8 rows + rows 64..67
 
 template <int RAD, bool NEED_B, int VCH = 0, int HCH = 16, int MODE = kStageLdg>
@@ -929,7 +932,7 @@ __device__ __forceinline__ void mse_hr_body(const MseHrArgs& a, const CUtensorMa
                                             const CUtensorMap* tmY) {
   // this tile's geometry (shadows the namespace's 16-row constants)
   constexpr int TLY = TY, THY = 4 * TY, NT = 32 * (TY / 2);
-  constexpr int RA = TY + 2, GR = THY + 4, HTH = THY + 4, HTF = HTW * HTH;
+  constexpr int RA = TY + 2, GR = THY + 4, HTH = THY + kTileBox, HTF = HTW * HTH;
   constexpr int kTileGroups = TY / 2 + 1;  // 8-row groups + the 4 extra rows
   static_assert(TY == jf::TLY || (MODE == kStageTapeTile && !MSE), "8-row tiles: tape + TMA only");
   extern __shared__ float4 smem4[];
@@ -1933,7 +1936,7 @@ void fused_joint_bwd(const float* lr_x, const float* lr_y, const float* hr_x, co
         void* args[] = {&tmG, &tmD, &a};
         if (g_joint_bwd_hr_tile == 8 && (h + 7) / 8 <= 65535) {  // 32-row tiles, 128 threads
           constexpr int TY = 8, GR8 = 4 * TY + 4;
-          const size_t sma = 128 + (2 * jf::HTW * GR8 + 2 * (TY + 2) * jf::CAP +
+          const size_t sma = 128 + (2 * jf::HTW * (4 * TY + jf::kTileBox) + 2 * (TY + 2) * jf::CAP +
                                     2 * GR8 * jf::TLX) * sizeof(float);
           set_smem(fns.hr_pass_at8, sma);
           dim3 grid8(grid.x, (unsigned)((h + TY - 1) / TY), grid.z);
